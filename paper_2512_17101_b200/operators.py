@@ -1,0 +1,372 @@
+"""The DG operator program: compressible Euler / Navier-Stokes right-hand sides and RK4,
+written ONCE against the array-context API of the reference
+(/root/reference/pkg/src/laze/frontend.py:257-302 op namespace, :222-250 subscripts,
+:488-519 ``outline``) and nothing else.
+
+The same functions run
+* on ``laze.ArrayContext(mode="eager")`` / ``mode="lazy"``   -- the CPU reference,
+* on ``oracle.laze_port.NumpyArrayContext``                  -- its travelling restatement,
+* on ``paper_2512_17101_b200.B200ArrayContext``              -- where the *outlined*
+  functions below (``dg_euler_rhs``, ``dg_ns_grad``, ``dg_ns_rhs``) are dispatched BY NAME to
+  the fused sm_100a kernels behind the C ABI (include/dgb200.h), exactly at the call
+  boundary the reference creates for an outlined function
+  (/root/reference/pkg/src/laze/adfg.py:722-803: arguments and results are materialised).
+
+The physics is not pinned by the reference ("parity unpinned" at the physics
+level); the formulation chosen here, following the paper's MIRGE-Com description
+(/root/reference/PAPER.md:1738-1739,1778-1791), is:
+
+* conserved state ``q = [rho, rho E, rho u_1..rho u_d]`` stored ``(C, E, Np)``;
+* weak-form nodal DG on affine simplices,
+  ``rhs = sum_{r,x} Sw_r (drdx[r,x] F_x) - lift(fscale * F*.n)``;
+* inviscid numerical flux: local Lax-Friedrichs / Rusanov with
+  ``lambda = max(|u-| + c-, |u+| + c+)``;
+* viscous terms: BR1 -- ``grad q`` by a weak-form gradient with the central flux (first
+  derivative pass), viscous flux from ``(q, grad q)`` with the central flux (second pass);
+* ideal gas ``p = (gamma-1)(rho E - rho |u|^2/2)``, ``T = p/(rho R)``, constant ``mu, kappa``;
+* boundary conditions by exterior ("plus") states: prescribed far-field state, or wall
+  (Euler: slip, momentum reflected about the normal; Navier-Stokes: adiabatic no-slip,
+  momentum negated); ``grad q`` plus-state equals the minus-state on boundary faces.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .discretization import BC_FARFIELD, BC_WALL, DGDiscretization
+from .dofarray import DOFArray
+
+# {{{ pointwise physics (array-context generic)
+
+
+def _split(q, dim):
+    rho, ener = q[0], q[1]
+    mom = [q[2 + i] for i in range(dim)]
+    return rho, ener, mom
+
+
+def _pressure(actx, gamma, rho, ener, mom, vel):
+    ke = mom[0] * vel[0]
+    for i in range(1, len(mom)):
+        ke = ke + mom[i] * vel[i]
+    return (gamma - 1.0) * (ener - 0.5 * ke)
+
+
+def inviscid_flux(actx, q, gamma, dim):
+    """``F[x][c]`` as nested lists of arrays shaped like ``q[0]``."""
+    rho, ener, mom = _split(q, dim)
+    vel = [m / rho for m in mom]
+    p = _pressure(actx, gamma, rho, ener, mom, vel)
+    flux = []
+    for x in range(dim):
+        fx = [mom[x], vel[x] * (ener + p)]
+        for i in range(dim):
+            mi = mom[i] * vel[x]
+            fx.append(mi + p if i == x else mi)
+        flux.append(fx)
+    return flux, vel, p
+
+
+def viscous_flux(actx, q, gq, vel, phys, dim):
+    """``Fv[x][c]`` from the state ``q`` and ``gq[x][c] = d q_c / d x_x``."""
+    gamma, mu, kappa, rgas = phys
+    rho, ener, mom = _split(q, dim)
+    inv_rho = 1.0 / rho
+    # velocity gradient  du[i][x] = d u_i / d x_x
+    du = [[(gq[x][2 + i] - vel[i] * gq[x][0]) * inv_rho for x in range(dim)] for i in range(dim)]
+    div = du[0][0]
+    for i in range(1, dim):
+        div = div + du[i][i]
+    etot = ener * inv_rho
+    # temperature gradient: T = (gamma-1)/R * (E/rho - |u|^2/2)
+    dT = []
+    for x in range(dim):
+        de = (gq[x][1] - etot * gq[x][0]) * inv_rho
+        for i in range(dim):
+            de = de - vel[i] * du[i][x]
+        dT.append(((gamma - 1.0) / rgas) * de)
+    tau = [[None] * dim for _ in range(dim)]
+    for i in range(dim):
+        for x in range(dim):
+            t = mu * (du[i][x] + du[x][i])
+            if i == x:
+                t = t - (2.0 / 3.0) * mu * div
+            tau[i][x] = t
+    flux = []
+    for x in range(dim):
+        work = vel[0] * tau[0][x]
+        for i in range(1, dim):
+            work = work + vel[i] * tau[i][x]
+        fx = [None, work + kappa * dT[x]]
+        for i in range(dim):
+            fx.append(tau[i][x])
+        flux.append(fx)
+    return flux
+
+
+def _normal_dot(flux, nrm, dim, comps):
+    out = []
+    for c in comps:
+        acc = None
+        for x in range(dim):
+            if flux[x][c] is None:
+                continue
+            term = flux[x][c] * nrm[x]
+            acc = term if acc is None else acc + term
+        out.append(acc)
+    return out
+
+
+def _wavespeed(actx, gamma, q, vel, p, dim):
+    v2 = vel[0] * vel[0]
+    for i in range(1, dim):
+        v2 = v2 + vel[i] * vel[i]
+    return actx.np.sqrt(v2) + actx.np.sqrt(gamma * p / q[0])
+
+# }}}
+
+
+# {{{ traces and boundary states
+
+def _traces(actx, q, ghost, vmap_m, vmap_p, lead, E, Np, Nf, Nfp):
+    """Minus/plus face traces ``(lead, E, Nf, Nfp)`` through the flat int64 index maps
+    (/root/reference/pkg/src/laze/adfg.py:502-560: one index array per subscript)."""
+    flat = actx.np.reshape(q, (lead, E * Np))
+    tm = actx.np.reshape(flat[:, vmap_m], (lead, E, Nf, Nfp))
+    if ghost is not None:
+        G = ghost.shape[-2]
+        flat = actx.np.concatenate([flat, actx.np.reshape(ghost, (lead, G * Np))], axis=1)
+    tp = actx.np.reshape(flat[:, vmap_p], (lead, E, Nf, Nfp))
+    return tm, tp
+
+
+def _bc_state(actx, qm, qp, nrm, bc_kind, qfar, dim, wall):
+    """Exterior state per field: interior faces keep ``qp``."""
+    C = dim + 2
+    is_far = actx.np.equal(bc_kind, BC_FARFIELD)
+    is_wall = actx.np.equal(bc_kind, BC_WALL)
+    mom_m = [qm[2 + i] for i in range(dim)]
+    if wall == "slip":
+        mn = mom_m[0] * nrm[0]
+        for i in range(1, dim):
+            mn = mn + mom_m[i] * nrm[i]
+        mom_w = [mom_m[i] - 2.0 * mn * nrm[i] for i in range(dim)]
+    else:  # no-slip
+        mom_w = [-mom_m[i] for i in range(dim)]
+    wall_state = [qm[0], qm[1]] + mom_w
+    out = []
+    for c in range(C):
+        v = actx.np.where(is_wall, wall_state[c], qp[c])
+        v = actx.np.where(is_far, qfar[c], v)
+        out.append(v)
+    return out
+
+# }}}
+
+
+# {{{ the three outlined DG functions -- the plugin boundary
+
+def _make_euler_rhs(dim, with_ghost):
+    def body(actx, q, ghost, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, phys):
+        C, E, Np = q.shape
+        Nf = dim + 1
+        Nfp = lift.shape[1] // Nf
+        gamma = phys[0]
+        qc = [q[c] for c in range(C)]
+        flux, _, _ = inviscid_flux(actx, qc, gamma, dim)
+        fstack = actx.np.stack([actx.np.stack(fx) for fx in flux])            # (d, C, E, Np)
+        vol = actx.np.einsum("rij,rxe,xcej->cei", Sw, drdx, fstack)
+        tm, tp = _traces(actx, q, ghost, vmap_m, vmap_p, C, E, Np, Nf, Nfp)
+        nrm = [normals[x] for x in range(dim)]
+        qm = [tm[c] for c in range(C)]
+        qp = _bc_state(actx, qm, [tp[c] for c in range(C)], nrm, bc_kind,
+                       [qfar[c] for c in range(C)], dim, "slip")
+        fm, vm, pm = inviscid_flux(actx, qm, gamma, dim)
+        fp, vp, pp = inviscid_flux(actx, qp, gamma, dim)
+        lam = actx.np.maximum(_wavespeed(actx, gamma, qm, vm, pm, dim),
+                              _wavespeed(actx, gamma, qp, vp, pp, dim))
+        fnm = _normal_dot(fm, nrm, dim, range(C))
+        fnp = _normal_dot(fp, nrm, dim, range(C))
+        fstar = [fscale * (0.5 * (fnm[c] + fnp[c]) + 0.5 * lam * (qm[c] - qp[c])) for c in range(C)]
+        fs = actx.np.reshape(actx.np.stack(fstar), (C, E, Nf * Nfp))
+        return vol - actx.np.einsum("if,cef->cei", lift, fs)
+
+    if with_ghost:
+        def dg_euler_rhs(q, ghost, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, phys):
+            return body(dg_euler_rhs.actx, q, ghost, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p,
+                        bc_kind, qfar, phys)
+    else:
+        def dg_euler_rhs(q, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, phys):
+            return body(dg_euler_rhs.actx, q, None, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p,
+                        bc_kind, qfar, phys)
+    return dg_euler_rhs
+
+
+def _make_ns_grad(dim, with_ghost):
+    def body(actx, q, ghost, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar):
+        C, E, Np = q.shape
+        Nf = dim + 1
+        Nfp = lift.shape[1] // Nf
+        vol = actx.np.einsum("rij,rxe,cej->xcei", Sw, drdx, q)
+        tm, tp = _traces(actx, q, ghost, vmap_m, vmap_p, C, E, Np, Nf, Nfp)
+        nrm = [normals[x] for x in range(dim)]
+        qm = [tm[c] for c in range(C)]
+        qp = _bc_state(actx, qm, [tp[c] for c in range(C)], nrm, bc_kind,
+                       [qfar[c] for c in range(C)], dim, "noslip")
+        qstar = [fscale * (0.5 * (qm[c] + qp[c])) for c in range(C)]
+        fs = actx.np.stack([actx.np.stack([nrm[x] * qstar[c] for c in range(C)]) for x in range(dim)])
+        fs = actx.np.reshape(fs, (dim, C, E, Nf * Nfp))
+        return actx.np.einsum("if,xcef->xcei", lift, fs) - vol
+
+    if with_ghost:
+        def dg_ns_grad(q, ghost, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar):
+            return body(dg_ns_grad.actx, q, ghost, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p,
+                        bc_kind, qfar)
+    else:
+        def dg_ns_grad(q, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar):
+            return body(dg_ns_grad.actx, q, None, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p,
+                        bc_kind, qfar)
+    return dg_ns_grad
+
+
+def _make_ns_rhs(dim, with_ghost):
+    def body(actx, q, gq, ghost, gghost, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind,
+             qfar, phys):
+        C, E, Np = q.shape
+        Nf = dim + 1
+        Nfp = lift.shape[1] // Nf
+        ph = [phys[k] for k in range(4)]
+        gamma = ph[0]
+        qc = [q[c] for c in range(C)]
+        gc = [[gq[x][c] for c in range(C)] for x in range(dim)]
+        finv, vel, _ = inviscid_flux(actx, qc, gamma, dim)
+        fvis = viscous_flux(actx, qc, gc, vel, ph, dim)
+        ftot = [[finv[x][c] if fvis[x][c] is None else finv[x][c] - fvis[x][c] for c in range(C)]
+                for x in range(dim)]
+        fstack = actx.np.stack([actx.np.stack(fx) for fx in ftot])            # (d, C, E, Np)
+        vol = actx.np.einsum("rij,rxe,xcej->cei", Sw, drdx, fstack)
+
+        tm, tp = _traces(actx, q, ghost, vmap_m, vmap_p, C, E, Np, Nf, Nfp)
+        gflat = actx.np.reshape(gq, (dim * C, E, Np))
+        gg = None if gghost is None else actx.np.reshape(gghost, (dim * C, gghost.shape[-2], Np))
+        gtm, gtp = _traces(actx, gflat, gg, vmap_m, vmap_p, dim * C, E, Np, Nf, Nfp)
+        nrm = [normals[x] for x in range(dim)]
+        qm = [tm[c] for c in range(C)]
+        qp = _bc_state(actx, qm, [tp[c] for c in range(C)], nrm, bc_kind,
+                       [qfar[c] for c in range(C)], dim, "noslip")
+        gm = [[gtm[x * C + c] for c in range(C)] for x in range(dim)]
+        gp = [[gtp[x * C + c] for c in range(C)] for x in range(dim)]
+        fm, vm, pm = inviscid_flux(actx, qm, gamma, dim)
+        fp, vp, pp = inviscid_flux(actx, qp, gamma, dim)
+        lam = actx.np.maximum(_wavespeed(actx, gamma, qm, vm, pm, dim),
+                              _wavespeed(actx, gamma, qp, vp, pp, dim))
+        fnm = _normal_dot(fm, nrm, dim, range(C))
+        fnp = _normal_dot(fp, nrm, dim, range(C))
+        vnm = _normal_dot(viscous_flux(actx, qm, gm, vm, ph, dim), nrm, dim, range(C))
+        vnp = _normal_dot(viscous_flux(actx, qp, gp, vp, ph, dim), nrm, dim, range(C))
+        fstar = []
+        for c in range(C):
+            f = 0.5 * (fnm[c] + fnp[c]) + 0.5 * lam * (qm[c] - qp[c])
+            if vnm[c] is not None:
+                f = f - 0.5 * (vnm[c] + vnp[c])
+            fstar.append(fscale * f)
+        fs = actx.np.reshape(actx.np.stack(fstar), (C, E, Nf * Nfp))
+        return vol - actx.np.einsum("if,cef->cei", lift, fs)
+
+    if with_ghost:
+        def dg_ns_rhs(q, gq, ghost, gghost, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind,
+                      qfar, phys):
+            return body(dg_ns_rhs.actx, q, gq, ghost, gghost, Sw, drdx, lift, normals, fscale, vmap_m,
+                        vmap_p, bc_kind, qfar, phys)
+    else:
+        def dg_ns_rhs(q, gq, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, phys):
+            return body(dg_ns_rhs.actx, q, gq, None, None, Sw, drdx, lift, normals, fscale, vmap_m,
+                        vmap_p, bc_kind, qfar, phys)
+    return dg_ns_rhs
+
+# }}}
+
+
+class _OperatorBase:
+    def __init__(self, dcoll: DGDiscretization, gamma=1.4, mu=0.0, prandtl=0.72, rgas=1.0,
+                 farfield=None):
+        self.dcoll = dcoll
+        self.actx = actx = dcoll.actx
+        self.dim = dim = dcoll.dim
+        self.gamma, self.mu, self.rgas = float(gamma), float(mu), float(rgas)
+        self.kappa = self.mu * (self.gamma * self.rgas / (self.gamma - 1.0)) / float(prandtl)
+        C = dim + 2
+        if farfield is None:
+            farfield = np.zeros(C)
+            farfield[0] = 1.0
+            farfield[1] = 1.0 / (self.gamma * (self.gamma - 1.0))
+        self.qfar_host = np.asarray(farfield, dtype=np.float64).reshape(C)
+        self.qfar = actx.from_numpy(self.qfar_host.reshape(C, 1, 1, 1))
+        self.phys_host = np.array([self.gamma, self.mu, self.kappa, self.rgas])
+        self.phys = actx.from_numpy(self.phys_host)
+
+    def _outlined(self, maker, with_ghost):
+        f = maker(self.dim, with_ghost)
+        f.actx = self.actx
+        f.dg_dim = self.dim
+        return self.actx.outline(f)
+
+    def _common(self):
+        d = self.dcoll
+        return (d.Sw, d.drdx, d.lift, d.normals, d.fscale, d.vmap_m, d.vmap_p, d.bc_kind, self.qfar)
+
+
+class EulerOperator(_OperatorBase):
+    """``rhs(q)`` of the compressible Euler equations; ``q`` is a ``DOFArray`` ``(C, E, Np)``."""
+
+    def __init__(self, dcoll, gamma=1.4, farfield=None):
+        super().__init__(dcoll, gamma=gamma, farfield=farfield)
+        self._f = self._outlined(_make_euler_rhs, False)
+        self._fg = self._outlined(_make_euler_rhs, True)
+
+    def rhs(self, q: DOFArray, t=0.0, ghost=None) -> DOFArray:
+        if ghost is None:
+            out = self._f(q.data, *self._common(), self.phys)
+        else:
+            out = self._fg(q.data, ghost, *self._common(), self.phys)
+        return DOFArray(self.actx, out)
+
+
+class NavierStokesOperator(_OperatorBase):
+    """Two-pass (BR1) compressible Navier-Stokes right-hand side."""
+
+    def __init__(self, dcoll, gamma=1.4, mu=1e-3, prandtl=0.72, rgas=1.0, farfield=None):
+        super().__init__(dcoll, gamma=gamma, mu=mu, prandtl=prandtl, rgas=rgas, farfield=farfield)
+        self._g = self._outlined(_make_ns_grad, False)
+        self._gg = self._outlined(_make_ns_grad, True)
+        self._f = self._outlined(_make_ns_rhs, False)
+        self._fg = self._outlined(_make_ns_rhs, True)
+
+    def grad(self, q: DOFArray, ghost=None) -> DOFArray:
+        if ghost is None:
+            out = self._g(q.data, *self._common())
+        else:
+            out = self._gg(q.data, ghost, *self._common())
+        return DOFArray(self.actx, out)
+
+    def rhs(self, q: DOFArray, t=0.0, ghost=None, grad_ghost_fn=None) -> DOFArray:
+        gq = self.grad(q, ghost)
+        if ghost is None:
+            out = self._f(q.data, gq.data, *self._common(), self.phys)
+        else:
+            gghost = grad_ghost_fn(gq)
+            out = self._fg(q.data, gq.data, ghost, gghost, *self._common(), self.phys)
+        return DOFArray(self.actx, out)
+
+
+# {{{ time stepping
+
+def rk4_step(rhs, q, t, dt):
+    """Classical fourth-order Runge-Kutta step in array-context arithmetic
+    (the paper's applications step with RK4: /root/reference/PAPER.md:1692)."""
+    k1 = rhs(q, t)
+    k2 = rhs(q + (0.5 * dt) * k1, t + 0.5 * dt)
+    k3 = rhs(q + (0.5 * dt) * k2, t + 0.5 * dt)
+    k4 = rhs(q + dt * k3, t + dt)
+    return q + (dt / 6.0) * (k1 + 2.0 * k2 + 2.0 * k3 + k4)
+
+# }}}
