@@ -1,0 +1,159 @@
+/*
+ * dgb200.h -- C ABI of the B200-native DG right-hand-side path.
+ *
+ * This is the drop-in boundary.  The reference is a pure-Python package
+ * and has no FFI of its own; what this library replaces is the *executor* behind the
+ * reference's array context for the outlined DG functions and the array ops they are
+ * written in.  Each entry point cites the reference interface it stands in for
+ * (paths relative to /root/reference/pkg/src/laze/).  INTEGRATION.md shows the ctypes
+ * binding a maintainer adds on the reference side.
+ *
+ * Conventions
+ *   - every function returns a dgb_status (0 = ok); dgb_last_error() gives the text.
+ *     The Python shim maps codes to the reference's exception classes (errors.py:11-119).
+ *   - all `dev` pointers are CUDA device pointers of the current device; `host` pointers
+ *     are ordinary host memory.  No torch / framework types cross this boundary.
+ *   - arrays are dense row-major (scalar_ir.py:147-151, backend.py:222-231), FP64 unless
+ *     stated, index maps int64 (adfg.py:540-541).
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream); all work
+ *     is enqueued asynchronously on it.
+ *   - inputs are never modified and never aliased by outputs (adfg.py:341-348 ownership).
+ */
+#ifndef DGB200_H
+#define DGB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DGB_OK = 0,
+  DGB_ERR_CUDA = 1,            /* CUDA runtime failure                       -> LazeError              */
+  DGB_ERR_INVALID = 2,         /* bad argument / unsupported (dim, order)    -> ShapeMismatch          */
+  DGB_ERR_OUT_OF_BOUNDS = 3,   /* gather index outside [0, extent)           -> OutOfBoundsIndex       */
+  DGB_ERR_BAD_MAP = 4,         /* index map is not a conforming face map     -> BindingMismatch        */
+  DGB_ERR_DTYPE = 5            /* unsupported element type                   -> DTypeMismatch          */
+} dgb_status;
+
+/* element types, adfg.py:39-45 */
+typedef enum { DGB_F64 = 0, DGB_I64 = 1, DGB_BOOL = 2 } dgb_dtype;
+
+const char* dgb_last_error(void);
+int dgb_version(void);
+
+/* ---- device memory + transfers: ArrayContext.from_numpy / to_numpy (frontend.py:327-343) ---- */
+int dgb_malloc(void** dev, size_t bytes);
+int dgb_free(void* dev);
+int dgb_host_alloc(void** host, size_t bytes);                 /* pinned host staging */
+int dgb_host_free(void* host);
+int dgb_memcpy_h2d(void* dev, const void* host, size_t bytes, void* stream);
+int dgb_memcpy_d2h(void* host, const void* dev, size_t bytes, void* stream);
+int dgb_memcpy_d2d(void* dst_dev, const void* src_dev, size_t bytes, void* stream);
+int dgb_stream_sync(void* stream);
+
+/* ---- discretisation handle ------------------------------------------------------------------
+ * Uploads the reference matrices and binds the per-mesh device arrays that the outlined DG
+ * functions receive as arguments.  The int64 face maps (`vmap_m`, `vmap_p`: flat indices into
+ * u.reshape(E*Np), used through Indexing, adfg.py:502-560) are range-checked ONCE here
+ * (backend.py:59-68 checks on every load) and compressed to (neighbour element, neighbour
+ * face, vertex permutation, bc) per face; dgb_disc_expand_maps() regenerates the int64 maps
+ * from the compressed form so that bit-exactness can be asserted.
+ *
+ *   Sw_host      (dim, Np, Np)      weak reference-derivative matrices
+ *   lift_host    (Np, Nf*Nfp)
+ *   face_nodes_host (Nf, Nfp) int64, face_perms_host (dim!, Nfp) int64
+ *   drdx_dev     (dim, dim, E)   [r, x, e]
+ *   normals_dev  (dim, E, Nf)
+ *   fscale_dev   (E, Nf)
+ *   vmap_m_dev, vmap_p_dev (E*Nf*Nfp) int64; entries of vmap_p in [E*Np, (E+G)*Np) address
+ *                ghost elements (halo copies of remote elements, G may be 0)
+ *   bc_kind_dev  (E, Nf) int64: 0 interior, 1 far-field, 2 wall
+ * The device arrays must stay alive (and unchanged) for the life of the handle.
+ */
+typedef struct dgb_disc dgb_disc;
+
+int dgb_disc_create(dgb_disc** out, int dim, int order, int64_t nelements, int64_t nghost,
+                    const double* Sw_host, const double* lift_host,
+                    const int64_t* face_nodes_host, const int64_t* face_perms_host,
+                    const double* drdx_dev, const double* normals_dev, const double* fscale_dev,
+                    const int64_t* vmap_m_dev, const int64_t* vmap_p_dev,
+                    const int64_t* bc_kind_dev, void* stream);
+int dgb_disc_destroy(dgb_disc* disc);
+int dgb_disc_expand_maps(const dgb_disc* disc, int64_t* vmap_m_dev, int64_t* vmap_p_dev, void* stream);
+
+/* ---- the outlined DG functions (operators.py; reference boundary: a Call to a
+ *      FunctionDefinition, adfg.py:722-803, executed as a CallStep, backend.py:90-96) ----------
+ *   q      (C, E, Np)          conserved state [rho, rho E, rho u...]
+ *   ghost  (C, G, Np) or NULL  halo elements
+ *   gradq  (dim, C, E, Np), gghost (dim, C, G, Np) or NULL
+ *   qfar_host (C)  far-field state;  phys_host (4) = gamma, mu, kappa, R
+ *   rhs    (C, E, Np)
+ */
+int dgb_euler_rhs(const dgb_disc* disc, const double* q_dev, const double* ghost_dev, double* rhs_dev,
+                  const double* qfar_host, const double* phys_host, void* stream);
+int dgb_ns_grad(const dgb_disc* disc, const double* q_dev, const double* ghost_dev, double* gradq_dev,
+                const double* qfar_host, void* stream);
+int dgb_ns_rhs(const dgb_disc* disc, const double* q_dev, const double* gradq_dev,
+               const double* ghost_dev, const double* gghost_dev, double* rhs_dev,
+               const double* qfar_host, const double* phys_host, void* stream);
+
+/* Same right-hand sides with the Runge-Kutta stage update fused into the epilogue (north-star
+ * item 3): instead of rhs, writes
+ *     out1 = a1 * x1 + b1 * rhs      (x1 may equal q; out1 must not alias q or x2)
+ *     out2 = a2 * x2 + b2 * rhs      (out2 may be NULL; out2 may alias x2)
+ * all (C, E, Np).  rk = {a1, b1, a2, b2} on the host.
+ */
+int dgb_euler_rhs_rk(const dgb_disc* disc, const double* q_dev, const double* ghost_dev,
+                     const double* x1_dev, double* out1_dev, const double* x2_dev, double* out2_dev,
+                     const double* rk_host, const double* qfar_host, const double* phys_host, void* stream);
+int dgb_ns_rhs_rk(const dgb_disc* disc, const double* q_dev, const double* gradq_dev,
+                  const double* ghost_dev, const double* gghost_dev,
+                  const double* x1_dev, double* out1_dev, const double* x2_dev, double* out2_dev,
+                  const double* rk_host, const double* qfar_host, const double* phys_host, void* stream);
+
+/* ---- halo packing: element rows <-> contiguous message (Send / Receive payloads,
+ *      adfg.py:380-399,834-869).  dst[c, i, :] = src[c, elems[i], :]                        ---- */
+int dgb_pack_elements(double* dst_dev, const double* src_dev, const int64_t* elems_dev,
+                      int64_t ncomp, int64_t nsrc_elems, int64_t nsel, int64_t ndofs, void* stream);
+
+/* ---- generic array ops of the context (frontend.py:257-302), for glue outside the fused
+ *      functions.  Shapes are given after broadcasting: `rank`, `shape[rank]`, and per-operand
+ *      element strides (0 on broadcast axes).  Outputs are dense row-major.                 ---- */
+/* binary: ops in the order of expr.py:265-281 */
+typedef enum { DGB_ADD = 0, DGB_SUB, DGB_MUL, DGB_TRUEDIV, DGB_FLOORDIV, DGB_MOD, DGB_POW, DGB_MIN,
+               DGB_MAX, DGB_LT, DGB_LE, DGB_GT, DGB_GE, DGB_EQ, DGB_NE } dgb_binop;
+typedef enum { DGB_NEG = 0, DGB_ABS, DGB_SQRT, DGB_EXP, DGB_LOG } dgb_unop;   /* expr.py:283-289 */
+
+int dgb_ew_binary(int op, void* out_dev, int out_dtype,
+                  const void* a_dev, int a_dtype, const int64_t* a_strides,
+                  const void* b_dev, int b_dtype, const int64_t* b_strides,
+                  int rank, const int64_t* shape, void* stream);
+int dgb_ew_unary(int op, void* out_dev, int out_dtype, const void* a_dev, int a_dtype,
+                 int64_t n, void* stream);
+int dgb_ew_where(void* out_dev, int out_dtype,
+                 const void* c_dev, int c_dtype, const int64_t* c_strides,
+                 const void* a_dev, int a_dtype, const int64_t* a_strides,
+                 const void* b_dev, int b_dtype, const int64_t* b_strides,
+                 int rank, const int64_t* shape, void* stream);
+/* strided copy / cast (reshape of views, slices, stack, concatenate): out dense */
+int dgb_copy_strided(void* out_dev, int out_dtype, const void* a_dev, int a_dtype,
+                     const int64_t* a_strides, int rank, const int64_t* shape, void* stream);
+/* same with explicit element strides on the output (writes into a slice: concatenate / stack) */
+int dgb_copy_scatter(void* out_dev, int out_dtype, const int64_t* out_strides, const void* a_dev, int a_dtype,
+                     const int64_t* a_strides, int rank, const int64_t* shape, void* stream);
+/* gather along one axis, array viewed as (outer, extent, inner): out[o, k, i] = a[o, idx[k], i];
+ * every index is range-checked, DGB_ERR_OUT_OF_BOUNDS otherwise (frontend.py:121-136) */
+int dgb_take(void* out_dev, const void* a_dev, int dtype, const int64_t* idx_dev,
+             int64_t outer, int64_t extent, int64_t inner, int64_t nidx, void* stream);
+/* einsum with up to 3 FP64 operands: loop extents `ext[nletters]` (output letters first, then
+ * summed letters, ascending accumulation like expr.py:344-364), per-operand strides per letter */
+int dgb_einsum(double* out_dev, int nops, const double* const* ops_dev, const int64_t* op_strides,
+               int nout_letters, int nletters, const int64_t* ext, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DGB200_H */

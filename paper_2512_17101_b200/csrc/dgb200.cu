@@ -1,0 +1,407 @@
+// C ABI of the B200 DG right-hand-side path: discretisation handle, kernel dispatch, halo
+// packing.  See include/dgb200.h for the contract and the reference interfaces replaced.
+#include "../../include/dgb200.h"
+#include "dgb_kernels.cuh"
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) { g_err = msg; return code; }
+
+#define DGB_CUDA(expr)                                                                      \
+  do {                                                                                      \
+    cudaError_t e_ = (expr);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return fail(DGB_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));        \
+  } while (0)
+
+int num_sms() {
+  static int n = 0;
+  if (!n) { int dev = 0; cudaGetDevice(&dev); cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev); }
+  return n;
+}
+
+}  // namespace
+
+struct dgb_disc {
+  int dim = 0, order = 0, Np = 0, Nf = 0, Nfp = 0, nperm = 0;
+  dgb::DiscDev dev{};
+  double *Wv = nullptr, *Wl = nullptr, *Wq = nullptr, *Wf = nullptr;
+  long long* conn = nullptr;
+  int* tables = nullptr;
+  const int64_t* bc_kind = nullptr;
+};
+
+// {{{ connectivity compression / expansion
+
+namespace {
+
+__global__ void k_build_conn(const long long* __restrict__ vm, const long long* __restrict__ vp,
+                             const long long* __restrict__ bc, const int* __restrict__ tables,
+                             long long E, long long G, int Np, int Nf, int Nfp, int nperm,
+                             long long* __restrict__ conn, int* __restrict__ err) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= E * Nf) return;
+  const long long e = idx / Nf;
+  const int f = (int)(idx - e * Nf);
+  const int* fn = tables;
+  const int* perm = tables + Nf * Nfp;
+  const long long base = idx * Nfp;
+  const long long limit = (E + G) * Np;
+  bool oob = false, bad = false;
+  for (int m = 0; m < Nfp; ++m) {
+    const long long a = vm[base + m], b = vp[base + m];
+    if (a < 0 || a >= E * (long long)Np || b < 0 || b >= limit) oob = true;
+    if (a != e * Np + fn[f * Nfp + m]) bad = true;
+  }
+  if (oob) { atomicMax(err, DGB_ERR_OUT_OF_BOUNDS + 100); return; }
+  const long long bck = bc[idx];
+  if (bck < 0 || bck > 2) bad = true;
+  long long packed = 0;
+  if (!bad && bck != 0) {
+    for (int m = 0; m < Nfp; ++m) if (vp[base + m] != vm[base + m]) bad = true;
+    packed = dgb::conn_pack(e, f, 0, (int)bck);
+  } else if (!bad) {
+    const long long nb = vp[base] / Np;
+    bool found = false;
+    for (int nf = 0; nf < Nf && !found; ++nf)
+      for (int p = 0; p < nperm && !found; ++p) {
+        bool ok = true;
+        for (int m = 0; m < Nfp; ++m)
+          if (vp[base + m] != nb * Np + fn[nf * Nfp + perm[p * Nfp + m]]) { ok = false; break; }
+        if (ok) { found = true; packed = dgb::conn_pack(nb, nf, p, 0); }
+      }
+    if (!found) bad = true;
+  }
+  if (bad) { atomicMax(err, DGB_ERR_BAD_MAP); return; }
+  conn[idx] = packed;
+}
+
+__global__ void k_expand_conn(const long long* __restrict__ conn, const int* __restrict__ tables,
+                              long long E, int Np, int Nf, int Nfp,
+                              long long* __restrict__ vm, long long* __restrict__ vp) {
+  const long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (n >= E * Nf * Nfp) return;
+  const long long ef = n / Nfp;
+  const int m = (int)(n - ef * Nfp);
+  const long long e = ef / Nf;
+  const int f = (int)(ef - e * Nf);
+  const int* fn = tables;
+  const int* perm = tables + Nf * Nfp;
+  const long long c = conn[ef];
+  const long long own = e * Np + fn[f * Nfp + m];
+  vm[n] = own;
+  vp[n] = DGB_CONN_BC(c) ? own
+                         : DGB_CONN_NB(c) * Np + fn[DGB_CONN_NF(c) * Nfp + perm[DGB_CONN_PERM(c) * Nfp + m]];
+}
+
+__global__ void k_pack_elements(double* __restrict__ dst, const double* __restrict__ src,
+                                const long long* __restrict__ elems, long long ncomp, long long nsrc,
+                                long long nsel, long long ndofs) {
+  const long long total = ncomp * nsel * ndofs;
+  for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < total;
+       n += (long long)gridDim.x * blockDim.x) {
+    const long long j = n % ndofs, ci = n / ndofs;
+    const long long i = ci % nsel, c = ci / nsel;
+    dst[n] = src[(c * nsrc + elems[i]) * ndofs + j];
+  }
+}
+
+}  // namespace
+
+// }}}
+
+// {{{ launch configuration per (dim, order)
+
+namespace {
+
+template <int DIM, int P> struct Cfg { static constexpr int K = 16, NW = DIM == 3 ? 5 : 4, MT = 2, KG = 16, NWG = DIM == 3 ? 5 : 4; };
+template <> struct Cfg<3, 4> { static constexpr int K = 8, NW = 5, MT = 1, KG = 8, NWG = 5; };
+
+template <typename Kern>
+int persistent_grid(Kern kern, int threads, size_t smem, int nblocks, int* grid) {
+  DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  DGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+  if (occ < 1) return fail(DGB_ERR_INVALID, "kernel does not fit on an SM");
+  long long g = (long long)occ * num_sms();
+  *grid = (int)(g < nblocks ? g : nblocks);
+  return DGB_OK;
+}
+
+template <int DIM, int P, bool VISCOUS>
+int launch_rhs(const dgb_disc* d, const double* q, const double* gq, const double* ghost, const double* gghost,
+               const dgb::Epilogue& ep, const dgb::Phys& ph, cudaStream_t st) {
+  using C = Cfg<DIM, P>;
+  auto kern = dgb::k_rhs<DIM, P, C::K, C::NW, C::MT, VISCOUS>;
+  const size_t smem = sizeof(dgb::RhsSmem<DIM, P, C::K, C::NW, C::MT, VISCOUS>);
+  const long long nb = (d->dev.E + C::K - 1) / C::K;
+  if (nb == 0) return DGB_OK;
+  static int grid_cache = 0; static long long nb_cache = -1;
+  if (nb_cache != nb) { int rc = persistent_grid(kern, C::NW * 32, smem, (int)nb, &grid_cache); if (rc) return rc; nb_cache = nb; }
+  kern<<<grid_cache, C::NW * 32, smem, st>>>(d->dev, q, gq, ghost, gghost, ep, ph, (int)nb);
+  DGB_CUDA(cudaGetLastError());
+  return DGB_OK;
+}
+
+template <int DIM, int P>
+int launch_grad(const dgb_disc* d, const double* q, const double* ghost, double* grad, const dgb::Phys& ph,
+                cudaStream_t st) {
+  using C = Cfg<DIM, P>;
+  auto kern = dgb::k_grad<DIM, P, C::KG, C::NWG>;
+  const size_t smem = sizeof(dgb::GradSmem<DIM, P, C::KG>);
+  const long long nb = (d->dev.E + C::KG - 1) / C::KG;
+  if (nb == 0) return DGB_OK;
+  static int grid_cache = 0; static long long nb_cache = -1;
+  if (nb_cache != nb) { int rc = persistent_grid(kern, C::NWG * 32, smem, (int)nb, &grid_cache); if (rc) return rc; nb_cache = nb; }
+  kern<<<grid_cache, C::NWG * 32, smem, st>>>(d->dev, q, ghost, grad, ph, (int)nb);
+  DGB_CUDA(cudaGetLastError());
+  return DGB_OK;
+}
+
+#define DGB_FOR_EACH_ELEMENT(X) X(2, 1) X(2, 2) X(2, 3) X(2, 4) X(3, 1) X(3, 2) X(3, 3) X(3, 4)
+
+int dispatch_rhs(const dgb_disc* d, bool viscous, const double* q, const double* gq, const double* ghost,
+                 const double* gghost, const dgb::Epilogue& ep, const dgb::Phys& ph, cudaStream_t st) {
+#define X(DIM, P)                                                                              \
+  if (d->dim == DIM && d->order == P)                                                          \
+    return viscous ? launch_rhs<DIM, P, true>(d, q, gq, ghost, gghost, ep, ph, st)             \
+                   : launch_rhs<DIM, P, false>(d, q, gq, ghost, gghost, ep, ph, st);
+  DGB_FOR_EACH_ELEMENT(X)
+#undef X
+  return fail(DGB_ERR_INVALID, "unsupported (dim, order)");
+}
+
+int dispatch_grad(const dgb_disc* d, const double* q, const double* ghost, double* grad, const dgb::Phys& ph,
+                  cudaStream_t st) {
+#define X(DIM, P) \
+  if (d->dim == DIM && d->order == P) return launch_grad<DIM, P>(d, q, ghost, grad, ph, st);
+  DGB_FOR_EACH_ELEMENT(X)
+#undef X
+  return fail(DGB_ERR_INVALID, "unsupported (dim, order)");
+}
+
+template <int DIM, int P>
+void fill_padded(const double* Sw, const double* lift, std::vector<double>& Wv, std::vector<double>& Wl,
+                 std::vector<double>& Wq, std::vector<double>& Wf) {
+  using EL = dgb::ElemT<DIM, P>;
+  Wv.assign((size_t)EL::NPR * EL::LDV, 0.0);
+  Wl.assign((size_t)EL::NPR * EL::LDF, 0.0);
+  Wq.assign((size_t)DIM * EL::NPR * EL::LDQ, 0.0);
+  Wf.assign((size_t)EL::NF * EL::NPR * EL::LDL, 0.0);
+  for (int r = 0; r < DIM; ++r)
+    for (int i = 0; i < EL::NP; ++i)
+      for (int j = 0; j < EL::NP; ++j) {
+        const double v = Sw[((size_t)r * EL::NP + i) * EL::NP + j];
+        Wv[(size_t)i * EL::LDV + r * EL::NPK + j] = v;
+        Wq[((size_t)r * EL::NPR + i) * EL::LDQ + j] = v;
+      }
+  for (int i = 0; i < EL::NP; ++i)
+    for (int f = 0; f < EL::NF; ++f)
+      for (int m = 0; m < EL::NFP; ++m) {
+        const double v = lift[(size_t)i * EL::NFT + f * EL::NFP + m];
+        Wl[(size_t)i * EL::LDF + f * EL::NFP + m] = v;
+        Wf[((size_t)f * EL::NPR + i) * EL::LDL + m] = v;
+      }
+}
+
+template <int DIM, int P> void elem_sizes(int* Np, int* Nf, int* Nfp, int* nperm) {
+  using EL = dgb::ElemT<DIM, P>;
+  *Np = EL::NP; *Nf = EL::NF; *Nfp = EL::NFP; *nperm = EL::NPERM;
+}
+
+template <typename T>
+int upload(T** dev, const std::vector<T>& host, cudaStream_t st) {
+  DGB_CUDA(cudaMalloc((void**)dev, host.size() * sizeof(T)));
+  DGB_CUDA(cudaMemcpyAsync(*dev, host.data(), host.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+  return DGB_OK;
+}
+
+void make_phys(dgb::Phys& ph, int C, const double* qfar, const double* phys) {
+  ph.gamma = phys ? phys[0] : 1.4; ph.mu = phys ? phys[1] : 0.0; ph.kappa = phys ? phys[2] : 0.0;
+  ph.rgas = phys ? phys[3] : 1.0;
+  for (int c = 0; c < 5; ++c) ph.qfar[c] = (qfar && c < C) ? qfar[c] : 0.0;
+}
+
+}  // namespace
+
+// }}}
+
+extern "C" {
+
+const char* dgb_last_error(void) { return g_err.c_str(); }
+int dgb_version(void) { return 100; }
+
+int dgb_malloc(void** dev, size_t bytes) { DGB_CUDA(cudaMalloc(dev, bytes ? bytes : 1)); return DGB_OK; }
+int dgb_free(void* dev) { DGB_CUDA(cudaFree(dev)); return DGB_OK; }
+int dgb_host_alloc(void** host, size_t bytes) { DGB_CUDA(cudaMallocHost(host, bytes ? bytes : 1)); return DGB_OK; }
+int dgb_host_free(void* host) { DGB_CUDA(cudaFreeHost(host)); return DGB_OK; }
+int dgb_memcpy_h2d(void* dev, const void* host, size_t bytes, void* stream) {
+  DGB_CUDA(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream)); return DGB_OK;
+}
+int dgb_memcpy_d2h(void* host, const void* dev, size_t bytes, void* stream) {
+  DGB_CUDA(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, (cudaStream_t)stream)); return DGB_OK;
+}
+int dgb_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream) {
+  DGB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream)); return DGB_OK;
+}
+int dgb_stream_sync(void* stream) { DGB_CUDA(cudaStreamSynchronize((cudaStream_t)stream)); return DGB_OK; }
+
+int dgb_disc_create(dgb_disc** out, int dim, int order, int64_t E, int64_t G, const double* Sw_host,
+                    const double* lift_host, const int64_t* face_nodes_host, const int64_t* face_perms_host,
+                    const double* drdx_dev, const double* normals_dev, const double* fscale_dev,
+                    const int64_t* vmap_m_dev, const int64_t* vmap_p_dev, const int64_t* bc_kind_dev,
+                    void* stream) {
+  if (!out) return fail(DGB_ERR_INVALID, "null output handle");
+  *out = nullptr;
+  if (E < 0 || G < 0 || E + G >= (1LL << 31)) return fail(DGB_ERR_INVALID, "element count out of range");
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<double> Wv, Wl, Wq, Wf;
+  int Np = 0, Nf = 0, Nfp = 0, nperm = 0;
+  bool ok = false;
+#define X(DIM, P)                                                        \
+  if (dim == DIM && order == P) {                                        \
+    fill_padded<DIM, P>(Sw_host, lift_host, Wv, Wl, Wq, Wf);             \
+    elem_sizes<DIM, P>(&Np, &Nf, &Nfp, &nperm);                          \
+    ok = true;                                                           \
+  }
+  DGB_FOR_EACH_ELEMENT(X)
+#undef X
+  if (!ok) return fail(DGB_ERR_INVALID, "unsupported (dim, order): dim in {2,3}, order in 1..4");
+  std::vector<int> tables((size_t)Nf * Nfp + (size_t)nperm * Nfp);
+  for (int n = 0; n < Nf * Nfp; ++n) {
+    if (face_nodes_host[n] < 0 || face_nodes_host[n] >= Np) return fail(DGB_ERR_OUT_OF_BOUNDS, "face node table out of range");
+    tables[n] = (int)face_nodes_host[n];
+  }
+  for (int n = 0; n < nperm * Nfp; ++n) {
+    if (face_perms_host[n] < 0 || face_perms_host[n] >= Nfp) return fail(DGB_ERR_OUT_OF_BOUNDS, "face permutation table out of range");
+    tables[(size_t)Nf * Nfp + n] = (int)face_perms_host[n];
+  }
+  dgb_disc* d = new dgb_disc();
+  d->dim = dim; d->order = order; d->Np = Np; d->Nf = Nf; d->Nfp = Nfp; d->nperm = nperm;
+  int rc;
+  if ((rc = upload(&d->Wv, Wv, st)) || (rc = upload(&d->Wl, Wl, st)) || (rc = upload(&d->Wq, Wq, st)) ||
+      (rc = upload(&d->Wf, Wf, st)) || (rc = upload(&d->tables, tables, st))) { dgb_disc_destroy(d); return rc; }
+  int* err_dev = nullptr;
+  cudaError_t ce = cudaMalloc((void**)&d->conn, sizeof(long long) * (size_t)(E * Nf ? E * Nf : 1));
+  if (ce == cudaSuccess) ce = cudaMalloc((void**)&err_dev, sizeof(int));
+  if (ce == cudaSuccess) ce = cudaMemsetAsync(err_dev, 0, sizeof(int), st);
+  if (ce != cudaSuccess) { dgb_disc_destroy(d); return fail(DGB_ERR_CUDA, cudaGetErrorString(ce)); }
+  int err_host = 0;
+  if (E > 0) {
+    const long long n = E * Nf;
+    k_build_conn<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(
+        (const long long*)vmap_m_dev, (const long long*)vmap_p_dev, (const long long*)bc_kind_dev, d->tables,
+        E, G, Np, Nf, Nfp, nperm, d->conn, err_dev);
+    ce = cudaGetLastError();
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(&err_host, err_dev, sizeof(int), cudaMemcpyDeviceToHost, st);
+  }
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+  cudaFree(err_dev);
+  if (ce != cudaSuccess) { dgb_disc_destroy(d); return fail(DGB_ERR_CUDA, cudaGetErrorString(ce)); }
+  if (err_host >= 100) { dgb_disc_destroy(d); return fail(DGB_ERR_OUT_OF_BOUNDS, "face index map leaves [0, (E+G)*Np)"); }
+  if (err_host) { dgb_disc_destroy(d); return fail(DGB_ERR_BAD_MAP, "face index maps are not a conforming simplex face map"); }
+  d->dev.E = E; d->dev.G = G;
+  d->dev.Wv = d->Wv; d->dev.Wl = d->Wl; d->dev.Wq = d->Wq; d->dev.Wf = d->Wf;
+  d->dev.drdx = drdx_dev; d->dev.normals = normals_dev; d->dev.fscale = fscale_dev;
+  d->dev.conn = d->conn; d->dev.tables = d->tables;
+  d->bc_kind = bc_kind_dev;
+  *out = d;
+  return DGB_OK;
+}
+
+int dgb_disc_destroy(dgb_disc* d) {
+  if (!d) return DGB_OK;
+  cudaFree(d->Wv); cudaFree(d->Wl); cudaFree(d->Wq); cudaFree(d->Wf); cudaFree(d->conn); cudaFree(d->tables);
+  delete d;
+  return DGB_OK;
+}
+
+int dgb_disc_expand_maps(const dgb_disc* d, int64_t* vm, int64_t* vp, void* stream) {
+  if (!d) return fail(DGB_ERR_INVALID, "null handle");
+  const long long n = d->dev.E * d->Nf * d->Nfp;
+  if (n == 0) return DGB_OK;
+  k_expand_conn<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      d->conn, d->tables, d->dev.E, d->Np, d->Nf, d->Nfp, (long long*)vm, (long long*)vp);
+  DGB_CUDA(cudaGetLastError());
+  return DGB_OK;
+}
+
+static int check_ghost(const dgb_disc* d, const void* ghost) {
+  if (!d) return fail(DGB_ERR_INVALID, "null handle");
+  if (d->dev.G > 0 && !ghost) return fail(DGB_ERR_INVALID, "discretisation has ghost elements but no ghost array was given");
+  return DGB_OK;
+}
+
+int dgb_euler_rhs(const dgb_disc* d, const double* q, const double* ghost, double* rhs, const double* qfar,
+                  const double* phys, void* stream) {
+  int rc = check_ghost(d, ghost); if (rc) return rc;
+  dgb::Phys ph; make_phys(ph, d->dim + 2, qfar, phys);
+  dgb::Epilogue ep{nullptr, rhs, nullptr, nullptr, 0.0, 1.0, 0.0, 0.0};
+  return dispatch_rhs(d, false, q, nullptr, ghost, nullptr, ep, ph, (cudaStream_t)stream);
+}
+
+int dgb_ns_grad(const dgb_disc* d, const double* q, const double* ghost, double* gradq, const double* qfar,
+                void* stream) {
+  int rc = check_ghost(d, ghost); if (rc) return rc;
+  dgb::Phys ph; make_phys(ph, d->dim + 2, qfar, nullptr);
+  return dispatch_grad(d, q, ghost, gradq, ph, (cudaStream_t)stream);
+}
+
+int dgb_ns_rhs(const dgb_disc* d, const double* q, const double* gradq, const double* ghost, const double* gghost,
+               double* rhs, const double* qfar, const double* phys, void* stream) {
+  int rc = check_ghost(d, ghost); if (rc) return rc;
+  if ((rc = check_ghost(d, gghost))) return rc;
+  dgb::Phys ph; make_phys(ph, d->dim + 2, qfar, phys);
+  dgb::Epilogue ep{nullptr, rhs, nullptr, nullptr, 0.0, 1.0, 0.0, 0.0};
+  return dispatch_rhs(d, true, q, gradq, ghost, gghost, ep, ph, (cudaStream_t)stream);
+}
+
+static int make_epilogue(dgb::Epilogue& ep, const double* q, const double* x1, double* out1, const double* x2,
+                         double* out2, const double* rk) {
+  if (!out1 || !rk) return fail(DGB_ERR_INVALID, "out1 and rk are required");
+  if (out1 == q || (out2 && out2 == q) || (x2 && out1 == x2))
+    return fail(DGB_ERR_INVALID, "RK outputs must not alias the stage input q (neighbours still read it)");
+  if (out2 && !x2) return fail(DGB_ERR_INVALID, "out2 needs x2");
+  ep = dgb::Epilogue{x1, out1, x2, out2, rk[0], rk[1], rk[2], rk[3]};
+  return DGB_OK;
+}
+
+int dgb_euler_rhs_rk(const dgb_disc* d, const double* q, const double* ghost, const double* x1, double* out1,
+                     const double* x2, double* out2, const double* rk, const double* qfar, const double* phys,
+                     void* stream) {
+  int rc = check_ghost(d, ghost); if (rc) return rc;
+  dgb::Phys ph; make_phys(ph, d->dim + 2, qfar, phys);
+  dgb::Epilogue ep; if ((rc = make_epilogue(ep, q, x1, out1, x2, out2, rk))) return rc;
+  return dispatch_rhs(d, false, q, nullptr, ghost, nullptr, ep, ph, (cudaStream_t)stream);
+}
+
+int dgb_ns_rhs_rk(const dgb_disc* d, const double* q, const double* gradq, const double* ghost,
+                  const double* gghost, const double* x1, double* out1, const double* x2, double* out2,
+                  const double* rk, const double* qfar, const double* phys, void* stream) {
+  int rc = check_ghost(d, ghost); if (rc) return rc;
+  if ((rc = check_ghost(d, gghost))) return rc;
+  dgb::Phys ph; make_phys(ph, d->dim + 2, qfar, phys);
+  dgb::Epilogue ep; if ((rc = make_epilogue(ep, q, x1, out1, x2, out2, rk))) return rc;
+  return dispatch_rhs(d, true, q, gradq, ghost, gghost, ep, ph, (cudaStream_t)stream);
+}
+
+int dgb_pack_elements(double* dst, const double* src, const int64_t* elems, int64_t ncomp, int64_t nsrc,
+                      int64_t nsel, int64_t ndofs, void* stream) {
+  const long long total = ncomp * nsel * ndofs;
+  if (total == 0) return DGB_OK;
+  long long blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_pack_elements<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(dst, src, (const long long*)elems, ncomp,
+                                                                       nsrc, nsel, ndofs);
+  DGB_CUDA(cudaGetLastError());
+  return DGB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,326 @@
+// Generic device array ops behind the array-context namespace (frontend.py:257-302): elementwise
+// with trailing-aligned broadcast, where, strided copy, gather, einsum.  These are glue for code
+// outside the fused DG functions (RK arithmetic, diagnostics); they are bandwidth-bound
+// grid-stride kernels, not the hot path.
+#include "../../include/dgb200.h"
+
+#include <cuda_runtime.h>
+#include <string>
+
+namespace {
+
+extern thread_local std::string g_err2;
+thread_local std::string g_err2;
+
+struct Dims {
+  int rank;
+  long long ext[8];
+  long long sa[8], sb[8], sc[8];
+};
+
+__device__ __forceinline__ double ld_f64(const void* p, int dt, long long off) {
+  switch (dt) {
+    case DGB_F64: return static_cast<const double*>(p)[off];
+    case DGB_I64: return (double)static_cast<const long long*>(p)[off];
+    default: return (double)static_cast<const unsigned char*>(p)[off];
+  }
+}
+__device__ __forceinline__ long long ld_i64(const void* p, int dt, long long off) {
+  switch (dt) {
+    case DGB_F64: return (long long)static_cast<const double*>(p)[off];
+    case DGB_I64: return static_cast<const long long*>(p)[off];
+    default: return (long long)static_cast<const unsigned char*>(p)[off];
+  }
+}
+__device__ __forceinline__ void st_any(void* p, int dt, long long off, double fv, long long iv, bool is_float) {
+  switch (dt) {
+    case DGB_F64: static_cast<double*>(p)[off] = is_float ? fv : (double)iv; break;
+    case DGB_I64: static_cast<long long*>(p)[off] = is_float ? (long long)fv : iv; break;
+    default: static_cast<unsigned char*>(p)[off] = is_float ? (fv != 0.0) : (iv != 0); break;
+  }
+}
+
+__device__ __forceinline__ void offsets(const Dims& d, long long n, long long& oa, long long& ob, long long& oc) {
+  oa = ob = oc = 0;
+#pragma unroll 1
+  for (int k = d.rank - 1; k >= 0; --k) {
+    const long long i = n % d.ext[k];
+    n /= d.ext[k];
+    oa += i * d.sa[k]; ob += i * d.sb[k]; oc += i * d.sc[k];
+  }
+}
+
+__device__ __forceinline__ long long floordiv_i(long long a, long long b) {
+  if (b == 0) return 0;   // numpy: 0 with a warning
+  long long q = a / b;
+  if ((a % b != 0) && ((a < 0) != (b < 0))) --q;
+  return q;
+}
+
+__global__ void k_binary(int op, void* out, int odt, const void* a, int adt, const void* b, int bdt, Dims d,
+                         long long total, bool fcomp) {
+  for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < total;
+       n += (long long)gridDim.x * blockDim.x) {
+    long long oa, ob, oc;
+    offsets(d, n, oa, ob, oc);
+    double fr = 0.0; long long ir = 0; bool res_float = fcomp;
+    if (fcomp) {
+      const double x = ld_f64(a, adt, oa), y = ld_f64(b, bdt, ob);
+      switch (op) {
+        case DGB_ADD: fr = x + y; break;
+        case DGB_SUB: fr = x - y; break;
+        case DGB_MUL: fr = x * y; break;
+        case DGB_TRUEDIV: fr = x / y; break;
+        case DGB_FLOORDIV: fr = floor(x / y); break;
+        case DGB_MOD: { fr = fmod(x, y); if (fr != 0.0 && ((fr < 0) != (y < 0))) fr += y; } break;
+        case DGB_POW: fr = pow(x, y); break;
+        case DGB_MIN: fr = (x != x || y != y) ? (x + y) : fmin(x, y); break;
+        case DGB_MAX: fr = (x != x || y != y) ? (x + y) : fmax(x, y); break;
+        case DGB_LT: ir = x < y; res_float = false; break;
+        case DGB_LE: ir = x <= y; res_float = false; break;
+        case DGB_GT: ir = x > y; res_float = false; break;
+        case DGB_GE: ir = x >= y; res_float = false; break;
+        case DGB_EQ: ir = x == y; res_float = false; break;
+        default: ir = x != y; res_float = false; break;
+      }
+    } else {
+      const long long x = ld_i64(a, adt, oa), y = ld_i64(b, bdt, ob);
+      switch (op) {
+        case DGB_ADD: ir = x + y; break;
+        case DGB_SUB: ir = x - y; break;
+        case DGB_MUL: ir = x * y; break;
+        case DGB_TRUEDIV: fr = (double)x / (double)y; res_float = true; break;
+        case DGB_FLOORDIV: ir = floordiv_i(x, y); break;
+        case DGB_MOD: ir = y == 0 ? 0 : x - floordiv_i(x, y) * y; break;
+        case DGB_POW: { long long r = 1, bb = x, ee = y; if (ee < 0) { r = 0; } else { while (ee) { if (ee & 1) r *= bb; bb *= bb; ee >>= 1; } } ir = r; } break;
+        case DGB_MIN: ir = x < y ? x : y; break;
+        case DGB_MAX: ir = x > y ? x : y; break;
+        case DGB_LT: ir = x < y; break;
+        case DGB_LE: ir = x <= y; break;
+        case DGB_GT: ir = x > y; break;
+        case DGB_GE: ir = x >= y; break;
+        case DGB_EQ: ir = x == y; break;
+        default: ir = x != y; break;
+      }
+    }
+    st_any(out, odt, n, fr, ir, res_float);
+  }
+}
+
+__global__ void k_unary(int op, void* out, int odt, const void* a, int adt, long long total) {
+  for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < total;
+       n += (long long)gridDim.x * blockDim.x) {
+    if (odt == DGB_F64) {
+      const double x = ld_f64(a, adt, n);
+      double r;
+      switch (op) {
+        case DGB_NEG: r = -x; break;
+        case DGB_ABS: r = fabs(x); break;
+        case DGB_SQRT: r = sqrt(x); break;
+        case DGB_EXP: r = exp(x); break;
+        default: r = log(x); break;
+      }
+      static_cast<double*>(out)[n] = r;
+    } else {
+      const long long x = ld_i64(a, adt, n);
+      st_any(out, odt, n, 0.0, op == DGB_NEG ? -x : (x < 0 ? -x : x), false);
+    }
+  }
+}
+
+__global__ void k_where(void* out, int odt, const void* c, int cdt, const void* a, int adt, const void* b, int bdt,
+                        Dims d, long long total) {
+  for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < total;
+       n += (long long)gridDim.x * blockDim.x) {
+    long long oa, ob, oc;
+    offsets(d, n, oa, ob, oc);
+    const bool cond = cdt == DGB_F64 ? (static_cast<const double*>(c)[oc] != 0.0) : (ld_i64(c, cdt, oc) != 0);
+    if (odt == DGB_F64) static_cast<double*>(out)[n] = cond ? ld_f64(a, adt, oa) : ld_f64(b, bdt, ob);
+    else st_any(out, odt, n, 0.0, cond ? ld_i64(a, adt, oa) : ld_i64(b, bdt, ob), false);
+  }
+}
+
+__global__ void k_copy_strided(void* out, int odt, const void* a, int adt, Dims d, long long total) {
+  for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < total;
+       n += (long long)gridDim.x * blockDim.x) {
+    long long oa, ob, oc;
+    offsets(d, n, oa, ob, oc);
+    if (odt == DGB_F64) static_cast<double*>(out)[n] = ld_f64(a, adt, oa);
+    else st_any(out, odt, n, 0.0, ld_i64(a, adt, oa), false);
+  }
+}
+
+__global__ void k_copy_scatter(void* out, int odt, const void* a, int adt, Dims d, long long total) {
+  for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < total;
+       n += (long long)gridDim.x * blockDim.x) {
+    long long oa, ob, oc;
+    offsets(d, n, oa, ob, oc);   // sb carries the output strides
+    if (odt == DGB_F64) static_cast<double*>(out)[ob] = ld_f64(a, adt, oa);
+    else st_any(out, odt, ob, 0.0, ld_i64(a, adt, oa), false);
+  }
+}
+
+template <typename T>
+__global__ void k_take(T* __restrict__ out, const T* __restrict__ a, const long long* __restrict__ idx,
+                       long long outer, long long extent, long long inner, long long nidx, int* err) {
+  const long long total = outer * nidx * inner;
+  for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < total;
+       n += (long long)gridDim.x * blockDim.x) {
+    const long long i = n % inner, ok = n / inner;
+    const long long k = ok % nidx, o = ok / nidx;
+    const long long src = idx[k];
+    if (src < 0 || src >= extent) { *err = 1; continue; }
+    out[n] = a[(o * extent + src) * inner + i];
+  }
+}
+
+struct EinsumDesc {
+  int nops, nout, nletters;
+  long long ext[8];
+  long long stride[3][8];
+};
+
+__global__ void k_einsum(double* __restrict__ out, const double* a, const double* b, const double* c, EinsumDesc d,
+                         long long nout_total, long long nred_total) {
+  for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < nout_total;
+       n += (long long)gridDim.x * blockDim.x) {
+    long long o0 = 0, o1 = 0, o2 = 0, rem = n;
+    for (int k = d.nout - 1; k >= 0; --k) {
+      const long long i = rem % d.ext[k]; rem /= d.ext[k];
+      o0 += i * d.stride[0][k]; o1 += i * d.stride[1][k]; o2 += i * d.stride[2][k];
+    }
+    double acc = 0.0;
+    // ascending, outer-letter-first accumulation (expr.py:344-364)
+    for (long long r = 0; r < nred_total; ++r) {
+      long long p0 = o0, p1 = o1, p2 = o2, rr = r;
+      for (int k = d.nletters - 1; k >= d.nout; --k) {
+        const long long i = rr % d.ext[k]; rr /= d.ext[k];
+        p0 += i * d.stride[0][k]; p1 += i * d.stride[1][k]; p2 += i * d.stride[2][k];
+      }
+      double v = a[p0];
+      if (d.nops > 1) v *= b[p1];
+      if (d.nops > 2) v *= c[p2];
+      acc += v;
+    }
+    out[n] = acc;
+  }
+}
+
+int grid_for(long long total) {
+  long long b = (total + 255) / 256;
+  return (int)(b < 1 ? 1 : (b > 148 * 32 ? 148 * 32 : b));
+}
+
+int fill_dims(Dims& d, int rank, const int64_t* shape, const int64_t* sa, const int64_t* sb, const int64_t* sc,
+              long long* total) {
+  if (rank < 0 || rank > 8) return DGB_ERR_INVALID;
+  d.rank = rank;
+  long long t = 1;
+  for (int k = 0; k < 8; ++k) {
+    d.ext[k] = k < rank ? shape[k] : 1;
+    d.sa[k] = (k < rank && sa) ? sa[k] : 0;
+    d.sb[k] = (k < rank && sb) ? sb[k] : 0;
+    d.sc[k] = (k < rank && sc) ? sc[k] : 0;
+    if (k < rank) t *= shape[k];
+  }
+  *total = t;
+  return DGB_OK;
+}
+
+}  // namespace
+
+#define DGB_CHECK_LAUNCH()                                                        \
+  do { cudaError_t e_ = cudaGetLastError(); if (e_ != cudaSuccess) return DGB_ERR_CUDA; } while (0)
+
+extern "C" {
+
+int dgb_ew_binary(int op, void* out, int odt, const void* a, int adt, const int64_t* sa, const void* b, int bdt,
+                  const int64_t* sb, int rank, const int64_t* shape, void* stream) {
+  Dims d; long long total;
+  if (fill_dims(d, rank, shape, sa, sb, nullptr, &total)) return DGB_ERR_INVALID;
+  if (total == 0) return DGB_OK;
+  const bool fcomp = adt == DGB_F64 || bdt == DGB_F64;
+  k_binary<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(op, out, odt, a, adt, b, bdt, d, total, fcomp);
+  DGB_CHECK_LAUNCH();
+  return DGB_OK;
+}
+
+int dgb_ew_unary(int op, void* out, int odt, const void* a, int adt, int64_t n, void* stream) {
+  if (n == 0) return DGB_OK;
+  k_unary<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(op, out, odt, a, adt, n);
+  DGB_CHECK_LAUNCH();
+  return DGB_OK;
+}
+
+int dgb_ew_where(void* out, int odt, const void* c, int cdt, const int64_t* sc, const void* a, int adt,
+                 const int64_t* sa, const void* b, int bdt, const int64_t* sb, int rank, const int64_t* shape,
+                 void* stream) {
+  Dims d; long long total;
+  if (fill_dims(d, rank, shape, sa, sb, sc, &total)) return DGB_ERR_INVALID;
+  if (total == 0) return DGB_OK;
+  k_where<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(out, odt, c, cdt, a, adt, b, bdt, d, total);
+  DGB_CHECK_LAUNCH();
+  return DGB_OK;
+}
+
+int dgb_copy_strided(void* out, int odt, const void* a, int adt, const int64_t* sa, int rank, const int64_t* shape,
+                     void* stream) {
+  Dims d; long long total;
+  if (fill_dims(d, rank, shape, sa, nullptr, nullptr, &total)) return DGB_ERR_INVALID;
+  if (total == 0) return DGB_OK;
+  k_copy_strided<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(out, odt, a, adt, d, total);
+  DGB_CHECK_LAUNCH();
+  return DGB_OK;
+}
+
+int dgb_copy_scatter(void* out, int odt, const int64_t* so, const void* a, int adt, const int64_t* sa, int rank,
+                     const int64_t* shape, void* stream) {
+  Dims d; long long total;
+  if (fill_dims(d, rank, shape, sa, so, nullptr, &total)) return DGB_ERR_INVALID;
+  if (total == 0) return DGB_OK;
+  k_copy_scatter<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(out, odt, a, adt, d, total);
+  DGB_CHECK_LAUNCH();
+  return DGB_OK;
+}
+
+int dgb_take(void* out, const void* a, int dtype, const int64_t* idx, int64_t outer, int64_t extent, int64_t inner,
+             int64_t nidx, void* stream) {
+  const long long total = outer * nidx * inner;
+  if (total == 0) return DGB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  int* err = nullptr;
+  if (cudaMalloc((void**)&err, sizeof(int)) != cudaSuccess) return DGB_ERR_CUDA;
+  cudaMemsetAsync(err, 0, sizeof(int), st);
+  if (dtype == DGB_BOOL)
+    k_take<unsigned char><<<grid_for(total), 256, 0, st>>>((unsigned char*)out, (const unsigned char*)a,
+                                                           (const long long*)idx, outer, extent, inner, nidx, err);
+  else
+    k_take<long long><<<grid_for(total), 256, 0, st>>>((long long*)out, (const long long*)a, (const long long*)idx,
+                                                       outer, extent, inner, nidx, err);
+  int h = 0;
+  cudaError_t ce = cudaGetLastError();
+  if (ce == cudaSuccess) ce = cudaMemcpyAsync(&h, err, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+  cudaFree(err);
+  if (ce != cudaSuccess) return DGB_ERR_CUDA;
+  return h ? DGB_ERR_OUT_OF_BOUNDS : DGB_OK;
+}
+
+int dgb_einsum(double* out, int nops, const double* const* ops, const int64_t* op_strides, int nout, int nletters,
+               const int64_t* ext, void* stream) {
+  if (nops < 1 || nops > 3 || nletters > 8 || nout > nletters) return DGB_ERR_INVALID;
+  EinsumDesc d; d.nops = nops; d.nout = nout; d.nletters = nletters;
+  long long no = 1, nr = 1;
+  for (int k = 0; k < 8; ++k) {
+    d.ext[k] = k < nletters ? ext[k] : 1;
+    for (int o = 0; o < 3; ++o) d.stride[o][k] = (o < nops && k < nletters) ? op_strides[o * nletters + k] : 0;
+    if (k < nout) no *= d.ext[k]; else if (k < nletters) nr *= d.ext[k];
+  }
+  if (no == 0) return DGB_OK;
+  k_einsum<<<grid_for(no), 256, 0, (cudaStream_t)stream>>>(out, ops[0], nops > 1 ? ops[1] : nullptr,
+                                                           nops > 2 ? ops[2] : nullptr, d, no, nr);
+  DGB_CHECK_LAUNCH();
+  return DGB_OK;
+}
+
+}  // extern "C"

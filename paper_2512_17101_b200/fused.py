@@ -1,0 +1,173 @@
+"""Fused implementations of the outlined DG functions, keyed by function name.
+
+``B200ArrayContext.outline(f)`` looks ``f.__name__`` up here.  Each implementation receives the
+same positional arrays the reference would bind to the ``FunctionDefinition`` parameters
+``_p0, _p1, ...`` (/root/reference/pkg/src/laze/frontend.py:501) and returns the array(s) the
+body would return, but computes them with one (or, for nothing here, more) fused sm_100a kernel
+through the C ABI (include/dgb200.h).  The per-mesh discretisation handle is created on first
+use from the argument arrays themselves and cached on their identity; creating it validates
+the int64 face maps on the device (range check + conformity) exactly once.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _cabi, errors
+from .dg.simplex import simplex_element
+
+_ORDER_OF_NP = {(2, 3): 1, (2, 6): 2, (2, 10): 3, (2, 15): 4, (3, 4): 1, (3, 10): 2, (3, 20): 3, (3, 35): 4}
+
+
+class _Disc:
+    def __init__(self, lib, handle, keep):
+        self.lib, self.handle, self.keep = lib, handle, keep
+
+    def __del__(self):
+        try:
+            if self.handle:
+                self.lib.dgb_disc_destroy(self.handle)
+        except Exception:
+            pass
+
+
+def _f64(actx, a, what):
+    from .actx import F64
+    if a.dtype_code != F64:
+        raise errors.DTypeMismatch(f"{what} must be f64")
+    return actx._contiguous(a)
+
+
+def _i64(actx, a, what):
+    from .actx import I64
+    if a.dtype_code != I64:
+        raise errors.DTypeMismatch(f"{what} must be i64")
+    return actx._contiguous(a)
+
+
+def get_disc(actx, dim, q, nghost, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind) -> _Disc:
+    key = (dim, nghost, id(Sw), id(drdx), id(lift), id(normals), id(fscale), id(vmap_m), id(vmap_p), id(bc_kind))
+    disc = actx._discs.get(key)
+    if disc is not None:
+        return disc
+    C_, E, Np = q.shape
+    if C_ != dim + 2:
+        raise errors.ShapeMismatch(f"state has {C_} fields, expected {dim + 2}")
+    order = _ORDER_OF_NP.get((dim, Np))
+    if order is None:
+        raise errors.ShapeMismatch(f"no simplex element with dim={dim}, Np={Np} (orders 1..4 are built)")
+    el = simplex_element(dim, order)
+    Nf, Nfp = el.Nf, el.Nfp
+    expect = {"Sw": (Sw, (dim, Np, Np)), "drdx": (drdx, (dim, dim, E)), "lift": (lift, (Np, Nf * Nfp)),
+              "normals": (normals, (dim, E, Nf, 1)), "fscale": (fscale, (E, Nf, 1)),
+              "vmap_m": (vmap_m, (E * Nf * Nfp,)), "vmap_p": (vmap_p, (E * Nf * Nfp,)),
+              "bc_kind": (bc_kind, (E, Nf, 1))}
+    for name, (arr, shape) in expect.items():
+        if tuple(arr.shape) != shape:
+            raise errors.BindingMismatch(f"{name} has shape {tuple(arr.shape)}, expected {shape}")
+    Sw_h = np.ascontiguousarray(Sw.host_value(), dtype=np.float64)
+    lift_h = np.ascontiguousarray(lift.host_value(), dtype=np.float64)
+    fn_h = np.ascontiguousarray(el.face_nodes, dtype=np.int64)
+    fp_h = np.ascontiguousarray(el.face_perms, dtype=np.int64)
+    keep = [_f64(actx, drdx, "drdx"), _f64(actx, normals, "normals"), _f64(actx, fscale, "fscale"),
+            _i64(actx, vmap_m, "vmap_m"), _i64(actx, vmap_p, "vmap_p"), _i64(actx, bc_kind, "bc_kind"),
+            Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind]
+    handle = C.c_void_p()
+    _cabi.check(actx.lib.dgb_disc_create(
+        C.byref(handle), dim, order, E, nghost,
+        Sw_h.ctypes.data, lift_h.ctypes.data, fn_h.ctypes.data, fp_h.ctypes.data,
+        keep[0].ptr, keep[1].ptr, keep[2].ptr, keep[3].ptr, keep[4].ptr, keep[5].ptr, actx._st), "face index maps")
+    actx.launch_count += 1
+    disc = _Disc(actx.lib, handle, keep)
+    disc.dim, disc.order, disc.E, disc.Np, disc.Nf, disc.Nfp, disc.G = dim, order, E, Np, Nf, Nfp, nghost
+    actx._discs[key] = disc
+    return disc
+
+
+def _host_vec(arr, n):
+    v = np.ascontiguousarray(np.asarray(arr.host_value(), dtype=np.float64).reshape(-1))
+    if v.size != n:
+        raise errors.BindingMismatch(f"expected {n} parameters, got {v.size}")
+    return v
+
+
+def _ghost_ptr(actx, ghost, lead, Np):
+    if ghost is None:
+        return 0, None, None
+    g = _f64(actx, ghost, "ghost")
+    if g.shape[:-2] != lead or g.shape[-1] != Np:
+        raise errors.BindingMismatch(f"ghost array has shape {g.shape}")
+    return g.shape[-2], g, g.ptr
+
+
+def _euler(actx, f, q, ghost, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, phys, epi=None):
+    dim = f.dg_dim
+    q = _f64(actx, q, "q")
+    G, g, gptr = _ghost_ptr(actx, ghost, (dim + 2,), q.shape[-1])
+    disc = get_disc(actx, dim, q, G, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind)
+    qf, ph = _host_vec(qfar, dim + 2), _host_vec(phys, 4)
+    out = actx.empty(q.shape)
+    _cabi.check(actx.lib.dgb_euler_rhs(disc.handle, q.ptr, gptr, out.ptr, qf.ctypes.data, ph.ctypes.data,
+                                       actx._st), "dg_euler_rhs")
+    actx.launch_count += 1
+    return out
+
+
+def dg_euler_rhs(actx, f, *args):
+    if len(args) == 11:
+        q, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, phys = args
+        ghost = None
+    elif len(args) == 12:
+        q, ghost, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, phys = args
+    else:
+        raise errors.BindingMismatch(f"dg_euler_rhs takes 11 or 12 arrays, got {len(args)}")
+    return _euler(actx, f, q, ghost, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, phys)
+
+
+def dg_ns_grad(actx, f, *args):
+    if len(args) == 10:
+        q, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar = args
+        ghost = None
+    elif len(args) == 11:
+        q, ghost, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar = args
+    else:
+        raise errors.BindingMismatch(f"dg_ns_grad takes 10 or 11 arrays, got {len(args)}")
+    dim = f.dg_dim
+    q = _f64(actx, q, "q")
+    G, g, gptr = _ghost_ptr(actx, ghost, (dim + 2,), q.shape[-1])
+    disc = get_disc(actx, dim, q, G, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind)
+    qf = _host_vec(qfar, dim + 2)
+    out = actx.empty((dim,) + q.shape)
+    _cabi.check(actx.lib.dgb_ns_grad(disc.handle, q.ptr, gptr, out.ptr, qf.ctypes.data, actx._st), "dg_ns_grad")
+    actx.launch_count += 1
+    return out
+
+
+def dg_ns_rhs(actx, f, *args):
+    if len(args) == 12:
+        q, gq, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, phys = args
+        ghost = gghost = None
+    elif len(args) == 14:
+        q, gq, ghost, gghost, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, phys = args
+    else:
+        raise errors.BindingMismatch(f"dg_ns_rhs takes 12 or 14 arrays, got {len(args)}")
+    dim = f.dg_dim
+    q = _f64(actx, q, "q")
+    gq = _f64(actx, gq, "grad q")
+    if gq.shape != (dim,) + q.shape:
+        raise errors.BindingMismatch(f"grad q has shape {gq.shape}, expected {(dim,) + q.shape}")
+    G, g, gptr = _ghost_ptr(actx, ghost, (dim + 2,), q.shape[-1])
+    GG, gg, ggptr = _ghost_ptr(actx, gghost, (dim, dim + 2), q.shape[-1])
+    if GG != G:
+        raise errors.BindingMismatch("ghost arrays of q and grad q disagree in size")
+    disc = get_disc(actx, dim, q, G, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind)
+    qf, ph = _host_vec(qfar, dim + 2), _host_vec(phys, 4)
+    out = actx.empty(q.shape)
+    _cabi.check(actx.lib.dgb_ns_rhs(disc.handle, q.ptr, gq.ptr, gptr, ggptr, out.ptr, qf.ctypes.data,
+                                    ph.ctypes.data, actx._st), "dg_ns_rhs")
+    actx.launch_count += 1
+    return out
+
+
+FUSED = {"dg_euler_rhs": dg_euler_rhs, "dg_ns_grad": dg_ns_grad, "dg_ns_rhs": dg_ns_rhs}

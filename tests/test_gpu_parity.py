@@ -1,0 +1,143 @@
+"""GPU parity: the operator program on B200ArrayContext (fused sm_100a kernels through the C ABI)
+against the CPU oracle (oracle/laze_port.py) on identical meshes and states.
+
+Tolerances are the north star's: max relative error <= 1e-12 per RHS evaluation and <= 1e-10 after
+100 RK4 steps, in the reference's norm max|d| / max(max|ref|, 1)
+(/root/reference/pkg/tests/test_acceptance.py:38-41); index maps bit-exact.
+"""
+import numpy as np
+import pytest
+
+from oracle.laze_port import NumpyArrayContext, rel_err
+from paper_2512_17101_b200.operators import EulerOperator, NavierStokesOperator, rk4_step
+from tests.common import FARFIELD, make_dcoll, random_state, smooth_state
+
+pytestmark = pytest.mark.gpu
+TOL_RHS = 1e-12
+TOL_RK = 1e-10
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    from paper_2512_17101_b200 import B200ArrayContext
+    return B200ArrayContext()
+
+
+CASES = [
+    (3, 3, 3, "periodic"), (3, 3, 2, "mixed"), (3, 3, 3, "farfield"),
+    (3, 4, 3, "periodic"), (3, 2, 3, "mixed"), (3, 1, 3, "periodic"), (3, 4, 2, "mixed"),
+    (2, 3, 4, "periodic"), (2, 3, 4, "mixed"), (2, 1, 3, "farfield"), (2, 2, 5, "periodic"), (2, 4, 3, "mixed"),
+]
+
+
+def _both(dim, order, n, bc):
+    cpu = NumpyArrayContext()
+    return make_dcoll(cpu, dim, order, n, bc), None
+
+
+@pytest.mark.parametrize("dim,order,n,bc", CASES)
+def test_index_maps_bit_exact(gpu, dim, order, n, bc):
+    """Compressed device connectivity expands to exactly the host int64 maps."""
+    import ctypes as C
+    from paper_2512_17101_b200 import _cabi
+    from paper_2512_17101_b200.fused import get_disc
+    d = make_dcoll(gpu, dim, order, n, bc)
+    q = d.from_numpy(random_state(dim, d.nelements, d.Np)).data
+    disc = get_disc(gpu, dim, q, 0, d.Sw, d.drdx, d.lift, d.normals, d.fscale, d.vmap_m, d.vmap_p, d.bc_kind)
+    vm = gpu.empty(d.vmap_m.shape, 1)
+    vp = gpu.empty(d.vmap_p.shape, 1)
+    _cabi.check(gpu.lib.dgb_disc_expand_maps(disc.handle, vm.ptr, vp.ptr, gpu._st))
+    assert np.array_equal(gpu.to_numpy(vm), d.vmap_m_host.reshape(-1))
+    assert np.array_equal(gpu.to_numpy(vp), d.vmap_p_host.reshape(-1))
+
+
+@pytest.mark.parametrize("dim,order,n,bc", CASES)
+def test_rhs_parity(gpu, dim, order, n, bc):
+    cpu = NumpyArrayContext()
+    dc, dg = make_dcoll(cpu, dim, order, n, bc), make_dcoll(gpu, dim, order, n, bc)
+    for seed, q0 in [(1, random_state(dim, dc.nelements, dc.Np, seed=1)), (0, smooth_state(dc.nodes()))]:
+        for Op, kw in [(EulerOperator, {}), (NavierStokesOperator, {"mu": 2e-2})]:
+            oc = Op(dc, farfield=FARFIELD[dim], **kw)
+            og = Op(dg, farfield=FARFIELD[dim], **kw)
+            ref = dc.to_numpy(oc.rhs(dc.from_numpy(q0)))
+            got = dg.to_numpy(og.rhs(dg.from_numpy(q0)))
+            assert got.shape == ref.shape
+            assert rel_err(got, ref) <= TOL_RHS, (Op.__name__, seed, rel_err(got, ref))
+            if Op is NavierStokesOperator:
+                gref = dc.to_numpy(oc.grad(dc.from_numpy(q0)))
+                ggot = dg.to_numpy(og.grad(dg.from_numpy(q0)))
+                assert rel_err(ggot, gref) <= TOL_RHS, ("grad", seed, rel_err(ggot, gref))
+
+
+@pytest.mark.parametrize("dim,order,n,bc", [(3, 3, 2, "mixed"), (2, 3, 3, "mixed"), (3, 2, 3, "periodic")])
+def test_generic_ops_parity(gpu, dim, order, n, bc):
+    """The same program with fused dispatch switched off runs op by op on the generic device
+    kernels (einsum, gather, where, stack, reshape, elementwise) and must agree as well."""
+    from paper_2512_17101_b200 import B200ArrayContext
+    plain = B200ArrayContext()
+    plain._fused = {}
+    cpu = NumpyArrayContext()
+    dc, dg = make_dcoll(cpu, dim, order, n, bc), make_dcoll(plain, dim, order, n, bc)
+    q0 = random_state(dim, dc.nelements, dc.Np, seed=3)
+    for Op, kw in [(EulerOperator, {}), (NavierStokesOperator, {"mu": 2e-2})]:
+        ref = dc.to_numpy(Op(dc, farfield=FARFIELD[dim], **kw).rhs(dc.from_numpy(q0)))
+        got = dg.to_numpy(Op(dg, farfield=FARFIELD[dim], **kw).rhs(dg.from_numpy(q0)))
+        assert rel_err(got, ref) <= TOL_RHS, (Op.__name__, rel_err(got, ref))
+
+
+@pytest.mark.parametrize("dim,order,n,Op,kw", [
+    (2, 3, 4, EulerOperator, {}), (3, 3, 3, EulerOperator, {}), (3, 3, 3, NavierStokesOperator, {"mu": 1e-2})])
+def test_rk4_100_steps(gpu, dim, order, n, Op, kw):
+    cpu = NumpyArrayContext()
+    dc, dg = make_dcoll(cpu, dim, order, n, "periodic"), make_dcoll(gpu, dim, order, n, "periodic")
+    q0 = smooth_state(dc.nodes())
+    oc, og = Op(dc, **kw), Op(dg, **kw)
+    qc, qg = dc.from_numpy(q0), dg.from_numpy(q0)
+    dt = 2e-3
+    t = 0.0
+    for _ in range(100):
+        qc = rk4_step(oc.rhs, qc, t, dt)
+        qg = rk4_step(og.rhs, qg, t, dt)
+        t += dt
+    ref, got = dc.to_numpy(qc), dg.to_numpy(qg)
+    assert np.all(np.isfinite(got))
+    assert rel_err(got, ref) <= TOL_RK, rel_err(got, ref)
+
+
+def test_tail_block_and_odd_sizes(gpu):
+    """Element counts that are not multiples of the CTA block (ragged last block)."""
+    cpu = NumpyArrayContext()
+    for n in (1, 2):   # E = 6, 48 in 3D (non-periodic so tiny meshes are legal)
+        dc, dg = make_dcoll(cpu, 3, 3, n, "farfield"), make_dcoll(gpu, 3, 3, n, "farfield")
+        q0 = random_state(3, dc.nelements, dc.Np, seed=7)
+        ref = dc.to_numpy(NavierStokesOperator(dc, farfield=FARFIELD[3], mu=1e-2).rhs(dc.from_numpy(q0)))
+        got = dg.to_numpy(NavierStokesOperator(dg, farfield=FARFIELD[3], mu=1e-2).rhs(dg.from_numpy(q0)))
+        assert rel_err(got, ref) <= TOL_RHS
+
+
+def test_out_of_bounds_map_rejected(gpu):
+    """An index map leaving [0, E*Np) raises OutOfBoundsIndex at upload, like the reference's
+    bounds-checked gather (/root/reference/pkg/tests/test_backend.py:72-80)."""
+    from paper_2512_17101_b200 import errors
+    d = make_dcoll(gpu, 3, 2, 2, "farfield")
+    bad = d.vmap_p_host.reshape(-1).copy()
+    bad[5] = d.nelements * d.Np + 3
+    d.vmap_p = gpu.from_numpy(bad)
+    op = EulerOperator(d, farfield=FARFIELD[3])
+    with pytest.raises(errors.OutOfBoundsIndex):
+        op.rhs(d.from_numpy(random_state(3, d.nelements, d.Np)))
+    bad2 = d.vmap_p_host.reshape(-1).copy()
+    bad2[[0, 1]] = bad2[[1, 0]]
+    d.vmap_p = gpu.from_numpy(bad2)
+    with pytest.raises(errors.BindingMismatch):
+        EulerOperator(d, farfield=FARFIELD[3]).rhs(d.from_numpy(random_state(3, d.nelements, d.Np)))
+
+
+def test_run_to_run_bitwise(gpu):
+    """No atomics anywhere on the path: two evaluations are bitwise identical."""
+    d = make_dcoll(gpu, 3, 3, 3, "periodic")
+    op = NavierStokesOperator(d, mu=1e-2)
+    q = d.from_numpy(random_state(3, d.nelements, d.Np))
+    a = d.to_numpy(op.rhs(q))
+    b = d.to_numpy(op.rhs(q))
+    assert np.array_equal(a, b)
