@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""Headline benchmark: 3D compressible Navier-Stokes DG right-hand side, order 3, ~100M DOFs
+per GPU (BASELINE.json configs[2]); metric GDOF/s and fraction of the HBM roofline.
+
+    python bench.py --gpus N --steps K --warmup W            # the B200 path
+    python bench.py --impl reference --steps K --warmup W    # the CPU reference path (oracle port)
+
+One "step" = one full RHS evaluation (gradient pass + flux/divergence pass, plus the halo
+exchanges when N > 1) on synthetic seeded data.  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DIM, ORDER = 3, 3
+NP = 20
+B_ALG_RHS = 360.0      # algorithmic bytes per node-DOF per NS RHS: (3C + 2Cd) * 8, C=5, d=3
+B_ALG_GRAD = 160.0     # pass 1: read q (40) + write grad q (120)
+B_ALG_DIV = 200.0      # pass 2: read q (40) + read grad q (120) + write rhs (40)
+PHYS = dict(gamma=1.4, mu=1e-3, prandtl=0.72, rgas=1.0)
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def state_for(nodes_shape, seed):
+    """SURVEY.md §8d config c2 generator: rho~U[.9,1.1], u~U[-.1,.1]^3, p~U[.9,1.1]/gamma."""
+    rng = np.random.default_rng(seed)
+    E, Np = nodes_shape
+    q = np.empty((DIM + 2, E, Np))
+    q[0] = rng.uniform(0.9, 1.1, (E, Np))
+    vel = rng.uniform(-0.1, 0.1, (DIM, E, Np))
+    p = rng.uniform(0.9, 1.1, (E, Np)) / PHYS["gamma"]
+    q[1] = p / (PHYS["gamma"] - 1.0) + 0.5 * q[0] * (vel ** 2).sum(axis=0)
+    q[2:] = q[0] * vel
+    return q
+
+
+# {{{ clocks sampling (B200_PROFILING.md)
+
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.file = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=self.file, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.file.flush()
+        self.file.seek(0)
+        sm, mx, reasons, power = [], [], set(), []
+        for line in self.file.read().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1])); mx.append(float(parts[2])); power.append(float(parts[3]))
+            except ValueError:
+                continue
+            for name, val in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), parts[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        os.unlink(self.file.name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        # "under load" = the upper half of the power samples
+        order = np.argsort(power)
+        load = [sm[i] for i in order[len(order) // 2:]]
+        return {"sm_mhz": float(np.median(load)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "power_w_max": float(max(power)), "samples": len(sm)}
+
+# }}}
+
+
+# {{{ CPU reference arm (oracle port = the reference's eager NumPy context, oracle/laze_port.py)
+
+def _cpu_worker(args):
+    n, reps, seed = args
+    from oracle.laze_port import NumpyArrayContext
+    from paper_2512_17101_b200 import DGDiscretization, NavierStokesOperator, box_mesh
+    actx = NumpyArrayContext()
+    mesh = box_mesh((n,) * DIM, (-1.0,) * DIM, (1.0,) * DIM, periodic=(True,) * DIM)
+    d = DGDiscretization(actx, mesh, ORDER)
+    op = NavierStokesOperator(d, **PHYS)
+    q = d.from_numpy(state_for((d.nelements, d.Np), seed))
+    op.rhs(q)                                   # warm-up
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        op.rhs(q)
+    return d.nelements * d.Np * reps, time.perf_counter() - t0
+
+
+def cpu_throughput(cores: int, n: int, reps: int):
+    """Aggregate DOF/s of `cores` independent processes, each evaluating the NS RHS `reps` times
+    on its own periodic n^3 Kuhn mesh (halo exchange ignored: favours the CPU)."""
+    import multiprocessing as mp
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    if cores == 1:
+        results = [_cpu_worker((n, reps, 1))]
+    else:
+        with ctx.Pool(cores) as pool:
+            results = pool.map(_cpu_worker, [(n, reps, 1 + k) for k in range(cores)])
+    wall = time.perf_counter() - t0
+    dofs = sum(r[0] for r in results)
+    busy = max(r[1] for r in results)
+    return dofs / busy / 1e9, dofs, busy, wall
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    n, reps = args.cpu_n, 1
+    for _ in range(args.warmup):
+        cpu_throughput(cores, n, reps)
+    t0 = time.perf_counter()
+    dofs = 0
+    busy = 0.0
+    for _ in range(args.steps):
+        _, d, b, _ = cpu_throughput(cores, n, reps)
+        dofs += d
+        busy += b
+    wall = time.perf_counter() - t0
+    value = dofs / busy / 1e9
+    sample = (f"{cores} processes x NS p3 RHS on a periodic {n}^3 Kuhn mesh ({6 * n ** 3} elements, "
+              f"{6 * n ** 3 * NP} DOFs each), {reps} evaluation(s) per step; NumPy eager context (oracle/laze_port.py)")
+    line = {
+        "impl": "reference", "metric": "3D Navier-Stokes DG RHS throughput", "value": value, "unit": "GDOF/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * busy / max(args.steps, 1), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "3D compressible Navier-Stokes DG RHS, tets order 3 (two derivative passes); "
+                               "bounded CPU sample of BASELINE configs[2]", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "GDOF/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": wall,
+    }
+    print(json.dumps(line))
+
+# }}}
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_17101_b200 import B200ArrayContext, DGDiscretization, NavierStokesOperator, box_mesh
+    from paper_2512_17101_b200.dofarray import DOFArray
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if world != args.gpus and rank == 0:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+
+    actx = B200ArrayContext(device=local_rank)
+    n = args.n
+    t_setup = time.perf_counter()
+    # weak scaling: every rank owns one periodic n^3 block of the same size (configs[2] per GPU)
+    mesh = box_mesh((n,) * DIM, (-1.0,) * DIM, (1.0,) * DIM, periodic=(True,) * DIM)
+    halo = None
+    if world > 1:
+        from paper_2512_17101_b200.halo import ring_slab_halo
+        mesh, halo = ring_slab_halo(actx, mesh, n, rank, world, ORDER)
+    d = DGDiscretization(actx, mesh, ORDER, ghost_elements=0 if halo is None else halo.nghost)
+    op = NavierStokesOperator(d, **PHYS)
+    E, Np = d.nelements, d.Np
+    ndof = E * Np
+    q_host = actx.pinned_empty((DIM + 2, E, Np))
+    q_host[...] = state_for((E, Np), 20251217 + rank)
+    out_host = actx.pinned_empty((DIM + 2, E, Np))
+    q = DOFArray(actx, actx.from_numpy(q_host))
+    actx.synchronize()
+    t_setup = time.perf_counter() - t_setup
+
+    def rhs_step(qarr):
+        if halo is None:
+            return op.rhs(qarr)
+        return halo.ns_rhs(op, qarr)
+
+    # ---- device-resident measurement --------------------------------------------------------
+    stream = actx.stream
+    for _ in range(max(args.warmup, 3)):
+        rhs_step(q)
+    actx.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local_rank) if rank == 0 else None
+    K = args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    launches0 = actx.launch_count
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for k in range(K):
+        if halo is None:
+            ev[k][0].record(stream)
+            gq = op.grad(q)
+            ev[k][1].record(stream)
+            op._f(q.data, gq.data, *op._common(), op.phys)
+            ev[k][2].record(stream)
+        else:
+            rhs_step(q)
+    stop.record(stream)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = sampler.stop() if sampler else None
+    launches = actx.launch_count - launches0
+    ms_total = start.elapsed_time(stop)
+    ms_step = ms_total / K
+    if world > 1:
+        t = torch.tensor([ms_step], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+    value = world * ndof / (ms_step * 1e-3) / 1e9
+
+    peak, peak_src = measured_peaks()
+    roofline = None
+    if halo is None:
+        ms_grad = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
+        ms_div = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
+        dom = ("k_rhs<viscous> (flux + divergence pass)", ms_div, B_ALG_DIV) if ms_div >= ms_grad else \
+              ("k_grad (BR1 gradient pass)", ms_grad, B_ALG_GRAD)
+        achieved = ndof * dom[2] / (dom[1] * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                    "algorithmic_bytes_per_dof": dom[2], "ms_per_launch": dom[1],
+                    "ms_grad_pass": ms_grad, "ms_div_pass": ms_div}
+    rhs_gbs = ndof * B_ALG_RHS / (ms_step * 1e-3) / 1e9
+
+    # ---- end to end through the public API with host buffers ---------------------------------
+    e2e = None
+    if not args.no_e2e:
+        Ke = max(1, min(K, args.e2e_steps))
+        for _ in range(2):
+            qd = DOFArray(actx, actx.from_numpy(q_host))
+            actx.to_numpy(rhs_step(qd).data, out=out_host)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(Ke):
+            qd = DOFArray(actx, actx.from_numpy(q_host))          # H2D from pinned host memory
+            actx.to_numpy(rhs_step(qd).data, out=out_host)        # D2H of the result
+        s1.record(stream)
+        torch.cuda.synchronize()
+        ms_e2e = s0.elapsed_time(s1) / Ke
+        if world > 1:
+            t = torch.tensor([ms_e2e], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_e2e = float(t.item())
+        e2e = {"value": world * ndof / (ms_e2e * 1e-3) / 1e9, "unit": "GDOF/s",
+               "h2d_bytes_per_step": int(q_host.nbytes), "d2h_bytes_per_step": int(out_host.nbytes),
+               "ms_per_step": ms_e2e, "steps": Ke, "checksum": float(out_host[0, 0, 0])}
+
+    # ---- CPU baseline beside it (rank 0, N=1 only, bounded sample) ---------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cores = os.cpu_count() or 1
+        v, dofs, busy, wall = cpu_throughput(cores, args.cpu_n, 1)
+        cpu = {"value": v, "unit": "GDOF/s", "cores": cores, "kind": "port",
+               "sample": f"{cores} processes x 1 NS p3 RHS on a periodic {args.cpu_n}^3 Kuhn mesh "
+                         f"({6 * args.cpu_n ** 3 * NP} DOFs each), oracle/laze_port.py NumPy eager context; "
+                         f"{busy:.1f} s busy"}
+
+    if rank == 0:
+        line = {
+            "metric": "3D Navier-Stokes DG RHS throughput", "value": value, "unit": "GDOF/s",
+            "n_gpus": world, "steps": K, "warmup": max(args.warmup, 3), "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"3D compressible Navier-Stokes DG RHS (BR1, two derivative passes), Kuhn tets "
+                                   f"order 3, periodic {n}^3 box per GPU: {E} elements, {ndof} DOFs per GPU "
+                                   f"(BASELINE configs[2])",
+                       "elements_per_gpu": E, "dofs_per_gpu": ndof, "order": ORDER, "dim": DIM,
+                       "l2_policy": "inputs larger than L2 (q 4.0 GB, grad q 12 GB per GPU vs 126 MB L2)"
+                       if ndof * 40 > 126e6 * 4 else "inputs comparable to L2: reduced size, not the headline config",
+                       "parallelism": f"mesh partition x{world}, NCCL face-halo exchange" if world > 1 else "single GPU",
+                       "setup_s": t_setup},
+            "roofline": roofline,
+            "rhs_roofline": {"bound": "hbm", "achieved": rhs_gbs, "peak": peak, "unit": "GB/s",
+                             "frac": rhs_gbs / peak, "algorithmic_bytes_per_dof": B_ALG_RHS,
+                             "peak_source": peak_src},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=94, help="cells per axis per GPU (94 -> 4,983,504 elements, 99.67M DOFs)")
+    ap.add_argument("--cpu-n", type=int, default=10, help="cells per axis of each CPU-baseline sample mesh")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

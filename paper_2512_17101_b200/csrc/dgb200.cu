@@ -4,6 +4,7 @@
 #include "dgb_kernels.cuh"
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -121,8 +122,20 @@ __global__ void k_pack_elements(double* __restrict__ dst, const double* __restri
 
 namespace {
 
-template <int DIM, int P> struct Cfg { static constexpr int K = 16, NW = DIM == 3 ? 5 : 4, MT = 2, KG = 16, NWG = DIM == 3 ? 5 : 4; };
-template <> struct Cfg<3, 4> { static constexpr int K = 8, NW = 5, MT = 1, KG = 8, NWG = 5; };
+// V = tuning variant (env DGB_VARIANT, default 0): block size K, warps NW, column tiles per warp MT,
+// minimum resident CTAs per SM MINB (register cap)
+template <int DIM, int P, int V> struct Cfg { static constexpr int K = 16, NW = DIM == 3 ? 5 : 4, MT = 2, MINB = 2, KG = 16, NWG = DIM == 3 ? 5 : 4, MINBG = 2; };
+template <int DIM, int P> struct Cfg<DIM, P, 1> { static constexpr int K = 16, NW = DIM == 3 ? 10 : 8, MT = 1, MINB = 2, KG = 16, NWG = DIM == 3 ? 10 : 8, MINBG = 2; };
+template <int DIM, int P> struct Cfg<DIM, P, 2> { static constexpr int K = 8, NW = DIM == 3 ? 5 : 4, MT = 1, MINB = 4, KG = 8, NWG = DIM == 3 ? 5 : 4, MINBG = 4; };
+template <int DIM, int P> struct Cfg<DIM, P, 3> { static constexpr int K = 8, NW = DIM == 3 ? 5 : 4, MT = 1, MINB = 3, KG = 16, NWG = DIM == 3 ? 5 : 4, MINBG = 3; };
+template <> struct Cfg<3, 4, 0> { static constexpr int K = 8, NW = 5, MT = 1, MINB = 1, KG = 8, NWG = 5, MINBG = 1; };
+template <> struct Cfg<3, 4, 1> { static constexpr int K = 8, NW = 10, MT = 1, MINB = 1, KG = 8, NWG = 10, MINBG = 1; };
+
+int variant() {
+  static int v = -1;
+  if (v < 0) { const char* e = getenv("DGB_VARIANT"); v = e ? atoi(e) : 0; if (v < 0 || v > 3) v = 0; }
+  return v;
+}
 
 template <typename Kern>
 int persistent_grid(Kern kern, int threads, size_t smem, int nblocks, int* grid) {
@@ -135,11 +148,11 @@ int persistent_grid(Kern kern, int threads, size_t smem, int nblocks, int* grid)
   return DGB_OK;
 }
 
-template <int DIM, int P, bool VISCOUS>
+template <int DIM, int P, bool VISCOUS, int V>
 int launch_rhs(const dgb_disc* d, const double* q, const double* gq, const double* ghost, const double* gghost,
                const dgb::Epilogue& ep, const dgb::Phys& ph, cudaStream_t st) {
-  using C = Cfg<DIM, P>;
-  auto kern = dgb::k_rhs<DIM, P, C::K, C::NW, C::MT, VISCOUS>;
+  using C = Cfg<DIM, P, V>;
+  auto kern = dgb::k_rhs<DIM, P, C::K, C::NW, C::MT, VISCOUS, C::MINB>;
   const size_t smem = sizeof(dgb::RhsSmem<DIM, P, C::K, C::NW, C::MT, VISCOUS>);
   const long long nb = (d->dev.E + C::K - 1) / C::K;
   if (nb == 0) return DGB_OK;
@@ -150,11 +163,11 @@ int launch_rhs(const dgb_disc* d, const double* q, const double* gq, const doubl
   return DGB_OK;
 }
 
-template <int DIM, int P>
+template <int DIM, int P, int V>
 int launch_grad(const dgb_disc* d, const double* q, const double* ghost, double* grad, const dgb::Phys& ph,
                 cudaStream_t st) {
-  using C = Cfg<DIM, P>;
-  auto kern = dgb::k_grad<DIM, P, C::KG, C::NWG>;
+  using C = Cfg<DIM, P, V>;
+  auto kern = dgb::k_grad<DIM, P, C::KG, C::NWG, C::MINBG>;
   const size_t smem = sizeof(dgb::GradSmem<DIM, P, C::KG>);
   const long long nb = (d->dev.E + C::KG - 1) / C::KG;
   if (nb == 0) return DGB_OK;
@@ -170,9 +183,21 @@ int launch_grad(const dgb_disc* d, const double* q, const double* ghost, double*
 int dispatch_rhs(const dgb_disc* d, bool viscous, const double* q, const double* gq, const double* ghost,
                  const double* gghost, const dgb::Epilogue& ep, const dgb::Phys& ph, cudaStream_t st) {
 #define X(DIM, P)                                                                              \
-  if (d->dim == DIM && d->order == P)                                                          \
-    return viscous ? launch_rhs<DIM, P, true>(d, q, gq, ghost, gghost, ep, ph, st)             \
-                   : launch_rhs<DIM, P, false>(d, q, gq, ghost, gghost, ep, ph, st);
+  if (d->dim == DIM && d->order == P) {                                                        \
+    if (DIM == 3 && P == 3) {                                                                  \
+      switch (variant()) {                                                                     \
+        case 1: return viscous ? launch_rhs<3, 3, true, 1>(d, q, gq, ghost, gghost, ep, ph, st) \
+                               : launch_rhs<3, 3, false, 1>(d, q, gq, ghost, gghost, ep, ph, st); \
+        case 2: return viscous ? launch_rhs<3, 3, true, 2>(d, q, gq, ghost, gghost, ep, ph, st) \
+                               : launch_rhs<3, 3, false, 2>(d, q, gq, ghost, gghost, ep, ph, st); \
+        case 3: return viscous ? launch_rhs<3, 3, true, 3>(d, q, gq, ghost, gghost, ep, ph, st) \
+                               : launch_rhs<3, 3, false, 3>(d, q, gq, ghost, gghost, ep, ph, st); \
+        default: break;                                                                        \
+      }                                                                                        \
+    }                                                                                          \
+    return viscous ? launch_rhs<DIM, P, true, 0>(d, q, gq, ghost, gghost, ep, ph, st)          \
+                   : launch_rhs<DIM, P, false, 0>(d, q, gq, ghost, gghost, ep, ph, st);        \
+  }
   DGB_FOR_EACH_ELEMENT(X)
 #undef X
   return fail(DGB_ERR_INVALID, "unsupported (dim, order)");
@@ -180,8 +205,18 @@ int dispatch_rhs(const dgb_disc* d, bool viscous, const double* q, const double*
 
 int dispatch_grad(const dgb_disc* d, const double* q, const double* ghost, double* grad, const dgb::Phys& ph,
                   cudaStream_t st) {
-#define X(DIM, P) \
-  if (d->dim == DIM && d->order == P) return launch_grad<DIM, P>(d, q, ghost, grad, ph, st);
+#define X(DIM, P)                                                              \
+  if (d->dim == DIM && d->order == P) {                                        \
+    if (DIM == 3 && P == 3) {                                                  \
+      switch (variant()) {                                                     \
+        case 1: return launch_grad<3, 3, 1>(d, q, ghost, grad, ph, st);        \
+        case 2: return launch_grad<3, 3, 2>(d, q, ghost, grad, ph, st);        \
+        case 3: return launch_grad<3, 3, 3>(d, q, ghost, grad, ph, st);        \
+        default: break;                                                        \
+      }                                                                        \
+    }                                                                          \
+    return launch_grad<DIM, P, 0>(d, q, ghost, grad, ph, st);                  \
+  }
   DGB_FOR_EACH_ELEMENT(X)
 #undef X
   return fail(DGB_ERR_INVALID, "unsupported (dim, order)");

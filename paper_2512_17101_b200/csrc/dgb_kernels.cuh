@@ -275,13 +275,14 @@ struct RhsSmem {
   double Wl[EL::NPR * EL::LDF];
   double Gs[EL::C * K * EL::LDV];
   double Fs[EL::C * K * EL::LDF];
+  double Lam[K * EL::NP];
   GeoSmem<DIM, P, K> geo;
   int fn[EL::NF * EL::NFP];
   int perm[EL::NPERM * EL::NFP];
 };
 
-template <int DIM, int P, int K, int NW, int MT, bool VISCOUS>
-__global__ void __launch_bounds__(NW * 32)
+template <int DIM, int P, int K, int NW, int MT, bool VISCOUS, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB)
 k_rhs(DiscDev d, const double* __restrict__ q, const double* __restrict__ gq,
       const double* __restrict__ ghost, const double* __restrict__ gghost,
       Epilogue ep, Phys ph, int nblocks) {
@@ -300,6 +301,7 @@ k_rhs(DiscDev d, const double* __restrict__ q, const double* __restrict__ gq,
   for (int n = tid; n < C * K * EL::LDF; n += NT) S.Fs[n] = 0.0;
   for (int n = tid; n < NF * NFP; n += NT) S.fn[n] = d.tables[n];
   for (int n = tid; n < EL::NPERM * NFP; n += NT) S.perm[n] = d.tables[NF * NFP + n];
+  __syncthreads();   // the zero fill above must not race with the first block's staging writes
 
   for (int blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
     const long long e0 = (long long)blk * K;
@@ -342,9 +344,16 @@ k_rhs(DiscDev d, const double* __restrict__ q, const double* __restrict__ gq,
           S.Gs[(c * K + e) * EL::LDV + r * EL::NPK + j] = acc;
         }
       }
+      S.Lam[n] = wavespeed<DIM>(s, ph.gamma);
     }
+    __syncthreads();
 
     // ---- phase 2: face gather + numerical flux --------------------------------------------
+    // Own side: the scaled normal flux fscale*(F.n)^- needs no recomputation.  On an affine simplex
+    // with face f opposite vertex f and r_k = 2*lambda_k - 1,
+    //     fscale_f * n_f . F = (f == 0) ? sum_r G_r : -G_{f-1},     G_r = sum_x drdx[r][x] F_x,
+    // and G_r at the face node is already in shared memory from phase 1 (as is the wave speed).
+    // Only the neighbour side is evaluated pointwise.
     for (int n = tid; n < nel * NFT; n += NT) {
       const int e = n / NFT, fm = n - e * NFT;
       const int f = fm / NFP, m = fm - f * NFP;
@@ -367,45 +376,51 @@ k_rhs(DiscDev d, const double* __restrict__ q, const double* __restrict__ gq,
         qm[c] = q[((long long)c * E + e0 + e) * NP + jm];
         qp[c] = pbase[((long long)c * pE + pe) * NP + jp];
       }
-      bc_state<DIM, VISCOUS>(bc, qm, nrm, ph, qp);
-      Prim<DIM> sm_, sp_;
-      make_prim<DIM>(qm, ph.gamma, sm_);
-      make_prim<DIM>(qp, ph.gamma, sp_);
-      double fnm[C], fnp[C];
-      inviscid_normal_flux<DIM>(sm_, nrm, fnm);
-      inviscid_normal_flux<DIM>(sp_, nrm, fnp);
-      const double lam = fmax(wavespeed<DIM>(sm_, ph.gamma), wavespeed<DIM>(sp_, ph.gamma));
-      double fstar[C];
-#pragma unroll
-      for (int c = 0; c < C; ++c) fstar[c] = 0.5 * (fnm[c] + fnp[c]) + 0.5 * lam * (qm[c] - qp[c]);
+      double gp[DIM][C];
       if (VISCOUS) {
         const double* gbase = in_ghost ? gghost : gq;
-        double gm[DIM][C], gp[DIM][C], Fvm[DIM][C], Fvp[DIM][C];
 #pragma unroll
         for (int x = 0; x < DIM; ++x)
 #pragma unroll
-          for (int c = 0; c < C; ++c) {
-            gm[x][c] = gq[((long long)(x * C + c) * E + e0 + e) * NP + jm];
-            gp[x][c] = gbase[((long long)(x * C + c) * pE + pe) * NP + jp];
-          }
-        viscous_flux<DIM>(sm_, gm, ph, Fvm);
+          for (int c = 0; c < C; ++c) gp[x][c] = gbase[((long long)(x * C + c) * pE + pe) * NP + jp];
+      }
+      bc_state<DIM, VISCOUS>(bc, qm, nrm, ph, qp);
+      Prim<DIM> sp_;
+      make_prim<DIM>(qp, ph.gamma, sp_);
+      double fnp[C];
+      inviscid_normal_flux<DIM>(sp_, nrm, fnp);
+      const double lam = fmax(S.Lam[e * NP + jm], wavespeed<DIM>(sp_, ph.gamma));
+      if (VISCOUS) {
+        double Fvp[DIM][C];
         viscous_flux<DIM>(sp_, gp, ph, Fvp);
 #pragma unroll
         for (int c = 1; c < C; ++c) {
           double vn = 0.0;
 #pragma unroll
-          for (int x = 0; x < DIM; ++x) vn += (Fvm[x][c] + Fvp[x][c]) * nrm[x];
-          fstar[c] -= 0.5 * vn;
+          for (int x = 0; x < DIM; ++x) vn += Fvp[x][c] * nrm[x];
+          fnp[c] -= vn;
         }
       }
 #pragma unroll
-      for (int c = 0; c < C; ++c) S.Fs[(c * K + e) * EL::LDF + fm] = -fs * fstar[c];
+      for (int c = 0; c < C; ++c) {
+        const double* grow = S.Gs + (c * K + e) * EL::LDV + jm;
+        double own;                       // fscale * (F^- . n), inviscid minus viscous
+        if (f == 0) {
+          own = grow[0];
+#pragma unroll
+          for (int r = 1; r < DIM; ++r) own += grow[r * EL::NPK];
+        } else {
+          own = -grow[(f - 1) * EL::NPK];
+        }
+        S.Fs[(c * K + e) * EL::LDF + fm] = -0.5 * (own + fs * (fnp[c] + lam * (qm[c] - qp[c])));
+      }
     }
     __syncthreads();
 
     // ---- phase 3: tensor-core contraction + (RK-fused) store -------------------------------
     constexpr int NTILES = C * K / 8;
     for (int t0 = warp * MT; t0 < NTILES; t0 += NW * MT) {
+      __syncwarp();
       double acc[MT][EL::NI][2];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
@@ -451,8 +466,8 @@ struct GradSmem {
   int perm[EL::NPERM * EL::NFP];
 };
 
-template <int DIM, int P, int K, int NW>
-__global__ void __launch_bounds__(NW * 32)
+template <int DIM, int P, int K, int NW, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB)
 k_grad(DiscDev d, const double* __restrict__ q, const double* __restrict__ ghost,
        double* __restrict__ grad, Phys ph, int nblocks) {
   using EL = ElemT<DIM, P>;
@@ -470,6 +485,7 @@ k_grad(DiscDev d, const double* __restrict__ q, const double* __restrict__ ghost
   for (int n = tid; n < C * K * EL::LDS; n += NT) S.Ss[n] = 0.0;
   for (int n = tid; n < NF * NFP; n += NT) S.fn[n] = d.tables[n];
   for (int n = tid; n < EL::NPERM * NFP; n += NT) S.perm[n] = d.tables[NF * NFP + n];
+  __syncthreads();   // the zero fill above must not race with the first block's staging writes
 
   for (int blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
     const long long e0 = (long long)blk * K;
@@ -520,6 +536,7 @@ k_grad(DiscDev d, const double* __restrict__ q, const double* __restrict__ ghost
 
     constexpr int NTILES = C * K / 8;
     for (int tile = warp; tile < NTILES; tile += NW) {
+      __syncwarp();
       double accT[DIM][1][NI][2], accU[NF][1][NI][2];
 #pragma unroll
       for (int s = 0; s < DIM; ++s)

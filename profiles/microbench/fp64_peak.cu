@@ -152,6 +152,34 @@ __global__ void __launch_bounds__(256) k_dmma_smem(double* out, const double* __
   out[blockIdx.x * blockDim.x + threadIdx.x] = tot;
 }
 
+// 7. concurrent DMMA + DFMA: even warps run DMMA chains, odd warps DFMA chains (are the pipes shared?)
+__global__ void __launch_bounds__(256) k_mixed(double* out, int iters_mma, int iters_fma, double a, double b) {
+  const int warp = threadIdx.x >> 5;
+  double s = 0;
+  if (warp & 1) {
+    double x[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = threadIdx.x * 1e-3 + i;
+    for (int it = 0; it < iters_fma; ++it) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) x[i] = fma(x[i], a, b);
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s += x[i];
+  } else {
+    double c0[8], c1[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { c0[i] = threadIdx.x * 1e-3 + i; c1[i] = i; }
+    for (int it = 0; it < iters_mma; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dmma884(c0[i], c1[i], a, b);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += c0[i] + c1[i];
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 // 6. HBM copy (double2 grid-stride) for a local bandwidth reference
 __global__ void k_copy(const double2* __restrict__ a, double2* __restrict__ b, size_t n) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) b[i] = a[i];
@@ -208,6 +236,16 @@ int main(int argc, char** argv) {
     double ms = time_ms([&] { k_dmma_smem<NT><<<p.multiProcessorCount, block, smem>>>(out, win, xin, iters); }, 5);
     double useful = (double)p.multiProcessorCount * 8 * NT * 8 * iters * 2000.0 * 2;
     printf("dmma_smem<NT=4> : %8.3f ms  %7.2f TFLOP/s useful (x1.2 issued)\n", ms, useful / ms * 1e-9); }
+  {
+    // each alone (half the warps idle), then together
+    int im = 20000, ifm = 20000;
+    double t_m = time_ms([&] { k_mixed<<<grid, block>>>(out, im, 0, 1.0000001, 1e-9); }, 5);
+    double t_f = time_ms([&] { k_mixed<<<grid, block>>>(out, 0, ifm, 1.0000001, 1e-9); }, 5);
+    double t_b = time_ms([&] { k_mixed<<<grid, block>>>(out, im, ifm, 1.0000001, 1e-9); }, 5);
+    double fl_m = nthreads / 2 / 32 * im * 8 * 512.0, fl_f = nthreads / 2 * ifm * 32.0;
+    printf("mixed: dmma alone %8.3f ms (%6.2f TF)  dfma alone %8.3f ms (%6.2f TF)  together %8.3f ms (%6.2f TF total)\n",
+           t_m, fl_m / t_m * 1e-9, t_f, fl_f / t_f * 1e-9, t_b, (fl_m + fl_f) / t_b * 1e-9);
+  }
   {
     size_t n = (size_t)1 << 27;  // 2 GiB each
     double2 *a, *b; CK(cudaMalloc(&a, n * 16)); CK(cudaMalloc(&b, n * 16)); CK(cudaMemset(a, 1, n * 16));
