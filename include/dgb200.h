@@ -83,6 +83,8 @@ int dgb_disc_create(dgb_disc** out, int dim, int order, int64_t nelements, int64
                     const int64_t* bc_kind_dev, void* stream);
 int dgb_disc_destroy(dgb_disc* disc);
 int dgb_disc_expand_maps(const dgb_disc* disc, int64_t* vmap_m_dev, int64_t* vmap_p_dev, void* stream);
+/* debug: per-phase cycle counters summed over CTAs (filled only by -DDGB_PHASE_TIMING builds); resets them */
+int dgb_debug_phase_cycles(const dgb_disc* disc, long long* out8_host);
 
 /* ---- the outlined DG functions (operators.py; reference boundary: a Call to a
  *      FunctionDefinition, adfg.py:722-803, executed as a CallStep, backend.py:90-96) ----------

@@ -11,13 +11,13 @@ import os
 from . import errors
 
 _LIB = None
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdgb200.so")
+LIB_PATH = os.environ.get("DGB_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdgb200.so")
 
 # every symbol include/dgb200.h declares (tests/test_cabi_symbols.py checks the two stay in sync)
 SYMBOLS = [
     "dgb_last_error", "dgb_version", "dgb_malloc", "dgb_free", "dgb_host_alloc", "dgb_host_free",
     "dgb_memcpy_h2d", "dgb_memcpy_d2h", "dgb_memcpy_d2d", "dgb_stream_sync",
-    "dgb_disc_create", "dgb_disc_destroy", "dgb_disc_expand_maps",
+    "dgb_disc_create", "dgb_disc_destroy", "dgb_disc_expand_maps", "dgb_debug_phase_cycles",
     "dgb_euler_rhs", "dgb_ns_grad", "dgb_ns_rhs", "dgb_euler_rhs_rk", "dgb_ns_rhs_rk",
     "dgb_pack_elements",
     "dgb_ew_binary", "dgb_ew_unary", "dgb_ew_where", "dgb_copy_strided", "dgb_copy_scatter", "dgb_take",
@@ -68,6 +68,7 @@ def load():
                                     vp, vp, vp, vp, dp, dp, dp, dp, dp, dp, vp]
     lib.dgb_disc_destroy.argtypes = [vp]
     lib.dgb_disc_expand_maps.argtypes = [vp, dp, dp, vp]
+    lib.dgb_debug_phase_cycles.argtypes = [vp, vp]
     lib.dgb_euler_rhs.argtypes = [vp, dp, dp, dp, vp, vp, vp]
     lib.dgb_ns_grad.argtypes = [vp, dp, dp, dp, vp, vp]
     lib.dgb_ns_rhs.argtypes = [vp, dp, dp, dp, dp, dp, vp, vp, vp]

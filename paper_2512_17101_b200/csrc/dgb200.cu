@@ -1,7 +1,8 @@
 // C ABI of the B200 DG right-hand-side path: discretisation handle, kernel dispatch, halo
 // packing.  See include/dgb200.h for the contract and the reference interfaces replaced.
 #include "../../include/dgb200.h"
-#include "dgb_kernels.cuh"
+#include "dgb_kernels_async.cuh"
+#include "dgb_kernels_warp.cuh"
 
 #include <cstdio>
 #include <cstdlib>
@@ -35,6 +36,7 @@ struct dgb_disc {
   dgb::DiscDev dev{};
   double *Wv = nullptr, *Wl = nullptr, *Wq = nullptr, *Wf = nullptr;
   long long* conn = nullptr;
+  long long* timing = nullptr;
   int* tables = nullptr;
   const int64_t* bc_kind = nullptr;
 };
@@ -131,9 +133,35 @@ template <int DIM, int P> struct Cfg<DIM, P, 3> { static constexpr int K = 8, NW
 template <> struct Cfg<3, 4, 0> { static constexpr int K = 8, NW = 5, MT = 1, MINB = 1, KG = 8, NWG = 5, MINBG = 1; };
 template <> struct Cfg<3, 4, 1> { static constexpr int K = 8, NW = 10, MT = 1, MINB = 1, KG = 8, NWG = 10, MINBG = 1; };
 
+// launch configuration of the asynchronous-pipeline kernels (dgb_kernels_async.cuh), the default path
+template <int DIM, int P> struct Cfg2 { static constexpr int K = 8, NW = 8, MINB = 2, KG = 8, NWG = DIM == 3 ? 5 : 4, MINBG = 3; };
+template <> struct Cfg2<3, 4> { static constexpr int K = 8, NW = 8, MINB = 1, KG = 8, NWG = 5, MINBG = 1; };
+
+// launch configuration of the warp-autonomous kernels (dgb_kernels_warp.cuh), the default path:
+// KW elements per warp (C*KW columns padded to whole 8-column tiles), as many warps per SM as fit
+#ifndef DGB_RHS_WARPS
+#define DGB_RHS_WARPS 12
+#endif
+constexpr int kSmemBudget = 232448 - 1024;   // 227 KB usable per CTA minus the 1 KB system reserve
+constexpr int fit_warps(size_t fixed, size_t per_warp, int cap) {
+  int n = (int)((kSmemBudget - fixed) / per_warp);
+  return n < 1 ? 1 : (n > cap ? cap : n);
+}
+template <int DIM, int P> struct Cfg3 {
+  static constexpr int KW = DIM == 3 ? 3 : 4;
+  static constexpr size_t rhs_per = sizeof(dgb::Rhs3Warp<DIM, P, KW>);
+  static constexpr size_t rhs_fixed = sizeof(dgb::Rhs3Smem<DIM, P, KW, 1>) - rhs_per;
+  static constexpr int NW = fit_warps(rhs_fixed, rhs_per, DGB_RHS_WARPS);
+  static constexpr size_t grad_per = sizeof(dgb::Grad3Warp<DIM, P, KW>);
+  static constexpr size_t grad_fixed = sizeof(dgb::Grad3Smem<DIM, P, KW, 1>) - grad_per;
+  static constexpr int NWG = fit_warps(grad_fixed, grad_per, 16);
+};
+
+// DGB_VARIANT: 5 (default) = warp-autonomous; 4 = CTA-phased asynchronous pipeline; 0..3 = first
+// generation CTA-phased kernels (kept for A/B measurements, see profiles/)
 int variant() {
   static int v = -1;
-  if (v < 0) { const char* e = getenv("DGB_VARIANT"); v = e ? atoi(e) : 0; if (v < 0 || v > 3) v = 0; }
+  if (v < 0) { const char* e = getenv("DGB_VARIANT"); v = e ? atoi(e) : 5; if (v < 0 || v > 5) v = 5; }
   return v;
 }
 
@@ -163,6 +191,80 @@ int launch_rhs(const dgb_disc* d, const double* q, const double* gq, const doubl
   return DGB_OK;
 }
 
+template <int DIM, int P, bool VISCOUS>
+int launch_rhs2(const dgb_disc* d, const double* q, const double* gq, const double* ghost, const double* gghost,
+                const dgb::Epilogue& ep, const dgb::Phys& ph, cudaStream_t st) {
+  using C = Cfg2<DIM, P>;
+  auto kern = dgb::k_rhs2<DIM, P, C::K, C::NW, VISCOUS, C::MINB>;
+  const size_t smem = sizeof(dgb::Rhs2Smem<DIM, P, C::K, VISCOUS>);
+  const long long nb = (d->dev.E + C::K - 1) / C::K;
+  if (nb == 0) return DGB_OK;
+  static int grid_cache = 0; static long long nb_cache = -1;
+  if (nb_cache != nb) { int rc = persistent_grid(kern, C::NW * 32, smem, (int)nb, &grid_cache); if (rc) return rc; nb_cache = nb; }
+  kern<<<grid_cache, C::NW * 32, smem, st>>>(d->dev, q, gq, ghost, gghost, ep, ph, (int)nb);
+  DGB_CUDA(cudaGetLastError());
+  return DGB_OK;
+}
+
+template <int DIM, int P, bool VISCOUS>
+int launch_rhs3(const dgb_disc* d, const double* q, const double* gq, const double* ghost, const double* gghost,
+                const dgb::Epilogue& ep, const dgb::Phys& ph, cudaStream_t st) {
+  using C = Cfg3<DIM, P>;
+  auto kern = dgb::k_rhs3<DIM, P, C::KW, C::NW, VISCOUS>;
+  const size_t smem = sizeof(dgb::Rhs3Smem<DIM, P, C::KW, C::NW>);
+  const long long nwb = (d->dev.E + C::KW - 1) / C::KW;
+  if (nwb == 0) return DGB_OK;
+  static bool configured = false;
+  if (!configured) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured = true; }
+  const long long need = (nwb + C::NW - 1) / C::NW;
+  const int grid = (int)(need < num_sms() ? need : num_sms());
+  kern<<<grid, C::NW * 32, smem, st>>>(d->dev, q, gq, ghost, gghost, ep, ph, nwb);
+  {
+    cudaError_t e_ = cudaGetLastError();
+    if (e_ != cudaSuccess) {
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, kern);
+      return fail(DGB_ERR_CUDA, std::string("k_rhs3 launch: ") + cudaGetErrorString(e_) + " (regs=" +
+                  std::to_string(fa.numRegs) + " maxThreads=" + std::to_string(fa.maxThreadsPerBlock) + " threads=" +
+                  std::to_string(C::NW * 32) + " smem=" + std::to_string(smem) + " static=" +
+                  std::to_string(fa.sharedSizeBytes) + " local=" + std::to_string(fa.localSizeBytes) + ")");
+    }
+  }
+  return DGB_OK;
+}
+
+template <int DIM, int P>
+int launch_grad3(const dgb_disc* d, const double* q, const double* ghost, double* grad, const dgb::Phys& ph,
+                 cudaStream_t st) {
+  using C = Cfg3<DIM, P>;
+  auto kern = dgb::k_grad3<DIM, P, C::KW, C::NWG>;
+  const size_t smem = sizeof(dgb::Grad3Smem<DIM, P, C::KW, C::NWG>);
+  const long long nwb = (d->dev.E + C::KW - 1) / C::KW;
+  if (nwb == 0) return DGB_OK;
+  static bool configured = false;
+  if (!configured) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured = true; }
+  const long long need = (nwb + C::NWG - 1) / C::NWG;
+  const int grid = (int)(need < num_sms() ? need : num_sms());
+  kern<<<grid, C::NWG * 32, smem, st>>>(d->dev, q, ghost, grad, ph, nwb);
+  DGB_CUDA(cudaGetLastError());
+  return DGB_OK;
+}
+
+template <int DIM, int P>
+int launch_grad2(const dgb_disc* d, const double* q, const double* ghost, double* grad, const dgb::Phys& ph,
+                 cudaStream_t st) {
+  using C = Cfg2<DIM, P>;
+  auto kern = dgb::k_grad2<DIM, P, C::KG, C::NWG, C::MINBG>;
+  const size_t smem = sizeof(dgb::Grad2Smem<DIM, P, C::KG>);
+  const long long nb = (d->dev.E + C::KG - 1) / C::KG;
+  if (nb == 0) return DGB_OK;
+  static int grid_cache = 0; static long long nb_cache = -1;
+  if (nb_cache != nb) { int rc = persistent_grid(kern, C::NWG * 32, smem, (int)nb, &grid_cache); if (rc) return rc; nb_cache = nb; }
+  kern<<<grid_cache, C::NWG * 32, smem, st>>>(d->dev, q, ghost, grad, ph, (int)nb);
+  DGB_CUDA(cudaGetLastError());
+  return DGB_OK;
+}
+
 template <int DIM, int P, int V>
 int launch_grad(const dgb_disc* d, const double* q, const double* ghost, double* grad, const dgb::Phys& ph,
                 cudaStream_t st) {
@@ -184,6 +286,12 @@ int dispatch_rhs(const dgb_disc* d, bool viscous, const double* q, const double*
                  const double* gghost, const dgb::Epilogue& ep, const dgb::Phys& ph, cudaStream_t st) {
 #define X(DIM, P)                                                                              \
   if (d->dim == DIM && d->order == P) {                                                        \
+    if (variant() == 5)                                                                        \
+      return viscous ? launch_rhs3<DIM, P, true>(d, q, gq, ghost, gghost, ep, ph, st)          \
+                     : launch_rhs3<DIM, P, false>(d, q, gq, ghost, gghost, ep, ph, st);        \
+    if (variant() == 4)                                                                        \
+      return viscous ? launch_rhs2<DIM, P, true>(d, q, gq, ghost, gghost, ep, ph, st)          \
+                     : launch_rhs2<DIM, P, false>(d, q, gq, ghost, gghost, ep, ph, st);        \
     if (DIM == 3 && P == 3) {                                                                  \
       switch (variant()) {                                                                     \
         case 1: return viscous ? launch_rhs<3, 3, true, 1>(d, q, gq, ghost, gghost, ep, ph, st) \
@@ -207,6 +315,8 @@ int dispatch_grad(const dgb_disc* d, const double* q, const double* ghost, doubl
                   cudaStream_t st) {
 #define X(DIM, P)                                                              \
   if (d->dim == DIM && d->order == P) {                                        \
+    if (variant() == 5) return launch_grad3<DIM, P>(d, q, ghost, grad, ph, st); \
+    if (variant() == 4) return launch_grad2<DIM, P>(d, q, ghost, grad, ph, st); \
     if (DIM == 3 && P == 3) {                                                  \
       switch (variant()) {                                                     \
         case 1: return launch_grad<3, 3, 1>(d, q, ghost, grad, ph, st);        \
@@ -342,6 +452,11 @@ int dgb_disc_create(dgb_disc** out, int dim, int order, int64_t E, int64_t G, co
   if (ce != cudaSuccess) { dgb_disc_destroy(d); return fail(DGB_ERR_CUDA, cudaGetErrorString(ce)); }
   if (err_host >= 100) { dgb_disc_destroy(d); return fail(DGB_ERR_OUT_OF_BOUNDS, "face index map leaves [0, (E+G)*Np)"); }
   if (err_host) { dgb_disc_destroy(d); return fail(DGB_ERR_BAD_MAP, "face index maps are not a conforming simplex face map"); }
+  if (cudaMalloc((void**)&d->timing, sizeof(long long) * 8 * 4096) != cudaSuccess ||
+      cudaMemsetAsync(d->timing, 0, sizeof(long long) * 8 * 4096, st) != cudaSuccess) {
+    dgb_disc_destroy(d); return fail(DGB_ERR_CUDA, "timing buffer");
+  }
+  d->dev.timing = d->timing;
   d->dev.E = E; d->dev.G = G;
   d->dev.Wv = d->Wv; d->dev.Wl = d->Wl; d->dev.Wq = d->Wq; d->dev.Wf = d->Wf;
   d->dev.drdx = drdx_dev; d->dev.normals = normals_dev; d->dev.fscale = fscale_dev;
@@ -353,8 +468,18 @@ int dgb_disc_create(dgb_disc** out, int dim, int order, int64_t E, int64_t G, co
 
 int dgb_disc_destroy(dgb_disc* d) {
   if (!d) return DGB_OK;
-  cudaFree(d->Wv); cudaFree(d->Wl); cudaFree(d->Wq); cudaFree(d->Wf); cudaFree(d->conn); cudaFree(d->tables);
+  cudaFree(d->Wv); cudaFree(d->Wl); cudaFree(d->Wq); cudaFree(d->Wf); cudaFree(d->conn); cudaFree(d->tables); cudaFree(d->timing);
   delete d;
+  return DGB_OK;
+}
+
+int dgb_debug_phase_cycles(const dgb_disc* d, long long* out8_host) {
+  // sum of the per-CTA phase cycle counters (only filled by builds with -DDGB_PHASE_TIMING); resets them
+  if (!d) return fail(DGB_ERR_INVALID, "null handle");
+  std::vector<long long> h(8 * 4096);
+  DGB_CUDA(cudaMemcpy(h.data(), d->timing, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost));
+  DGB_CUDA(cudaMemset(d->timing, 0, sizeof(long long) * h.size()));
+  for (int k = 0; k < 8; ++k) { out8_host[k] = 0; for (int b = 0; b < 4096; ++b) out8_host[k] += h[b * 8 + k]; }
   return DGB_OK;
 }
 

@@ -47,7 +47,14 @@ struct ElemT {
   static constexpr int NS = DIM + NF;            // partial products per column in the gradient pass
 };
 
+#ifdef DGB_PHASE_TIMING
+#define DGB_TICK(k) do { if (tid == 0) { long long t_ = clock64(); d.timing[blockIdx.x * 8 + (k)] += t_ - tlast; tlast = t_; } } while (0)
+#else
+#define DGB_TICK(k) do { } while (0)
+#endif
+
 struct DiscDev {
+  long long* timing;     // [grid][8] per-phase cycle counters (debug builds only)
   long long E, G;
   const double* Wv;      // [NPR][LDV]
   const double* Wl;      // [NPR][LDF]
@@ -159,6 +166,41 @@ __device__ __forceinline__ void viscous_flux(const Prim<DIM>& s, const double (&
   }
 }
 
+// (Fv . n)[c] directly, without forming the 3x5 tensor: ~65 FP64 ops instead of ~135
+template <int DIM>
+__device__ __forceinline__ void viscous_normal_flux(const Prim<DIM>& s, const double (&g)[DIM][DIM + 2],
+                                                    const double (&n)[DIM], const Phys& ph,
+                                                    double (&Fn)[DIM + 2]) {
+  double gn[DIM + 2];                       // normal derivative of every conserved field
+#pragma unroll
+  for (int c = 0; c < DIM + 2; ++c) {
+    gn[c] = g[0][c] * n[0];
+#pragma unroll
+    for (int x = 1; x < DIM; ++x) gn[c] += g[x][c] * n[x];
+  }
+  double un = 0.0, div = 0.0;
+#pragma unroll
+  for (int i = 0; i < DIM; ++i) { un += s.u[i] * n[i]; div += g[i][2 + i] - s.u[i] * g[i][0]; }
+  div *= s.inv_rho;
+  double work = 0.0, udun = 0.0;
+#pragma unroll
+  for (int i = 0; i < DIM; ++i) {
+    const double dun = (gn[2 + i] - s.u[i] * gn[0]) * s.inv_rho;        // sum_x du_i/dx_x n_x
+    double dnu = -un * g[i][0];                                         // sum_x du_x/dx_i n_x
+#pragma unroll
+    for (int x = 0; x < DIM; ++x) dnu += n[x] * g[i][2 + x];
+    dnu *= s.inv_rho;
+    const double t = ph.mu * (dun + dnu) - (2.0 / 3.0) * ph.mu * div * n[i];
+    Fn[2 + i] = t;
+    work += s.u[i] * t;
+    udun += s.u[i] * dun;
+  }
+  const double etot = s.E * s.inv_rho;
+  const double den = (gn[1] - etot * gn[0]) * s.inv_rho - udun;
+  Fn[0] = 0.0;
+  Fn[1] = work + ph.kappa * (((ph.gamma - 1.0) / ph.rgas) * den);
+}
+
 // exterior state for boundary faces (operators.py:_bc_state)
 template <int DIM, bool NOSLIP>
 __device__ __forceinline__ void bc_state(int bc, const double (&qm)[DIM + 2], const double (&n)[DIM],
@@ -178,6 +220,63 @@ __device__ __forceinline__ void bc_state(int bc, const double (&qm)[DIM + 2], co
 #pragma unroll
       for (int i = 0; i < DIM; ++i) qp[2 + i] = qm[2 + i] - 2.0 * mn * n[i];
     }
+  }
+}
+
+// }}}
+
+// {{{ compute-warp barrier and the L2 prefetch helper warp
+
+template <int NT>
+__device__ __forceinline__ void compute_sync() {   // named barrier over the NT compute threads only
+  asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// Software prefetch into L2, issued by the compute threads themselves (non-blocking):
+//  * at the top of iteration b: the own rows + geometry of block b+1 (addresses are arithmetic);
+//  * the packed connectivity of block b+2 is loaded into a register at the top of iteration b and
+//    used after phase 1 to prefetch that block's face-neighbour rows, so the load never stalls.
+// The compute phases then see L2-hit latency instead of HBM latency.
+template <int DIM, int P, int K, int NPLANES>
+__device__ __forceinline__ void prefetch_own(const DiscDev& d, const double* p0, const double* p1,
+                                             long long e0, int nel, int tid, int nthreads) {
+  using EL = ElemT<DIM, P>;
+  constexpr int NP = EL::NP, NF = EL::NF;
+  const long long E = d.E;
+  const int nlines = (nel * NP * 8 + 127) / 128 + 1;
+  for (int n = tid; n < NPLANES * nlines; n += nthreads) {
+    const int pl = n / nlines, ln = n - pl * nlines;
+    const double* base = pl < EL::C ? p0 : p1;
+    const int plane = pl < EL::C ? pl : pl - EL::C;
+    prefetch_l2(reinterpret_cast<const char*>(base + ((long long)plane * E + e0) * NP) + ln * 128);
+  }
+  if (tid < DIM * DIM) prefetch_l2(d.drdx + (long long)tid * E + e0);
+  if (tid < DIM) {
+    prefetch_l2(d.normals + ((long long)tid * E + e0) * NF);
+    prefetch_l2(reinterpret_cast<const char*>(d.normals + ((long long)tid * E + e0) * NF) + 128);
+  }
+  if (tid == DIM) { prefetch_l2(d.fscale + e0 * NF); prefetch_l2(d.conn + e0 * NF); }
+}
+
+template <int DIM, int P, int NPLANES>
+__device__ __forceinline__ void prefetch_nbr(const DiscDev& d, const double* p0, const double* p1,
+                                             long long cn, long long e0, int nel) {
+  using EL = ElemT<DIM, P>;
+  constexpr int NP = EL::NP;
+  const long long E = d.E;
+  const long long nb = DGB_CONN_NB(cn);
+  if (DGB_CONN_BC(cn) != 0 || nb >= E || (nb >= e0 && nb < e0 + nel)) return;
+#pragma unroll 4
+  for (int pl = 0; pl < NPLANES; ++pl) {
+    const double* base = pl < EL::C ? p0 : p1;
+    const int plane = pl < EL::C ? pl : pl - EL::C;
+    const char* a = reinterpret_cast<const char*>(base + ((long long)plane * E + nb) * NP);
+    prefetch_l2(a);
+    prefetch_l2(a + NP * 8 - 8);
   }
 }
 
@@ -301,13 +400,17 @@ k_rhs(DiscDev d, const double* __restrict__ q, const double* __restrict__ gq,
   for (int n = tid; n < C * K * EL::LDF; n += NT) S.Fs[n] = 0.0;
   for (int n = tid; n < NF * NFP; n += NT) S.fn[n] = d.tables[n];
   for (int n = tid; n < EL::NPERM * NFP; n += NT) S.perm[n] = d.tables[NF * NFP + n];
-  __syncthreads();   // the zero fill above must not race with the first block's staging writes
+  compute_sync<NT>();   // the zero fill above must not race with the first block's staging writes
 
+#ifdef DGB_PHASE_TIMING
+  long long tlast = clock64();
+#endif
   for (int blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
     const long long e0 = (long long)blk * K;
     const int nel = (int)((E - e0) < (long long)K ? (E - e0) : (long long)K);
     stage_geo<DIM, P, K>(S.geo, d, e0, nel, tid, NT);
-    __syncthreads();
+    compute_sync<NT>();
+    DGB_TICK(0);
 
     // ---- phase 1: volume flux ------------------------------------------------------------
     for (int n = tid; n < nel * NP; n += NT) {
@@ -346,7 +449,8 @@ k_rhs(DiscDev d, const double* __restrict__ q, const double* __restrict__ gq,
       }
       S.Lam[n] = wavespeed<DIM>(s, ph.gamma);
     }
-    __syncthreads();
+    compute_sync<NT>();
+    DGB_TICK(1);
 
     // ---- phase 2: face gather + numerical flux --------------------------------------------
     // Own side: the scaled normal flux fscale*(F.n)^- needs no recomputation.  On an affine simplex
@@ -391,15 +495,10 @@ k_rhs(DiscDev d, const double* __restrict__ q, const double* __restrict__ gq,
       inviscid_normal_flux<DIM>(sp_, nrm, fnp);
       const double lam = fmax(S.Lam[e * NP + jm], wavespeed<DIM>(sp_, ph.gamma));
       if (VISCOUS) {
-        double Fvp[DIM][C];
-        viscous_flux<DIM>(sp_, gp, ph, Fvp);
+        double fvn[C];
+        viscous_normal_flux<DIM>(sp_, gp, nrm, ph, fvn);
 #pragma unroll
-        for (int c = 1; c < C; ++c) {
-          double vn = 0.0;
-#pragma unroll
-          for (int x = 0; x < DIM; ++x) vn += Fvp[x][c] * nrm[x];
-          fnp[c] -= vn;
-        }
+        for (int c = 1; c < C; ++c) fnp[c] -= fvn[c];
       }
 #pragma unroll
       for (int c = 0; c < C; ++c) {
@@ -415,7 +514,8 @@ k_rhs(DiscDev d, const double* __restrict__ q, const double* __restrict__ gq,
         S.Fs[(c * K + e) * EL::LDF + fm] = -0.5 * (own + fs * (fnp[c] + lam * (qm[c] - qp[c])));
       }
     }
-    __syncthreads();
+    compute_sync<NT>();
+    DGB_TICK(2);
 
     // ---- phase 3: tensor-core contraction + (RK-fused) store -------------------------------
     constexpr int NTILES = C * K / 8;
@@ -445,7 +545,8 @@ k_rhs(DiscDev d, const double* __restrict__ q, const double* __restrict__ gq,
         }
       }
     }
-    __syncthreads();
+    compute_sync<NT>();
+    DGB_TICK(3);
   }
 }
 
@@ -485,8 +586,11 @@ k_grad(DiscDev d, const double* __restrict__ q, const double* __restrict__ ghost
   for (int n = tid; n < C * K * EL::LDS; n += NT) S.Ss[n] = 0.0;
   for (int n = tid; n < NF * NFP; n += NT) S.fn[n] = d.tables[n];
   for (int n = tid; n < EL::NPERM * NFP; n += NT) S.perm[n] = d.tables[NF * NFP + n];
-  __syncthreads();   // the zero fill above must not race with the first block's staging writes
+  compute_sync<NT>();   // the zero fill above must not race with the first block's staging writes
 
+#ifdef DGB_PHASE_TIMING
+  long long tlast = clock64();
+#endif
   for (int blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
     const long long e0 = (long long)blk * K;
     const int nel = (int)((E - e0) < (long long)K ? (E - e0) : (long long)K);
@@ -497,7 +601,8 @@ k_grad(DiscDev d, const double* __restrict__ q, const double* __restrict__ ghost
       const int e = ej / NP, j = ej - e * NP;
       S.Qs[(c * K + e) * EL::LDQ + j] = q[((long long)c * E + e0) * NP + ej];
     }
-    __syncthreads();
+    compute_sync<NT>();
+    DGB_TICK(4);
 
     // combination coefficients per element
     for (int n = tid; n < nel * DIM * EL::NS; n += NT) {
@@ -532,7 +637,8 @@ k_grad(DiscDev d, const double* __restrict__ q, const double* __restrict__ ghost
 #pragma unroll
       for (int c = 0; c < C; ++c) S.Ss[(c * K + e) * EL::LDS + f * EL::NFPK + m] = 0.5 * (qm[c] + qp[c]);
     }
-    __syncthreads();
+    compute_sync<NT>();
+    DGB_TICK(5);
 
     constexpr int NTILES = C * K / 8;
     for (int tile = warp; tile < NTILES; tile += NW) {
@@ -580,7 +686,8 @@ k_grad(DiscDev d, const double* __restrict__ q, const double* __restrict__ ghost
         }
       }
     }
-    __syncthreads();
+    compute_sync<NT>();
+    DGB_TICK(6);
   }
 }
 
