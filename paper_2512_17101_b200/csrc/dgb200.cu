@@ -139,6 +139,9 @@ template <> struct Cfg2<3, 4> { static constexpr int K = 8, NW = 8, MINB = 1, KG
 
 // launch configuration of the warp-autonomous kernels (dgb_kernels_warp.cuh), the default path:
 // KW elements per warp (C*KW columns padded to whole 8-column tiles), as many warps per SM as fit
+#ifndef DGB_GRAD_WARPS
+#define DGB_GRAD_WARPS 16
+#endif
 #ifndef DGB_RHS_WARPS
 #define DGB_RHS_WARPS 12
 #endif
@@ -154,7 +157,7 @@ template <int DIM, int P> struct Cfg3 {
   static constexpr int NW = fit_warps(rhs_fixed, rhs_per, DGB_RHS_WARPS);
   static constexpr size_t grad_per = sizeof(dgb::Grad3Warp<DIM, P, KW>);
   static constexpr size_t grad_fixed = sizeof(dgb::Grad3Smem<DIM, P, KW, 1>) - grad_per;
-  static constexpr int NWG = fit_warps(grad_fixed, grad_per, 16);
+  static constexpr int NWG = fit_warps(grad_fixed, grad_per, DGB_GRAD_WARPS);
 };
 
 // DGB_VARIANT: 5 (default) = warp-autonomous; 4 = CTA-phased asynchronous pipeline; 0..3 = first
