@@ -1,0 +1,107 @@
+"""The N>1 path on CPU: world_size-2 `gloo` process groups run the partition-aware right-hand side
+(halo pack -> batched isend/irecv -> ghost arrays) with the oracle context and must reproduce the
+single-domain result."""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, mode, outq):
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.laze_port import NumpyArrayContext
+        from paper_2512_17101_b200 import DGDiscretization, EulerOperator, NavierStokesOperator, box_mesh
+        from paper_2512_17101_b200.dg.partition import partition_elements, rank_mesh, ring_slab
+        from paper_2512_17101_b200.halo import HaloExchange, TorchCommunicator
+        from tests.common import random_state
+        actx = NumpyArrayContext()
+        comm = TorchCommunicator()
+        base = box_mesh((3,) * 3, (-1,) * 3, (1,) * 3, periodic=(True,) * 3)
+        if mode == "partition":
+            part = partition_elements(base, world)
+            local, plan = rank_mesh(base, part, rank)
+            q0 = random_state(3, base.nelements, 10, seed=9)[:, plan.global_ids, :]
+        else:
+            local, plan = ring_slab(base, 3, rank, world, -1.0, 1.0)
+            q0 = random_state(3, base.nelements, 10, seed=9 + rank)
+        d = DGDiscretization(actx, local, 2, ghost_elements=plan.nghost)
+        halo = HaloExchange(actx, plan, comm, d.Np)
+        e = d.to_numpy(halo.euler_rhs(EulerOperator(d), d.from_numpy(q0)))
+        v = d.to_numpy(halo.ns_rhs(NavierStokesOperator(d, mu=2e-2), d.from_numpy(q0)))
+        outq.put((rank, plan.global_ids, e, v, halo.messages_per_exchange, halo.bytes_per_exchange))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(mode):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, mode, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=180) for _ in procs], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return res
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_partition_matches_single_domain():
+    sys.path.insert(0, ROOT)
+    from oracle.laze_port import NumpyArrayContext, rel_err
+    from paper_2512_17101_b200 import DGDiscretization, EulerOperator, NavierStokesOperator, box_mesh
+    from tests.common import random_state
+    res = _run("partition")
+    actx = NumpyArrayContext()
+    mesh = box_mesh((3,) * 3, (-1,) * 3, (1,) * 3, periodic=(True,) * 3)
+    d = DGDiscretization(actx, mesh, 2)
+    q0 = random_state(3, mesh.nelements, 10, seed=9)
+    ref_e = d.to_numpy(EulerOperator(d).rhs(d.from_numpy(q0)))
+    ref_v = d.to_numpy(NavierStokesOperator(d, mu=2e-2).rhs(d.from_numpy(q0)))
+    full_e, full_v = np.empty_like(ref_e), np.empty_like(ref_v)
+    for rank, ids, e, v, nmsg, nbytes in res:
+        full_e[:, ids, :], full_v[:, ids, :] = e, v
+        assert nmsg == 1 and nbytes > 0
+    assert rel_err(full_e, ref_e) <= 1e-13 and rel_err(full_v, ref_v) <= 1e-13
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_ring_matches_double_box():
+    """Two periodic boxes wired as a ring (bench.py's weak-scaling layout) == one 6x3x3 periodic box."""
+    sys.path.insert(0, ROOT)
+    from oracle.laze_port import NumpyArrayContext, rel_err
+    from paper_2512_17101_b200 import DGDiscretization, NavierStokesOperator, box_mesh
+    from tests.common import random_state
+    res = _run("ring")
+    actx = NumpyArrayContext()
+    glob = box_mesh((6, 3, 3), (-1, -1, -1), (3, 1, 1), periodic=(True,) * 3)
+    base = box_mesh((3,) * 3, (-1,) * 3, (1,) * 3, periodic=(True,) * 3)
+    d = DGDiscretization(actx, glob, 2)
+    gkey = {tuple(np.round(c, 9)): e for e, c in enumerate(glob.vertices.mean(axis=1))}
+    q0 = np.empty((5, glob.nelements, 10))
+    idx = []
+    for r in range(2):
+        cent = base.vertices.mean(axis=1) + np.array([2.0 * r, 0, 0])
+        idx.append(np.array([gkey[tuple(np.round(c, 9))] for c in cent]))
+        q0[:, idx[r], :] = random_state(3, base.nelements, 10, seed=9 + r)
+    ref = d.to_numpy(NavierStokesOperator(d, mu=2e-2).rhs(d.from_numpy(q0)))
+    for rank, _, e, v, nmsg, nbytes in res:
+        assert nmsg == 2
+        assert rel_err(v, ref[:, idx[rank], :]) <= 1e-12
