@@ -9,7 +9,7 @@ Public surface:
 """
 from .dofarray import DOFArray
 from .discretization import BC_FARFIELD, BC_NONE, BC_WALL, DGDiscretization
-from .operators import EulerOperator, NavierStokesOperator, rk4_step
+from .operators import EulerOperator, NavierStokesOperator, rk4_step, rk4_step_fused
 from .dg.mesh import box_mesh
 from . import errors
 

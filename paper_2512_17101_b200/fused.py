@@ -170,4 +170,39 @@ def dg_ns_rhs(actx, f, *args):
     return out
 
 
-FUSED = {"dg_euler_rhs": dg_euler_rhs, "dg_ns_grad": dg_ns_grad, "dg_ns_rhs": dg_ns_rhs}
+def _rk_common(actx, q, x1, x2, coef):
+    x1 = _f64(actx, x1, "x1")
+    x2 = _f64(actx, x2, "x2")
+    if x1.shape != q.shape or x2.shape != q.shape:
+        raise errors.BindingMismatch("RK operands must have the shape of the state")
+    rk = _host_vec(coef, 4)
+    return x1, x2, rk, actx.empty(q.shape), actx.empty(q.shape)
+
+
+def dg_euler_rhs_rk(actx, f, q, x1, x2, coef, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, phys):
+    dim = f.dg_dim
+    q = _f64(actx, q, "q")
+    disc = get_disc(actx, dim, q, 0, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind)
+    qf, ph = _host_vec(qfar, dim + 2), _host_vec(phys, 4)
+    x1, x2, rk, o1, o2 = _rk_common(actx, q, x1, x2, coef)
+    _cabi.check(actx.lib.dgb_euler_rhs_rk(disc.handle, q.ptr, None, x1.ptr, o1.ptr, x2.ptr, o2.ptr, rk.ctypes.data,
+                                          qf.ctypes.data, ph.ctypes.data, actx._st), "dg_euler_rhs_rk")
+    actx.launch_count += 1
+    return {"out1": o1, "out2": o2}
+
+
+def dg_ns_rhs_rk(actx, f, q, gq, x1, x2, coef, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, phys):
+    dim = f.dg_dim
+    q = _f64(actx, q, "q")
+    gq = _f64(actx, gq, "grad q")
+    disc = get_disc(actx, dim, q, 0, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind)
+    qf, ph = _host_vec(qfar, dim + 2), _host_vec(phys, 4)
+    x1, x2, rk, o1, o2 = _rk_common(actx, q, x1, x2, coef)
+    _cabi.check(actx.lib.dgb_ns_rhs_rk(disc.handle, q.ptr, gq.ptr, None, None, x1.ptr, o1.ptr, x2.ptr, o2.ptr,
+                                       rk.ctypes.data, qf.ctypes.data, ph.ctypes.data, actx._st), "dg_ns_rhs_rk")
+    actx.launch_count += 1
+    return {"out1": o1, "out2": o2}
+
+
+FUSED = {"dg_euler_rhs": dg_euler_rhs, "dg_ns_grad": dg_ns_grad, "dg_ns_rhs": dg_ns_rhs,
+         "dg_euler_rhs_rk": dg_euler_rhs_rk, "dg_ns_rhs_rk": dg_ns_rhs_rk}

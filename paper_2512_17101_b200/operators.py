@@ -283,6 +283,32 @@ def _make_ns_rhs(dim, with_ghost):
                         vmap_p, bc_kind, qfar, phys)
     return dg_ns_rhs
 
+
+def _axpby_outputs(rhs, x1, x2, coef):
+    """RK stage update fused behind the right-hand side (north-star item 3):
+    ``out1 = a1*x1 + b1*rhs``, ``out2 = a2*x2 + b2*rhs`` with ``coef = [a1, b1, a2, b2]``."""
+    return {"out1": coef[0] * x1 + coef[1] * rhs, "out2": coef[2] * x2 + coef[3] * rhs}
+
+
+def _make_euler_rhs_rk(dim, with_ghost):
+    inner = _make_euler_rhs(dim, False)
+
+    def dg_euler_rhs_rk(q, x1, x2, coef, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, phys):
+        inner.actx = dg_euler_rhs_rk.actx
+        rhs = inner(q, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, phys)
+        return _axpby_outputs(rhs, x1, x2, coef)
+    return dg_euler_rhs_rk
+
+
+def _make_ns_rhs_rk(dim, with_ghost):
+    inner = _make_ns_rhs(dim, False)
+
+    def dg_ns_rhs_rk(q, gq, x1, x2, coef, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, phys):
+        inner.actx = dg_ns_rhs_rk.actx
+        rhs = inner(q, gq, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, phys)
+        return _axpby_outputs(rhs, x1, x2, coef)
+    return dg_ns_rhs_rk
+
 # }}}
 
 
@@ -330,6 +356,14 @@ class EulerOperator(_OperatorBase):
             out = self._fg(q.data, ghost, *self._common(), self.phys)
         return DOFArray(self.actx, out)
 
+    def rhs_rk(self, q: DOFArray, x1: DOFArray, x2: DOFArray, coef, t=0.0):
+        """``(a1*x1 + b1*rhs(q), a2*x2 + b2*rhs(q))`` in one fused pass; ``coef = (a1, b1, a2, b2)``."""
+        if not hasattr(self, "_frk"):
+            self._frk = self._outlined(_make_euler_rhs_rk, False)
+        c = self.actx.from_numpy(np.asarray(coef, dtype=np.float64))
+        out = self._frk(q.data, x1.data, x2.data, c, *self._common(), self.phys)
+        return DOFArray(self.actx, out["out1"]), DOFArray(self.actx, out["out2"])
+
 
 class NavierStokesOperator(_OperatorBase):
     """Two-pass (BR1) compressible Navier-Stokes right-hand side."""
@@ -357,6 +391,15 @@ class NavierStokesOperator(_OperatorBase):
             out = self._fg(q.data, gq.data, ghost, gghost, *self._common(), self.phys)
         return DOFArray(self.actx, out)
 
+    def rhs_rk(self, q: DOFArray, x1: DOFArray, x2: DOFArray, coef, t=0.0):
+        """``(a1*x1 + b1*rhs(q), a2*x2 + b2*rhs(q))`` with the stage update fused into the second pass."""
+        if not hasattr(self, "_frk"):
+            self._frk = self._outlined(_make_ns_rhs_rk, False)
+        gq = self.grad(q)
+        c = self.actx.from_numpy(np.asarray(coef, dtype=np.float64))
+        out = self._frk(q.data, gq.data, x1.data, x2.data, c, *self._common(), self.phys)
+        return DOFArray(self.actx, out["out1"]), DOFArray(self.actx, out["out2"])
+
 
 # {{{ time stepping
 
@@ -368,5 +411,17 @@ def rk4_step(rhs, q, t, dt):
     k3 = rhs(q + (0.5 * dt) * k2, t + 0.5 * dt)
     k4 = rhs(q + dt * k3, t + dt)
     return q + (dt / 6.0) * (k1 + 2.0 * k2 + 2.0 * k3 + k4)
+
+
+def rk4_step_fused(op, q, t, dt):
+    """Classical RK4 with every stage update fused into the right-hand-side pass
+    (``op.rhs_rk``): per stage one read of the stage state and of the two update operands and one
+    write of each output, instead of separate axpy sweeps.  Same scheme as ``rk4_step``; the final
+    combination is accumulated stage by stage."""
+    q1, acc = op.rhs_rk(q, q, q, (1.0, 0.5 * dt, 1.0, dt / 6.0), t)
+    q2, acc = op.rhs_rk(q1, q, acc, (1.0, 0.5 * dt, 1.0, dt / 3.0), t + 0.5 * dt)
+    q3, acc = op.rhs_rk(q2, q, acc, (1.0, dt, 1.0, dt / 3.0), t + 0.5 * dt)
+    qn, _ = op.rhs_rk(q3, acc, acc, (1.0, dt / 6.0, 0.0, 0.0), t + dt)
+    return qn
 
 # }}}

@@ -11,7 +11,7 @@ import pytest
 from oracle.laze_port import NumpyArrayContext, OutOfBoundsIndex, checked_take, rel_err
 from paper_2512_17101_b200.operators import EulerOperator, NavierStokesOperator, rk4_step
 from tests.common import FARFIELD, make_dcoll
-from tests.golden.make_golden import CASES
+from tests.common import GOLDEN_CASES as CASES
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 
