@@ -37,6 +37,7 @@ struct dgb_disc {
   double *Wv = nullptr, *Wl = nullptr, *Wq = nullptr, *Wf = nullptr;
   long long* conn = nullptr;
   long long* timing = nullptr;
+  unsigned long long* counters = nullptr;   // [0] gradient pass, [1] flux/divergence pass work counters
   int* tables = nullptr;
   const int64_t* bc_kind = nullptr;
 };
@@ -221,7 +222,8 @@ int launch_rhs3(const dgb_disc* d, const double* q, const double* gq, const doub
   if (!configured) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured = true; }
   const long long need = (nwb + C::NW - 1) / C::NW;
   const int grid = (int)(need < num_sms() ? need : num_sms());
-  kern<<<grid, C::NW * 32, smem, st>>>(d->dev, q, gq, ghost, gghost, ep, ph, nwb);
+  DGB_CUDA(cudaMemsetAsync(d->counters + 1, 0, sizeof(unsigned long long), st));
+  kern<<<grid, C::NW * 32, smem, st>>>(d->dev, q, gq, ghost, gghost, ep, ph, nwb, d->counters + 1);
   {
     cudaError_t e_ = cudaGetLastError();
     if (e_ != cudaSuccess) {
@@ -248,7 +250,8 @@ int launch_grad3(const dgb_disc* d, const double* q, const double* ghost, double
   if (!configured) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured = true; }
   const long long need = (nwb + C::NWG - 1) / C::NWG;
   const int grid = (int)(need < num_sms() ? need : num_sms());
-  kern<<<grid, C::NWG * 32, smem, st>>>(d->dev, q, ghost, grad, ph, nwb);
+  DGB_CUDA(cudaMemsetAsync(d->counters, 0, sizeof(unsigned long long), st));
+  kern<<<grid, C::NWG * 32, smem, st>>>(d->dev, q, ghost, grad, ph, nwb, d->counters);
   DGB_CUDA(cudaGetLastError());
   return DGB_OK;
 }
@@ -460,6 +463,9 @@ int dgb_disc_create(dgb_disc** out, int dim, int order, int64_t E, int64_t G, co
     dgb_disc_destroy(d); return fail(DGB_ERR_CUDA, "timing buffer");
   }
   d->dev.timing = d->timing;
+  if (cudaMalloc((void**)&d->counters, 2 * sizeof(unsigned long long)) != cudaSuccess) {
+    dgb_disc_destroy(d); return fail(DGB_ERR_CUDA, "work counters");
+  }
   d->dev.E = E; d->dev.G = G;
   d->dev.Wv = d->Wv; d->dev.Wl = d->Wl; d->dev.Wq = d->Wq; d->dev.Wf = d->Wf;
   d->dev.drdx = drdx_dev; d->dev.normals = normals_dev; d->dev.fscale = fscale_dev;
@@ -471,7 +477,7 @@ int dgb_disc_create(dgb_disc** out, int dim, int order, int64_t E, int64_t G, co
 
 int dgb_disc_destroy(dgb_disc* d) {
   if (!d) return DGB_OK;
-  cudaFree(d->Wv); cudaFree(d->Wl); cudaFree(d->Wq); cudaFree(d->Wf); cudaFree(d->conn); cudaFree(d->tables); cudaFree(d->timing);
+  cudaFree(d->Wv); cudaFree(d->Wl); cudaFree(d->Wq); cudaFree(d->Wf); cudaFree(d->conn); cudaFree(d->tables); cudaFree(d->timing); cudaFree(d->counters);
   delete d;
   return DGB_OK;
 }
