@@ -13,6 +13,7 @@
 // padded column's operand row stays zero and its results are never stored.
 #pragma once
 #include "dgb_kernels.cuh"
+#include "dgb_kernels_async.cuh"
 
 namespace dgb {
 
@@ -312,11 +313,36 @@ struct Grad3Warp {
   static constexpr int NCOL = EL::C * KW;
   static constexpr int NTILE = (NCOL + 7) / 8;
   static constexpr int NCOLP = NTILE * 8;
-  double Qs[NCOLP * EL::LDQ];
+  double Qs[2][NCOLP * EL::LDQ];     // own rows, double-buffered: the next block arrives by cp.async
   double Ss[NCOLP * EL::LDS];
   double coef[KW][DIM][EL::NS];
-  WarpGeo<DIM, P, KW> geo;
+  WarpGeo<DIM, P, KW> geo[2];
 };
+
+template <int DIM, int P, int KW>
+__device__ __forceinline__ void warp_stage_async(double* Qs, WarpGeo<DIM, P, KW>& g, const DiscDev& d, const double* q,
+                                                 long long e0, int nel, int lane) {
+  using EL = ElemT<DIM, P>;
+  constexpr int C = EL::C, NP = EL::NP, NF = EL::NF;
+  const long long E = d.E;
+  for (int n = lane; n < C * nel * NP; n += 32) {
+    const int c = n / (nel * NP), ej = n - c * (nel * NP);
+    const int e = ej / NP, j = ej - e * NP;
+    cp_async8(Qs + (c * KW + e) * EL::LDQ + j, q + ((long long)c * E + e0) * NP + ej);
+  }
+  for (int n = lane; n < DIM * DIM * KW; n += 32) {
+    const int rx = n / KW, e = n - rx * KW;
+    if (e < nel) cp_async8(&g.drdx[rx][e], d.drdx + (long long)rx * E + e0 + e);
+  }
+  for (int n = lane; n < DIM * KW * NF; n += 32) {
+    const int x = n / (KW * NF), ef = n - x * (KW * NF);
+    if (ef < nel * NF) cp_async8(&g.nrm[x][0][ef], d.normals + ((long long)x * E + e0) * NF + ef);
+  }
+  for (int n = lane; n < nel * NF; n += 32) {
+    cp_async8(&g.fsc[0][n], d.fscale + e0 * NF + n);
+    cp_async8(&g.conn[0][n], d.conn + e0 * NF + n);
+  }
+}
 
 template <int DIM, int P, int KW, int NWARPS>
 struct Grad3Smem {
@@ -346,31 +372,44 @@ k_grad3(DiscDev d, const double* __restrict__ q, const double* __restrict__ ghos
   for (int n = tid; n < NF * NFP; n += NT) S.fn[n] = d.tables[n];
   for (int n = tid; n < EL::NPERM * NFP; n += NT) S.perm[n] = d.tables[NF * NFP + n];
   WS& W = S.w[warp];
-  for (int n = lane; n < WS::NCOLP * EL::LDQ; n += 32) W.Qs[n] = 0.0;
+  for (int n = lane; n < 2 * WS::NCOLP * EL::LDQ; n += 32) W.Qs[0][n] = 0.0;
   for (int n = lane; n < WS::NCOLP * EL::LDS; n += 32) W.Ss[n] = 0.0;
   __syncthreads();
 
   const long long wstride = (long long)gridDim.x * NWARPS;
-  for (long long wb = (long long)blockIdx.x * NWARPS + warp; wb < nwblocks; wb = next_block(counter, wstride, lane)) {
+  long long wb = (long long)blockIdx.x * NWARPS + warp;
+  int buf = 0;
+  if (wb < nwblocks) {
+    const long long e0 = wb * KW;
+    warp_stage_async<DIM, P, KW>(W.Qs[0], W.geo[0], d, q, e0, (int)((E - e0) < (long long)KW ? (E - e0) : (long long)KW), lane);
+  }
+  cp_async_commit();
+
+  while (wb < nwblocks) {
     const long long e0 = wb * KW;
     const int nel = (int)((E - e0) < (long long)KW ? (E - e0) : (long long)KW);
-    warp_stage_geo<DIM, P, KW>(W.geo, d, e0, nel, lane);
-    for (int n = lane; n < C * nel * NP; n += 32) {
-      const int c = n / (nel * NP), ej = n - c * (nel * NP);
-      const int e = ej / NP, j = ej - e * NP;
-      W.Qs[(c * KW + e) * EL::LDQ + j] = q[((long long)c * E + e0) * NP + ej];
+    cp_async_wait<0>();
+    __syncwarp();                        // this block's rows + geometry have landed (all lanes' copies)
+    const double* Qs = W.Qs[buf];
+    const WarpGeo<DIM, P, KW>& geo = W.geo[buf];
+    // take the next block and start its copies; they land while this block computes
+    const long long wb_next = next_block(counter, wstride, lane);
+    if (wb_next < nwblocks) {
+      const long long e1 = wb_next * KW;
+      warp_stage_async<DIM, P, KW>(W.Qs[buf ^ 1], W.geo[buf ^ 1], d, q, e1,
+                                   (int)((E - e1) < (long long)KW ? (E - e1) : (long long)KW), lane);
     }
-    __syncwarp();
+    cp_async_commit();
 
     for (int n = lane; n < nel * DIM * EL::NS; n += 32) {
       const int e = n / (DIM * EL::NS), xs = n - e * (DIM * EL::NS);
       const int x = xs / EL::NS, s = xs - x * EL::NS;
-      W.coef[e][x][s] = s < DIM ? -W.geo.drdx[s * DIM + x][e] : W.geo.fsc[e][s - DIM] * W.geo.nrm[x][e][s - DIM];
+      W.coef[e][x][s] = s < DIM ? -geo.drdx[s * DIM + x][e] : geo.fsc[e][s - DIM] * geo.nrm[x][e][s - DIM];
     }
     for (int n = lane; n < nel * NFT; n += 32) {
       const int e = n / NFT, fm = n - e * NFT;
       const int f = fm / NFP, m = fm - f * NFP;
-      const long long cn = W.geo.conn[e][f];
+      const long long cn = geo.conn[e][f];
       const long long nb = DGB_CONN_NB(cn);
       const int nf = DGB_CONN_NF(cn), pid = DGB_CONN_PERM(cn), bc = DGB_CONN_BC(cn);
       const int jm = S.fn[f * NFP + m];
@@ -382,12 +421,12 @@ k_grad3(DiscDev d, const double* __restrict__ q, const double* __restrict__ ghos
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         qp[c] = pbase[(long long)c * pE * NP];
-        qm[c] = W.Qs[(c * KW + e) * EL::LDQ + jm];
+        qm[c] = Qs[(c * KW + e) * EL::LDQ + jm];
       }
       if (bc != 0) {
         double nrm[DIM];
 #pragma unroll
-        for (int x = 0; x < DIM; ++x) nrm[x] = W.geo.nrm[x][e][f];
+        for (int x = 0; x < DIM; ++x) nrm[x] = geo.nrm[x][e][f];
         bc_state<DIM, true>(bc, qm, nrm, ph, qp);
       }
 #pragma unroll
@@ -408,7 +447,7 @@ k_grad3(DiscDev d, const double* __restrict__ q, const double* __restrict__ ghos
         for (int ni = 0; ni < NI; ++ni) { accU[s][0][ni][0] = 0.0; accU[s][0][ni][1] = 0.0; }
 #pragma unroll
       for (int r = 0; r < DIM; ++r)
-        mma_block<NI, 1>(accT[r], W.Qs + tile * 8 * EL::LDQ, EL::LDQ, S.Wq + r * EL::NPR * EL::LDQ, EL::LDQ,
+        mma_block<NI, 1>(accT[r], Qs + tile * 8 * EL::LDQ, EL::LDQ, S.Wq + r * EL::NPR * EL::LDQ, EL::LDQ,
                          EL::NPK / 4, lane);
 #pragma unroll
       for (int f = 0; f < NF; ++f)
@@ -442,7 +481,10 @@ k_grad3(DiscDev d, const double* __restrict__ q, const double* __restrict__ ghos
       }
       __syncwarp();
     }
+    wb = wb_next;
+    buf ^= 1;
   }
+  cp_async_wait<0>();
 }
 
 }  // namespace dgb
