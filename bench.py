@@ -256,11 +256,19 @@ def run_b200(args):
     if halo is None:
         ms_grad = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
         ms_div = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
-        dom = ("k_rhs<viscous> (flux + divergence pass)", ms_div, B_ALG_DIV) if ms_div >= ms_grad else \
-              ("k_grad (BR1 gradient pass)", ms_grad, B_ALG_GRAD)
+        dom = ("k_rhs3<viscous> (flux + divergence pass)", ms_div, B_ALG_DIV) if ms_div >= ms_grad else \
+              ("k_grad3 (BR1 gradient pass)", ms_grad, B_ALG_GRAD)
         achieved = ndof * dom[2] / (dom[1] * 1e-3) / 1e9
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
+        if os.path.exists(tpath):
+            with open(tpath) as fh:
+                tj = json.load(fh)
+            if tj.get("n") == n:      # ncu capture of exactly this workload (bytes per launch)
+                key = "k_rhs3_viscous" if ms_div >= ms_grad else "k_grad3"
+                traffic = tj[key]["dram_read_bytes"] + tj[key]["dram_write_bytes"]
         roofline = {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                    "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                     "algorithmic_bytes_per_dof": dom[2], "ms_per_launch": dom[1],
                     "ms_grad_pass": ms_grad, "ms_div_pass": ms_div}
     rhs_gbs = ndof * B_ALG_RHS / (ms_step * 1e-3) / 1e9
