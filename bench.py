@@ -29,6 +29,16 @@ B_ALG_RHS = 360.0      # algorithmic bytes per node-DOF per NS RHS: (3C + 2Cd) *
 B_ALG_GRAD = 160.0     # pass 1: read q (40) + write grad q (120)
 B_ALG_DIV = 200.0      # pass 2: read q (40) + read grad q (120) + write rhs (40)
 PHYS = dict(gamma=1.4, mu=1e-3, prandtl=0.72, rgas=1.0)
+CPU_REPS = 16          # RHS evaluations per process in one CPU sample (~10-15 s of CPU work)
+
+
+def workload_name(n, workload="ns"):
+    E = 6 * n ** 3
+    if workload == "euler":
+        return (f"3D compressible Euler DG RHS, Kuhn tets order {ORDER}, periodic {n}^3 box per GPU: {E} elements, "
+                f"{E * NP} DOFs per GPU (BASELINE configs[1])")
+    return (f"3D compressible Navier-Stokes DG RHS (BR1, two derivative passes), Kuhn tets order {ORDER}, periodic "
+            f"{n}^3 box per GPU: {E} elements, {E * NP} DOFs per GPU (BASELINE configs[2])")
 
 
 def measured_peaks():
@@ -144,7 +154,7 @@ def run_reference(args):
         return
     cores = os.cpu_count() or 1
     n, reps = args.cpu_n, 1
-    for _ in range(args.warmup):
+    for _ in range(min(args.warmup, 1)):
         cpu_throughput(cores, n, reps)
     t0 = time.perf_counter()
     dofs = 0
@@ -162,8 +172,7 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * busy / max(args.steps, 1), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "3D compressible Navier-Stokes DG RHS, tets order 3 (two derivative passes); "
-                               "bounded CPU sample of BASELINE configs[2]", "sample": sample},
+        "config": {"workload": workload_name(args.n), "sample": sample},
         "cpu_baseline": {"value": value, "unit": "GDOF/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": wall,
@@ -199,7 +208,12 @@ def run_b200(args):
         from paper_2512_17101_b200.halo import ring_slab_halo
         mesh, halo = ring_slab_halo(actx, mesh, n, rank, world, ORDER)
     d = DGDiscretization(actx, mesh, ORDER, ghost_elements=0 if halo is None else halo.nghost)
-    op = NavierStokesOperator(d, **PHYS)
+    euler = args.workload == "euler"
+    if euler:
+        from paper_2512_17101_b200 import EulerOperator
+        op = EulerOperator(d, gamma=PHYS["gamma"])
+    else:
+        op = NavierStokesOperator(d, **PHYS)
     E, Np = d.nelements, d.Np
     ndof = E * Np
     q_host = actx.pinned_empty((DIM + 2, E, Np))
@@ -212,7 +226,7 @@ def run_b200(args):
     def rhs_step(qarr):
         if halo is None:
             return op.rhs(qarr)
-        return halo.ns_rhs(op, qarr)
+        return halo.euler_rhs(op, qarr) if euler else halo.ns_rhs(op, qarr)
 
     # ---- device-resident measurement --------------------------------------------------------
     stream = actx.stream
@@ -229,11 +243,16 @@ def run_b200(args):
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record(stream)
     for k in range(K):
-        if halo is None:
+        if halo is None and not euler:
             ev[k][0].record(stream)
             gq = op.grad(q)
             ev[k][1].record(stream)
             op._f(q.data, gq.data, *op._common(), op.phys)
+            ev[k][2].record(stream)
+        elif halo is None:
+            ev[k][0].record(stream)
+            ev[k][1].record(stream)
+            op.rhs(q)
             ev[k][2].record(stream)
         else:
             rhs_step(q)
@@ -256,22 +275,26 @@ def run_b200(args):
     if halo is None:
         ms_grad = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
         ms_div = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
-        dom = ("k_rhs3<viscous> (flux + divergence pass)", ms_div, B_ALG_DIV) if ms_div >= ms_grad else \
-              ("k_grad3 (BR1 gradient pass)", ms_grad, B_ALG_GRAD)
+        if euler:
+            dom = ("k_rhs3<inviscid> (fused Euler RHS)", ms_div, 80.0)
+        else:
+            dom = ("k_rhs3<viscous> (flux + divergence pass)", ms_div, B_ALG_DIV) if ms_div >= ms_grad else \
+                  ("k_grad3 (BR1 gradient pass)", ms_grad, B_ALG_GRAD)
         achieved = ndof * dom[2] / (dom[1] * 1e-3) / 1e9
         traffic = None
         tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
         if os.path.exists(tpath):
             with open(tpath) as fh:
                 tj = json.load(fh)
-            if tj.get("n") == n:      # ncu capture of exactly this workload (bytes per launch)
+            if tj.get("n") == n and ORDER == 3 and not euler:      # ncu capture of exactly this workload (bytes per launch)
                 key = "k_rhs3_viscous" if ms_div >= ms_grad else "k_grad3"
                 traffic = tj[key]["dram_read_bytes"] + tj[key]["dram_write_bytes"]
         roofline = {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                     "algorithmic_bytes_per_dof": dom[2], "ms_per_launch": dom[1],
                     "ms_grad_pass": ms_grad, "ms_div_pass": ms_div}
-    rhs_gbs = ndof * B_ALG_RHS / (ms_step * 1e-3) / 1e9
+    b_alg = 80.0 if euler else B_ALG_RHS
+    rhs_gbs = ndof * b_alg / (ms_step * 1e-3) / 1e9
 
     # ---- end to end through the public API with host buffers ---------------------------------
     e2e = None
@@ -304,21 +327,19 @@ def run_b200(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cores = os.cpu_count() or 1
-        v, dofs, busy, wall = cpu_throughput(cores, args.cpu_n, 1)
+        v, dofs, busy, wall = cpu_throughput(cores, args.cpu_n, CPU_REPS)
         cpu = {"value": v, "unit": "GDOF/s", "cores": cores, "kind": "port",
-               "sample": f"{cores} processes x 1 NS p3 RHS on a periodic {args.cpu_n}^3 Kuhn mesh "
+               "sample": f"{cores} processes x {CPU_REPS} NS p3 RHS on a periodic {args.cpu_n}^3 Kuhn mesh "
                          f"({6 * args.cpu_n ** 3 * NP} DOFs each), oracle/laze_port.py NumPy eager context; "
                          f"{busy:.1f} s busy"}
 
     if rank == 0:
         line = {
-            "metric": "3D Navier-Stokes DG RHS throughput", "value": value, "unit": "GDOF/s",
-            "n_gpus": world, "steps": K, "warmup": max(args.warmup, 3), "ms_per_step": ms_step,
+            "metric": "3D Navier-Stokes DG RHS throughput" if not euler else "3D Euler DG RHS throughput",
+            "value": value, "unit": "GDOF/s", "n_gpus": world, "steps": K, "warmup": max(args.warmup, 3), "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": f"3D compressible Navier-Stokes DG RHS (BR1, two derivative passes), Kuhn tets "
-                                   f"order 3, periodic {n}^3 box per GPU: {E} elements, {ndof} DOFs per GPU "
-                                   f"(BASELINE configs[2])",
+            "config": {"workload": workload_name(n, args.workload),
                        "elements_per_gpu": E, "dofs_per_gpu": ndof, "order": ORDER, "dim": DIM,
                        "l2_policy": "inputs larger than L2 (q 4.0 GB, grad q 12 GB per GPU vs 126 MB L2)"
                        if ndof * 40 > 126e6 * 4 else "inputs comparable to L2: reduced size, not the headline config",
@@ -326,7 +347,7 @@ def run_b200(args):
                        "setup_s": t_setup},
             "roofline": roofline,
             "rhs_roofline": {"bound": "hbm", "achieved": rhs_gbs, "peak": peak, "unit": "GB/s",
-                             "frac": rhs_gbs / peak, "algorithmic_bytes_per_dof": B_ALG_RHS,
+                             "frac": rhs_gbs / peak, "algorithmic_bytes_per_dof": b_alg,
                              "peak_source": peak_src},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         }
@@ -346,7 +367,13 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--order", type=int, default=3, help="polynomial order (headline: 3)")
+    ap.add_argument("--workload", default="ns", choices=["ns", "euler"],
+                    help="ns = BASELINE configs[2] (headline); euler = configs[1] (3D Euler, read q + write rhs = 80 B/DOF)")
     args = ap.parse_args()
+    global ORDER, NP
+    ORDER = args.order
+    NP = (ORDER + 1) * (ORDER + 2) * (ORDER + 3) // 6
     if args.impl == "reference":
         run_reference(args)
     else:
