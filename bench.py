@@ -306,12 +306,19 @@ def run_b200(args):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
+        # Pipelined like a streaming user would: the H2D copy of step k+1 (copy stream) overlaps the
+        # compute + D2H of step k (compute stream).  Every step still uploads its full input from pinned
+        # host memory and downloads its full result; both are inside the timed region.
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record(stream)
-        for _ in range(Ke):
-            qd = DOFArray(actx, actx.from_numpy(q_host))          # H2D from pinned host memory
-            actx.to_numpy(rhs_step(qd).data, out=out_host)        # D2H of the result
+        actx.copy_stream.wait_event(s0)
+        nxt = actx.from_numpy_async(q_host)
+        for k in range(Ke):
+            cur = actx.wait_for(nxt)
+            res = rhs_step(DOFArray(actx, cur)).data
+            if k + 1 < Ke:
+                nxt = actx.from_numpy_async(q_host)               # H2D of step k+1 into a fresh buffer
+            actx.to_numpy_async(res, out_host)                    # D2H of step k's result
         s1.record(stream)
         torch.cuda.synchronize()
         ms_e2e = s0.elapsed_time(s1) / Ke

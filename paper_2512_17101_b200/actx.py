@@ -295,6 +295,51 @@ class B200ArrayContext:
             out._host = shadow
         return out
 
+    # -- asynchronous upload on a second stream, so that the H2D copy of the next batch overlaps the
+    #    compute + D2H of the current one (PCIe is full duplex) --------------------------------------
+    @property
+    def copy_stream(self):
+        if getattr(self, "_copy_stream", None) is None:
+            self._copy_stream = _torch().cuda.Stream(device=self.device)
+        return self._copy_stream
+
+    def from_numpy_async(self, value, after=None) -> DeviceArray:
+        """Upload a PINNED host array on the copy stream.  ``after``: an event the copy must wait for
+        (e.g. the last kernel that read a buffer being recycled).  The result carries ``.ready``; call
+        ``actx.wait_for(arr)`` before using it on the compute stream."""
+        torch = _torch()
+        host = np.ascontiguousarray(value)
+        if not self._is_pinned(host):
+            raise errors.LazeError("from_numpy_async needs a page-locked buffer (actx.pinned_empty)")
+        cs = self.copy_stream
+        with torch.cuda.stream(cs):
+            t = torch.empty(host.shape, dtype=_torch_dtype(_code_of_numpy(host.dtype)), device=self.device)
+        if after is not None:
+            cs.wait_event(after)
+        out = DeviceArray(self, t)
+        _cabi.check(self.lib.dgb_memcpy_h2d(C.c_void_p(out.ptr), C.c_void_p(host.ctypes.data), host.nbytes,
+                                            C.c_void_p(cs.cuda_stream)), "from_numpy_async")
+        out.ready = torch.cuda.Event()
+        out.ready.record(cs)
+        t.record_stream(self.stream)
+        return out
+
+    def wait_for(self, arr: DeviceArray) -> DeviceArray:
+        ev = getattr(arr, "ready", None)
+        if ev is not None:
+            self.stream.wait_event(ev)
+        return arr
+
+    def to_numpy_async(self, value: DeviceArray, out: np.ndarray):
+        """D2H into a pinned buffer on the compute stream without synchronising; returns an event."""
+        src = self._contiguous(value)
+        _cabi.check(self.lib.dgb_memcpy_d2h(C.c_void_p(out.ctypes.data), C.c_void_p(src.ptr), out.nbytes, self._st),
+                    "to_numpy_async")
+        ev = _torch().cuda.Event()
+        ev.record(self.stream)
+        self._keepalive = [src]
+        return ev
+
     def to_numpy(self, value, out=None) -> np.ndarray:
         if not isinstance(value, DeviceArray):
             return np.asarray(value)
