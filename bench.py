@@ -289,10 +289,13 @@ def run_b200(args):
             if tj.get("n") == n and ORDER == 3 and not euler:      # ncu capture of exactly this workload (bytes per launch)
                 key = "k_rhs3_viscous" if ms_div >= ms_grad else "k_grad3"
                 traffic = tj[key]["dram_read_bytes"] + tj[key]["dram_write_bytes"]
+        per_step = [e[0].elapsed_time(e[2]) for e in ev]
         roofline = {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                     "algorithmic_bytes_per_dof": dom[2], "ms_per_launch": dom[1],
-                    "ms_grad_pass": ms_grad, "ms_div_pass": ms_div}
+                    "ms_grad_pass": ms_grad, "ms_div_pass": ms_div,
+                    "ms_step_min_median_max": [float(np.min(per_step)), float(np.median(per_step)),
+                                               float(np.max(per_step))]}
     b_alg = 80.0 if euler else B_ALG_RHS
     rhs_gbs = ndof * b_alg / (ms_step * 1e-3) / 1e9
 
