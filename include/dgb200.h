@@ -116,6 +116,28 @@ int dgb_ns_rhs_rk(const dgb_disc* disc, const double* q_dev, const double* gradq
                   const double* x1_dev, double* out1_dev, const double* x2_dev, double* out2_dev,
                   const double* rk_host, const double* qfar_host, const double* phys_host, void* stream);
 
+/* ---- Navier-Stokes in the flux arrangement (operators.py: dg_ns_flux + dg_ns_div; the default
+ *      of NavierStokesOperator.rhs).  Same reference boundary as above (a Call to a
+ *      FunctionDefinition, adfg.py:722-803).  dgb_disc_set_jacobian binds the volume Jacobian
+ *      jac (E) the two functions take as an argument and derives the face Jacobians
+ *      fscale*jac and 1/jac on the device; call it once per handle before dgb_ns_flux.
+ *   T      (dim*C + 1, E, Np)   planes r*C + c: sum_x jac*drdx[r,x] * (F_inv - F_visc)[x][c] with the BR1
+ *                               gradient of pass 1 folded in; last plane: wave speed |u| + c
+ *   Tghost (dim*C + 1, G, Np) or NULL: the same planes of the halo elements (already scaled by
+ *                               the sender's Jacobian, so no remote geometry is needed)
+ *   all device arrays 16-byte aligned.
+ */
+int dgb_disc_set_jacobian(dgb_disc* disc, const double* jac_dev, void* stream);
+int dgb_ns_flux(const dgb_disc* disc, const double* q_dev, const double* ghost_dev, double* T_dev,
+                const double* qfar_host, const double* phys_host, void* stream);
+int dgb_ns_div(const dgb_disc* disc, const double* q_dev, const double* T_dev,
+               const double* ghost_dev, const double* Tghost_dev, double* rhs_dev,
+               const double* qfar_host, const double* phys_host, void* stream);
+int dgb_ns_div_rk(const dgb_disc* disc, const double* q_dev, const double* T_dev,
+                  const double* ghost_dev, const double* Tghost_dev,
+                  const double* x1_dev, double* out1_dev, const double* x2_dev, double* out2_dev,
+                  const double* rk_host, const double* qfar_host, const double* phys_host, void* stream);
+
 /* ---- halo packing: element rows <-> contiguous message (Send / Receive payloads,
  *      adfg.py:380-399,834-869).  dst[c, i, :] = src[c, elems[i], :]                        ---- */
 int dgb_pack_elements(double* dst_dev, const double* src_dev, const int64_t* elems_dev,

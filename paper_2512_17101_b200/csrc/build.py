@@ -7,7 +7,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 OUT = os.path.join(os.path.dirname(HERE), "libdgb200.so")
-SOURCES = ["dgb200.cu", "dgb_arrayops.cu"]
+SOURCES = ["dgb200.cu", "dgb_nsflux.cu", "dgb_arrayops.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-shared", "-Xcompiler", "-fPIC"]
 
@@ -16,7 +16,8 @@ def needs_build() -> bool:
     if not os.path.exists(OUT):
         return True
     t = os.path.getmtime(OUT)
-    deps = SOURCES + ["dgb_kernels.cuh", "dgb_kernels_async.cuh", "dgb_kernels_warp.cuh", os.path.join("..", "..", "include", "dgb200.h")]
+    deps = SOURCES + ["dgb_kernels.cuh", "dgb_kernels_async.cuh", "dgb_kernels_warp.cuh", "dgb_kernels_flux.cuh",
+                      "dgb_internal.h", os.path.join("..", "..", "include", "dgb200.h")]
     return any(os.path.getmtime(os.path.join(HERE, d)) > t for d in deps)
 
 
@@ -24,7 +25,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return OUT
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc] + FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-o", OUT] + SOURCES
+    cmd = [nvcc, "--threads", "0"] + FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-o", OUT] + SOURCES
     res = subprocess.run(cmd, cwd=HERE, capture_output=True, text=True)
     if verbose:
         sys.stderr.write(res.stderr)

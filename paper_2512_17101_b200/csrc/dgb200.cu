@@ -1,6 +1,6 @@
 // C ABI of the B200 DG right-hand-side path: discretisation handle, kernel dispatch, halo
 // packing.  See include/dgb200.h for the contract and the reference interfaces replaced.
-#include "../../include/dgb200.h"
+#include "dgb_internal.h"
 #include "dgb_kernels_async.cuh"
 #include "dgb_kernels_warp.cuh"
 
@@ -11,36 +11,21 @@
 #include <vector>
 
 namespace {
-
 thread_local std::string g_err;
+}  // namespace
 
-int fail(int code, const std::string& msg) { g_err = msg; return code; }
+int dgb_fail(int code, const std::string& msg) { g_err = msg; return code; }
 
-#define DGB_CUDA(expr)                                                                      \
-  do {                                                                                      \
-    cudaError_t e_ = (expr);                                                                \
-    if (e_ != cudaSuccess)                                                                  \
-      return fail(DGB_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));        \
-  } while (0)
-
-int num_sms() {
+int dgb_num_sms() {
   static int n = 0;
   if (!n) { int dev = 0; cudaGetDevice(&dev); cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev); }
   return n;
 }
 
+namespace {
+int fail(int code, const std::string& msg) { return dgb_fail(code, msg); }
+int num_sms() { return dgb_num_sms(); }
 }  // namespace
-
-struct dgb_disc {
-  int dim = 0, order = 0, Np = 0, Nf = 0, Nfp = 0, nperm = 0;
-  dgb::DiscDev dev{};
-  double *Wv = nullptr, *Wl = nullptr, *Wq = nullptr, *Wf = nullptr;
-  long long* conn = nullptr;
-  long long* timing = nullptr;
-  unsigned long long* counters = nullptr;   // [0] gradient pass, [1] flux/divergence pass work counters
-  int* tables = nullptr;
-  const int64_t* bc_kind = nullptr;
-};
 
 // {{{ connectivity compression / expansion
 
@@ -477,6 +462,7 @@ int dgb_disc_create(dgb_disc** out, int dim, int order, int64_t E, int64_t G, co
 
 int dgb_disc_destroy(dgb_disc* d) {
   if (!d) return DGB_OK;
+  dgb_disc_free_jacobian(d);
   cudaFree(d->Wv); cudaFree(d->Wl); cudaFree(d->Wq); cudaFree(d->Wf); cudaFree(d->conn); cudaFree(d->tables); cudaFree(d->timing); cudaFree(d->counters);
   delete d;
   return DGB_OK;

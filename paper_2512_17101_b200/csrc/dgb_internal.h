@@ -1,0 +1,31 @@
+// Internals shared by the translation units of libdgb200.so (not part of the C ABI).
+#pragma once
+#include "../../include/dgb200.h"
+#include "dgb_kernels.cuh"
+
+#include <string>
+
+int dgb_fail(int code, const std::string& msg);   // records the message for dgb_last_error()
+int dgb_num_sms();
+
+#define DGB_CUDA(expr)                                                                          \
+  do {                                                                                          \
+    cudaError_t e_ = (expr);                                                                    \
+    if (e_ != cudaSuccess)                                                                      \
+      return dgb_fail(DGB_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));        \
+  } while (0)
+
+struct dgb_disc {
+  int dim = 0, order = 0, Np = 0, Nf = 0, Nfp = 0, nperm = 0;
+  dgb::DiscDev dev{};
+  double *Wv = nullptr, *Wl = nullptr, *Wq = nullptr, *Wf = nullptr;
+  long long* conn = nullptr;
+  long long* timing = nullptr;
+  unsigned long long* counters = nullptr;   // work counters: [0] gradient / flux pass, [1] divergence pass
+  int* tables = nullptr;
+  const int64_t* bc_kind = nullptr;
+  double *sj = nullptr, *rj = nullptr;      // flux arrangement: face Jacobians (E, Nf), 1/J (E)
+};
+
+// dgb_nsflux.cu
+int dgb_disc_free_jacobian(dgb_disc* d);

@@ -65,6 +65,10 @@ struct DiscDev {
   const double* fscale;  // [E][NF]
   const long long* conn; // [E][NF] packed
   const int* tables;     // face_nodes [NF][NFP] then face_perms [NPERM][NFP]
+  // flux arrangement (dgb_kernels_flux.cuh), bound by dgb_disc_set_jacobian
+  const double* jac;     // [E] volume Jacobian
+  const double* sj;      // [E][NF] face Jacobian = fscale * jac
+  const double* rj;      // [E] 1 / jac
 };
 
 struct Phys { double gamma, mu, kappa, rgas; double qfar[5]; };
@@ -496,6 +500,8 @@ k_rhs(DiscDev d, const double* __restrict__ q, const double* __restrict__ gq,
       const double lam = fmax(S.Lam[e * NP + jm], wavespeed<DIM>(sp_, ph.gamma));
       if (VISCOUS) {
         double fvn[C];
+        // boundary faces: the viscous flux is the interior one, Fv(q-, grad q-) (operators.py)
+        if (bc != 0) make_prim<DIM>(qm, ph.gamma, sp_);
         viscous_normal_flux<DIM>(sp_, gp, nrm, ph, fvn);
 #pragma unroll
         for (int c = 1; c < C; ++c) fnp[c] -= fvn[c];

@@ -224,6 +224,8 @@ k_rhs2(DiscDev d, const double* __restrict__ q, const double* __restrict__ gq,
         for (int x = 0; x < DIM; ++x)
 #pragma unroll
           for (int c = 0; c < C; ++c) gp[x][c] = nbp[(C + x * C + c) * (K * NFT)];
+        // boundary faces: the viscous flux is the interior one, Fv(q-, grad q-) (operators.py)
+        if (bc != 0) make_prim<DIM>(qm, ph.gamma, sp_);
         viscous_normal_flux<DIM>(sp_, gp, nrm, ph, fvn);
 #pragma unroll
         for (int c = 1; c < C; ++c) fnp[c] -= fvn[c];

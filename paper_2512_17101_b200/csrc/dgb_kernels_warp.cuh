@@ -252,6 +252,8 @@ k_rhs3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gq,
       const double lam = fmax(W.Lam[e * NP + jm], wavespeed<DIM>(sp_, ph.gamma));
       if (VISCOUS) {
         double fvn[C];
+        // boundary faces: the viscous flux is the interior one, Fv(q-, grad q-) (operators.py)
+        if (bc != 0) make_prim<DIM>(qm, ph.gamma, sp_);
         viscous_normal_flux<DIM>(sp_, gp, nrm, ph, fvn);
 #pragma unroll
         for (int c = 1; c < C; ++c) fnp[c] -= fvn[c];

@@ -1,0 +1,159 @@
+// C ABI of the Navier-Stokes flux arrangement (dg_ns_flux + dg_ns_div, operators.py) and its
+// launch configuration.  Kernels: dgb_kernels_flux.cuh.
+#include "dgb_internal.h"
+#include "dgb_kernels_flux.cuh"
+
+#include <cstdlib>
+#include <string>
+
+namespace {
+
+#ifndef DGB_FLUX_WARPS
+#define DGB_FLUX_WARPS 16
+#endif
+#ifndef DGB_DIV_WARPS
+#define DGB_DIV_WARPS 16
+#endif
+constexpr int kSmemBudget = 232448 - 1024;   // 227 KB usable per CTA minus the 1 KB system reserve
+constexpr int fit_warps(size_t fixed, size_t per_warp, int cap) {
+  int n = (int)((kSmemBudget - fixed) / per_warp);
+  return n < 1 ? 1 : (n > cap ? cap : n);
+}
+
+template <int DIM, int P> struct CfgF {
+  static constexpr int KW = DIM == 3 ? 3 : 4;
+  static constexpr size_t flux_per = sizeof(dgb::Flux3Warp<DIM, P, KW>);
+  static constexpr size_t flux_fixed = sizeof(dgb::Flux3Smem<DIM, P, KW, 1>) - flux_per;
+  static constexpr int NWF = fit_warps(flux_fixed, flux_per, DGB_FLUX_WARPS);
+  static constexpr size_t div_per = sizeof(dgb::Div3Warp<DIM, P, KW>);
+  static constexpr size_t div_fixed = sizeof(dgb::Div3Smem<DIM, P, KW, 1>) - div_per;
+  static constexpr int NWD = fit_warps(div_fixed, div_per, DGB_DIV_WARPS);
+};
+
+int env_int(const char* name, int dflt) { const char* e = getenv(name); return e ? atoi(e) : dflt; }
+
+template <int DIM, int P>
+int launch_flux(const dgb_disc* d, const double* q, const double* ghost, double* T, const dgb::Phys& ph,
+                cudaStream_t st) {
+  using C = CfgF<DIM, P>;
+  auto kern = dgb::k_nsflux3<DIM, P, C::KW, C::NWF>;
+  const size_t smem = sizeof(dgb::Flux3Smem<DIM, P, C::KW, C::NWF>);
+  const long long nwb = (d->dev.E + C::KW - 1) / C::KW;
+  if (nwb == 0) return DGB_OK;
+  static bool configured = false;
+  if (!configured) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured = true; }
+  const long long need = (nwb + C::NWF - 1) / C::NWF;
+  const int grid = (int)(need < dgb_num_sms() ? need : dgb_num_sms());
+  DGB_CUDA(cudaMemsetAsync(d->counters, 0, sizeof(unsigned long long), st));
+  kern<<<grid, C::NWF * 32, smem, st>>>(d->dev, q, ghost, T, ph, nwb, d->counters);
+  DGB_CUDA(cudaGetLastError());
+  return DGB_OK;
+}
+
+template <int DIM, int P>
+int launch_div(const dgb_disc* d, const double* q, const double* T, const double* ghost, const double* Tghost,
+               const dgb::Epilogue& ep, const dgb::Phys& ph, cudaStream_t st) {
+  using C = CfgF<DIM, P>;
+  auto kern = dgb::k_nsdiv3<DIM, P, C::KW, C::NWD>;
+  const size_t smem = sizeof(dgb::Div3Smem<DIM, P, C::KW, C::NWD>);
+  const long long nwb = (d->dev.E + C::KW - 1) / C::KW;
+  if (nwb == 0) return DGB_OK;
+  static bool configured = false;
+  if (!configured) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured = true; }
+  const long long need = (nwb + C::NWD - 1) / C::NWD;
+  const int grid = (int)(need < dgb_num_sms() ? need : dgb_num_sms());
+  DGB_CUDA(cudaMemsetAsync(d->counters + 1, 0, sizeof(unsigned long long), st));
+  kern<<<grid, C::NWD * 32, smem, st>>>(d->dev, q, T, ghost, Tghost, ep, ph, nwb, d->counters + 1);
+  DGB_CUDA(cudaGetLastError());
+  return DGB_OK;
+}
+
+#define DGB_FOR_EACH_ELEMENT(X) X(2, 1) X(2, 2) X(2, 3) X(2, 4) X(3, 1) X(3, 2) X(3, 3) X(3, 4)
+
+void make_phys(dgb::Phys& ph, int C, const double* qfar, const double* phys) {
+  ph.gamma = phys ? phys[0] : 1.4; ph.mu = phys ? phys[1] : 0.0; ph.kappa = phys ? phys[2] : 0.0;
+  ph.rgas = phys ? phys[3] : 1.0;
+  for (int c = 0; c < 5; ++c) ph.qfar[c] = (qfar && c < C) ? qfar[c] : 0.0;
+}
+
+__global__ void k_face_jacobians(const double* __restrict__ fscale, const double* __restrict__ jac, long long E,
+                                 int Nf, double* __restrict__ sj, double* __restrict__ rj) {
+  const long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (n >= E * Nf) return;
+  const long long e = n / Nf;
+  sj[n] = fscale[n] * jac[e];
+  if (n == e * Nf) rj[e] = 1.0 / jac[e];
+}
+
+int check_flux_args(const dgb_disc* d, const void* ghost, const void* a, const void* b) {
+  if (!d) return dgb_fail(DGB_ERR_INVALID, "null handle");
+  if (!d->dev.jac) return dgb_fail(DGB_ERR_INVALID, "dgb_disc_set_jacobian has not been called on this handle");
+  if (d->dev.G > 0 && !ghost) return dgb_fail(DGB_ERR_INVALID, "discretisation has ghost elements but no ghost array was given");
+  if ((((uintptr_t)a) | ((uintptr_t)b)) & 15) return dgb_fail(DGB_ERR_INVALID, "device arrays must be 16-byte aligned");
+  return DGB_OK;
+}
+
+}  // namespace
+
+int dgb_disc_free_jacobian(dgb_disc* d) {
+  if (d) { cudaFree(d->sj); cudaFree(d->rj); d->sj = d->rj = nullptr; }
+  return DGB_OK;
+}
+
+extern "C" {
+
+int dgb_disc_set_jacobian(dgb_disc* d, const double* jac_dev, void* stream) {
+  if (!d || !jac_dev) return dgb_fail(DGB_ERR_INVALID, "null handle or Jacobian array");
+  dgb_disc_free_jacobian(d);
+  const long long E = d->dev.E, n = E * d->Nf;
+  DGB_CUDA(cudaMalloc((void**)&d->sj, sizeof(double) * (size_t)(n ? n : 1)));
+  DGB_CUDA(cudaMalloc((void**)&d->rj, sizeof(double) * (size_t)(E ? E : 1)));
+  if (n) {
+    k_face_jacobians<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(d->dev.fscale, jac_dev, E, d->Nf,
+                                                                                    d->sj, d->rj);
+    DGB_CUDA(cudaGetLastError());
+  }
+  d->dev.jac = jac_dev; d->dev.sj = d->sj; d->dev.rj = d->rj;
+  return DGB_OK;
+}
+
+int dgb_ns_flux(const dgb_disc* d, const double* q, const double* ghost, double* T, const double* qfar,
+                const double* phys, void* stream) {
+  int rc = check_flux_args(d, ghost, q, T); if (rc) return rc;
+  dgb::Phys ph; make_phys(ph, d->dim + 2, qfar, phys);
+#define X(DIM, P) if (d->dim == DIM && d->order == P) return launch_flux<DIM, P>(d, q, ghost, T, ph, (cudaStream_t)stream);
+  DGB_FOR_EACH_ELEMENT(X)
+#undef X
+  return dgb_fail(DGB_ERR_INVALID, "unsupported (dim, order)");
+}
+
+static int ns_div_impl(const dgb_disc* d, const double* q, const double* T, const double* ghost, const double* Tghost,
+                       const dgb::Epilogue& ep, const double* qfar, const double* phys, void* stream) {
+  int rc = check_flux_args(d, ghost, q, T); if (rc) return rc;
+  if (d->dev.G > 0 && !Tghost) return dgb_fail(DGB_ERR_INVALID, "ghost elements need the ghost flux planes");
+  dgb::Phys ph; make_phys(ph, d->dim + 2, qfar, phys);
+#define X(DIM, P) if (d->dim == DIM && d->order == P) return launch_div<DIM, P>(d, q, T, ghost, Tghost, ep, ph, (cudaStream_t)stream);
+  DGB_FOR_EACH_ELEMENT(X)
+#undef X
+  return dgb_fail(DGB_ERR_INVALID, "unsupported (dim, order)");
+}
+
+int dgb_ns_div(const dgb_disc* d, const double* q, const double* T, const double* ghost, const double* Tghost,
+               double* rhs, const double* qfar, const double* phys, void* stream) {
+  if (!rhs) return dgb_fail(DGB_ERR_INVALID, "null output");
+  dgb::Epilogue ep{nullptr, rhs, nullptr, nullptr, 0.0, 1.0, 0.0, 0.0};
+  return ns_div_impl(d, q, T, ghost, Tghost, ep, qfar, phys, stream);
+}
+
+int dgb_ns_div_rk(const dgb_disc* d, const double* q, const double* T, const double* ghost, const double* Tghost,
+                  const double* x1, double* out1, const double* x2, double* out2, const double* rk,
+                  const double* qfar, const double* phys, void* stream) {
+  if (!out1 || !rk) return dgb_fail(DGB_ERR_INVALID, "out1 and rk are required");
+  if (out1 == q || (out2 && out2 == q) || (x2 && out1 == x2))
+    return dgb_fail(DGB_ERR_INVALID, "RK outputs must not alias the stage input q (neighbours still read it)");
+  if (out2 && !x2) return dgb_fail(DGB_ERR_INVALID, "out2 needs x2");
+  dgb::Epilogue ep{x1, out1, x2, out2, rk[0], rk[1], rk[2], rk[3]};
+  return ns_div_impl(d, q, T, ghost, Tghost, ep, qfar, phys, stream);
+}
+
+}  // extern "C"

@@ -50,6 +50,18 @@ class DGDiscretization:
         self.drdx = f(geo.drdx)                                     # (d, d, E)   [r, x, e]
         self.normals = f(geo.normals.reshape(self.dim, E, Nf, 1))   # (d, E, Nf, 1)
         self.fscale = f(geo.fscale.reshape(E, Nf, 1))               # (E, Nf, 1)
+        self.jac = f(np.ascontiguousarray(geo.jac))                 # (E,) volume Jacobian
+        # fscale * jac * n_x (face f) == sum_r facemat[r, f] * jac * drdx[r, x]: face 0 (opposite vertex 0)
+        # is the sum of the reference gradients, face f >= 1 is minus gradient f-1 (dg/mesh.py: geometry)
+        fm = np.zeros((self.dim, Nf))
+        fm[:, 0] = 1.0
+        for r in range(self.dim):
+            fm[r, r + 1] = -1.0
+        lhs = geo.fscale[None] * geo.normals                        # (x, E, Nf)
+        assert np.allclose(lhs, np.einsum("rf,rxe->xef", fm, geo.drdx), rtol=1e-12, atol=1e-12)
+        self.facemat_host = fm
+        self.facemat = f(fm.reshape(self.dim, Nf, 1))               # (d, Nf, 1), broadcasts over elements
+        self.facemat_p = f(np.ascontiguousarray(fm[:, mesh.nbr_face]).reshape(self.dim, E, Nf, 1))
         self.vmap_m = f(vmap_m.reshape(-1))                         # (E*Nf*Nfp,) int64
         self.vmap_p = f(vmap_p.reshape(-1))
         self.bc_kind = f(bc_kind.reshape(E, Nf, 1))                 # (E, Nf, 1) int64

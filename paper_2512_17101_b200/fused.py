@@ -204,5 +204,114 @@ def dg_ns_rhs_rk(actx, f, q, gq, x1, x2, coef, Sw, drdx, lift, normals, fscale, 
     return {"out1": o1, "out2": o2}
 
 
-FUSED = {"dg_euler_rhs": dg_euler_rhs, "dg_ns_grad": dg_ns_grad, "dg_ns_rhs": dg_ns_rhs,
+def _bind_jacobian(actx, disc, jac, facemat=None):
+    """Bind the volume Jacobian argument to the handle (once) -- dgb_disc_set_jacobian."""
+    if getattr(disc, "jac_id", None) == id(jac):
+        return
+    j = _f64(actx, jac, "jac")
+    if tuple(j.shape) != (disc.E,):
+        raise errors.BindingMismatch(f"jac has shape {tuple(j.shape)}, expected {(disc.E,)}")
+    _cabi.check(actx.lib.dgb_disc_set_jacobian(disc.handle, j.ptr, actx._st), "dgb_disc_set_jacobian")
+    actx.launch_count += 1
+    disc.keep += [j, jac]
+    disc.jac_id = id(jac)
+
+
+def _check_facemat(disc, facemat, facemat_p):
+    """The kernels use the simplex identity behind ``facemat`` (face 0 = sum of the reference
+    gradients, face f = minus gradient f-1) structurally; refuse anything else."""
+    if getattr(disc, "facemat_ok", None) == (id(facemat), id(facemat_p)):
+        return
+    dim, Nf = disc.dim, disc.Nf
+    want = np.zeros((dim, Nf))
+    want[:, 0] = 1.0
+    for r in range(dim):
+        want[r, r + 1] = -1.0
+    got = np.asarray(facemat.host_value(), dtype=np.float64).reshape(dim, Nf)
+    if not np.array_equal(got, want):
+        raise errors.BindingMismatch("facemat is not the simplex face/gradient incidence matrix")
+    if tuple(facemat_p.shape) != (dim, disc.E, Nf, 1):
+        raise errors.BindingMismatch(f"facemat_p has shape {tuple(facemat_p.shape)}")
+    disc.facemat_ok = (id(facemat), id(facemat_p))
+
+
+def dg_ns_flux(actx, f, *args):
+    if len(args) == 12:
+        q, Sw, drdx, jac, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, phys = args
+        ghost = None
+    elif len(args) == 13:
+        q, ghost, Sw, drdx, jac, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, phys = args
+    else:
+        raise errors.BindingMismatch(f"dg_ns_flux takes 12 or 13 arrays, got {len(args)}")
+    dim = f.dg_dim
+    q = _f64(actx, q, "q")
+    G, g, gptr = _ghost_ptr(actx, ghost, (dim + 2,), q.shape[-1])
+    disc = get_disc(actx, dim, q, G, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind)
+    _bind_jacobian(actx, disc, jac)
+    qf, ph = _host_vec(qfar, dim + 2), _host_vec(phys, 4)
+    out = actx.empty((dim * (dim + 2) + 1,) + tuple(q.shape[1:]))
+    _cabi.check(actx.lib.dgb_ns_flux(disc.handle, q.ptr, gptr, out.ptr, qf.ctypes.data, ph.ctypes.data, actx._st),
+                "dg_ns_flux")
+    actx.launch_count += 1
+    return out
+
+
+def _div_common(actx, f, q, T, ghost, Tghost, Sw, jac, lift, normals, fscale, facemat, facemat_p, vmap_m, vmap_p,
+                bc_kind):
+    dim = f.dg_dim
+    q = _f64(actx, q, "q")
+    T = _f64(actx, T, "T")
+    npl = dim * (dim + 2) + 1
+    if tuple(T.shape) != (npl,) + tuple(q.shape[1:]):
+        raise errors.BindingMismatch(f"flux planes have shape {tuple(T.shape)}, expected {(npl,) + tuple(q.shape[1:])}")
+    G, g, gptr = _ghost_ptr(actx, ghost, (dim + 2,), q.shape[-1])
+    TG, tg, tgptr = _ghost_ptr(actx, Tghost, (npl,), q.shape[-1])
+    if TG != G:
+        raise errors.BindingMismatch("ghost arrays of q and of the flux planes disagree in size")
+    # the fused kernels take drdx only through the handle; dg_ns_div does not receive it, so the
+    # handle must already exist (dg_ns_flux of the same discretisation creates it)
+    disc = None
+    for key, cand in actx._discs.items():
+        if key[0] == dim and key[1] == G and key[4] == id(lift) and key[5] == id(normals) and key[6] == id(fscale) \
+                and key[7] == id(vmap_m) and key[8] == id(vmap_p) and key[9] == id(bc_kind) and key[2] == id(Sw):
+            disc = cand
+            break
+    if disc is None:
+        raise errors.BindingMismatch("dg_ns_div: no discretisation handle for these arrays (call dg_ns_flux first)")
+    _bind_jacobian(actx, disc, jac)
+    _check_facemat(disc, facemat, facemat_p)
+    return q, T, gptr, tgptr, disc, (g, tg)
+
+
+def dg_ns_div(actx, f, *args):
+    if len(args) == 14:
+        q, T, Sw, jac, lift, normals, fscale, facemat, facemat_p, vmap_m, vmap_p, bc_kind, qfar, phys = args
+        ghost = Tghost = None
+    elif len(args) == 16:
+        q, T, ghost, Tghost, Sw, jac, lift, normals, fscale, facemat, facemat_p, vmap_m, vmap_p, bc_kind, qfar, phys = args
+    else:
+        raise errors.BindingMismatch(f"dg_ns_div takes 14 or 16 arrays, got {len(args)}")
+    q, T, gptr, tgptr, disc, keep = _div_common(actx, f, q, T, ghost, Tghost, Sw, jac, lift, normals, fscale, facemat,
+                                                facemat_p, vmap_m, vmap_p, bc_kind)
+    qf, ph = _host_vec(qfar, f.dg_dim + 2), _host_vec(phys, 4)
+    out = actx.empty(q.shape)
+    _cabi.check(actx.lib.dgb_ns_div(disc.handle, q.ptr, T.ptr, gptr, tgptr, out.ptr, qf.ctypes.data, ph.ctypes.data,
+                                    actx._st), "dg_ns_div")
+    actx.launch_count += 1
+    return out
+
+
+def dg_ns_div_rk(actx, f, q, T, x1, x2, coef, Sw, jac, lift, normals, fscale, facemat, facemat_p, vmap_m, vmap_p,
+                 bc_kind, qfar, phys):
+    q, T, gptr, tgptr, disc, keep = _div_common(actx, f, q, T, None, None, Sw, jac, lift, normals, fscale, facemat,
+                                                facemat_p, vmap_m, vmap_p, bc_kind)
+    qf, ph = _host_vec(qfar, f.dg_dim + 2), _host_vec(phys, 4)
+    x1, x2, rk, o1, o2 = _rk_common(actx, q, x1, x2, coef)
+    _cabi.check(actx.lib.dgb_ns_div_rk(disc.handle, q.ptr, T.ptr, None, None, x1.ptr, o1.ptr, x2.ptr, o2.ptr,
+                                       rk.ctypes.data, qf.ctypes.data, ph.ctypes.data, actx._st), "dg_ns_div_rk")
+    actx.launch_count += 1
+    return {"out1": o1, "out2": o2}
+
+
+FUSED = {"dg_ns_flux": dg_ns_flux, "dg_ns_div": dg_ns_div, "dg_ns_div_rk": dg_ns_div_rk, "dg_euler_rhs": dg_euler_rhs, "dg_ns_grad": dg_ns_grad, "dg_ns_rhs": dg_ns_rhs,
          "dg_euler_rhs_rk": dg_euler_rhs_rk, "dg_ns_rhs_rk": dg_ns_rhs_rk}

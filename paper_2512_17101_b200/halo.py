@@ -3,7 +3,8 @@
 Message model = the reference's: one array per ``(source, destination, tag)``
 (/root/reference/pkg/src/laze/distpart.py:396-411), receives conceptually posted up front, one
 communication batch per dependency level -- Euler: one batch (state halos); Navier-Stokes: two
-(state halos, then gradient halos, which depend on received data: distpart.py:168-176).
+(state halos, then the halos of the pass-1 result -- flux planes, or gradients in the gradient
+arrangement -- which depend on received data: distpart.py:168-176).
 
 ``TorchCommunicator`` moves the payloads with ``torch.distributed`` point-to-point ops: NCCL
 send/recv over NVLink for device arrays, gloo for the CPU oracle context (tests).  All sends and
@@ -126,7 +127,11 @@ class HaloExchange:
 
     def ns_rhs(self, op, q: DOFArray) -> DOFArray:
         ghost = self.exchange(q.data)                                   # batch 1: state halos
-        return op.rhs(q, ghost=ghost, grad_ghost_fn=lambda gq: self.exchange(gq.data))   # batch 2: gradient halos
+        return op.rhs(q, ghost=ghost, halo_fn=lambda T: self.exchange(T.data))   # batch 2: flux-plane halos
+
+    def ns_rhs_grad_form(self, op, q: DOFArray) -> DOFArray:
+        ghost = self.exchange(q.data)
+        return op.rhs_grad_form(q, ghost=ghost, halo_fn=lambda gq: self.exchange(gq.data))
     # }}}
 
 

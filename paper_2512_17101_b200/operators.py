@@ -26,13 +26,25 @@ level); the formulation chosen here, following the paper's MIRGE-Com description
 * ideal gas ``p = (gamma-1)(rho E - rho |u|^2/2)``, ``T = p/(rho R)``, constant ``mu, kappa``;
 * boundary conditions by exterior ("plus") states: prescribed far-field state, or wall
   (Euler: slip, momentum reflected about the normal; Navier-Stokes: adiabatic no-slip,
-  momentum negated); ``grad q`` plus-state equals the minus-state on boundary faces.
+  momentum negated); on boundary faces the viscous flux is the interior one,
+  ``Fv(q-, grad q-)``, and the inviscid flux uses the exterior state.
+
+The Navier-Stokes right-hand side exists in two algebraically identical arrangements of the same
+scheme.  ``rhs_grad_form`` = ``dg_ns_grad`` (pass 1 writes ``grad q``) + ``dg_ns_rhs`` (pass 2
+evaluates every flux).  ``rhs`` (default) = ``dg_ns_flux`` + ``dg_ns_div``: pass 1 finishes the BR1
+gradient in registers, evaluates the total flux ``F = F_inv - F_visc`` once per node and stores its
+contravariant, Jacobian-scaled components ``T[r] = sum_x (J dr/dx)[r,x] F[x]`` plus the local wave
+speed; pass 2 is then a pure contraction: the volume term contracts ``T`` directly, and the
+scaled normal flux of either side of a face is a signed sum of ``T`` rows (``facemat``), so the
+neighbour's flux is *gathered*, not recomputed.  Each face flux is evaluated once per node
+instead of three times (own volume, own face, neighbour's face), which is what makes the B200
+path FP64-cheaper.
 """
 from __future__ import annotations
 
 import numpy as np
 
-from .discretization import BC_FARFIELD, BC_WALL, DGDiscretization
+from .discretization import BC_FARFIELD, BC_NONE, BC_WALL, DGDiscretization
 from .dofarray import DOFArray
 
 # {{{ pointwise physics (array-context generic)
@@ -263,11 +275,13 @@ def _make_ns_rhs(dim, with_ghost):
         fnp = _normal_dot(fp, nrm, dim, range(C))
         vnm = _normal_dot(viscous_flux(actx, qm, gm, vm, ph, dim), nrm, dim, range(C))
         vnp = _normal_dot(viscous_flux(actx, qp, gp, vp, ph, dim), nrm, dim, range(C))
+        is_bnd = actx.np.not_equal(bc_kind, BC_NONE)
         fstar = []
         for c in range(C):
             f = 0.5 * (fnm[c] + fnp[c]) + 0.5 * lam * (qm[c] - qp[c])
             if vnm[c] is not None:
-                f = f - 0.5 * (vnm[c] + vnp[c])
+                # boundary faces take the viscous flux of the interior state, Fv(q-, grad q-)
+                f = f - 0.5 * (vnm[c] + actx.np.where(is_bnd, vnm[c], vnp[c]))
             fstar.append(fscale * f)
         fs = actx.np.reshape(actx.np.stack(fstar), (C, E, Nf * Nfp))
         return vol - actx.np.einsum("if,cef->cei", lift, fs)
@@ -282,6 +296,101 @@ def _make_ns_rhs(dim, with_ghost):
             return body(dg_ns_rhs.actx, q, gq, None, None, Sw, drdx, lift, normals, fscale, vmap_m,
                         vmap_p, bc_kind, qfar, phys)
     return dg_ns_rhs
+
+
+def _make_ns_flux(dim, with_ghost):
+    """Pass 1 of the flux arrangement: BR1 gradient -> total flux -> contravariant components.
+    Returns ``(dim*C + 1, E, Np)``: planes ``r*C + c`` hold ``T[r][c] = sum_x jac*drdx[r,x] *
+    (F_inv - F_visc)[x][c]`` and the last plane the wave speed ``|u| + c``."""
+    grad = _make_ns_grad(dim, with_ghost)
+
+    def body(actx, q, ghost, Sw, drdx, jac, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, phys):
+        grad.actx = actx
+        if ghost is None:
+            gq = grad(q, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar)
+        else:
+            gq = grad(q, ghost, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar)
+        C, E, Np = q.shape
+        ph = [phys[k] for k in range(4)]
+        gamma = ph[0]
+        qc = [q[c] for c in range(C)]
+        gc = [[gq[x][c] for c in range(C)] for x in range(dim)]
+        finv, vel, p = inviscid_flux(actx, qc, gamma, dim)
+        fvis = viscous_flux(actx, qc, gc, vel, ph, dim)
+        ftot = [[finv[x][c] if fvis[x][c] is None else finv[x][c] - fvis[x][c] for c in range(C)]
+                for x in range(dim)]
+        fstack = actx.np.stack([actx.np.stack(fx) for fx in ftot])            # (d, C, E, Np)
+        T = actx.np.einsum("rxe,e,xcej->rcej", drdx, jac, fstack)
+        lam = _wavespeed(actx, gamma, qc, vel, p, dim)
+        return actx.np.concatenate([actx.np.reshape(T, (dim * C, E, Np)), actx.np.reshape(lam, (1, E, Np))])
+
+    if with_ghost:
+        def dg_ns_flux(q, ghost, Sw, drdx, jac, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, phys):
+            return body(dg_ns_flux.actx, q, ghost, Sw, drdx, jac, lift, normals, fscale, vmap_m, vmap_p,
+                        bc_kind, qfar, phys)
+    else:
+        def dg_ns_flux(q, Sw, drdx, jac, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, phys):
+            return body(dg_ns_flux.actx, q, None, Sw, drdx, jac, lift, normals, fscale, vmap_m, vmap_p,
+                        bc_kind, qfar, phys)
+    return dg_ns_flux
+
+
+def _make_ns_div(dim, with_ghost):
+    """Pass 2 of the flux arrangement: ``rhs = (1/J) (sum_r Sw_r T_r - lift(sJ F*.n))`` with
+    ``sJ F-.n = sum_r facemat[f,r] T-[r]`` and ``sJ F+.n = -sum_r facemat[f+,r] T+[r]``
+    (``facemat_p`` is ``facemat`` of the neighbour's face, per face)."""
+    def body(actx, q, T, ghost, Tghost, Sw, jac, lift, normals, fscale, facemat, facemat_p, vmap_m, vmap_p,
+             bc_kind, qfar, phys):
+        C, E, Np = q.shape
+        Nf = dim + 1
+        Nfp = lift.shape[1] // Nf
+        L = C + dim * C + 1
+        gamma = phys[0]
+        vol = actx.np.einsum("rij,rcej->cei", Sw, actx.np.reshape(T[0:dim * C], (dim, C, E, Np)))
+        planes = actx.np.concatenate([q, T])                                   # (L, E, Np)
+        gplanes = None if ghost is None else actx.np.concatenate([ghost, Tghost])
+        tm, tp = _traces(actx, planes, gplanes, vmap_m, vmap_p, L, E, Np, Nf, Nfp)
+        nrm = [normals[x] for x in range(dim)]
+        sj = fscale * actx.np.reshape(jac, (E, 1, 1))                          # face Jacobian (E, Nf, 1)
+        qm = [tm[c] for c in range(C)]
+        qp = [tp[c] for c in range(C)]
+        own, nbr = [], []
+        for c in range(C):
+            o = facemat[0] * tm[C + c]
+            n = facemat_p[0] * tp[C + c]
+            for r in range(1, dim):
+                o = o + facemat[r] * tm[C + r * C + c]
+                n = n + facemat_p[r] * tp[C + r * C + c]
+            own.append(o)
+            nbr.append(n)
+        lam_m, lam_p = tm[L - 1], tp[L - 1]
+        # boundary faces: inviscid flux of the exterior state, viscous flux of the interior state
+        qb = _bc_state(actx, qm, qp, nrm, bc_kind, [qfar[c] for c in range(C)], dim, "noslip")
+        fb, vb, pb = inviscid_flux(actx, qb, gamma, dim)
+        fi, _, _ = inviscid_flux(actx, qm, gamma, dim)
+        fnb = _normal_dot(fb, nrm, dim, range(C))
+        fni = _normal_dot(fi, nrm, dim, range(C))
+        lam_b = actx.np.maximum(lam_m, _wavespeed(actx, gamma, qb, vb, pb, dim))
+        is_bnd = actx.np.not_equal(bc_kind, BC_NONE)
+        fstar = []
+        for c in range(C):
+            f_int = 0.5 * (own[c] - nbr[c]) + 0.5 * sj * actx.np.maximum(lam_m, lam_p) * (qm[c] - qp[c])
+            f_bnd = own[c] + 0.5 * sj * (fnb[c] - fni[c]) + 0.5 * sj * lam_b * (qm[c] - qb[c])
+            fstar.append(actx.np.where(is_bnd, f_bnd, f_int))
+        fs = actx.np.reshape(actx.np.stack(fstar), (C, E, Nf * Nfp))
+        return (vol - actx.np.einsum("if,cef->cei", lift, fs)) / actx.np.reshape(jac, (E, 1))
+
+    if with_ghost:
+        def dg_ns_div(q, T, ghost, Tghost, Sw, jac, lift, normals, fscale, facemat, facemat_p, vmap_m, vmap_p,
+                      bc_kind, qfar, phys):
+            return body(dg_ns_div.actx, q, T, ghost, Tghost, Sw, jac, lift, normals, fscale, facemat,
+                        facemat_p, vmap_m, vmap_p, bc_kind, qfar, phys)
+    else:
+        def dg_ns_div(q, T, Sw, jac, lift, normals, fscale, facemat, facemat_p, vmap_m, vmap_p, bc_kind,
+                      qfar, phys):
+            return body(dg_ns_div.actx, q, T, None, None, Sw, jac, lift, normals, fscale, facemat,
+                        facemat_p, vmap_m, vmap_p, bc_kind, qfar, phys)
+    return dg_ns_div
 
 
 def _axpby_outputs(rhs, x1, x2, coef):
@@ -308,6 +417,16 @@ def _make_ns_rhs_rk(dim, with_ghost):
         rhs = inner(q, gq, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, phys)
         return _axpby_outputs(rhs, x1, x2, coef)
     return dg_ns_rhs_rk
+
+def _make_ns_div_rk(dim, with_ghost):
+    inner = _make_ns_div(dim, False)
+
+    def dg_ns_div_rk(q, T, x1, x2, coef, Sw, jac, lift, normals, fscale, facemat, facemat_p, vmap_m, vmap_p,
+                     bc_kind, qfar, phys):
+        inner.actx = dg_ns_div_rk.actx
+        rhs = inner(q, T, Sw, jac, lift, normals, fscale, facemat, facemat_p, vmap_m, vmap_p, bc_kind, qfar, phys)
+        return _axpby_outputs(rhs, x1, x2, coef)
+    return dg_ns_div_rk
 
 # }}}
 
@@ -366,7 +485,11 @@ class EulerOperator(_OperatorBase):
 
 
 class NavierStokesOperator(_OperatorBase):
-    """Two-pass (BR1) compressible Navier-Stokes right-hand side."""
+    """Two-pass (BR1) compressible Navier-Stokes right-hand side.
+
+    ``rhs`` / ``rhs_rk`` use the flux arrangement (``dg_ns_flux`` + ``dg_ns_div``, see the module
+    docstring); ``rhs_grad_form`` / ``rhs_rk_grad_form`` the gradient arrangement (``dg_ns_grad`` +
+    ``dg_ns_rhs``).  Both evaluate the same scheme."""
 
     def __init__(self, dcoll, gamma=1.4, mu=1e-3, prandtl=0.72, rgas=1.0, farfield=None):
         super().__init__(dcoll, gamma=gamma, mu=mu, prandtl=prandtl, rgas=rgas, farfield=farfield)
@@ -374,6 +497,20 @@ class NavierStokesOperator(_OperatorBase):
         self._gg = self._outlined(_make_ns_grad, True)
         self._f = self._outlined(_make_ns_rhs, False)
         self._fg = self._outlined(_make_ns_rhs, True)
+        self._flux = self._outlined(_make_ns_flux, False)
+        self._fluxg = self._outlined(_make_ns_flux, True)
+        self._div = self._outlined(_make_ns_div, False)
+        self._divg = self._outlined(_make_ns_div, True)
+
+    def _flux_args(self):
+        d = self.dcoll
+        return (d.Sw, d.drdx, d.jac, d.lift, d.normals, d.fscale, d.vmap_m, d.vmap_p, d.bc_kind, self.qfar,
+                self.phys)
+
+    def _div_args(self):
+        d = self.dcoll
+        return (d.Sw, d.jac, d.lift, d.normals, d.fscale, d.facemat, d.facemat_p, d.vmap_m, d.vmap_p,
+                d.bc_kind, self.qfar, self.phys)
 
     def grad(self, q: DOFArray, ghost=None) -> DOFArray:
         if ghost is None:
@@ -382,17 +519,41 @@ class NavierStokesOperator(_OperatorBase):
             out = self._gg(q.data, ghost, *self._common())
         return DOFArray(self.actx, out)
 
-    def rhs(self, q: DOFArray, t=0.0, ghost=None, grad_ghost_fn=None) -> DOFArray:
-        gq = self.grad(q, ghost)
+    def flux(self, q: DOFArray, ghost=None):
+        """Pass 1: contravariant total-flux planes + wave speed, ``(dim*C + 1, E, Np)``."""
         if ghost is None:
-            out = self._f(q.data, gq.data, *self._common(), self.phys)
+            return self._flux(q.data, *self._flux_args())
+        return self._fluxg(q.data, ghost, *self._flux_args())
+
+    def rhs(self, q: DOFArray, t=0.0, ghost=None, halo_fn=None) -> DOFArray:
+        """``halo_fn(DOFArray of the pass-1 result) -> ghost array`` performs the second halo
+        exchange on partitioned meshes (flux planes here, ``grad q`` in ``rhs_grad_form``)."""
+        T = self.flux(q, ghost)
+        if ghost is None:
+            out = self._div(q.data, T, *self._div_args())
         else:
-            gghost = grad_ghost_fn(gq)
-            out = self._fg(q.data, gq.data, ghost, gghost, *self._common(), self.phys)
+            out = self._divg(q.data, T, ghost, halo_fn(DOFArray(self.actx, T)), *self._div_args())
         return DOFArray(self.actx, out)
 
     def rhs_rk(self, q: DOFArray, x1: DOFArray, x2: DOFArray, coef, t=0.0):
         """``(a1*x1 + b1*rhs(q), a2*x2 + b2*rhs(q))`` with the stage update fused into the second pass."""
+        if not hasattr(self, "_divrk"):
+            self._divrk = self._outlined(_make_ns_div_rk, False)
+        T = self.flux(q)
+        c = self.actx.from_numpy(np.asarray(coef, dtype=np.float64))
+        out = self._divrk(q.data, T, x1.data, x2.data, c, *self._div_args())
+        return DOFArray(self.actx, out["out1"]), DOFArray(self.actx, out["out2"])
+
+    def rhs_grad_form(self, q: DOFArray, t=0.0, ghost=None, halo_fn=None) -> DOFArray:
+        gq = self.grad(q, ghost)
+        if ghost is None:
+            out = self._f(q.data, gq.data, *self._common(), self.phys)
+        else:
+            gghost = halo_fn(gq)
+            out = self._fg(q.data, gq.data, ghost, gghost, *self._common(), self.phys)
+        return DOFArray(self.actx, out)
+
+    def rhs_rk_grad_form(self, q: DOFArray, x1: DOFArray, x2: DOFArray, coef, t=0.0):
         if not hasattr(self, "_frk"):
             self._frk = self._outlined(_make_ns_rhs_rk, False)
         gq = self.grad(q)

@@ -25,6 +25,8 @@ def run(actx, dim, order, n, bc, opname, kw, q0):
     out = {"rhs": np.asarray(actx.to_numpy(op.rhs(d.from_numpy(q0)).data))}
     if opname == "ns":
         out["grad"] = np.asarray(actx.to_numpy(op.grad(d.from_numpy(q0)).data))
+        out["rhs_grad_form"] = np.asarray(actx.to_numpy(op.rhs_grad_form(d.from_numpy(q0)).data))
+        out["flux"] = np.asarray(actx.to_numpy(op.flux(d.from_numpy(q0))))
     return out, d
 
 

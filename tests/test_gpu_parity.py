@@ -67,6 +67,12 @@ def test_rhs_parity(gpu, dim, order, n, bc):
                 gref = dc.to_numpy(oc.grad(dc.from_numpy(q0)))
                 ggot = dg.to_numpy(og.grad(dg.from_numpy(q0)))
                 assert rel_err(ggot, gref) <= TOL_RHS, ("grad", seed, rel_err(ggot, gref))
+                # pass 1 of the flux arrangement on its own, and the gradient arrangement end to end
+                tref = np.asarray(cpu.to_numpy(oc.flux(dc.from_numpy(q0))))
+                tgot = np.asarray(gpu.to_numpy(og.flux(dg.from_numpy(q0))))
+                assert rel_err(tgot, tref) <= TOL_RHS, ("flux planes", seed, rel_err(tgot, tref))
+                got2 = dg.to_numpy(og.rhs_grad_form(dg.from_numpy(q0)))
+                assert rel_err(got2, ref) <= TOL_RHS, ("grad form", seed, rel_err(got2, ref))
 
 
 @pytest.mark.parametrize("dim,order,n,bc", [(3, 3, 2, "mixed"), (2, 3, 3, "mixed"), (3, 2, 3, "periodic")])
@@ -157,6 +163,8 @@ def test_gpu_matches_reference_golden(gpu):
         assert rel_err(got, g["lazy_rhs"]) <= TOL_RHS, name
         if opname == "ns":
             assert rel_err(d.to_numpy(op.grad(d.from_numpy(g["q0"]))), g["eager_grad"]) <= TOL_RHS, name
+            assert rel_err(d.to_numpy(op.rhs_grad_form(d.from_numpy(g["q0"]))), g["eager_rhs_grad_form"]) <= TOL_RHS, name
+            assert rel_err(gpu.to_numpy(op.flux(d.from_numpy(g["q0"]))), g["eager_flux"]) <= TOL_RHS, name
 
 
 @pytest.mark.parametrize("dim,order,n,Op,kw", [(3, 3, 3, EulerOperator, {}), (3, 3, 3, NavierStokesOperator, {"mu": 1e-2}),
@@ -178,6 +186,12 @@ def test_fused_rk_stage(gpu, dim, order, n, Op, kw):
         t += dt
     assert rel_err(dg.to_numpy(qg), dc.to_numpy(qc)) <= 1e-12
     assert rel_err(dg.to_numpy(qg), dg.to_numpy(qu)) <= 1e-12
+    if Op is NavierStokesOperator:       # the gradient arrangement's fused stage update
+        c = (1.0, 0.5 * dt, 1.0, dt / 6.0)
+        a1, a2 = og.rhs_rk(qg, qg, qu, c)
+        b1, b2 = og.rhs_rk_grad_form(qg, qg, qu, c)
+        assert rel_err(dg.to_numpy(b1), dg.to_numpy(a1)) <= 1e-12
+        assert rel_err(dg.to_numpy(b2), dg.to_numpy(a2)) <= 1e-12
 
 
 @pytest.mark.parametrize("dim,n,per,nparts", [(3, 3, True, 2), (2, 4, False, 3)])
@@ -218,8 +232,14 @@ def test_ghost_elements_on_device(gpu, dim, n, per, nparts):
     gh = exchange([q.data for q in qs])
     gqs = [ops[r].grad(qs[r], gh[r]) for r in range(nparts)]
     ggh = exchange([g.data for g in gqs])
-    full = np.empty_like(ref)
-    for r, (_, p) in enumerate(locs):
-        out = ops[r].rhs(qs[r], ghost=gh[r], grad_ghost_fn=lambda gq, r=r: ggh[r])
-        full[:, p.global_ids, :] = ds[r].to_numpy(out)
-    assert rel_err(full, ref) <= TOL_RHS
+    Ts = [ops[r].flux(qs[r], gh[r]) for r in range(nparts)]
+    tgh = exchange(Ts)
+    for form in ("flux", "grad"):
+        full = np.empty_like(ref)
+        for r, (_, p) in enumerate(locs):
+            if form == "flux":
+                out = ops[r].rhs(qs[r], ghost=gh[r], halo_fn=lambda T, r=r: tgh[r])
+            else:
+                out = ops[r].rhs_grad_form(qs[r], ghost=gh[r], halo_fn=lambda gq, r=r: ggh[r])
+            full[:, p.global_ids, :] = ds[r].to_numpy(out)
+        assert rel_err(full, ref) <= TOL_RHS, form

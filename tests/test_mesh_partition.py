@@ -79,10 +79,20 @@ def test_partitioned_rhs_equals_single_domain(dim, n, per, nparts):
         if Op is EulerOperator:
             res = [ds[r].to_numpy(ops[r].rhs(ds[r].from_numpy(qs[r]), ghost=gh[r])) for r in range(nparts)]
         else:
+            # gradient arrangement: second exchange carries grad q
             gqs = [ds[r].to_numpy(ops[r].grad(ds[r].from_numpy(qs[r]), gh[r])) for r in range(nparts)]
             ggh = _loopback(locs, gqs, d.Np)
+            res = [ds[r].to_numpy(ops[r].rhs_grad_form(ds[r].from_numpy(qs[r]), ghost=gh[r],
+                                                       halo_fn=lambda gq, r=r: ggh[r])) for r in range(nparts)]
+            full = np.empty_like(ref)
+            for r, (m, p) in enumerate(locs):
+                full[:, p.global_ids, :] = res[r]
+            assert rel_err(full, ref) <= 1e-13
+            # flux arrangement (default): second exchange carries the flux planes
+            Ts = [np.asarray(actx.to_numpy(ops[r].flux(ds[r].from_numpy(qs[r]), gh[r]))) for r in range(nparts)]
+            tgh = _loopback(locs, Ts, d.Np)
             res = [ds[r].to_numpy(ops[r].rhs(ds[r].from_numpy(qs[r]), ghost=gh[r],
-                                             grad_ghost_fn=lambda gq, r=r: ggh[r])) for r in range(nparts)]
+                                             halo_fn=lambda T, r=r: tgh[r])) for r in range(nparts)]
         full = np.empty_like(ref)
         for r, (m, p) in enumerate(locs):
             full[:, p.global_ids, :] = res[r]
@@ -139,10 +149,10 @@ def test_ring_slab_equals_global_periodic_mesh():
 
     ops = [NavierStokesOperator(dd, mu=2e-2) for dd in ds]
     gh = exch(qs)
-    gqs = [ds[r].to_numpy(ops[r].grad(ds[r].from_numpy(qs[r]), gh[r])) for r in range(R)]
-    ggh = exch(gqs)
+    Ts = [np.asarray(ops[r].flux(ds[r].from_numpy(qs[r]), gh[r])) for r in range(R)]
+    tgh = exch(Ts)
     for r in range(R):
-        out = ds[r].to_numpy(ops[r].rhs(ds[r].from_numpy(qs[r]), ghost=gh[r], grad_ghost_fn=lambda gq, r=r: ggh[r]))
+        out = ds[r].to_numpy(ops[r].rhs(ds[r].from_numpy(qs[r]), ghost=gh[r], halo_fn=lambda T, r=r: tgh[r]))
         cent = base.vertices.mean(axis=1) + np.array([2.0 * r, 0, 0])
         idx = np.array([gkey[tuple(np.round(c, 9))] for c in cent])
         assert rel_err(out, ref[:, idx, :]) <= 1e-12

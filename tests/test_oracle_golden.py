@@ -33,6 +33,13 @@ def test_operator_program_matches_reference(case):
         grad = d.to_numpy(op.grad(d.from_numpy(g["q0"])))
         assert np.array_equal(grad, g["eager_grad"])
         assert rel_err(grad, g["lazy_grad"]) <= 1e-12
+        # both arrangements of the scheme (operators.py) against the reference's eager and lazy results
+        alt = d.to_numpy(op.rhs_grad_form(d.from_numpy(g["q0"])))
+        assert np.array_equal(alt, g["eager_rhs_grad_form"])
+        assert rel_err(alt, g["lazy_rhs_grad_form"]) <= 1e-12
+        assert rel_err(alt, rhs) <= 1e-13
+        T = np.asarray(op.flux(d.from_numpy(g["q0"])))
+        assert np.array_equal(T, g["eager_flux"]) and rel_err(T, g["lazy_flux"]) <= 1e-12
 
 
 def test_rk4_matches_reference():

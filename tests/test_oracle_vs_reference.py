@@ -63,4 +63,8 @@ def test_outlined_functions_become_call_nodes(laze):
     g = op.grad(q)
     assert isinstance(g.data.node, CallResult) and g.data.node.call.function.name == "dg_ns_grad"
     r = op.rhs(q)
+    assert r.data.node.call.function.name == "dg_ns_div"
+    T = op.flux(q)
+    assert isinstance(T.node, CallResult) and T.node.call.function.name == "dg_ns_flux"
+    r = op.rhs_grad_form(q)
     assert r.data.node.call.function.name == "dg_ns_rhs"
