@@ -28,6 +28,9 @@ NP = 20
 B_ALG_RHS = 360.0      # algorithmic bytes per node-DOF per NS RHS: (3C + 2Cd) * 8, C=5, d=3
 B_ALG_GRAD = 160.0     # pass 1: read q (40) + write grad q (120)
 B_ALG_DIV = 200.0      # pass 2: read q (40) + read grad q (120) + write rhs (40)
+# The flux arrangement (default) stores 16 planes (15 contravariant flux + wave speed) instead of 15; its
+# roofline fractions are still quoted against the SURVEY figures above (160 / 200 / 360 B per DOF), i.e.
+# the extra plane counts as overhead, not as useful traffic.
 PHYS = dict(gamma=1.4, mu=1e-3, prandtl=0.72, rgas=1.0)
 CPU_REPS = 16          # RHS evaluations per process in one CPU sample (~10-15 s of CPU work)
 
@@ -223,39 +226,57 @@ def run_b200(args):
     actx.synchronize()
     t_setup = time.perf_counter() - t_setup
 
+    grad_form = args.form == "grad" and not euler
+
     def rhs_step(qarr):
         if halo is None:
-            return op.rhs(qarr)
-        return halo.euler_rhs(op, qarr) if euler else halo.ns_rhs(op, qarr)
+            return op.rhs_grad_form(qarr) if grad_form else op.rhs(qarr)
+        if euler:
+            return halo.euler_rhs(op, qarr)
+        return halo.ns_rhs_grad_form(op, qarr) if grad_form else halo.ns_rhs(op, qarr)
 
     # ---- device-resident measurement --------------------------------------------------------
     stream = actx.stream
+    K = args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+
+    def one_step(marks=None):
+        """One RHS evaluation; `marks` = three events recorded before pass 1, between the passes and
+        after pass 2.  Warm-up and timed steps run this same code, so the caching allocator sees the
+        same request pattern and never calls cudaMalloc inside the timed region."""
+        rec = (lambda i: marks[i].record(stream)) if marks is not None else (lambda i: None)
+        if halo is None and not euler and grad_form:
+            rec(0)
+            gq = op.grad(q)
+            rec(1)
+            op._f(q.data, gq.data, *op._common(), op.phys)
+            rec(2)
+        elif halo is None and not euler:
+            rec(0)
+            T = op.flux(q)
+            rec(1)
+            op._div(q.data, T, *op._div_args())
+            rec(2)
+        elif halo is None:
+            rec(0)
+            rec(1)
+            op.rhs(q)
+            rec(2)
+        else:
+            rhs_step(q)
+
     for _ in range(max(args.warmup, 3)):
-        rhs_step(q)
+        one_step()
     actx.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     sampler = ClockSampler(local_rank) if rank == 0 else None
-    K = args.steps
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
     launches0 = actx.launch_count
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record(stream)
     for k in range(K):
-        if halo is None and not euler:
-            ev[k][0].record(stream)
-            gq = op.grad(q)
-            ev[k][1].record(stream)
-            op._f(q.data, gq.data, *op._common(), op.phys)
-            ev[k][2].record(stream)
-        elif halo is None:
-            ev[k][0].record(stream)
-            ev[k][1].record(stream)
-            op.rhs(q)
-            ev[k][2].record(stream)
-        else:
-            rhs_step(q)
+        one_step(ev[k])
     stop.record(stream)
     if world > 1:
         dist.barrier()
@@ -278,8 +299,9 @@ def run_b200(args):
         if euler:
             dom = ("k_rhs3<inviscid> (fused Euler RHS)", ms_div, 80.0)
         else:
-            dom = ("k_rhs3<viscous> (flux + divergence pass)", ms_div, B_ALG_DIV) if ms_div >= ms_grad else \
-                  ("k_grad3 (BR1 gradient pass)", ms_grad, B_ALG_GRAD)
+            names = ("k_rhs3<viscous> (flux + divergence pass)", "k_grad3 (BR1 gradient pass)") if grad_form else \
+                    ("k_nsdiv3 (divergence + face pass)", "k_nsflux3 (BR1 gradient + flux pass)")
+            dom = (names[0], ms_div, B_ALG_DIV) if ms_div >= ms_grad else (names[1], ms_grad, B_ALG_GRAD)
         achieved = ndof * dom[2] / (dom[1] * 1e-3) / 1e9
         traffic = None
         tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
@@ -287,8 +309,12 @@ def run_b200(args):
             with open(tpath) as fh:
                 tj = json.load(fh)
             if tj.get("n") == n and ORDER == 3 and not euler:      # ncu capture of exactly this workload (bytes per launch)
-                key = "k_rhs3_viscous" if ms_div >= ms_grad else "k_grad3"
-                traffic = tj[key]["dram_read_bytes"] + tj[key]["dram_write_bytes"]
+                if grad_form:
+                    key = "k_rhs3_viscous" if ms_div >= ms_grad else "k_grad3"
+                else:
+                    key = "k_nsdiv3" if ms_div >= ms_grad else "k_nsflux3"
+                if key in tj:
+                    traffic = tj[key]["dram_read_bytes"] + tj[key]["dram_write_bytes"]
         per_step = [e[0].elapsed_time(e[2]) for e in ev]
         roofline = {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
@@ -353,6 +379,8 @@ def run_b200(args):
                        "elements_per_gpu": E, "dofs_per_gpu": ndof, "order": ORDER, "dim": DIM,
                        "l2_policy": "inputs larger than L2 (q 4.0 GB, grad q 12 GB per GPU vs 126 MB L2)"
                        if ndof * 40 > 126e6 * 4 else "inputs comparable to L2: reduced size, not the headline config",
+                       "arrangement": ("euler single pass" if euler else
+                                       "gradient (dg_ns_grad + dg_ns_rhs)" if grad_form else "flux (dg_ns_flux + dg_ns_div)"),
                        "parallelism": f"mesh partition x{world}, NCCL face-halo exchange" if world > 1 else "single GPU",
                        "setup_s": t_setup},
             "roofline": roofline,
@@ -378,6 +406,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--order", type=int, default=3, help="polynomial order (headline: 3)")
+    ap.add_argument("--form", default="flux", choices=["flux", "grad"],
+                    help="arrangement of the NS scheme: flux (default; dg_ns_flux + dg_ns_div) or grad (dg_ns_grad + dg_ns_rhs)")
     ap.add_argument("--workload", default="ns", choices=["ns", "euler"],
                     help="ns = BASELINE configs[2] (headline); euler = configs[1] (3D Euler, read q + write rhs = 80 B/DOF)")
     args = ap.parse_args()

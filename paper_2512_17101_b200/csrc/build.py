@@ -21,17 +21,21 @@ def needs_build() -> bool:
     return any(os.path.getmtime(os.path.join(HERE, d)) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, defines: list[str] | None = None, out: str | None = None,
+          sources: list[str] | None = None) -> str:
+    """``defines``/``out`` build a tuning variant beside the default library (select it with
+    the environment variable DGB_LIB, see _cabi.py); used by scripts/ab_variants.py."""
+    if out is None and not force and not needs_build():
         return OUT
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, "--threads", "0"] + FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-o", OUT] + SOURCES
+    cmd = [nvcc, "--threads", "0"] + FLAGS + (["-Xptxas", "-v"] if verbose else []) + \
+          [f"-D{d}" for d in (defines or [])] + ["-o", out or OUT] + (sources or SOURCES)
     res = subprocess.run(cmd, cwd=HERE, capture_output=True, text=True)
     if verbose:
         sys.stderr.write(res.stderr)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed:\n{res.stderr}")
-    return OUT
+    return out or OUT
 
 
 if __name__ == "__main__":

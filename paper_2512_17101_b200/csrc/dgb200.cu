@@ -324,8 +324,8 @@ int dispatch_grad(const dgb_disc* d, const double* q, const double* ghost, doubl
 }
 
 template <int DIM, int P>
-void fill_padded(const double* Sw, const double* lift, std::vector<double>& Wv, std::vector<double>& Wl,
-                 std::vector<double>& Wq, std::vector<double>& Wf) {
+void fill_padded(const double* Sw, const double* lift, const int64_t* face_nodes, std::vector<double>& Wv,
+                 std::vector<double>& Wl, std::vector<double>& Wq, std::vector<double>& Wf, std::vector<double>& Wv2) {
   using EL = dgb::ElemT<DIM, P>;
   Wv.assign((size_t)EL::NPR * EL::LDV, 0.0);
   Wl.assign((size_t)EL::NPR * EL::LDF, 0.0);
@@ -344,6 +344,21 @@ void fill_padded(const double* Sw, const double* lift, std::vector<double>& Wv, 
         const double v = lift[(size_t)i * EL::NFT + f * EL::NFP + m];
         Wl[(size_t)i * EL::LDF + f * EL::NFP + m] = v;
         Wf[((size_t)f * EL::NPR + i) * EL::LDL + m] = v;
+      }
+  // flux arrangement: sJ F-.n at face node (f, m) is sum_r a[f][r] T[r][fn[f][m]] with a[0][r] = 1,
+  // a[f][r] = -delta(r, f-1); the numerical flux contains half of it, which therefore folds into
+  // the volume matrix:  Wv2[i][r, j] = Sw_r[i][j] - 1/2 sum_{(f,m): fn[f][m] = j} a[f][r] lift[i][f, m]
+  Wv2 = Wv;
+  for (int i = 0; i < EL::NP; ++i)
+    for (int f = 0; f < EL::NF; ++f)
+      for (int m = 0; m < EL::NFP; ++m) {
+        const int j = (int)face_nodes[f * EL::NFP + m];
+        if (j < 0 || j >= EL::NP) continue;          // rejected by dgb_disc_create right after this
+        const double v = lift[(size_t)i * EL::NFT + f * EL::NFP + m];
+        for (int r = 0; r < DIM; ++r) {
+          const double a = f == 0 ? 1.0 : (r == f - 1 ? -1.0 : 0.0);
+          Wv2[(size_t)i * EL::LDV + r * EL::NPK + j] -= 0.5 * a * v;
+        }
       }
 }
 
@@ -398,12 +413,12 @@ int dgb_disc_create(dgb_disc** out, int dim, int order, int64_t E, int64_t G, co
   *out = nullptr;
   if (E < 0 || G < 0 || E + G >= (1LL << 31)) return fail(DGB_ERR_INVALID, "element count out of range");
   cudaStream_t st = (cudaStream_t)stream;
-  std::vector<double> Wv, Wl, Wq, Wf;
+  std::vector<double> Wv, Wl, Wq, Wf, Wv2;
   int Np = 0, Nf = 0, Nfp = 0, nperm = 0;
   bool ok = false;
 #define X(DIM, P)                                                        \
   if (dim == DIM && order == P) {                                        \
-    fill_padded<DIM, P>(Sw_host, lift_host, Wv, Wl, Wq, Wf);             \
+    fill_padded<DIM, P>(Sw_host, lift_host, face_nodes_host, Wv, Wl, Wq, Wf, Wv2); \
     elem_sizes<DIM, P>(&Np, &Nf, &Nfp, &nperm);                          \
     ok = true;                                                           \
   }
@@ -423,7 +438,7 @@ int dgb_disc_create(dgb_disc** out, int dim, int order, int64_t E, int64_t G, co
   d->dim = dim; d->order = order; d->Np = Np; d->Nf = Nf; d->Nfp = Nfp; d->nperm = nperm;
   int rc;
   if ((rc = upload(&d->Wv, Wv, st)) || (rc = upload(&d->Wl, Wl, st)) || (rc = upload(&d->Wq, Wq, st)) ||
-      (rc = upload(&d->Wf, Wf, st)) || (rc = upload(&d->tables, tables, st))) { dgb_disc_destroy(d); return rc; }
+      (rc = upload(&d->Wf, Wf, st)) || (rc = upload(&d->Wv2, Wv2, st)) || (rc = upload(&d->tables, tables, st))) { dgb_disc_destroy(d); return rc; }
   int* err_dev = nullptr;
   cudaError_t ce = cudaMalloc((void**)&d->conn, sizeof(long long) * (size_t)(E * Nf ? E * Nf : 1));
   if (ce == cudaSuccess) ce = cudaMalloc((void**)&err_dev, sizeof(int));
@@ -452,7 +467,7 @@ int dgb_disc_create(dgb_disc** out, int dim, int order, int64_t E, int64_t G, co
     dgb_disc_destroy(d); return fail(DGB_ERR_CUDA, "work counters");
   }
   d->dev.E = E; d->dev.G = G;
-  d->dev.Wv = d->Wv; d->dev.Wl = d->Wl; d->dev.Wq = d->Wq; d->dev.Wf = d->Wf;
+  d->dev.Wv = d->Wv; d->dev.Wl = d->Wl; d->dev.Wq = d->Wq; d->dev.Wf = d->Wf; d->dev.Wv2 = d->Wv2;
   d->dev.drdx = drdx_dev; d->dev.normals = normals_dev; d->dev.fscale = fscale_dev;
   d->dev.conn = d->conn; d->dev.tables = d->tables;
   d->bc_kind = bc_kind_dev;
@@ -463,7 +478,7 @@ int dgb_disc_create(dgb_disc** out, int dim, int order, int64_t E, int64_t G, co
 int dgb_disc_destroy(dgb_disc* d) {
   if (!d) return DGB_OK;
   dgb_disc_free_jacobian(d);
-  cudaFree(d->Wv); cudaFree(d->Wl); cudaFree(d->Wq); cudaFree(d->Wf); cudaFree(d->conn); cudaFree(d->tables); cudaFree(d->timing); cudaFree(d->counters);
+  cudaFree(d->Wv2); cudaFree(d->Wv); cudaFree(d->Wl); cudaFree(d->Wq); cudaFree(d->Wf); cudaFree(d->conn); cudaFree(d->tables); cudaFree(d->timing); cudaFree(d->counters);
   delete d;
   return DGB_OK;
 }

@@ -18,7 +18,7 @@ int dgb_num_sms();
 struct dgb_disc {
   int dim = 0, order = 0, Np = 0, Nf = 0, Nfp = 0, nperm = 0;
   dgb::DiscDev dev{};
-  double *Wv = nullptr, *Wl = nullptr, *Wq = nullptr, *Wf = nullptr;
+  double *Wv = nullptr, *Wl = nullptr, *Wq = nullptr, *Wf = nullptr, *Wv2 = nullptr;
   long long* conn = nullptr;
   long long* timing = nullptr;
   unsigned long long* counters = nullptr;   // work counters: [0] gradient / flux pass, [1] divergence pass

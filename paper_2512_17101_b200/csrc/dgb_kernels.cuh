@@ -69,6 +69,7 @@ struct DiscDev {
   const double* jac;     // [E] volume Jacobian
   const double* sj;      // [E][NF] face Jacobian = fscale * jac
   const double* rj;      // [E] 1 / jac
+  const double* Wv2;     // [NPR][LDV] volume matrix minus half the lifted own-side face term
 };
 
 struct Phys { double gamma, mu, kappa, rgas; double qfar[5]; };

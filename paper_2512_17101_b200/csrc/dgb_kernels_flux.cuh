@@ -20,11 +20,47 @@
 #include "dgb_kernels_async.cuh"
 #include "dgb_kernels_warp.cuh"
 
+#ifndef DGB_FLUX_NB
+#define DGB_FLUX_NB 2
+#endif
+#ifndef DGB_DIV_NB
+#define DGB_DIV_NB 2
+#endif
+#ifndef DGB_DIV_LAZY_EX
+#define DGB_DIV_LAZY_EX 0
+#endif
+
 namespace dgb {
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+
+// Split-phase dynamic work distribution: the ticket is drawn (atomicAdd on lane 0) one block ahead of
+// its use, so the atomic's round trip to L2 overlaps a whole block of work instead of stalling the warp.
+__device__ __forceinline__ unsigned long long draw_ticket(unsigned long long* counter, int lane) {
+  // predicated atom inside the asm block: no select on the result, so nothing waits for it until
+  // ticket_block() shuffles lane 0's value out (a C++ `if (lane == 0) v = atomicAdd()` merges the
+  // result into `v` right away and stalled every warp for the full L2 round trip: 13 % of samples)
+  unsigned long long v;
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.eq.s32 p, %2, 0;\n\t@p atom.global.add.u64 %0, [%1], 1;\n\t}"
+               : "=l"(v) : "l"(counter), "r"(lane) : "memory");
+  return v;
+}
+__device__ __forceinline__ long long ticket_block(unsigned long long v, long long first_dynamic) {
+  return first_dynamic + (long long)__shfl_sync(0xffffffffu, v, 0);
+}
+
+// Face node n = lane + 32*k of a warp's block, decoded once per lane: bits 0-1 element, 2-3 face,
+// 4-7 node within the face, 8-15 own volume node, 16-23 f*NFP + m; negative = no such face node.
+template <int DIM, int P, int KW>
+__device__ __forceinline__ int face_lane_code(const int* fn, int n) {
+  using EL = ElemT<DIM, P>;
+  if (n >= KW * EL::NFT) return -1;
+  const int e = n / EL::NFT, fm = n - e * EL::NFT;
+  const int f = fm / EL::NFP, m = fm - f * EL::NFP;
+  return e | (f << 2) | (m << 4) | (fn[fm] << 8) | (fm << 16);
 }
 
 template <int DIM, int P>
@@ -68,6 +104,7 @@ struct Flux3Smem {
   Flux3Warp<DIM, P, KW> w[NWARPS];
   int fn[EL::NF * EL::NFP];
   int perm[EL::NPERM * EL::NFP];
+  int flc[((KW * EL::NFT + 31) / 32) * 32];      // face_lane_code of every face node of a block
 };
 
 template <int DIM, int P, int KW>
@@ -76,31 +113,38 @@ __device__ __forceinline__ void flux_stage_async(double* Qs, FluxGeo<DIM, P, KW>
   using EL = ElemT<DIM, P>;
   constexpr int C = EL::C, NP = EL::NP, NF = EL::NF;
   const long long E = d.E;
-  if (NP % 2 == 0) {
-    constexpr int H = NP / 2;
-    for (int n = lane; n < C * nel * H; n += 32) {
-      const int c = n / (nel * H), ej = n - c * (nel * H);
-      const int e = ej / H, j = 2 * (ej - e * H);
-      cp_async16(Qs + (c * KW + e) * EL::LDQ + j, q + ((long long)c * E + e0 + e) * NP + j);
+  // a block's rows are KW*NP consecutive doubles of every plane; lane t copies chunk t of each plane
+  constexpr int CH = (NP % 2 == 0) ? 2 : 1, NPC = NP / CH;
+#pragma unroll
+  for (int t0 = 0; t0 < KW * NPC; t0 += 32) {
+    const int t = t0 + lane;
+    const int e = t / NPC, j = CH * (t - e * NPC);
+    if (t < KW * NPC && e < nel) {
+      double* dst = Qs + e * EL::LDQ + j;
+      const double* src = q + (e0 + e) * NP + j;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        if (CH == 2) cp_async16(dst + c * (KW * EL::LDQ), src + (long long)c * E * NP);
+        else cp_async8(dst + c * (KW * EL::LDQ), src + (long long)c * E * NP);
+      }
     }
-  } else {
-    for (int n = lane; n < C * nel * NP; n += 32) {
-      const int c = n / (nel * NP), ej = n - c * (nel * NP);
-      const int e = ej / NP, j = ej - e * NP;
-      cp_async8(Qs + (c * KW + e) * EL::LDQ + j, q + ((long long)c * E + e0) * NP + ej);
+  }
+  {
+    const int e = lane % KW, rx = lane / KW;        // drdx[rx][e]
+    if (KW * DIM * DIM <= 32) {
+      if (rx < DIM * DIM && e < nel) cp_async8(&g.drdx[rx][e], d.drdx + (long long)rx * E + e0 + e);
+    } else {
+      for (int n = lane; n < DIM * DIM * KW; n += 32) {
+        const int rx2 = n / KW, e2 = n - rx2 * KW;
+        if (e2 < nel) cp_async8(&g.drdx[rx2][e2], d.drdx + (long long)rx2 * E + e0 + e2);
+      }
     }
   }
-  for (int n = lane; n < DIM * DIM * KW; n += 32) {
-    const int rx = n / KW, e = n - rx * KW;
-    if (e < nel) cp_async8(&g.drdx[rx][e], d.drdx + (long long)rx * E + e0 + e);
-  }
-  for (int n = lane; n < DIM * KW * NF; n += 32) {
-    const int x = n / (KW * NF), ef = n - x * (KW * NF);
-    if (ef < nel * NF) cp_async8(&g.nrm[x][0][ef], d.normals + ((long long)x * E + e0) * NF + ef);
-  }
-  for (int n = lane; n < nel * NF; n += 32) {
-    cp_async8(&g.fsc[0][n], d.fscale + e0 * NF + n);
-    cp_async8(&g.conn[0][n], d.conn + e0 * NF + n);
+  if (lane < nel * NF) {
+#pragma unroll
+    for (int x = 0; x < DIM; ++x) cp_async8(&g.nrm[x][0][lane], d.normals + ((long long)x * E + e0) * NF + lane);
+    cp_async8(&g.fsc[0][lane], d.fscale + e0 * NF + lane);
+    cp_async8(&g.conn[0][lane], d.conn + e0 * NF + lane);
   }
   if (lane < nel) cp_async8(&g.jac[lane], d.jac + e0 + lane);
 }
@@ -114,6 +158,8 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
   constexpr int C = EL::C, NP = EL::NP, NF = EL::NF, NFP = EL::NFP, NFT = EL::NFT, NI = EL::NI;
   constexpr int LDSX = FluxT<DIM, P>::LDSX;
   constexpr int NT = NWARPS * 32;
+  constexpr int NR = (KW * NFT + 31) / 32;        // face-node rounds per block
+  constexpr int NBF = DGB_FLUX_NB;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   auto& S = *reinterpret_cast<Flux3Smem<DIM, P, KW, NWARPS>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -128,6 +174,9 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
   for (int n = lane; n < WS::NCOLP * LDSX; n += 32) W.Ss[n] = 0.0;
   __syncthreads();
 
+  for (int n = tid; n < NR * 32; n += NT) S.flc[n] = face_lane_code<DIM, P, KW>(S.fn, n);
+  __syncthreads();
+
   const long long wstride = (long long)gridDim.x * NWARPS;
   long long wb = (long long)blockIdx.x * NWARPS + warp;
   int buf = 0;
@@ -136,21 +185,24 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
     flux_stage_async<DIM, P, KW>(W.Qs[0], W.geo[0], d, q, e0, (int)((E - e0) < (long long)KW ? (E - e0) : (long long)KW), lane);
   }
   cp_async_commit();
+  unsigned long long ticket = draw_ticket(counter, lane);
 
   while (wb < nwblocks) {
     const long long e0 = wb * KW;
     const int nel = (int)((E - e0) < (long long)KW ? (E - e0) : (long long)KW);
+    // the next block (its ticket was drawn one block ago) starts its trip from HBM now
+    const long long wb_next = ticket_block(ticket, wstride);
     cp_async_wait<0>();
     __syncwarp();
     const double* Qs = W.Qs[buf];
     const FluxGeo<DIM, P, KW>& geo = W.geo[buf];
-    const long long wb_next = next_block(counter, wstride, lane);
     if (wb_next < nwblocks) {
       const long long e1 = wb_next * KW;
       flux_stage_async<DIM, P, KW>(W.Qs[buf ^ 1], W.geo[buf ^ 1], d, q, e1,
                                    (int)((E - e1) < (long long)KW ? (E - e1) : (long long)KW), lane);
     }
     cp_async_commit();
+    ticket = draw_ticket(counter, lane);
 
     // ---- face averages q* (central flux, boundary states) -> Ss; metric coefficients ---------
     for (int n = lane; n < nel * DIM * EL::NS; n += 32) {
@@ -166,31 +218,51 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
         W.Ss[col * LDSX + f * EL::NFPK + m] = 0.0;
       }
     }
-    for (int n = lane; n < nel * NFT; n += 32) {
-      const int e = n / NFT, fm = n - e * NFT;
-      const int f = fm / NFP, m = fm - f * NFP;
-      const long long cn = geo.conn[e][f];
-      const long long nb = DGB_CONN_NB(cn);
-      const int nf = DGB_CONN_NF(cn), pid = DGB_CONN_PERM(cn), bc = DGB_CONN_BC(cn);
-      const int jm = S.fn[f * NFP + m];
-      const int jp = S.fn[nf * NFP + S.perm[pid * NFP + m]];
-      const bool in_ghost = nb >= E;
-      const long long pE = in_ghost ? G : E;
-      const double* pbase = (in_ghost ? ghost : q) + (in_ghost ? nb - E : nb) * NP + jp;
-      double qm[C], qp[C];
+    // NBF face nodes per lane have their neighbour loads in flight together
+#pragma unroll 1
+    for (int k0 = 0; k0 < NR; k0 += NBF) {
+      double qp[NBF][C];
+      long long cnk[NBF];
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-        qp[c] = pbase[(long long)c * pE * NP];
-        qm[c] = Qs[(c * KW + e) * EL::LDQ + jm];
+      for (int b = 0; b < NBF; ++b) {
+        const int k = k0 + b;
+        cnk[b] = -1;
+        if (k < NR) {
+          const int flk = S.flc[k * 32 + lane];
+          const int e = flk & 3, f = (flk >> 2) & 3, m = (flk >> 4) & 15;
+          if (flk >= 0 && e < nel) {
+            const long long cn = geo.conn[e][f];
+            cnk[b] = cn;
+            const long long nb = DGB_CONN_NB(cn);
+            const int jp = S.fn[DGB_CONN_NF(cn) * NFP + S.perm[DGB_CONN_PERM(cn) * NFP + m]];
+            const bool in_ghost = nb >= E;
+            const long long pstride = (in_ghost ? G : E) * NP;
+            const double* pbase = (in_ghost ? ghost : q) + (in_ghost ? nb - E : nb) * NP + jp;
+#pragma unroll
+            for (int c = 0; c < C; ++c) qp[b][c] = pbase[c * pstride];
+          }
+        }
       }
-      if (bc != 0) {
-        double nrm[DIM];
 #pragma unroll
-        for (int x = 0; x < DIM; ++x) nrm[x] = geo.nrm[x][e][f];
-        bc_state<DIM, true>(bc, qm, nrm, ph, qp);
+      for (int b = 0; b < NBF; ++b) {
+        const int k = k0 + b;
+        if (k < NR && cnk[b] >= 0) {
+          const int flk = S.flc[k * 32 + lane];
+          const int e = flk & 3, f = (flk >> 2) & 3, m = (flk >> 4) & 15, jm = (flk >> 8) & 255;
+          const int bc = DGB_CONN_BC(cnk[b]);
+          double qm[C];
+#pragma unroll
+          for (int c = 0; c < C; ++c) qm[c] = Qs[(c * KW + e) * EL::LDQ + jm];
+          if (bc != 0) {
+            double nrm[DIM];
+#pragma unroll
+            for (int x = 0; x < DIM; ++x) nrm[x] = geo.nrm[x][e][f];
+            bc_state<DIM, true>(bc, qm, nrm, ph, qp[b]);
+          }
+#pragma unroll
+          for (int c = 0; c < C; ++c) W.Ss[(c * KW + e) * LDSX + f * EL::NFPK + m] = 0.5 * (qm[c] + qp[b][c]);
+        }
       }
-#pragma unroll
-      for (int c = 0; c < C; ++c) W.Ss[(c * KW + e) * LDSX + f * EL::NFPK + m] = 0.5 * (qm[c] + qp[c]);
     }
     __syncwarp();
 
@@ -233,8 +305,12 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
 #pragma unroll
             for (int s = 0; s < NF; ++s) { v0 += cf[DIM + s] * accU[s][0][ni][0]; v1 += cf[DIM + s] * accU[s][0][ni][1]; }
             const int i = ni * 8 + 2 * (lane & 3);
-            if (i < NP) sg[(x * 8 + k8) * NP + i] = v0;
-            if (i + 1 < NP) sg[(x * 8 + k8) * NP + i + 1] = v1;
+            if (NP % 2 == 0) {
+              if (i < NP) *reinterpret_cast<double2*>(sg + (x * 8 + k8) * NP + i) = make_double2(v0, v1);
+            } else {
+              if (i < NP) sg[(x * 8 + k8) * NP + i] = v0;
+              if (i + 1 < NP) sg[(x * 8 + k8) * NP + i + 1] = v1;
+            }
           }
         }
       }
@@ -242,42 +318,46 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
     __syncwarp();
 
     // ---- pointwise: total flux at every node, contravariant + Jacobian-scaled, and the wave speed ----
-    for (int n = lane; n < nel * NP; n += 32) {
+#pragma unroll
+    for (int n0 = 0; n0 < KW * NP; n0 += 32) {
+      const int n = n0 + lane;
       const int e = n / NP, j = n - e * NP;
-      double qq[C], g[DIM][C];
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        const int col = c * KW + e;
-        qq[c] = Qs[col * EL::LDQ + j];
-        const double* sg = W.Ss + (col >> 3) * 8 * LDSX + (col & 7) * NP + j;
-#pragma unroll
-        for (int x = 0; x < DIM; ++x) g[x][c] = sg[x * 8 * NP];
-      }
-      Prim<DIM> s;
-      make_prim<DIM>(qq, ph.gamma, s);
-      double F[DIM][C], Fv[DIM][C];
-      inviscid_flux<DIM>(s, F);
-      viscous_flux<DIM>(s, g, ph, Fv);
-#pragma unroll
-      for (int x = 0; x < DIM; ++x)
-#pragma unroll
-        for (int c = 1; c < C; ++c) F[x][c] -= Fv[x][c];
-      const double J = geo.jac[e];
-      double* out = T + e0 * NP + n;
-#pragma unroll
-      for (int r = 0; r < DIM; ++r) {
-        double m[DIM];
-#pragma unroll
-        for (int x = 0; x < DIM; ++x) m[x] = J * geo.drdx[r * DIM + x][e];
+      if (n < KW * NP && e < nel) {
+        double qq[C], g[DIM][C];
 #pragma unroll
         for (int c = 0; c < C; ++c) {
-          double acc = m[0] * F[0][c];
+          const int col = c * KW + e;
+          qq[c] = Qs[col * EL::LDQ + j];
+          const double* sg = W.Ss + (col >> 3) * 8 * LDSX + (col & 7) * NP + j;
 #pragma unroll
-          for (int x = 1; x < DIM; ++x) acc += m[x] * F[x][c];
-          out[(long long)(r * C + c) * E * NP] = acc;
+          for (int x = 0; x < DIM; ++x) g[x][c] = sg[x * 8 * NP];
         }
+        Prim<DIM> s;
+        make_prim<DIM>(qq, ph.gamma, s);
+        double F[DIM][C], Fv[DIM][C];
+        inviscid_flux<DIM>(s, F);
+        viscous_flux<DIM>(s, g, ph, Fv);
+#pragma unroll
+        for (int x = 0; x < DIM; ++x)
+#pragma unroll
+          for (int c = 1; c < C; ++c) F[x][c] -= Fv[x][c];
+        const double J = geo.jac[e];
+        double* out = T + e0 * NP + n;
+#pragma unroll
+        for (int r = 0; r < DIM; ++r) {
+          double m[DIM];
+#pragma unroll
+          for (int x = 0; x < DIM; ++x) m[x] = J * geo.drdx[r * DIM + x][e];
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            double acc = m[0] * F[0][c];
+#pragma unroll
+            for (int x = 1; x < DIM; ++x) acc += m[x] * F[x][c];
+            out[(long long)(r * C + c) * E * NP] = acc;
+          }
+        }
+        out[(long long)(DIM * C) * E * NP] = wavespeed<DIM>(s, ph.gamma);
       }
-      out[(long long)(DIM * C) * E * NP] = wavespeed<DIM>(s, ph.gamma);
     }
     __syncwarp();
     wb = wb_next;
@@ -289,6 +369,17 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
 // ------------------------------------------------------------------------------------------
 // pass 2: divergence of the stored flux + face terms
 // ------------------------------------------------------------------------------------------
+// Per-block inputs of the face phase: small, double-buffered, prefetched one block ahead.
+template <int DIM, int P, int KW>
+struct alignas(16) Div3Small {
+  using EL = ElemT<DIM, P>;
+  double Qs[EL::C * KW * EL::NP];
+  double Lam[KW * EL::NP];
+  double sj[KW][EL::NF];
+  long long conn[KW][EL::NF];
+  double rj[KW];
+};
+
 template <int DIM, int P, int KW>
 struct alignas(16) Div3Warp {
   using EL = ElemT<DIM, P>;
@@ -299,80 +390,105 @@ struct alignas(16) Div3Warp {
   // stored and DMMA rows do not mix
   double Ts[NCOL * EL::LDV];
   double Fs[NCOL * EL::LDF];
-  double Qs[NCOL * EL::NP];
-  double Lam[KW * EL::NP];
-  double sj[KW][EL::NF];
-  long long conn[KW][EL::NF];
-  double rj[KW];
+  Div3Small<DIM, P, KW> sm[2];
 };
 
 template <int DIM, int P, int KW, int NWARPS>
 struct Div3Smem {
   using EL = ElemT<DIM, P>;
-  double Wv[EL::NPR * EL::LDV];
+  double Wv[EL::NPR * EL::LDV];      // volume matrix with the own-side face term folded in (Wv2)
   double Wl[EL::NPR * EL::LDF];
   Div3Warp<DIM, P, KW> w[NWARPS];
   int fn[EL::NF * EL::NFP];
   int perm[EL::NPERM * EL::NFP];
+  int flc[((KW * EL::NFT + 31) / 32) * 32];      // face_lane_code of every face node of a block
 };
 
+// chunk t of every plane of a block: CH doubles at element e, node j
 template <int DIM, int P, int KW>
-__device__ __forceinline__ void div_stage_async(Div3Warp<DIM, P, KW>& W, const DiscDev& d, const double* q,
+__device__ __forceinline__ void div_stage_small(Div3Small<DIM, P, KW>& M, const DiscDev& d, const double* q,
                                                 const double* T, long long e0, int nel, int lane) {
   using EL = ElemT<DIM, P>;
   constexpr int C = EL::C, NP = EL::NP, NF = EL::NF;
-  const long long E = d.E;
-  if (NP % 2 == 0) {
-    constexpr int H = NP / 2;
-    const int per = nel * H;                       // 16-byte chunks per plane
-    for (int n = lane; n < DIM * C * per; n += 32) {
-      const int pl = n / per, ej = n - pl * per;
-      const int r = pl / C, c = pl - r * C;
-      const int e = ej / H, j = 2 * (ej - e * H);
-      cp_async16(W.Ts + (c * KW + e) * EL::LDV + r * EL::NPK + j, T + ((long long)pl * E + e0 + e) * NP + j);
+  const long long pstride = d.E * NP;
+  constexpr int CH = (NP % 2 == 0) ? 2 : 1, NPC = NP / CH;
+#pragma unroll
+  for (int t0 = 0; t0 < KW * NPC; t0 += 32) {
+    const int t = t0 + lane;
+    const int e = t / NPC, j = CH * (t - e * NPC);
+    if (t < KW * NPC && e < nel) {
+      const long long g0 = (e0 + e) * NP + j;
+      double* qs = M.Qs + e * NP + j;
+      const double* qg = q + g0;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        if (CH == 2) cp_async16(qs + c * (KW * NP), qg + c * pstride);
+        else cp_async8(qs + c * (KW * NP), qg + c * pstride);
+      }
+      if (CH == 2) cp_async16(M.Lam + e * NP + j, T + g0 + (DIM * C) * pstride);
+      else cp_async8(M.Lam + e * NP + j, T + g0 + (DIM * C) * pstride);
     }
-    for (int n = lane; n < C * per; n += 32) {
-      const int c = n / per, ej = n - c * per;
-      const int e = ej / H, j = 2 * (ej - e * H);
-      cp_async16(W.Qs + (c * KW + e) * NP + j, q + ((long long)c * E + e0 + e) * NP + j);
-    }
-    for (int n = lane; n < per; n += 32)
-      cp_async16(W.Lam + 2 * n, T + ((long long)(DIM * C) * E + e0) * NP + 2 * n);
-  } else {
-    const int per = nel * NP;
-    for (int n = lane; n < DIM * C * per; n += 32) {
-      const int pl = n / per, ej = n - pl * per;
-      const int r = pl / C, c = pl - r * C;
-      const int e = ej / NP, j = ej - e * NP;
-      cp_async8(W.Ts + (c * KW + e) * EL::LDV + r * EL::NPK + j, T + ((long long)pl * E + e0) * NP + ej);
-    }
-    for (int n = lane; n < C * per; n += 32) {
-      const int c = n / per, ej = n - c * per;
-      const int e = ej / NP, j = ej - e * NP;
-      cp_async8(W.Qs + (c * KW + e) * NP + j, q + ((long long)c * E + e0) * NP + ej);
-    }
-    for (int n = lane; n < per; n += 32) cp_async8(W.Lam + n, T + ((long long)(DIM * C) * E + e0) * NP + n);
   }
-  for (int n = lane; n < nel * NF; n += 32) {
-    cp_async8(&W.sj[0][n], d.sj + e0 * NF + n);
-    cp_async8(&W.conn[0][n], d.conn + e0 * NF + n);
+  if (lane < nel * NF) {
+    cp_async8(&M.sj[0][lane], d.sj + e0 * NF + lane);
+    cp_async8(&M.conn[0][lane], d.conn + e0 * NF + lane);
   }
-  if (lane < nel) cp_async8(&W.rj[lane], d.rj + e0 + lane);
+  if (lane < nel) cp_async8(&M.rj[lane], d.rj + e0 + lane);
+}
+
+template <int DIM, int P, int KW>
+__device__ __forceinline__ void div_stage_rows(double* Ts, const DiscDev& d, const double* T, long long e0, int nel,
+                                               int lane) {
+  using EL = ElemT<DIM, P>;
+  constexpr int C = EL::C, NP = EL::NP;
+  const long long pstride = d.E * NP;
+  constexpr int CH = (NP % 2 == 0) ? 2 : 1, NPC = NP / CH;
+#pragma unroll
+  for (int t0 = 0; t0 < KW * NPC; t0 += 32) {
+    const int t = t0 + lane;
+    const int e = t / NPC, j = CH * (t - e * NPC);
+    if (t < KW * NPC && e < nel) {
+      double* ts = Ts + e * EL::LDV + j;
+      const double* tg = T + (e0 + e) * NP + j;
+#pragma unroll 1
+      for (int r = 0; r < DIM; ++r) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          if (CH == 2) cp_async16(ts + c * (KW * EL::LDV), tg + c * pstride);
+          else cp_async8(ts + c * (KW * EL::LDV), tg + c * pstride);
+        }
+        ts += EL::NPK;
+        tg += C * pstride;
+      }
+    }
+  }
 }
 
 template <int DIM> struct VecC { double v[DIM + 2]; };
 
 // Boundary face node (rare): inviscid flux of the exterior state, viscous flux of the interior
-// state.  Returns sJ F*.n per field (operators.py: f_bnd).
+// state (operators.py: f_bnd = own + B).  The own-side term is read from HBM here (the block's
+// rows may still be in flight), and half of it is already in the folded volume matrix, so this
+// returns the operand entry  -(own/2 + B).
 template <int DIM>
-__device__ __noinline__ VecC<DIM> boundary_flux(int bc, VecC<DIM> qm_, VecC<DIM> own_, double lam_m, double sj,
-                                               const double* __restrict__ normals, long long nstride, Phys ph) {
+__device__ __noinline__ VecC<DIM> boundary_operand(int bc, int f, VecC<DIM> qm_, const double* __restrict__ Tnode,
+                                                   long long pstride, double lam_m, double sj,
+                                                   const double* __restrict__ normals, long long nstride, Phys ph) {
   constexpr int C = DIM + 2;
-  double nrm[DIM], qm[C], qb[C];
+  double nrm[DIM], qm[C], qb[C], own[C];
 #pragma unroll
   for (int x = 0; x < DIM; ++x) nrm[x] = normals[x * nstride];
 #pragma unroll
-  for (int c = 0; c < C; ++c) { qm[c] = qm_.v[c]; qb[c] = qm_.v[c]; }
+  for (int c = 0; c < C; ++c) {
+    qm[c] = qm_.v[c]; qb[c] = qm_.v[c];
+    if (f == 0) {
+      own[c] = Tnode[c * pstride];
+#pragma unroll
+      for (int r = 1; r < DIM; ++r) own[c] += Tnode[(r * C + c) * pstride];
+    } else {
+      own[c] = -Tnode[((f - 1) * C + c) * pstride];
+    }
+  }
   bc_state<DIM, true>(bc, qm, nrm, ph, qb);
   Prim<DIM> sb, sm;
   make_prim<DIM>(qb, ph.gamma, sb);
@@ -384,7 +500,7 @@ __device__ __noinline__ VecC<DIM> boundary_flux(int bc, VecC<DIM> qm_, VecC<DIM>
   VecC<DIM> out;
 #pragma unroll
   for (int c = 0; c < C; ++c)
-    out.v[c] = own_.v[c] + 0.5 * sj * (fnb[c] - fni[c]) + 0.5 * sj * lam * (qm[c] - qb[c]);
+    out.v[c] = -(0.5 * own[c] + 0.5 * sj * (fnb[c] - fni[c]) + 0.5 * sj * lam * (qm[c] - qb[c]));
   return out;
 }
 
@@ -397,12 +513,14 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
   using WS = Div3Warp<DIM, P, KW>;
   constexpr int C = EL::C, NP = EL::NP, NF = EL::NF, NFP = EL::NFP, NFT = EL::NFT;
   constexpr int NT = NWARPS * 32;
+  constexpr int NR = (KW * NFT + 31) / 32;        // face-node rounds per block
+  constexpr int NB = DGB_DIV_NB;                  // face nodes per lane whose gathers are in flight together
   extern __shared__ __align__(16) unsigned char smem_raw[];
   auto& S = *reinterpret_cast<Div3Smem<DIM, P, KW, NWARPS>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long E = d.E, G = d.G;
 
-  for (int n = tid; n < EL::NPR * EL::LDV; n += NT) S.Wv[n] = d.Wv[n];
+  for (int n = tid; n < EL::NPR * EL::LDV; n += NT) S.Wv[n] = d.Wv2[n];
   for (int n = tid; n < EL::NPR * EL::LDF; n += NT) S.Wl[n] = d.Wl[n];
   for (int n = tid; n < NF * NFP; n += NT) S.fn[n] = d.tables[n];
   for (int n = tid; n < EL::NPERM * NFP; n += NT) S.perm[n] = d.tables[NF * NFP + n];
@@ -412,82 +530,149 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
     for (int n = lane; n < (int)(sizeof(WS) / 8); n += 32) z[n] = 0.0;
   }
   __syncthreads();
+  for (int n = tid; n < NR * 32; n += NT) S.flc[n] = face_lane_code<DIM, P, KW>(S.fn, n);
+  __syncthreads();
 
   const long long wstride = (long long)gridDim.x * NWARPS;
   long long wb = (long long)blockIdx.x * NWARPS + warp;
+  int buf = 0;
   if (wb < nwblocks) {
     const long long e0 = wb * KW;
-    div_stage_async<DIM, P, KW>(W, d, q, T, e0, (int)((E - e0) < (long long)KW ? (E - e0) : (long long)KW), lane);
+    const int nel0 = (int)((E - e0) < (long long)KW ? (E - e0) : (long long)KW);
+    div_stage_small<DIM, P, KW>(W.sm[0], d, q, T, e0, nel0, lane);
+    cp_async_commit();
+    div_stage_rows<DIM, P, KW>(W.Ts, d, T, e0, nel0, lane);
+    cp_async_commit();
+  } else {
+    cp_async_commit();
+    cp_async_commit();
   }
-  cp_async_commit();
+  unsigned long long ticket = draw_ticket(counter, lane);
 
+  // cp.async groups retire in order: S(b), T(b), S(b+1), T(b+1), ...
   while (wb < nwblocks) {
     const long long e0 = wb * KW;
     const int nel = (int)((E - e0) < (long long)KW ? (E - e0) : (long long)KW);
-    cp_async_wait<0>();
+    const long long wb_next = ticket_block(ticket, wstride);
+    const long long e1 = wb_next * KW;
+    const int nel1 = wb_next < nwblocks ? (int)((E - e1) < (long long)KW ? (E - e1) : (long long)KW) : 0;
+    if (nel1 > 0) div_stage_small<DIM, P, KW>(W.sm[buf ^ 1], d, q, T, e1, nel1, lane);
+    cp_async_commit();                   // S(b+1)
+    ticket = draw_ticket(counter, lane);
+    cp_async_wait<2>();                  // S(b) has landed; T(b) and S(b+1) may still be in flight
     __syncwarp();
+    const Div3Small<DIM, P, KW>& M = W.sm[buf];
 
-    // ---- face gather + Rusanov: Fs = -(sJ F*.n) ----------------------------------------------
-#pragma unroll 2
-    for (int n = lane; n < nel * NFT; n += 32) {
-      const int e = n / NFT, fm = n - e * NFT;
-      const int f = fm / NFP, m = fm - f * NFP;
-      const long long cn = W.conn[e][f];
-      const long long nb = DGB_CONN_NB(cn);
-      const int nf = DGB_CONN_NF(cn), pid = DGB_CONN_PERM(cn), bc = DGB_CONN_BC(cn);
-      const int jm = S.fn[f * NFP + m];
-      const int jp = S.fn[nf * NFP + S.perm[pid * NFP + m]];
-      const bool in_ghost = nb >= E;
-      const long long pstride = (in_ghost ? G : E) * NP;
-      const long long off = (in_ghost ? nb - E : nb) * NP + jp;
-      const double* qbase = (in_ghost ? ghost : q) + off;
-      const double* tbase = (in_ghost ? Tghost : T) + off;
-      const int r0 = nf == 0 ? 0 : nf - 1;
-      double qp[C], nbr[C];
+    // ---- face gather + Rusanov.  The own-side flux is linear in the block's own T rows with
+    //      constant coefficients and lives in the folded volume matrix, so this phase needs only
+    //      q, lam and the connectivity of the block -- not its T rows, which are still landing.
+    //      Fs = (nbr - sJ max(lam-, lam+) (q- - q+)) / 2,  nbr = sJ F+.n+ gathered from the neighbour.
+#pragma unroll 1
+    for (int k0 = 0; k0 < NR; k0 += NB) {
+      double qp[NB][C], nbr[NB][C], ex[NB][(DIM - 1) * C], lam_p[NB];
+      long long cnk[NB];
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-        qp[c] = qbase[c * pstride];
-        nbr[c] = tbase[(r0 * C + c) * pstride];
-      }
-      const double lam_p = tbase[(DIM * C) * pstride];
-      if (nf == 0) {
+      for (int b = 0; b < NB; ++b) {
+        const int k = k0 + b;
+        cnk[b] = -1;
+        if (k < NR) {
+          const int flk = S.flc[k * 32 + lane];
+          const int e = flk & 3, f = (flk >> 2) & 3, m = (flk >> 4) & 15;
+          if (flk >= 0 && e < nel) {
+            const long long cn = M.conn[e][f];
+            cnk[b] = cn;
+            const long long nb = DGB_CONN_NB(cn);
+            const int nf = DGB_CONN_NF(cn);
+            const int jp = S.fn[nf * NFP + S.perm[DGB_CONN_PERM(cn) * NFP + m]];
+            const bool in_ghost = nb >= E;
+            const long long pstride = (in_ghost ? G : E) * NP;
+            const long long off = (in_ghost ? nb - E : nb) * NP + jp;
+            const double* qbase = (in_ghost ? ghost : q) + off;
+            const double* tbase = (in_ghost ? Tghost : T) + off;
+            const int r0 = nf == 0 ? 0 : nf - 1;
 #pragma unroll
-        for (int r = 1; r < DIM; ++r)
+            for (int c = 0; c < C; ++c) {
+              qp[b][c] = qbase[c * pstride];
+              nbr[b][c] = tbase[(r0 * C + c) * pstride];
+            }
+            lam_p[b] = tbase[(DIM * C) * pstride];
+#if !DGB_DIV_LAZY_EX
+            if (nf == 0) {
 #pragma unroll
-          for (int c = 0; c < C; ++c) nbr[c] += tbase[(r * C + c) * pstride];
-      } else {
-#pragma unroll
-        for (int c = 0; c < C; ++c) nbr[c] = -nbr[c];
-      }
-      const double sj = W.sj[e][f];
-      const double lam_m = W.Lam[e * NP + jm];
-      double qm[C], own[C];
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        qm[c] = W.Qs[(c * KW + e) * NP + jm];
-        const double* trow = W.Ts + (c * KW + e) * EL::LDV + jm;
-        if (f == 0) {
-          own[c] = trow[0];
-#pragma unroll
-          for (int r = 1; r < DIM; ++r) own[c] += trow[r * EL::NPK];
-        } else {
-          own[c] = -trow[(f - 1) * EL::NPK];
+              for (int rc = 0; rc < (DIM - 1) * C; ++rc) ex[b][rc] = tbase[(C + rc) * pstride];
+            }
+#endif
+          }
         }
       }
-      if (bc == 0) {
-        const double pen = sj * fmax(lam_m, lam_p);
+#if DGB_DIV_LAZY_EX
+      // face 0 of a neighbour is the sum of its DIM rows: the other DIM-1 are fetched in a second wave
 #pragma unroll
-        for (int c = 0; c < C; ++c)
-          W.Fs[(c * KW + e) * EL::LDF + fm] = -0.5 * ((own[c] - nbr[c]) + pen * (qm[c] - qp[c]));
-      } else {
-        VecC<DIM> a, b;
+      for (int b = 0; b < NB; ++b) {
+        const int k = k0 + b;
+        if (k < NR && cnk[b] >= 0 && DGB_CONN_NF(cnk[b]) == 0 && DGB_CONN_BC(cnk[b]) == 0) {
+          const int flk = S.flc[k * 32 + lane];
+          const long long nb = DGB_CONN_NB(cnk[b]);
+          const int m = (flk >> 4) & 15;
+          const int jp = S.fn[S.perm[DGB_CONN_PERM(cnk[b]) * NFP + m]];
+          const bool in_ghost = nb >= E;
+          const long long pstride = (in_ghost ? G : E) * NP;
+          const double* tbase = (in_ghost ? Tghost : T) + (in_ghost ? nb - E : nb) * NP + jp;
 #pragma unroll
-        for (int c = 0; c < C; ++c) { a.v[c] = qm[c]; b.v[c] = own[c]; }
-        const VecC<DIM> fb = boundary_flux<DIM>(bc, a, b, lam_m, sj, d.normals + (e0 + e) * NF + f, E * NF, ph);
+          for (int c = 0; c < C; ++c) {
+            double t = tbase[(C + c) * pstride];
 #pragma unroll
-        for (int c = 0; c < C; ++c) W.Fs[(c * KW + e) * EL::LDF + fm] = -fb.v[c];
+            for (int r = 2; r < DIM; ++r) t += tbase[(r * C + c) * pstride];
+            ex[b][c] = t;
+          }
+        }
+      }
+#endif
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int k = k0 + b;
+        if (k < NR && cnk[b] >= 0) {
+          const int flk = S.flc[k * 32 + lane];
+          const int e = flk & 3, f = (flk >> 2) & 3, jm = (flk >> 8) & 255, fm = (flk >> 16) & 255;
+          const int nf = DGB_CONN_NF(cnk[b]), bc = DGB_CONN_BC(cnk[b]);
+          const double sj = M.sj[e][f];
+          const double lam_m = M.Lam[e * NP + jm];
+          double qm[C];
+#pragma unroll
+          for (int c = 0; c < C; ++c) qm[c] = M.Qs[(c * KW + e) * NP + jm];
+          double* fs = W.Fs + e * EL::LDF + fm;
+          if (bc == 0) {
+            if (nf == 0) {
+#if DGB_DIV_LAZY_EX
+#pragma unroll
+              for (int c = 0; c < C; ++c) nbr[b][c] += ex[b][c];
+#else
+#pragma unroll
+              for (int c = 0; c < C; ++c) {
+#pragma unroll
+                for (int r = 1; r < DIM; ++r) nbr[b][c] += ex[b][(r - 1) * C + c];
+              }
+#endif
+            } else {
+#pragma unroll
+              for (int c = 0; c < C; ++c) nbr[b][c] = -nbr[b][c];
+            }
+            const double pen = sj * fmax(lam_m, lam_p[b]);
+#pragma unroll
+            for (int c = 0; c < C; ++c) fs[c * (KW * EL::LDF)] = 0.5 * (nbr[b][c] - pen * (qm[c] - qp[b][c]));
+          } else {
+            VecC<DIM> a_;
+#pragma unroll
+            for (int c = 0; c < C; ++c) a_.v[c] = qm[c];
+            const VecC<DIM> fb = boundary_operand<DIM>(bc, f, a_, T + (e0 + e) * NP + jm, E * NP, lam_m, sj,
+                                                       d.normals + (e0 + e) * NF + f, E * NF, ph);
+#pragma unroll
+            for (int c = 0; c < C; ++c) fs[c * (KW * EL::LDF)] = fb.v[c];
+          }
+        }
       }
     }
+    cp_async_wait<1>();                  // T(b) has landed
     __syncwarp();
 
     // ---- tensor-core contraction -------------------------------------------------------------
@@ -500,19 +685,10 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
     mma_block<EL::NI, WS::NTILE>(acc, W.Fs, EL::LDF, S.Wl, EL::LDF, EL::KF / 4, lane);
     double rj[WS::NTILE];
 #pragma unroll
-    for (int mt = 0; mt < WS::NTILE; ++mt) {
-      const int col = mt * 8 + (lane >> 2);
-      const int e = col % KW;
-      rj[mt] = W.rj[e];
-    }
+    for (int mt = 0; mt < WS::NTILE; ++mt) rj[mt] = M.rj[(mt * 8 + (lane >> 2)) % KW];
     __syncwarp();                        // all operand rows consumed: the next block may land on them
-
-    const long long wb_next = next_block(counter, wstride, lane);
-    if (wb_next < nwblocks) {
-      const long long e1 = wb_next * KW;
-      div_stage_async<DIM, P, KW>(W, d, q, T, e1, (int)((E - e1) < (long long)KW ? (E - e1) : (long long)KW), lane);
-    }
-    cp_async_commit();
+    if (nel1 > 0) div_stage_rows<DIM, P, KW>(W.Ts, d, T, e1, nel1, lane);
+    cp_async_commit();                   // T(b+1)
 
     // ---- 1/J and the (RK-fused) store --------------------------------------------------------
 #pragma unroll
@@ -529,6 +705,7 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
       }
     }
     wb = wb_next;
+    buf ^= 1;
   }
   cp_async_wait<0>();
 }

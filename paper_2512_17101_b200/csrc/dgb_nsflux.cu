@@ -8,11 +8,13 @@
 
 namespace {
 
+// Measured on B200 (profiles/r01_flux_variants.md): pass 1 is fastest with 12 warps (168 registers, two
+// face nodes per lane in flight), pass 2 with 8 warps (235 registers, no spills, NB = 2).
 #ifndef DGB_FLUX_WARPS
-#define DGB_FLUX_WARPS 16
+#define DGB_FLUX_WARPS 12
 #endif
 #ifndef DGB_DIV_WARPS
-#define DGB_DIV_WARPS 16
+#define DGB_DIV_WARPS 8
 #endif
 constexpr int kSmemBudget = 232448 - 1024;   // 227 KB usable per CTA minus the 1 KB system reserve
 constexpr int fit_warps(size_t fixed, size_t per_warp, int cap) {

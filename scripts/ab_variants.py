@@ -1,0 +1,64 @@
+"""Build tuning variants of libdgb200.so (compile-time knobs of the flux-arrangement kernels) and,
+with --run, bench each one on the GPU (A/B numbers for profiles/).
+
+    python scripts/ab_variants.py --build            # here (CPU box): nvcc each variant
+    python scripts/ab_variants.py --run --n 64       # on the GPU box: one JSON line per variant
+"""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+PKG = os.path.join(ROOT, "paper_2512_17101_b200")
+
+VARIANTS = {
+    "w8_nb1_2": ["DGB_FLUX_WARPS=8", "DGB_DIV_WARPS=8", "DGB_DIV_NB=1", "DGB_FLUX_NB=2"],
+    "w6_nb2_2": ["DGB_FLUX_WARPS=6", "DGB_DIV_WARPS=6", "DGB_DIV_NB=2", "DGB_FLUX_NB=2"],
+    "w10_nb1_2": ["DGB_FLUX_WARPS=10", "DGB_DIV_WARPS=10", "DGB_DIV_NB=1", "DGB_FLUX_NB=2"],
+    "w10_nb2_1": ["DGB_FLUX_WARPS=10", "DGB_DIV_WARPS=10", "DGB_DIV_NB=2", "DGB_FLUX_NB=1"],
+    "w4_nb2_4": ["DGB_FLUX_WARPS=4", "DGB_DIV_WARPS=4", "DGB_DIV_NB=2", "DGB_FLUX_NB=4"],
+}
+
+
+def lib(name):
+    return os.path.join(PKG, f"libdgb200_{name}.so")
+
+
+def main():
+    names = [a for a in sys.argv[1:] if a in VARIANTS] or list(VARIANTS)
+    if "--build" in sys.argv:
+        # only dgb_nsflux.cu depends on the knobs: compile the other translation units once
+        from paper_2512_17101_b200.csrc.build import FLAGS, HERE
+        cflags = [f for f in FLAGS if f != "-shared"]
+        objs = []
+        for src in ("dgb200.cu", "dgb_arrayops.cu"):
+            obj = os.path.join("/tmp", src.replace(".cu", ".o"))
+            if not os.path.exists(obj) or os.path.getmtime(obj) < max(
+                    os.path.getmtime(os.path.join(HERE, f)) for f in os.listdir(HERE) if f.endswith((".cu", ".cuh", ".h"))):
+                subprocess.run(["nvcc"] + cflags + ["-c", src, "-o", obj], cwd=HERE, check=True)
+            objs.append(obj)
+        for name in names:
+            obj = f"/tmp/dgb_nsflux_{name}.o"
+            subprocess.run(["nvcc"] + cflags + [f"-D{d}" for d in VARIANTS[name]] + ["-c", "dgb_nsflux.cu", "-o", obj],
+                           cwd=HERE, check=True)
+            subprocess.run(["nvcc", "-shared", "-o", lib(name), obj] + objs, cwd=HERE, check=True)
+            print("built", lib(name), flush=True)
+    if "--run" in sys.argv:
+        n = sys.argv[sys.argv.index("--n") + 1] if "--n" in sys.argv else "64"
+        for name in names:
+            env = dict(os.environ, DGB_LIB=lib(name))
+            res = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--no-e2e", "--no-cpu", "--n", n,
+                                  "--steps", "10"], env=env, capture_output=True, text=True)
+            try:
+                d = json.loads(res.stdout.strip().splitlines()[-1])
+                r = d["roofline"]
+                print(f"{name:18s} n={n} {d['value']:.3f} GDOF/s  pass1 {r['ms_grad_pass']:.3f} ms  pass2 {r['ms_div_pass']:.3f} ms"
+                      f"  step min/med/max {r['ms_step_min_median_max']}", flush=True)
+            except Exception:
+                print(name, "FAILED", res.stderr[-500:], flush=True)
+
+
+if __name__ == "__main__":
+    main()
