@@ -335,8 +335,8 @@ def run_b200(args):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        # Pipelined like a streaming user would: the H2D copy of step k+1 (copy stream) overlaps the
-        # compute + D2H of step k (compute stream).  Every step still uploads its full input from pinned
+        # Pipelined like a streaming user would: the H2D copy of step k+1 (upload stream), the compute of
+        # step k (compute stream) and the D2H of step k-1 (download stream) overlap.  Every step still uploads its full input from pinned
         # host memory and downloads its full result; both are inside the timed region.
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record(stream)
@@ -347,7 +347,8 @@ def run_b200(args):
             res = rhs_step(DOFArray(actx, cur)).data
             if k + 1 < Ke:
                 nxt = actx.from_numpy_async(q_host)               # H2D of step k+1 into a fresh buffer
-            actx.to_numpy_async(res, out_host)                    # D2H of step k's result
+            d2h_done = actx.to_numpy_async(res, out_host)         # D2H of step k's result (download stream)
+        stream.wait_event(d2h_done)                               # the last result is on the host
         s1.record(stream)
         torch.cuda.synchronize()
         ms_e2e = s0.elapsed_time(s1) / Ke

@@ -138,6 +138,23 @@ int dgb_ns_div_rk(const dgb_disc* disc, const double* q_dev, const double* T_dev
                   const double* x1_dev, double* out1_dev, const double* x2_dev, double* out2_dev,
                   const double* rk_host, const double* qfar_host, const double* phys_host, void* stream);
 
+/* ---- element sub-ranges: the same three right-hand-side kernels restricted to the elements
+ *      [ebegin, eend) of the mesh (outputs of other elements are not touched).  A partitioned
+ *      mesh orders its elements [interior | adjacent to a partition boundary]; the interior range
+ *      needs no halo data and runs while the exchange (Send / Receive, adfg.py:380-399,834-869) is
+ *      in flight on another stream -- the overlap the reference lists as missing.
+ */
+int dgb_euler_rhs_range(const dgb_disc* disc, const double* q_dev, const double* ghost_dev, double* rhs_dev,
+                        const double* qfar_host, const double* phys_host,
+                        int64_t ebegin, int64_t eend, void* stream);
+int dgb_ns_flux_range(const dgb_disc* disc, const double* q_dev, const double* ghost_dev, double* T_dev,
+                      const double* qfar_host, const double* phys_host,
+                      int64_t ebegin, int64_t eend, void* stream);
+int dgb_ns_div_range(const dgb_disc* disc, const double* q_dev, const double* T_dev,
+                     const double* ghost_dev, const double* Tghost_dev, double* rhs_dev,
+                     const double* qfar_host, const double* phys_host,
+                     int64_t ebegin, int64_t eend, void* stream);
+
 /* ---- halo packing: element rows <-> contiguous message (Send / Receive payloads,
  *      adfg.py:380-399,834-869).  dst[c, i, :] = src[c, elems[i], :]                        ---- */
 int dgb_pack_elements(double* dst_dev, const double* src_dev, const int64_t* elems_dev,

@@ -20,6 +20,7 @@ SYMBOLS = [
     "dgb_disc_create", "dgb_disc_destroy", "dgb_disc_expand_maps", "dgb_debug_phase_cycles",
     "dgb_euler_rhs", "dgb_ns_grad", "dgb_ns_rhs", "dgb_euler_rhs_rk", "dgb_ns_rhs_rk",
     "dgb_disc_set_jacobian", "dgb_ns_flux", "dgb_ns_div", "dgb_ns_div_rk",
+    "dgb_euler_rhs_range", "dgb_ns_flux_range", "dgb_ns_div_range",
     "dgb_pack_elements",
     "dgb_ew_binary", "dgb_ew_unary", "dgb_ew_where", "dgb_copy_strided", "dgb_copy_scatter", "dgb_take",
     "dgb_einsum",
@@ -79,6 +80,9 @@ def load():
     lib.dgb_ns_flux.argtypes = [vp, dp, dp, dp, vp, vp, vp]
     lib.dgb_ns_div.argtypes = [vp, dp, dp, dp, dp, dp, vp, vp, vp]
     lib.dgb_ns_div_rk.argtypes = [vp, dp, dp, dp, dp, dp, dp, dp, dp, vp, vp, vp, vp]
+    lib.dgb_euler_rhs_range.argtypes = [vp, dp, dp, dp, vp, vp, i64, i64, vp]
+    lib.dgb_ns_flux_range.argtypes = [vp, dp, dp, dp, vp, vp, i64, i64, vp]
+    lib.dgb_ns_div_range.argtypes = [vp, dp, dp, dp, dp, dp, vp, vp, i64, i64, vp]
     lib.dgb_pack_elements.argtypes = [dp, dp, dp, i64, i64, i64, i64, vp]
     lib.dgb_ew_binary.argtypes = [C.c_int, dp, C.c_int, dp, C.c_int, vp, dp, C.c_int, vp, C.c_int, vp, vp]
     lib.dgb_ew_unary.argtypes = [C.c_int, dp, C.c_int, dp, C.c_int, i64, vp]

@@ -330,13 +330,27 @@ class B200ArrayContext:
             self.stream.wait_event(ev)
         return arr
 
+    @property
+    def d2h_stream(self):
+        if getattr(self, "_d2h_stream", None) is None:
+            self._d2h_stream = _torch().cuda.Stream(device=self.device)
+        return self._d2h_stream
+
     def to_numpy_async(self, value: DeviceArray, out: np.ndarray):
-        """D2H into a pinned buffer on the compute stream without synchronising; returns an event."""
+        """D2H into a pinned buffer on a dedicated download stream, ordered after everything enqueued
+        so far on the compute stream; does not block the host or later kernels.  Returns the event
+        that marks the copy done (``stream.wait_event(ev)`` / ``ev.synchronize()`` before reading)."""
+        torch = _torch()
         src = self._contiguous(value)
-        _cabi.check(self.lib.dgb_memcpy_d2h(C.c_void_p(out.ctypes.data), C.c_void_p(src.ptr), out.nbytes, self._st),
-                    "to_numpy_async")
-        ev = _torch().cuda.Event()
-        ev.record(self.stream)
+        done = torch.cuda.Event()
+        done.record(self.stream)
+        ds = self.d2h_stream
+        ds.wait_event(done)
+        _cabi.check(self.lib.dgb_memcpy_d2h(C.c_void_p(out.ctypes.data), C.c_void_p(src.ptr), out.nbytes,
+                                            C.c_void_p(ds.cuda_stream)), "to_numpy_async")
+        ev = torch.cuda.Event()
+        ev.record(ds)
+        src.t.record_stream(ds)
         self._keepalive = [src]
         return ev
 

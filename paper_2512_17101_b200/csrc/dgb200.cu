@@ -197,18 +197,19 @@ int launch_rhs2(const dgb_disc* d, const double* q, const double* gq, const doub
 
 template <int DIM, int P, bool VISCOUS>
 int launch_rhs3(const dgb_disc* d, const double* q, const double* gq, const double* ghost, const double* gghost,
-                const dgb::Epilogue& ep, const dgb::Phys& ph, cudaStream_t st) {
+                const dgb::Epilogue& ep, const dgb::Phys& ph, cudaStream_t st, long long ebeg = 0, long long eend = -1) {
   using C = Cfg3<DIM, P>;
   auto kern = dgb::k_rhs3<DIM, P, C::KW, C::NW, VISCOUS>;
   const size_t smem = sizeof(dgb::Rhs3Smem<DIM, P, C::KW, C::NW>);
-  const long long nwb = (d->dev.E + C::KW - 1) / C::KW;
+  if (eend < 0) eend = d->dev.E;
+  const long long nwb = (eend - ebeg + C::KW - 1) / C::KW;
   if (nwb == 0) return DGB_OK;
   static bool configured = false;
   if (!configured) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured = true; }
   const long long need = (nwb + C::NW - 1) / C::NW;
   const int grid = (int)(need < num_sms() ? need : num_sms());
   DGB_CUDA(cudaMemsetAsync(d->counters + 1, 0, sizeof(unsigned long long), st));
-  kern<<<grid, C::NW * 32, smem, st>>>(d->dev, q, gq, ghost, gghost, ep, ph, nwb, d->counters + 1);
+  kern<<<grid, C::NW * 32, smem, st>>>(d->dev, q, gq, ghost, gghost, ep, ph, nwb, d->counters + 1, ebeg, eend);
   {
     cudaError_t e_ = cudaGetLastError();
     if (e_ != cudaSuccess) {
@@ -274,12 +275,15 @@ int launch_grad(const dgb_disc* d, const double* q, const double* ghost, double*
 #define DGB_FOR_EACH_ELEMENT(X) X(2, 1) X(2, 2) X(2, 3) X(2, 4) X(3, 1) X(3, 2) X(3, 3) X(3, 4)
 
 int dispatch_rhs(const dgb_disc* d, bool viscous, const double* q, const double* gq, const double* ghost,
-                 const double* gghost, const dgb::Epilogue& ep, const dgb::Phys& ph, cudaStream_t st) {
+                 const double* gghost, const dgb::Epilogue& ep, const dgb::Phys& ph, cudaStream_t st,
+                 long long ebeg = 0, long long eend = -1) {
+  if ((ebeg != 0 || eend >= 0) && variant() != 5)
+    return fail(DGB_ERR_INVALID, "element ranges need the default kernels (DGB_VARIANT=5)");
 #define X(DIM, P)                                                                              \
   if (d->dim == DIM && d->order == P) {                                                        \
     if (variant() == 5)                                                                        \
-      return viscous ? launch_rhs3<DIM, P, true>(d, q, gq, ghost, gghost, ep, ph, st)          \
-                     : launch_rhs3<DIM, P, false>(d, q, gq, ghost, gghost, ep, ph, st);        \
+      return viscous ? launch_rhs3<DIM, P, true>(d, q, gq, ghost, gghost, ep, ph, st, ebeg, eend)   \
+                     : launch_rhs3<DIM, P, false>(d, q, gq, ghost, gghost, ep, ph, st, ebeg, eend); \
     if (variant() == 4)                                                                        \
       return viscous ? launch_rhs2<DIM, P, true>(d, q, gq, ghost, gghost, ep, ph, st)          \
                      : launch_rhs2<DIM, P, false>(d, q, gq, ghost, gghost, ep, ph, st);        \
@@ -515,6 +519,15 @@ int dgb_euler_rhs(const dgb_disc* d, const double* q, const double* ghost, doubl
   dgb::Phys ph; make_phys(ph, d->dim + 2, qfar, phys);
   dgb::Epilogue ep{nullptr, rhs, nullptr, nullptr, 0.0, 1.0, 0.0, 0.0};
   return dispatch_rhs(d, false, q, nullptr, ghost, nullptr, ep, ph, (cudaStream_t)stream);
+}
+
+int dgb_euler_rhs_range(const dgb_disc* d, const double* q, const double* ghost, double* rhs, const double* qfar,
+                        const double* phys, int64_t ebegin, int64_t eend, void* stream) {
+  int rc = check_ghost(d, ghost); if (rc) return rc;
+  if (ebegin < 0 || eend > d->dev.E || ebegin > eend) return fail(DGB_ERR_INVALID, "element range outside [0, E]");
+  dgb::Phys ph; make_phys(ph, d->dim + 2, qfar, phys);
+  dgb::Epilogue ep{nullptr, rhs, nullptr, nullptr, 0.0, 1.0, 0.0, 0.0};
+  return dispatch_rhs(d, false, q, nullptr, ghost, nullptr, ep, ph, (cudaStream_t)stream, ebegin, eend);
 }
 
 int dgb_ns_grad(const dgb_disc* d, const double* q, const double* ghost, double* gradq, const double* qfar,

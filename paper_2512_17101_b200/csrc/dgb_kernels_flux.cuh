@@ -152,7 +152,8 @@ __device__ __forceinline__ void flux_stage_async(double* Qs, FluxGeo<DIM, P, KW>
 template <int DIM, int P, int KW, int NWARPS>
 __global__ void __launch_bounds__(NWARPS * 32, 1)
 k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ ghost,
-          double* __restrict__ T, Phys ph, long long nwblocks, unsigned long long* __restrict__ counter) {
+          double* __restrict__ T, Phys ph, long long ebeg, long long eend, long long nwblocks,
+          unsigned long long* __restrict__ counter) {
   using EL = ElemT<DIM, P>;
   using WS = Flux3Warp<DIM, P, KW>;
   constexpr int C = EL::C, NP = EL::NP, NF = EL::NF, NFP = EL::NFP, NFT = EL::NFT, NI = EL::NI;
@@ -181,15 +182,15 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
   long long wb = (long long)blockIdx.x * NWARPS + warp;
   int buf = 0;
   if (wb < nwblocks) {
-    const long long e0 = wb * KW;
-    flux_stage_async<DIM, P, KW>(W.Qs[0], W.geo[0], d, q, e0, (int)((E - e0) < (long long)KW ? (E - e0) : (long long)KW), lane);
+    const long long e0 = ebeg + wb * KW;
+    flux_stage_async<DIM, P, KW>(W.Qs[0], W.geo[0], d, q, e0, (int)((eend - e0) < (long long)KW ? (eend - e0) : (long long)KW), lane);
   }
   cp_async_commit();
   unsigned long long ticket = draw_ticket(counter, lane);
 
   while (wb < nwblocks) {
-    const long long e0 = wb * KW;
-    const int nel = (int)((E - e0) < (long long)KW ? (E - e0) : (long long)KW);
+    const long long e0 = ebeg + wb * KW;
+    const int nel = (int)((eend - e0) < (long long)KW ? (eend - e0) : (long long)KW);
     // the next block (its ticket was drawn one block ago) starts its trip from HBM now
     const long long wb_next = ticket_block(ticket, wstride);
     cp_async_wait<0>();
@@ -197,9 +198,9 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
     const double* Qs = W.Qs[buf];
     const FluxGeo<DIM, P, KW>& geo = W.geo[buf];
     if (wb_next < nwblocks) {
-      const long long e1 = wb_next * KW;
+      const long long e1 = ebeg + wb_next * KW;
       flux_stage_async<DIM, P, KW>(W.Qs[buf ^ 1], W.geo[buf ^ 1], d, q, e1,
-                                   (int)((E - e1) < (long long)KW ? (E - e1) : (long long)KW), lane);
+                                   (int)((eend - e1) < (long long)KW ? (eend - e1) : (long long)KW), lane);
     }
     cp_async_commit();
     ticket = draw_ticket(counter, lane);
@@ -508,7 +509,8 @@ template <int DIM, int P, int KW, int NWARPS>
 __global__ void __launch_bounds__(NWARPS * 32, 1)
 k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
          const double* __restrict__ ghost, const double* __restrict__ Tghost,
-         Epilogue ep, Phys ph, long long nwblocks, unsigned long long* __restrict__ counter) {
+         Epilogue ep, Phys ph, long long ebeg, long long eend, long long nwblocks,
+         unsigned long long* __restrict__ counter) {
   using EL = ElemT<DIM, P>;
   using WS = Div3Warp<DIM, P, KW>;
   constexpr int C = EL::C, NP = EL::NP, NF = EL::NF, NFP = EL::NFP, NFT = EL::NFT;
@@ -537,8 +539,8 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
   long long wb = (long long)blockIdx.x * NWARPS + warp;
   int buf = 0;
   if (wb < nwblocks) {
-    const long long e0 = wb * KW;
-    const int nel0 = (int)((E - e0) < (long long)KW ? (E - e0) : (long long)KW);
+    const long long e0 = ebeg + wb * KW;
+    const int nel0 = (int)((eend - e0) < (long long)KW ? (eend - e0) : (long long)KW);
     div_stage_small<DIM, P, KW>(W.sm[0], d, q, T, e0, nel0, lane);
     cp_async_commit();
     div_stage_rows<DIM, P, KW>(W.Ts, d, T, e0, nel0, lane);
@@ -551,11 +553,11 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
 
   // cp.async groups retire in order: S(b), T(b), S(b+1), T(b+1), ...
   while (wb < nwblocks) {
-    const long long e0 = wb * KW;
-    const int nel = (int)((E - e0) < (long long)KW ? (E - e0) : (long long)KW);
+    const long long e0 = ebeg + wb * KW;
+    const int nel = (int)((eend - e0) < (long long)KW ? (eend - e0) : (long long)KW);
     const long long wb_next = ticket_block(ticket, wstride);
-    const long long e1 = wb_next * KW;
-    const int nel1 = wb_next < nwblocks ? (int)((E - e1) < (long long)KW ? (E - e1) : (long long)KW) : 0;
+    const long long e1 = ebeg + wb_next * KW;
+    const int nel1 = wb_next < nwblocks ? (int)((eend - e1) < (long long)KW ? (eend - e1) : (long long)KW) : 0;
     if (nel1 > 0) div_stage_small<DIM, P, KW>(W.sm[buf ^ 1], d, q, T, e1, nel1, lane);
     cp_async_commit();                   // S(b+1)
     ticket = draw_ticket(counter, lane);

@@ -86,7 +86,8 @@ template <int DIM, int P, int KW, int NWARPS, bool VISCOUS>
 __global__ void __launch_bounds__(NWARPS * 32, 1)
 k_rhs3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gq,
        const double* __restrict__ ghost, const double* __restrict__ gghost,
-       Epilogue ep, Phys ph, long long nwblocks, unsigned long long* __restrict__ counter) {
+       Epilogue ep, Phys ph, long long nwblocks, unsigned long long* __restrict__ counter,
+       long long ebeg, long long eend) {
   using EL = ElemT<DIM, P>;
   using WS = Rhs3Warp<DIM, P, KW>;
   constexpr int C = EL::C, NP = EL::NP, NF = EL::NF, NFP = EL::NFP, NFT = EL::NFT;
@@ -114,8 +115,8 @@ k_rhs3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gq,
   double pre[NPL];
   double pgeo[GPL];
   auto prefetch = [&](long long wbn) {
-    const long long e1 = wbn * KW;
-    const int nel1 = (int)((E - e1) < (long long)KW ? (E - e1) : (long long)KW);
+    const long long e1 = ebeg + wbn * KW;
+    const int nel1 = (int)((eend - e1) < (long long)KW ? (eend - e1) : (long long)KW);
     if (lane < nel1 * NP) {
 #pragma unroll
       for (int c = 0; c < C; ++c) pre[c] = q[((long long)c * E + e1) * NP + lane];
@@ -150,8 +151,8 @@ k_rhs3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gq,
 
   while (wb < nwblocks) {
     long long wb_next = nwblocks;
-    const long long e0 = wb * KW;
-    const int nel = (int)((E - e0) < (long long)KW ? (E - e0) : (long long)KW);
+    const long long e0 = ebeg + wb * KW;
+    const int nel = (int)((eend - e0) < (long long)KW ? (eend - e0) : (long long)KW);
     {
       double* gw = reinterpret_cast<double*>(&W.geo);
 #pragma unroll

@@ -36,36 +36,36 @@ int env_int(const char* name, int dflt) { const char* e = getenv(name); return e
 
 template <int DIM, int P>
 int launch_flux(const dgb_disc* d, const double* q, const double* ghost, double* T, const dgb::Phys& ph,
-                cudaStream_t st) {
+                long long ebeg, long long eend, cudaStream_t st) {
   using C = CfgF<DIM, P>;
   auto kern = dgb::k_nsflux3<DIM, P, C::KW, C::NWF>;
   const size_t smem = sizeof(dgb::Flux3Smem<DIM, P, C::KW, C::NWF>);
-  const long long nwb = (d->dev.E + C::KW - 1) / C::KW;
+  const long long nwb = (eend - ebeg + C::KW - 1) / C::KW;
   if (nwb == 0) return DGB_OK;
   static bool configured = false;
   if (!configured) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured = true; }
   const long long need = (nwb + C::NWF - 1) / C::NWF;
   const int grid = (int)(need < dgb_num_sms() ? need : dgb_num_sms());
   DGB_CUDA(cudaMemsetAsync(d->counters, 0, sizeof(unsigned long long), st));
-  kern<<<grid, C::NWF * 32, smem, st>>>(d->dev, q, ghost, T, ph, nwb, d->counters);
+  kern<<<grid, C::NWF * 32, smem, st>>>(d->dev, q, ghost, T, ph, ebeg, eend, nwb, d->counters);
   DGB_CUDA(cudaGetLastError());
   return DGB_OK;
 }
 
 template <int DIM, int P>
 int launch_div(const dgb_disc* d, const double* q, const double* T, const double* ghost, const double* Tghost,
-               const dgb::Epilogue& ep, const dgb::Phys& ph, cudaStream_t st) {
+               const dgb::Epilogue& ep, const dgb::Phys& ph, long long ebeg, long long eend, cudaStream_t st) {
   using C = CfgF<DIM, P>;
   auto kern = dgb::k_nsdiv3<DIM, P, C::KW, C::NWD>;
   const size_t smem = sizeof(dgb::Div3Smem<DIM, P, C::KW, C::NWD>);
-  const long long nwb = (d->dev.E + C::KW - 1) / C::KW;
+  const long long nwb = (eend - ebeg + C::KW - 1) / C::KW;
   if (nwb == 0) return DGB_OK;
   static bool configured = false;
   if (!configured) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured = true; }
   const long long need = (nwb + C::NWD - 1) / C::NWD;
   const int grid = (int)(need < dgb_num_sms() ? need : dgb_num_sms());
   DGB_CUDA(cudaMemsetAsync(d->counters + 1, 0, sizeof(unsigned long long), st));
-  kern<<<grid, C::NWD * 32, smem, st>>>(d->dev, q, T, ghost, Tghost, ep, ph, nwb, d->counters + 1);
+  kern<<<grid, C::NWD * 32, smem, st>>>(d->dev, q, T, ghost, Tghost, ep, ph, ebeg, eend, nwb, d->counters + 1);
   DGB_CUDA(cudaGetLastError());
   return DGB_OK;
 }
@@ -119,22 +119,37 @@ int dgb_disc_set_jacobian(dgb_disc* d, const double* jac_dev, void* stream) {
   return DGB_OK;
 }
 
-int dgb_ns_flux(const dgb_disc* d, const double* q, const double* ghost, double* T, const double* qfar,
-                const double* phys, void* stream) {
+static int check_range(const dgb_disc* d, int64_t ebegin, int64_t eend) {
+  if (ebegin < 0 || eend > d->dev.E || ebegin > eend) return dgb_fail(DGB_ERR_INVALID, "element range outside [0, E]");
+  return DGB_OK;
+}
+
+int dgb_ns_flux_range(const dgb_disc* d, const double* q, const double* ghost, double* T, const double* qfar,
+                      const double* phys, int64_t ebegin, int64_t eend, void* stream) {
   int rc = check_flux_args(d, ghost, q, T); if (rc) return rc;
+  if ((rc = check_range(d, ebegin, eend))) return rc;
   dgb::Phys ph; make_phys(ph, d->dim + 2, qfar, phys);
-#define X(DIM, P) if (d->dim == DIM && d->order == P) return launch_flux<DIM, P>(d, q, ghost, T, ph, (cudaStream_t)stream);
+#define X(DIM, P) if (d->dim == DIM && d->order == P) return launch_flux<DIM, P>(d, q, ghost, T, ph, ebegin, eend, (cudaStream_t)stream);
   DGB_FOR_EACH_ELEMENT(X)
 #undef X
   return dgb_fail(DGB_ERR_INVALID, "unsupported (dim, order)");
 }
 
+int dgb_ns_flux(const dgb_disc* d, const double* q, const double* ghost, double* T, const double* qfar,
+                const double* phys, void* stream) {
+  if (!d) return dgb_fail(DGB_ERR_INVALID, "null handle");
+  return dgb_ns_flux_range(d, q, ghost, T, qfar, phys, 0, d->dev.E, stream);
+}
+
 static int ns_div_impl(const dgb_disc* d, const double* q, const double* T, const double* ghost, const double* Tghost,
-                       const dgb::Epilogue& ep, const double* qfar, const double* phys, void* stream) {
+                       const dgb::Epilogue& ep, const double* qfar, const double* phys, void* stream,
+                       int64_t ebegin = 0, int64_t eend = -1) {
   int rc = check_flux_args(d, ghost, q, T); if (rc) return rc;
+  if (eend < 0) eend = d->dev.E;
+  if ((rc = check_range(d, ebegin, eend))) return rc;
   if (d->dev.G > 0 && !Tghost) return dgb_fail(DGB_ERR_INVALID, "ghost elements need the ghost flux planes");
   dgb::Phys ph; make_phys(ph, d->dim + 2, qfar, phys);
-#define X(DIM, P) if (d->dim == DIM && d->order == P) return launch_div<DIM, P>(d, q, T, ghost, Tghost, ep, ph, (cudaStream_t)stream);
+#define X(DIM, P) if (d->dim == DIM && d->order == P) return launch_div<DIM, P>(d, q, T, ghost, Tghost, ep, ph, ebegin, eend, (cudaStream_t)stream);
   DGB_FOR_EACH_ELEMENT(X)
 #undef X
   return dgb_fail(DGB_ERR_INVALID, "unsupported (dim, order)");
@@ -145,6 +160,13 @@ int dgb_ns_div(const dgb_disc* d, const double* q, const double* T, const double
   if (!rhs) return dgb_fail(DGB_ERR_INVALID, "null output");
   dgb::Epilogue ep{nullptr, rhs, nullptr, nullptr, 0.0, 1.0, 0.0, 0.0};
   return ns_div_impl(d, q, T, ghost, Tghost, ep, qfar, phys, stream);
+}
+
+int dgb_ns_div_range(const dgb_disc* d, const double* q, const double* T, const double* ghost, const double* Tghost,
+                     double* rhs, const double* qfar, const double* phys, int64_t ebegin, int64_t eend, void* stream) {
+  if (!rhs) return dgb_fail(DGB_ERR_INVALID, "null output");
+  dgb::Epilogue ep{nullptr, rhs, nullptr, nullptr, 0.0, 1.0, 0.0, 0.0};
+  return ns_div_impl(d, q, T, ghost, Tghost, ep, qfar, phys, stream, ebegin, eend);
 }
 
 int dgb_ns_div_rk(const dgb_disc* d, const double* q, const double* T, const double* ghost, const double* Tghost,

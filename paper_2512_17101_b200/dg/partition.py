@@ -32,6 +32,7 @@ class HaloPlan:
     send_local: list[np.ndarray]              # per peer: local element ids to send (int64)
     recv_slots: list[tuple[int, int]]         # per peer: [start, stop) ghost slots filled by its message
     global_ids: np.ndarray | None = None      # (nlocal,) global element id of each local element
+    n_interior: int | None = None             # elements [0, n_interior) touch no ghost (interior_first)
 
     def validate_against(self, other: "HaloPlan") -> None:
         """Symmetric, shape-matched plan check before the first exchange (the reference validates
@@ -138,3 +139,30 @@ def ring_slab(mesh: Mesh, ncells_x: int, rank: int, nranks: int, lo_x: float, hi
                     recv_slots=[(0, need_left.size), (need_left.size, need_left.size + need_right.size)])
     plan.send_tags = [1, 2]                                  # ... travelling left (1); to the right peer tag 2
     return local, plan
+
+
+def interior_first(local: Mesh, plan: HaloPlan) -> tuple[Mesh, HaloPlan]:
+    """Renumber a rank's elements as [interior | adjacent to a ghost element] (stable inside each
+    group, so the space-filling-curve locality survives).  The interior range needs no halo data:
+    the fused kernels run it while the exchange is in flight (halo.py), then the rest.  Ghost slots
+    and message contents keep their order (both are defined by ids the peers share), only the
+    local ids inside ``send_local`` are translated."""
+    E = plan.nlocal
+    touches = np.any(local.nbr_elem >= E, axis=1)
+    perm = np.concatenate([np.nonzero(~touches)[0], np.nonzero(touches)[0]])     # new -> old
+    inv = np.empty(E, dtype=np.int64)
+    inv[perm] = np.arange(E)
+    nbr = local.nbr_elem[perm].copy()
+    loc = nbr < E
+    nbr[loc] = inv[nbr[loc]]
+    mesh = Mesh(local.dim, local.vertices[perm], local.vertex_ids[perm], nbr, local.nbr_face[perm].copy(),
+                local.nbr_perm[perm].copy(), local.btag[perm].copy(),
+                nbr_rank=None if local.nbr_rank is None else local.nbr_rank[perm].copy())
+    new = HaloPlan(plan.rank, plan.nranks, plan.nlocal, plan.nghost, list(plan.peers), list(plan.tags),
+                   [inv[np.asarray(sl, dtype=np.int64)] for sl in plan.send_local], list(plan.recv_slots),
+                   global_ids=None if plan.global_ids is None else plan.global_ids[perm],
+                   n_interior=int((~touches).sum()))
+    if hasattr(plan, "send_tags"):
+        new.send_tags = list(plan.send_tags)
+    new.local_perm = perm
+    return mesh, new

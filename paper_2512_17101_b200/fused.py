@@ -313,5 +313,50 @@ def dg_ns_div_rk(actx, f, q, T, x1, x2, coef, Sw, jac, lift, normals, fscale, fa
     return {"out1": o1, "out2": o2}
 
 
+# {{{ element sub-ranges (halo.py overlaps the interior range with the exchange)
+
+def _op_disc(actx, op, q, nghost):
+    d = op.dcoll
+    disc = get_disc(actx, op.dim, q, nghost, d.Sw, d.drdx, d.lift, d.normals, d.fscale, d.vmap_m, d.vmap_p, d.bc_kind)
+    return disc
+
+
+def euler_rhs_range(actx, op, q, ghost, out, lo, hi):
+    """``out[:, lo:hi] = dg_euler_rhs(q)[:, lo:hi]`` (dgb_euler_rhs_range)."""
+    q = _f64(actx, q, "q")
+    G, g, gptr = _ghost_ptr(actx, ghost, (op.dim + 2,), q.shape[-1])
+    disc = _op_disc(actx, op, q, G)
+    _cabi.check(actx.lib.dgb_euler_rhs_range(disc.handle, q.ptr, gptr, out.ptr, op.qfar_host.ctypes.data,
+                                             op.phys_host.ctypes.data, int(lo), int(hi), actx._st), "dg_euler_rhs (range)")
+    actx.launch_count += 1
+
+
+def ns_flux_range(actx, op, q, ghost, T, lo, hi):
+    """``T[:, lo:hi] = dg_ns_flux(q)[:, lo:hi]`` (dgb_ns_flux_range)."""
+    q = _f64(actx, q, "q")
+    G, g, gptr = _ghost_ptr(actx, ghost, (op.dim + 2,), q.shape[-1])
+    disc = _op_disc(actx, op, q, G)
+    _bind_jacobian(actx, disc, op.dcoll.jac)
+    _cabi.check(actx.lib.dgb_ns_flux_range(disc.handle, q.ptr, gptr, T.ptr, op.qfar_host.ctypes.data,
+                                           op.phys_host.ctypes.data, int(lo), int(hi), actx._st), "dg_ns_flux (range)")
+    actx.launch_count += 1
+
+
+def ns_div_range(actx, op, q, T, ghost, Tghost, out, lo, hi):
+    """``out[:, lo:hi] = dg_ns_div(q, T)[:, lo:hi]`` (dgb_ns_div_range)."""
+    q = _f64(actx, q, "q")
+    npl = op.dim * (op.dim + 2) + 1
+    G, g, gptr = _ghost_ptr(actx, ghost, (op.dim + 2,), q.shape[-1])
+    TG, tg, tgptr = _ghost_ptr(actx, Tghost, (npl,), q.shape[-1])
+    disc = _op_disc(actx, op, q, G)
+    _bind_jacobian(actx, disc, op.dcoll.jac)
+    _check_facemat(disc, op.dcoll.facemat, op.dcoll.facemat_p)
+    _cabi.check(actx.lib.dgb_ns_div_range(disc.handle, q.ptr, T.ptr, gptr, tgptr, out.ptr, op.qfar_host.ctypes.data,
+                                          op.phys_host.ctypes.data, int(lo), int(hi), actx._st), "dg_ns_div (range)")
+    actx.launch_count += 1
+
+# }}}
+
+
 FUSED = {"dg_ns_flux": dg_ns_flux, "dg_ns_div": dg_ns_div, "dg_ns_div_rk": dg_ns_div_rk, "dg_euler_rhs": dg_euler_rhs, "dg_ns_grad": dg_ns_grad, "dg_ns_rhs": dg_ns_rhs,
          "dg_euler_rhs_rk": dg_euler_rhs_rk, "dg_ns_rhs_rk": dg_ns_rhs_rk}

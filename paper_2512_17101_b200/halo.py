@@ -30,11 +30,23 @@ class TorchCommunicator:
         self.group = group
         self.rank = dist.get_rank(group)
         self.size = dist.get_world_size(group)
+        self.backend = dist.get_backend(group)
 
     def exchange(self, sends, recvs):
         """``sends``: list of (tensor, peer, tag); ``recvs``: list of (tensor, peer, tag).
         Posts everything as one batch and waits."""
         dist = self.dist
+        if self.backend == "gloo" and any(t.is_cuda for t, _, _ in list(sends) + list(recvs)):
+            # test configuration only (two ranks sharing one GPU): gloo has no device send/recv, so the
+            # payloads are staged through host memory.  The NCCL path below never does this.
+            import torch
+            torch.cuda.current_stream().synchronize()
+            hs = [(t.detach().cpu(), peer, tag) for t, peer, tag in sends]
+            hr = [(torch.empty(t.shape, dtype=t.dtype), peer, tag) for t, peer, tag in recvs]
+            self.exchange(hs, hr)
+            for (t, _, _), (h, _, _) in zip(recvs, hr):
+                t.copy_(h)
+            return
         ops = []
         # a deterministic global order keeps NCCL's paired send/recv matching happy: receives and
         # sends are sorted by (tag, peer)
@@ -62,6 +74,9 @@ class HaloExchange:
             self._send_idx = [actx.from_numpy(np.ascontiguousarray(s, dtype=np.int64)) for s in plan.send_local]
         self.bytes_per_exchange = 0
         self.messages_per_exchange = len(plan.peers)
+        # interior elements first + a communication stream: the exchange hides behind the interior
+        # range of each pass (set ``overlap = False`` for the plain exchange-then-compute order)
+        self.overlap = True
 
     # {{{ packing
     def _pack(self, data, k):
@@ -121,13 +136,87 @@ class HaloExchange:
         self.bytes_per_exchange = sum(t.numel() * 8 for t, _, _ in sends)
         return self.actx.from_numpy(ghost)
 
+    # {{{ asynchronous exchange on a communication stream (device contexts)
+    @property
+    def comm_stream(self):
+        if getattr(self, "_comm_stream", None) is None:
+            import torch
+            self._comm_stream = torch.cuda.Stream(device=self.actx.device)
+        return self._comm_stream
+
+    def exchange_begin(self, data):
+        """Pack on the compute stream, then post the whole batch on the communication stream
+        (NCCL group of sends and receives over NVLink).  Returns a ticket for ``exchange_end``;
+        kernels enqueued on the compute stream in between overlap the transfer."""
+        import torch
+        plan, actx = self.plan, self.actx
+        lead = tuple(data.shape[:-2])
+        ghost = actx.empty(lead + (plan.nghost, self.ndofs))
+        sends, recvs, keep = [], [], []
+        for k, (peer, tag) in enumerate(zip(plan.peers, plan.tags)):
+            a, b = plan.recv_slots[k]
+            buf = actx.empty(lead + (b - a, self.ndofs))
+            recvs.append((buf.t, peer, tag)); keep.append((buf, a, b))
+            packed = self._pack(data, k)
+            sends.append((packed.t, peer, self.send_tags[k]))
+        packed_ready = torch.cuda.Event()
+        packed_ready.record(actx.stream)
+        cs = self.comm_stream
+        cs.wait_event(packed_ready)
+        with torch.cuda.stream(cs):
+            for t, _, _ in sends + recvs:
+                t.record_stream(cs)
+            self.comm.exchange(sends, recvs)
+            done = torch.cuda.Event()
+            done.record(cs)
+        self.bytes_per_exchange = sum(t.numel() * 8 for t, _, _ in sends)
+        return ghost, keep, done, sends
+
+    def exchange_end(self, ticket):
+        """Make the compute stream wait for the transfer and place the received slabs in the ghost array."""
+        ghost, keep, done, _sends = ticket
+        actx = self.actx
+        actx.stream.wait_event(done)
+        for buf, a, b in keep:
+            actx._scatter_into(ghost, ghost.t[..., a:b, :], buf)
+        return ghost
+    # }}}
+
     # {{{ partition-aware right-hand sides
+    def _can_overlap(self):
+        return (self.on_device and self.overlap and self.plan.nranks > 1 and bool(self.plan.peers)
+                and self.plan.n_interior is not None)
+
     def euler_rhs(self, op, q: DOFArray) -> DOFArray:
-        return op.rhs(q, ghost=self.exchange(q.data))
+        if not self._can_overlap():
+            return op.rhs(q, ghost=self.exchange(q.data))
+        from . import fused
+        actx, nI, E = self.actx, self.plan.n_interior, self.plan.nlocal
+        ticket = self.exchange_begin(q.data)                            # state halos in flight ...
+        out = actx.empty(q.data.shape)
+        fused.euler_rhs_range(actx, op, q.data, ticket[0], out, 0, nI)  # ... under the interior elements
+        ghost = self.exchange_end(ticket)
+        fused.euler_rhs_range(actx, op, q.data, ghost, out, nI, E)
+        return DOFArray(actx, out)
 
     def ns_rhs(self, op, q: DOFArray) -> DOFArray:
-        ghost = self.exchange(q.data)                                   # batch 1: state halos
-        return op.rhs(q, ghost=ghost, halo_fn=lambda T: self.exchange(T.data))   # batch 2: flux-plane halos
+        if not self._can_overlap():
+            ghost = self.exchange(q.data)                                   # batch 1: state halos
+            return op.rhs(q, ghost=ghost, halo_fn=lambda T: self.exchange(T.data))   # batch 2: flux-plane halos
+        from . import fused
+        actx, nI, E = self.actx, self.plan.n_interior, self.plan.nlocal
+        dim = op.dim
+        t1 = self.exchange_begin(q.data)                                    # batch 1 in flight ...
+        T = actx.empty((dim * (dim + 2) + 1,) + tuple(q.data.shape[1:]))
+        fused.ns_flux_range(actx, op, q.data, t1[0], T, 0, nI)              # ... under pass 1 of the interior
+        ghost = self.exchange_end(t1)
+        fused.ns_flux_range(actx, op, q.data, ghost, T, nI, E)              # pass 1 next to the partition boundary
+        t2 = self.exchange_begin(T)                                         # batch 2 in flight ...
+        out = actx.empty(q.data.shape)
+        fused.ns_div_range(actx, op, q.data, T, ghost, t2[0], out, 0, nI)   # ... under pass 2 of the interior
+        tghost = self.exchange_end(t2)
+        fused.ns_div_range(actx, op, q.data, T, ghost, tghost, out, nI, E)
+        return DOFArray(actx, out)
 
     def ns_rhs_grad_form(self, op, q: DOFArray) -> DOFArray:
         ghost = self.exchange(q.data)
@@ -139,6 +228,9 @@ def ring_slab_halo(actx, mesh, ncells_x, rank, nranks, order, lo_x=-1.0, hi_x=1.
     """Weak-scaling helper for bench.py: local mesh + ``HaloExchange`` of one rank of a ring."""
     from .dg.partition import ring_slab
     from .dg.simplex import simplex_element
+    from .dg.partition import interior_first
     local, plan = ring_slab(mesh, ncells_x, rank, nranks, lo_x, hi_x)
+    if nranks > 1:
+        local, plan = interior_first(local, plan)
     comm = TorchCommunicator() if nranks > 1 else None
     return local, HaloExchange(actx, plan, comm, simplex_element(mesh.dim, order).Np)

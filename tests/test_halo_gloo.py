@@ -18,18 +18,22 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, mode, outq):
+def _worker(rank, world, port, mode, outq, device=False):
     sys.path.insert(0, ROOT)
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from oracle.laze_port import NumpyArrayContext
         from paper_2512_17101_b200 import DGDiscretization, EulerOperator, NavierStokesOperator, box_mesh
-        from paper_2512_17101_b200.dg.partition import partition_elements, rank_mesh, ring_slab
+        from paper_2512_17101_b200.dg.partition import interior_first, partition_elements, rank_mesh, ring_slab
         from paper_2512_17101_b200.halo import HaloExchange, TorchCommunicator
         from tests.common import random_state
-        actx = NumpyArrayContext()
+        if device:        # both ranks share cuda:0; gloo stages the payloads through the host
+            from paper_2512_17101_b200 import B200ArrayContext
+            actx = B200ArrayContext()
+        else:
+            from oracle.laze_port import NumpyArrayContext
+            actx = NumpyArrayContext()
         comm = TorchCommunicator()
         base = box_mesh((3,) * 3, (-1,) * 3, (1,) * 3, periodic=(True,) * 3)
         if mode == "partition":
@@ -39,20 +43,32 @@ def _worker(rank, world, port, mode, outq):
         else:
             local, plan = ring_slab(base, 3, rank, world, -1.0, 1.0)
             q0 = random_state(3, base.nelements, 10, seed=9 + rank)
+        if device:
+            local, plan2 = interior_first(local, plan)
+            q0 = q0[:, plan2.local_perm, :]
+            ids = plan2.global_ids if plan2.global_ids is not None else plan2.local_perm
+            plan = plan2
+        else:
+            ids = plan.global_ids
         d = DGDiscretization(actx, local, 2, ghost_elements=plan.nghost)
         halo = HaloExchange(actx, plan, comm, d.Np)
+        assert halo._can_overlap() == device
         e = d.to_numpy(halo.euler_rhs(EulerOperator(d), d.from_numpy(q0)))
         v = d.to_numpy(halo.ns_rhs(NavierStokesOperator(d, mu=2e-2), d.from_numpy(q0)))
-        outq.put((rank, plan.global_ids, e, v, halo.messages_per_exchange, halo.bytes_per_exchange))
+        if device:      # the plain exchange-then-compute order gives the same bits
+            halo.overlap = False
+            v2 = d.to_numpy(halo.ns_rhs(NavierStokesOperator(d, mu=2e-2), d.from_numpy(q0)))
+            assert np.array_equal(v, v2)
+        outq.put((rank, ids, e, v, halo.messages_per_exchange, halo.bytes_per_exchange))
     finally:
         dist.destroy_process_group()
 
 
-def _run(mode):
+def _run(mode, device=False):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, mode, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, mode, q, device)) for r in range(2)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=180) for _ in procs], key=lambda t: t[0])
@@ -105,3 +121,44 @@ def test_two_rank_ring_matches_double_box():
     for rank, _, e, v, nmsg, nbytes in res:
         assert nmsg == 2
         assert rel_err(v, ref[:, idx[rank], :]) <= 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(600)
+def test_two_ranks_one_gpu_overlapped_exchange():
+    """The device path of the N>1 run -- interior-first renumbering, element-range kernels, exchange on a
+    communication stream overlapped with the interior range of each pass -- with two ranks sharing the
+    one GPU of the test box (gloo stages the messages through the host; NCCL refuses two ranks per
+    device).  Must reproduce the single-domain oracle and the non-overlapped order bit for bit."""
+    sys.path.insert(0, ROOT)
+    from oracle.laze_port import NumpyArrayContext, rel_err
+    from paper_2512_17101_b200 import DGDiscretization, EulerOperator, NavierStokesOperator, box_mesh
+    from tests.common import random_state
+    actx = NumpyArrayContext()
+    # partition of one periodic box
+    res = _run("partition", device=True)
+    mesh = box_mesh((3,) * 3, (-1,) * 3, (1,) * 3, periodic=(True,) * 3)
+    d = DGDiscretization(actx, mesh, 2)
+    q0 = random_state(3, mesh.nelements, 10, seed=9)
+    ref_e = d.to_numpy(EulerOperator(d).rhs(d.from_numpy(q0)))
+    ref_v = d.to_numpy(NavierStokesOperator(d, mu=2e-2).rhs(d.from_numpy(q0)))
+    full_e, full_v = np.empty_like(ref_e), np.empty_like(ref_v)
+    for rank, ids, e, v, nmsg, nbytes in res:
+        full_e[:, ids, :], full_v[:, ids, :] = e, v
+    assert rel_err(full_e, ref_e) <= 1e-12 and rel_err(full_v, ref_v) <= 1e-12
+    # bench.py's ring of periodic boxes
+    res = _run("ring", device=True)
+    glob = box_mesh((6, 3, 3), (-1, -1, -1), (3, 1, 1), periodic=(True,) * 3)
+    base = box_mesh((3,) * 3, (-1,) * 3, (1,) * 3, periodic=(True,) * 3)
+    d = DGDiscretization(actx, glob, 2)
+    gkey = {tuple(np.round(c, 9)): e for e, c in enumerate(glob.vertices.mean(axis=1))}
+    q0 = np.empty((5, glob.nelements, 10))
+    idx = []
+    for r in range(2):
+        cent = base.vertices.mean(axis=1) + np.array([2.0 * r, 0, 0])
+        idx.append(np.array([gkey[tuple(np.round(c, 9))] for c in cent]))
+        q0[:, idx[r], :] = random_state(3, base.nelements, 10, seed=9 + r)
+    ref = d.to_numpy(NavierStokesOperator(d, mu=2e-2).rhs(d.from_numpy(q0)))
+    for rank, perm, e, v, nmsg, nbytes in res:
+        assert nmsg == 2
+        assert rel_err(v, ref[:, idx[rank][perm], :]) <= 1e-12

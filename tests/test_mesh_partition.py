@@ -5,7 +5,7 @@ import pytest
 from oracle.laze_port import NumpyArrayContext, rel_err
 from paper_2512_17101_b200 import DGDiscretization, EulerOperator, NavierStokesOperator, box_mesh
 from paper_2512_17101_b200.dg.mesh import face_index_maps, geometry
-from paper_2512_17101_b200.dg.partition import partition_elements, rank_mesh, ring_slab
+from paper_2512_17101_b200.dg.partition import interior_first, partition_elements, rank_mesh, ring_slab
 from paper_2512_17101_b200.dg.simplex import simplex_element
 from paper_2512_17101_b200.discretization import BC_FARFIELD, BC_WALL
 from tests.common import FARFIELD, random_state
@@ -57,7 +57,7 @@ def _loopback(locs, fields, Np):
 
 
 @pytest.mark.parametrize("dim,n,per,nparts", [(3, 3, True, 2), (3, 3, True, 4), (2, 4, False, 3)])
-def test_partitioned_rhs_equals_single_domain(dim, n, per, nparts):
+def test_partitioned_rhs_equals_single_domain(dim, n, per, nparts, reorder=False):
     actx = NumpyArrayContext()
     mesh = box_mesh((n,) * dim, (-1,) * dim, (1,) * dim, periodic=(per,) * dim)
     bc = None if per else {k: (BC_WALL if k % 2 else BC_FARFIELD) for k in range(1, 2 * dim + 1)}
@@ -66,6 +66,12 @@ def test_partitioned_rhs_equals_single_domain(dim, n, per, nparts):
     part = partition_elements(mesh, nparts)
     assert np.bincount(part).min() >= mesh.nelements // nparts - 1
     locs = [rank_mesh(mesh, part, r) for r in range(nparts)]
+    if reorder:       # [interior | next to a ghost] renumbering used for the exchange/compute overlap
+        locs = [interior_first(m, p) for m, p in locs]
+        for m, p in locs:
+            assert not np.any(m.nbr_elem[:p.n_interior] >= p.nlocal)
+            assert np.all(np.any(m.nbr_elem[p.n_interior:] >= p.nlocal, axis=1))
+            assert sorted(p.global_ids.tolist()) == sorted(np.nonzero(part == p.rank)[0].tolist())
     for a in range(nparts):
         for b in range(nparts):
             if a != b:
@@ -97,6 +103,11 @@ def test_partitioned_rhs_equals_single_domain(dim, n, per, nparts):
         for r, (m, p) in enumerate(locs):
             full[:, p.global_ids, :] = res[r]
         assert rel_err(full, ref) <= 1e-13
+
+
+@pytest.mark.parametrize("dim,n,per,nparts", [(3, 3, True, 2), (2, 4, False, 3)])
+def test_interior_first_renumbering(dim, n, per, nparts):
+    test_partitioned_rhs_equals_single_domain(dim, n, per, nparts, reorder=True)
 
 
 def test_mismatched_plan_is_rejected():
