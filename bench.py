@@ -195,9 +195,17 @@ def run_b200(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # DGB_BENCH_SHARE_GPU=1: dry run of the N>1 code path on a box with a single GPU (all ranks on cuda:0,
+    # gloo with host-staged messages).  Its numbers mean nothing; the driver never sets it.
+    share = os.environ.get("DGB_BENCH_SHARE_GPU") == "1"
+    if share:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     if world != args.gpus and rank == 0:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
 
@@ -286,7 +294,7 @@ def run_b200(args):
     ms_total = start.elapsed_time(stop)
     ms_step = ms_total / K
     if world > 1:
-        t = torch.tensor([ms_step], device="cuda", dtype=torch.float64)
+        t = torch.tensor([ms_step], device="cpu" if share else "cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step = float(t.item())
     value = world * ndof / (ms_step * 1e-3) / 1e9
@@ -353,7 +361,7 @@ def run_b200(args):
         torch.cuda.synchronize()
         ms_e2e = s0.elapsed_time(s1) / Ke
         if world > 1:
-            t = torch.tensor([ms_e2e], device="cuda", dtype=torch.float64)
+            t = torch.tensor([ms_e2e], device="cpu" if share else "cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms_e2e = float(t.item())
         e2e = {"value": world * ndof / (ms_e2e * 1e-3) / 1e9, "unit": "GDOF/s",
@@ -401,9 +409,9 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=94, help="cells per axis per GPU (94 -> 4,983,504 elements, 99.67M DOFs)")
+    ap.add_argument("--n", "--cells", dest="n", type=int, default=94, help="cells per axis per GPU (94 -> 4,983,504 elements, 99.67M DOFs)")
     ap.add_argument("--cpu-n", type=int, default=10, help="cells per axis of each CPU-baseline sample mesh")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--order", type=int, default=3, help="polynomial order (headline: 3)")

@@ -29,6 +29,12 @@
 #ifndef DGB_DIV_LAZY_EX
 #define DGB_DIV_LAZY_EX 0
 #endif
+#ifndef DGB_DIV4_NB
+#define DGB_DIV4_NB 2
+#endif
+#ifndef DGB_DIV4_LAZY_EX
+#define DGB_DIV4_LAZY_EX 1
+#endif
 
 namespace dgb {
 
@@ -505,6 +511,125 @@ __device__ __noinline__ VecC<DIM> boundary_operand(int bc, int f, VecC<DIM> qm_,
   return out;
 }
 
+// Face phase of pass 2 for one block: gather the neighbour's q, lam and signed T rows of every face
+// node, Rusanov penalty, operand rows  Fs = (nbr - sJ max(lam-, lam+) (q- - q+)) / 2  with
+// nbr = sJ F+.n+ (the own-side half lives in the folded volume matrix Wv2).  NB face nodes per
+// lane have their gathers in flight together; with LAZY the DIM-1 extra rows a neighbour's face 0
+// needs are fetched in a second wave (fewer live registers).
+template <int DIM, int P, int KW, int NB, bool LAZY>
+__device__ __forceinline__ void div_face_phase(const int* flc, const int* fn, const int* perm,
+                                               const Div3Small<DIM, P, KW>& M, double* Fs, const DiscDev& d,
+                                               const double* __restrict__ q, const double* __restrict__ T,
+                                               const double* __restrict__ ghost, const double* __restrict__ Tghost,
+                                               const Phys& ph, long long e0, int nel, int lane) {
+  using EL = ElemT<DIM, P>;
+  constexpr int C = EL::C, NP = EL::NP, NF = EL::NF, NFP = EL::NFP, NFT = EL::NFT;
+  constexpr int NR = (KW * NFT + 31) / 32;
+  constexpr int NEX = LAZY ? C : (DIM - 1) * C;
+  const long long E = d.E, G = d.G;
+#pragma unroll 1
+  for (int k0 = 0; k0 < NR; k0 += NB) {
+    double qp[NB][C], nbr[NB][C], ex[NB][NEX], lam_p[NB];
+    long long cnk[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int k = k0 + b;
+      cnk[b] = -1;
+      if (k < NR) {
+        const int flk = flc[k * 32 + lane];
+        const int e = flk & 3, f = (flk >> 2) & 3, m = (flk >> 4) & 15;
+        if (flk >= 0 && e < nel) {
+          const long long cn = M.conn[e][f];
+          cnk[b] = cn;
+          const long long nb = DGB_CONN_NB(cn);
+          const int nf = DGB_CONN_NF(cn);
+          const int jp = fn[nf * NFP + perm[DGB_CONN_PERM(cn) * NFP + m]];
+          const bool in_ghost = nb >= E;
+          const long long pstride = (in_ghost ? G : E) * NP;
+          const long long off = (in_ghost ? nb - E : nb) * NP + jp;
+          const double* qbase = (in_ghost ? ghost : q) + off;
+          const double* tbase = (in_ghost ? Tghost : T) + off;
+          const int r0 = nf == 0 ? 0 : nf - 1;
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            qp[b][c] = qbase[c * pstride];
+            nbr[b][c] = tbase[(r0 * C + c) * pstride];
+          }
+          lam_p[b] = tbase[(DIM * C) * pstride];
+          if (!LAZY && nf == 0) {
+#pragma unroll
+            for (int rc = 0; rc < (DIM - 1) * C; ++rc) ex[b][rc] = tbase[(C + rc) * pstride];
+          }
+        }
+      }
+    }
+    if (LAZY) {
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int k = k0 + b;
+        if (k < NR && cnk[b] >= 0 && DGB_CONN_NF(cnk[b]) == 0 && DGB_CONN_BC(cnk[b]) == 0) {
+          const int flk = flc[k * 32 + lane];
+          const long long nb = DGB_CONN_NB(cnk[b]);
+          const int m = (flk >> 4) & 15;
+          const int jp = fn[perm[DGB_CONN_PERM(cnk[b]) * NFP + m]];
+          const bool in_ghost = nb >= E;
+          const long long pstride = (in_ghost ? G : E) * NP;
+          const double* tbase = (in_ghost ? Tghost : T) + (in_ghost ? nb - E : nb) * NP + jp;
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            double t = tbase[(C + c) * pstride];
+#pragma unroll
+            for (int r = 2; r < DIM; ++r) t += tbase[(r * C + c) * pstride];
+            ex[b][c] = t;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int k = k0 + b;
+      if (k < NR && cnk[b] >= 0) {
+        const int flk = flc[k * 32 + lane];
+        const int e = flk & 3, f = (flk >> 2) & 3, jm = (flk >> 8) & 255, fm = (flk >> 16) & 255;
+        const int nf = DGB_CONN_NF(cnk[b]), bc = DGB_CONN_BC(cnk[b]);
+        const double sj = M.sj[e][f];
+        const double lam_m = M.Lam[e * NP + jm];
+        double qm[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) qm[c] = M.Qs[(c * KW + e) * NP + jm];
+        double* fs = Fs + e * EL::LDF + fm;
+        if (bc == 0) {
+          if (nf == 0) {
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+              if (LAZY) {
+                nbr[b][c] += ex[b][c];
+              } else {
+#pragma unroll
+                for (int r = 1; r < DIM; ++r) nbr[b][c] += ex[b][(r - 1) * C + c];
+              }
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < C; ++c) nbr[b][c] = -nbr[b][c];
+          }
+          const double pen = sj * fmax(lam_m, lam_p[b]);
+#pragma unroll
+          for (int c = 0; c < C; ++c) fs[c * (KW * EL::LDF)] = 0.5 * (nbr[b][c] - pen * (qm[c] - qp[b][c]));
+        } else {
+          VecC<DIM> a_;
+#pragma unroll
+          for (int c = 0; c < C; ++c) a_.v[c] = qm[c];
+          const VecC<DIM> fb = boundary_operand<DIM>(bc, f, a_, T + (e0 + e) * NP + jm, E * NP, lam_m, sj,
+                                                     d.normals + (e0 + e) * NF + f, E * NF, ph);
+#pragma unroll
+          for (int c = 0; c < C; ++c) fs[c * (KW * EL::LDF)] = fb.v[c];
+        }
+      }
+    }
+  }
+}
+
 template <int DIM, int P, int KW, int NWARPS>
 __global__ void __launch_bounds__(NWARPS * 32, 1)
 k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
@@ -569,111 +694,7 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
     //      constant coefficients and lives in the folded volume matrix, so this phase needs only
     //      q, lam and the connectivity of the block -- not its T rows, which are still landing.
     //      Fs = (nbr - sJ max(lam-, lam+) (q- - q+)) / 2,  nbr = sJ F+.n+ gathered from the neighbour.
-#pragma unroll 1
-    for (int k0 = 0; k0 < NR; k0 += NB) {
-      double qp[NB][C], nbr[NB][C], ex[NB][(DIM - 1) * C], lam_p[NB];
-      long long cnk[NB];
-#pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        const int k = k0 + b;
-        cnk[b] = -1;
-        if (k < NR) {
-          const int flk = S.flc[k * 32 + lane];
-          const int e = flk & 3, f = (flk >> 2) & 3, m = (flk >> 4) & 15;
-          if (flk >= 0 && e < nel) {
-            const long long cn = M.conn[e][f];
-            cnk[b] = cn;
-            const long long nb = DGB_CONN_NB(cn);
-            const int nf = DGB_CONN_NF(cn);
-            const int jp = S.fn[nf * NFP + S.perm[DGB_CONN_PERM(cn) * NFP + m]];
-            const bool in_ghost = nb >= E;
-            const long long pstride = (in_ghost ? G : E) * NP;
-            const long long off = (in_ghost ? nb - E : nb) * NP + jp;
-            const double* qbase = (in_ghost ? ghost : q) + off;
-            const double* tbase = (in_ghost ? Tghost : T) + off;
-            const int r0 = nf == 0 ? 0 : nf - 1;
-#pragma unroll
-            for (int c = 0; c < C; ++c) {
-              qp[b][c] = qbase[c * pstride];
-              nbr[b][c] = tbase[(r0 * C + c) * pstride];
-            }
-            lam_p[b] = tbase[(DIM * C) * pstride];
-#if !DGB_DIV_LAZY_EX
-            if (nf == 0) {
-#pragma unroll
-              for (int rc = 0; rc < (DIM - 1) * C; ++rc) ex[b][rc] = tbase[(C + rc) * pstride];
-            }
-#endif
-          }
-        }
-      }
-#if DGB_DIV_LAZY_EX
-      // face 0 of a neighbour is the sum of its DIM rows: the other DIM-1 are fetched in a second wave
-#pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        const int k = k0 + b;
-        if (k < NR && cnk[b] >= 0 && DGB_CONN_NF(cnk[b]) == 0 && DGB_CONN_BC(cnk[b]) == 0) {
-          const int flk = S.flc[k * 32 + lane];
-          const long long nb = DGB_CONN_NB(cnk[b]);
-          const int m = (flk >> 4) & 15;
-          const int jp = S.fn[S.perm[DGB_CONN_PERM(cnk[b]) * NFP + m]];
-          const bool in_ghost = nb >= E;
-          const long long pstride = (in_ghost ? G : E) * NP;
-          const double* tbase = (in_ghost ? Tghost : T) + (in_ghost ? nb - E : nb) * NP + jp;
-#pragma unroll
-          for (int c = 0; c < C; ++c) {
-            double t = tbase[(C + c) * pstride];
-#pragma unroll
-            for (int r = 2; r < DIM; ++r) t += tbase[(r * C + c) * pstride];
-            ex[b][c] = t;
-          }
-        }
-      }
-#endif
-#pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        const int k = k0 + b;
-        if (k < NR && cnk[b] >= 0) {
-          const int flk = S.flc[k * 32 + lane];
-          const int e = flk & 3, f = (flk >> 2) & 3, jm = (flk >> 8) & 255, fm = (flk >> 16) & 255;
-          const int nf = DGB_CONN_NF(cnk[b]), bc = DGB_CONN_BC(cnk[b]);
-          const double sj = M.sj[e][f];
-          const double lam_m = M.Lam[e * NP + jm];
-          double qm[C];
-#pragma unroll
-          for (int c = 0; c < C; ++c) qm[c] = M.Qs[(c * KW + e) * NP + jm];
-          double* fs = W.Fs + e * EL::LDF + fm;
-          if (bc == 0) {
-            if (nf == 0) {
-#if DGB_DIV_LAZY_EX
-#pragma unroll
-              for (int c = 0; c < C; ++c) nbr[b][c] += ex[b][c];
-#else
-#pragma unroll
-              for (int c = 0; c < C; ++c) {
-#pragma unroll
-                for (int r = 1; r < DIM; ++r) nbr[b][c] += ex[b][(r - 1) * C + c];
-              }
-#endif
-            } else {
-#pragma unroll
-              for (int c = 0; c < C; ++c) nbr[b][c] = -nbr[b][c];
-            }
-            const double pen = sj * fmax(lam_m, lam_p[b]);
-#pragma unroll
-            for (int c = 0; c < C; ++c) fs[c * (KW * EL::LDF)] = 0.5 * (nbr[b][c] - pen * (qm[c] - qp[b][c]));
-          } else {
-            VecC<DIM> a_;
-#pragma unroll
-            for (int c = 0; c < C; ++c) a_.v[c] = qm[c];
-            const VecC<DIM> fb = boundary_operand<DIM>(bc, f, a_, T + (e0 + e) * NP + jm, E * NP, lam_m, sj,
-                                                       d.normals + (e0 + e) * NF + f, E * NF, ph);
-#pragma unroll
-            for (int c = 0; c < C; ++c) fs[c * (KW * EL::LDF)] = fb.v[c];
-          }
-        }
-      }
-    }
+    div_face_phase<DIM, P, KW, NB, (DGB_DIV_LAZY_EX != 0)>(S.flc, S.fn, S.perm, M, W.Fs, d, q, T, ghost, Tghost, ph, e0, nel, lane);
     cp_async_wait<1>();                  // T(b) has landed
     __syncwarp();
 
@@ -710,6 +731,183 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
     buf ^= 1;
   }
   cp_async_wait<0>();
+}
+
+// ------------------------------------------------------------------------------------------
+// pass 2, producer/consumer version.
+//
+// ncu on k_nsdiv3 (8 warps, 235 registers): 2.0 warps per scheduler, 0.34 eligible, 6.8 cycles between
+// two issues of a warp -- each warp alternates between a latency-bound gather phase and a DMMA phase
+// and there are too few warps to cover one with the other.  Here a block is handled by a PAIR of
+// warps: the producer stages q/lam/connectivity, gathers the neighbour values and writes the face
+// operand rows Fs (double-buffered); the consumer streams the T rows, runs the DMMA contraction and
+// stores.  Neither holds the other's registers (gather values vs. accumulators), so 16 warps fit
+// where 8 did, and the two phases of consecutive blocks overlap by construction.  Hand-off: two
+// mbarriers per buffer (full / empty) in shared memory; block ids travel through a 4-slot mailbox.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, int parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@p bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}"
+      ::"r"(a), "r"(parity) : "memory");
+}
+
+template <int DIM, int P, int KW>
+struct alignas(16) Div4Pair {
+  using EL = ElemT<DIM, P>;
+  static constexpr int NCOL = EL::C * KW;
+  static constexpr int NTILE = (NCOL + 7) / 8;
+  double Ts[NCOL * EL::LDV];
+  double Fs[2][NCOL * EL::LDF];
+  Div3Small<DIM, P, KW> sm[2];          // producer-private
+  unsigned long long full[2], empty[2];
+  long long blk[4];                     // block id of block i at slot i & 3
+};
+
+template <int DIM, int P, int KW, int NPAIR>
+struct Div4Smem {
+  using EL = ElemT<DIM, P>;
+  double Wv[EL::NPR * EL::LDV];
+  double Wl[EL::NPR * EL::LDF];
+  Div4Pair<DIM, P, KW> w[NPAIR];
+  int fn[EL::NF * EL::NFP];
+  int perm[EL::NPERM * EL::NFP];
+  int flc[((KW * EL::NFT + 31) / 32) * 32];
+};
+
+template <int DIM, int P, int KW, int NPAIR>
+__global__ void __launch_bounds__(NPAIR * 64, 1)
+k_nsdiv4(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
+         const double* __restrict__ ghost, const double* __restrict__ Tghost,
+         Epilogue ep, Phys ph, long long ebeg, long long eend, long long nwblocks,
+         unsigned long long* __restrict__ counter) {
+  using EL = ElemT<DIM, P>;
+  using WS = Div4Pair<DIM, P, KW>;
+  constexpr int C = EL::C, NP = EL::NP, NF = EL::NF, NFP = EL::NFP, NFT = EL::NFT;
+  constexpr int NT = NPAIR * 64;
+  constexpr int NR = (KW * NFT + 31) / 32;
+  constexpr int NB = DGB_DIV_NB;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  auto& S = *reinterpret_cast<Div4Smem<DIM, P, KW, NPAIR>*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool producer = warp >= NPAIR;
+  const int pair = producer ? warp - NPAIR : warp;
+  const long long E = d.E, G = d.G;
+
+  for (int n = tid; n < EL::NPR * EL::LDV; n += NT) S.Wv[n] = d.Wv2[n];
+  for (int n = tid; n < EL::NPR * EL::LDF; n += NT) S.Wl[n] = d.Wl[n];
+  for (int n = tid; n < NF * NFP; n += NT) S.fn[n] = d.tables[n];
+  for (int n = tid; n < EL::NPERM * NFP; n += NT) S.perm[n] = d.tables[NF * NFP + n];
+  for (int n = tid; n < NPAIR * (int)(sizeof(WS) / 8); n += NT) reinterpret_cast<double*>(&S.w[0])[n] = 0.0;
+  __syncthreads();
+  for (int n = tid; n < NR * 32; n += NT) S.flc[n] = face_lane_code<DIM, P, KW>(S.fn, n);
+  WS& W = S.w[pair];
+  const long long wstride = (long long)gridDim.x * NPAIR;
+  const long long wb0 = (long long)blockIdx.x * NPAIR + pair;
+  if (!producer && lane == 0) {
+    mbar_init(&W.full[0], 32); mbar_init(&W.full[1], 32);
+    mbar_init(&W.empty[0], 32); mbar_init(&W.empty[1], 32);
+    W.blk[0] = wb0;
+  }
+  __syncthreads();
+  if (wb0 >= nwblocks) return;
+
+  if (producer) {
+    // ================================ producer warp ================================
+    long long wb = wb0;
+    {
+      const long long e0 = ebeg + wb * KW;
+      div_stage_small<DIM, P, KW>(W.sm[0], d, q, T, e0, (int)((eend - e0) < (long long)KW ? (eend - e0) : (long long)KW), lane);
+      cp_async_commit();
+    }
+    unsigned long long ticket = draw_ticket(counter, lane);
+    for (int i = 0;; ++i) {
+      const int buf = i & 1;
+      const long long e0 = ebeg + wb * KW;
+      const int nel = (int)((eend - e0) < (long long)KW ? (eend - e0) : (long long)KW);
+      const long long wb_next = ticket_block(ticket, wstride);
+      if (lane == 0) W.blk[(i + 1) & 3] = wb_next;          // published by this block's full-arrive
+      const long long e1 = ebeg + wb_next * KW;
+      const int nel1 = wb_next < nwblocks ? (int)((eend - e1) < (long long)KW ? (eend - e1) : (long long)KW) : 0;
+      if (nel1 > 0) div_stage_small<DIM, P, KW>(W.sm[buf ^ 1], d, q, T, e1, nel1, lane);
+      cp_async_commit();
+      ticket = draw_ticket(counter, lane);
+      cp_async_wait<1>();                 // this block's q / lam / connectivity have landed
+      __syncwarp();
+      if (i >= 2) mbar_wait(&W.empty[buf], ((i >> 1) - 1) & 1);   // the consumer is done with Fs[buf] of block i-2
+      const Div3Small<DIM, P, KW>& M = W.sm[buf];
+      double* Fs = W.Fs[buf];
+      div_face_phase<DIM, P, KW, DGB_DIV4_NB, (DGB_DIV4_LAZY_EX != 0)>(S.flc, S.fn, S.perm, M, Fs, d, q, T, ghost, Tghost, ph, e0, nel, lane);
+      mbar_arrive(&W.full[buf]);          // all 32 lanes arrive: Fs[buf] and blk[(i+1)&3] are published
+      if (wb_next >= nwblocks) break;
+      wb = wb_next;
+    }
+    cp_async_wait<0>();
+  } else {
+    // ================================ consumer warp ================================
+    long long wb = wb0;
+    {
+      const long long e0 = ebeg + wb * KW;
+      div_stage_rows<DIM, P, KW>(W.Ts, d, T, e0, (int)((eend - e0) < (long long)KW ? (eend - e0) : (long long)KW), lane);
+      cp_async_commit();
+    }
+    for (int i = 0;; ++i) {
+      const int buf = i & 1;
+      const long long e0 = ebeg + wb * KW;
+      const int nel = (int)((eend - e0) < (long long)KW ? (eend - e0) : (long long)KW);
+      double rj[WS::NTILE];
+#pragma unroll
+      for (int mt = 0; mt < WS::NTILE; ++mt) {
+        const int e = (mt * 8 + (lane >> 2)) % KW;
+        rj[mt] = e < nel ? d.rj[e0 + e] : 0.0;
+      }
+      double acc[WS::NTILE][EL::NI][2];
+#pragma unroll
+      for (int mt = 0; mt < WS::NTILE; ++mt)
+#pragma unroll
+        for (int ni = 0; ni < EL::NI; ++ni) { acc[mt][ni][0] = 0.0; acc[mt][ni][1] = 0.0; }
+      cp_async_wait<0>();                 // this block's T rows have landed
+      __syncwarp();
+      mma_block<EL::NI, WS::NTILE>(acc, W.Ts, EL::LDV, S.Wv, EL::LDV, EL::KV / 4, lane);
+      __syncwarp();                       // T rows consumed
+      mbar_wait(&W.full[buf], (i >> 1) & 1);
+      const long long wb_next = W.blk[(i + 1) & 3];
+      if (wb_next < nwblocks) {           // next block's rows start their trip while the face part is contracted
+        const long long e1 = ebeg + wb_next * KW;
+        div_stage_rows<DIM, P, KW>(W.Ts, d, T, e1, (int)((eend - e1) < (long long)KW ? (eend - e1) : (long long)KW), lane);
+      }
+      cp_async_commit();
+      mma_block<EL::NI, WS::NTILE>(acc, W.Fs[buf], EL::LDF, S.Wl, EL::LDF, EL::KF / 4, lane);
+      mbar_arrive(&W.empty[buf]);         // Fs[buf] may be refilled (block i + 2)
+#pragma unroll
+      for (int mt = 0; mt < WS::NTILE; ++mt) {
+        const int col = mt * 8 + (lane >> 2);
+        const int c = col / KW, e = col - c * KW;
+        if (col < WS::NCOL && e < nel) {
+          const long long rowbase = ((long long)c * E + e0 + e) * NP;
+#pragma unroll
+          for (int ni = 0; ni < EL::NI; ++ni) {
+            const int i2 = ni * 8 + 2 * (lane & 3);
+            store_pair<NP>(ep, rowbase + i2, i2, rj[mt] * acc[mt][ni][0], rj[mt] * acc[mt][ni][1]);
+          }
+        }
+      }
+      if (wb_next >= nwblocks) break;
+      wb = wb_next;
+    }
+    cp_async_wait<0>();
+  }
 }
 
 }  // namespace dgb

@@ -70,6 +70,42 @@ int launch_div(const dgb_disc* d, const double* q, const double* T, const double
   return DGB_OK;
 }
 
+#ifndef DGB_DIV_PAIRS
+#define DGB_DIV_PAIRS 8
+#endif
+template <int DIM, int P> struct CfgP {
+  static constexpr int KW = DIM == 3 ? 3 : 4;
+  static constexpr size_t per = sizeof(dgb::Div4Pair<DIM, P, KW>);
+  static constexpr size_t fixed = sizeof(dgb::Div4Smem<DIM, P, KW, 1>) - per;
+  static constexpr int NPAIR = fit_warps(fixed, per, DGB_DIV_PAIRS);
+};
+
+// DGB_DIV_KERNEL=4 selects the producer/consumer warp-pair kernel (k_nsdiv4): correct, measured slower
+// (profiles/r01_flux_variants.md), kept for the A/B record; default 3 = k_nsdiv3
+int div_kernel() {
+  static int v = -1;
+  if (v < 0) v = env_int("DGB_DIV_KERNEL", 3);
+  return v;
+}
+
+template <int DIM, int P>
+int launch_div4(const dgb_disc* d, const double* q, const double* T, const double* ghost, const double* Tghost,
+                const dgb::Epilogue& ep, const dgb::Phys& ph, long long ebeg, long long eend, cudaStream_t st) {
+  using C = CfgP<DIM, P>;
+  auto kern = dgb::k_nsdiv4<DIM, P, C::KW, C::NPAIR>;
+  const size_t smem = sizeof(dgb::Div4Smem<DIM, P, C::KW, C::NPAIR>);
+  const long long nwb = (eend - ebeg + C::KW - 1) / C::KW;
+  if (nwb == 0) return DGB_OK;
+  static bool configured = false;
+  if (!configured) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured = true; }
+  const long long need = (nwb + C::NPAIR - 1) / C::NPAIR;
+  const int grid = (int)(need < dgb_num_sms() ? need : dgb_num_sms());
+  DGB_CUDA(cudaMemsetAsync(d->counters + 1, 0, sizeof(unsigned long long), st));
+  kern<<<grid, C::NPAIR * 64, smem, st>>>(d->dev, q, T, ghost, Tghost, ep, ph, ebeg, eend, nwb, d->counters + 1);
+  DGB_CUDA(cudaGetLastError());
+  return DGB_OK;
+}
+
 #define DGB_FOR_EACH_ELEMENT(X) X(2, 1) X(2, 2) X(2, 3) X(2, 4) X(3, 1) X(3, 2) X(3, 3) X(3, 4)
 
 void make_phys(dgb::Phys& ph, int C, const double* qfar, const double* phys) {
@@ -149,7 +185,9 @@ static int ns_div_impl(const dgb_disc* d, const double* q, const double* T, cons
   if ((rc = check_range(d, ebegin, eend))) return rc;
   if (d->dev.G > 0 && !Tghost) return dgb_fail(DGB_ERR_INVALID, "ghost elements need the ghost flux planes");
   dgb::Phys ph; make_phys(ph, d->dim + 2, qfar, phys);
-#define X(DIM, P) if (d->dim == DIM && d->order == P) return launch_div<DIM, P>(d, q, T, ghost, Tghost, ep, ph, ebegin, eend, (cudaStream_t)stream);
+#define X(DIM, P) if (d->dim == DIM && d->order == P)                                                         \
+    return div_kernel() == 3 ? launch_div<DIM, P>(d, q, T, ghost, Tghost, ep, ph, ebegin, eend, (cudaStream_t)stream)  \
+                             : launch_div4<DIM, P>(d, q, T, ghost, Tghost, ep, ph, ebegin, eend, (cudaStream_t)stream);
   DGB_FOR_EACH_ELEMENT(X)
 #undef X
   return dgb_fail(DGB_ERR_INVALID, "unsupported (dim, order)");

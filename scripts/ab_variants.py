@@ -14,11 +14,12 @@ sys.path.insert(0, ROOT)
 PKG = os.path.join(ROOT, "paper_2512_17101_b200")
 
 VARIANTS = {
-    "w8_nb1_2": ["DGB_FLUX_WARPS=8", "DGB_DIV_WARPS=8", "DGB_DIV_NB=1", "DGB_FLUX_NB=2"],
-    "w6_nb2_2": ["DGB_FLUX_WARPS=6", "DGB_DIV_WARPS=6", "DGB_DIV_NB=2", "DGB_FLUX_NB=2"],
-    "w10_nb1_2": ["DGB_FLUX_WARPS=10", "DGB_DIV_WARPS=10", "DGB_DIV_NB=1", "DGB_FLUX_NB=2"],
-    "w10_nb2_1": ["DGB_FLUX_WARPS=10", "DGB_DIV_WARPS=10", "DGB_DIV_NB=2", "DGB_FLUX_NB=1"],
-    "w4_nb2_4": ["DGB_FLUX_WARPS=4", "DGB_DIV_WARPS=4", "DGB_DIV_NB=2", "DGB_FLUX_NB=4"],
+    "p8_nb2lazy": [],
+    "p8_nb1": ["DGB_DIV4_NB=1"],
+    "p8_nb2": ["DGB_DIV4_NB=2", "DGB_DIV4_LAZY_EX=0"],
+    "p6_nb2": ["DGB_DIV_PAIRS=6", "DGB_DIV4_NB=2", "DGB_DIV4_LAZY_EX=0"],
+    "p6_nb4lazy": ["DGB_DIV_PAIRS=6", "DGB_DIV4_NB=4", "DGB_DIV4_LAZY_EX=1"],
+    "p4_nb2": ["DGB_DIV_PAIRS=4", "DGB_DIV4_NB=2", "DGB_DIV4_LAZY_EX=0"],
 }
 
 
