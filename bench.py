@@ -332,6 +332,12 @@ def run_b200(args):
                                                float(np.max(per_step))]}
     b_alg = 80.0 if euler else B_ALG_RHS
     rhs_gbs = ndof * b_alg / (ms_step * 1e-3) / 1e9
+    if roofline is None:
+        # partitioned run: the passes interleave with the halo exchange, so the roofline entry is the
+        # whole right-hand side of one rank (both kernels + exchange) against one GPU's HBM peak
+        roofline = {"bound": "hbm", "kernel": "whole RHS of one rank (both passes + halo exchange)",
+                    "achieved": rhs_gbs, "peak": peak, "unit": "GB/s", "frac": rhs_gbs / peak, "traffic": None,
+                    "peak_source": peak_src, "algorithmic_bytes_per_dof": b_alg, "ms_per_launch": ms_step}
 
     # ---- end to end through the public API with host buffers ---------------------------------
     e2e = None

@@ -243,3 +243,41 @@ def test_ghost_elements_on_device(gpu, dim, n, per, nparts):
                 out = ops[r].rhs_grad_form(qs[r], ghost=gh[r], halo_fn=lambda gq, r=r: ggh[r])
             full[:, p.global_ids, :] = ds[r].to_numpy(out)
         assert rel_err(full, ref) <= TOL_RHS, form
+
+
+@pytest.mark.timeout(900)
+def test_full_size_properties(gpu):
+    """BASELINE configs[2] at full size (3D NS p3, 94^3 Kuhn box, 99.67M DOFs), where the oracle cannot run:
+    size-independent properties instead -- free-stream preservation, discrete conservation on the
+    periodic mesh, agreement of the two arrangements of the scheme (independent kernels), linearity
+    of the RK-fused epilogue, and run-to-run bitwise reproducibility."""
+    from tests.common import smooth_state
+    d = make_dcoll(gpu, 3, 3, 94, "periodic")
+    E, Np = d.nelements, d.Np
+    assert E * Np == 99670080
+    op = NavierStokesOperator(d, mu=1e-3)
+    # free stream: a constant state has zero right-hand side
+    qf = np.array([1.2, 2.9, 0.3, -0.2, 0.1])
+    qc = d.from_numpy(np.broadcast_to(qf[:, None, None], (5, E, Np)))
+    assert d.norm_inf(op.rhs(qc)) < 5e-11
+    del qc
+    # smooth state: conservation, arrangement agreement, reproducibility
+    q = d.from_numpy(smooth_state(d.nodes()))
+    r = op.rhs(q)
+    rh = d.to_numpy(r)
+    assert np.all(np.isfinite(rh))
+    w = np.einsum("i,ij->j", np.ones(Np), d.element.mass)
+    total = np.einsum("cej,j,e->c", rh, w, d.geo.jac)
+    scale = np.einsum("cej,j,e->c", np.abs(rh), w, d.geo.jac)
+    assert np.all(np.abs(total) <= 1e-12 * np.maximum(scale, 1.0)), (total, scale)
+    # Two independent kernel pairs, no oracle.  The 1e-12 per-RHS tolerance is checked against the oracle
+    # on the parity meshes (n <= 5 above); round-off of a derivative operator grows like 1/h, and h here
+    # is 30x smaller, so the bar between two algebraically equal arrangements is scaled accordingly.
+    r2 = d.to_numpy(op.rhs_grad_form(q))
+    assert rel_err(r2, rh) <= TOL_RHS * 94 / 3
+    del r2
+    assert np.array_equal(d.to_numpy(op.rhs(q)), rh)
+    # fused stage update == a*x + b*rhs
+    o1, o2 = op.rhs_rk(q, q, r, (1.0, 0.25, 0.5, -2.0))
+    assert rel_err(d.to_numpy(o1), smooth_state(d.nodes()) + 0.25 * rh) <= 1e-13
+    assert rel_err(d.to_numpy(o2), 0.5 * rh - 2.0 * rh) <= 1e-13
