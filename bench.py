@@ -352,15 +352,21 @@ def run_b200(args):
         # Pipelined like a streaming user would: the H2D copy of step k+1 (upload stream), the compute of
         # step k (compute stream) and the D2H of step k-1 (download stream) overlap.  Every step still uploads its full input from pinned
         # host memory and downloads its full result; both are inside the timed region.
+        # two device input buffers, ping-ponged (a streaming caller allocates them once)
+        dev_in = [actx.empty(q_host.shape), actx.empty(q_host.shape)]
+        read_done = [None, None]
+        actx.synchronize()
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record(stream)
         actx.copy_stream.wait_event(s0)
-        nxt = actx.from_numpy_async(q_host)
+        nxt = actx.from_numpy_async(q_host, out=dev_in[0])
         for k in range(Ke):
             cur = actx.wait_for(nxt)
             res = rhs_step(DOFArray(actx, cur)).data
-            if k + 1 < Ke:
-                nxt = actx.from_numpy_async(q_host)               # H2D of step k+1 into a fresh buffer
+            read_done[k % 2] = torch.cuda.Event()
+            read_done[k % 2].record(stream)                       # step k no longer reads dev_in[k % 2]
+            if k + 1 < Ke:                                        # H2D of step k+1 into the other buffer
+                nxt = actx.from_numpy_async(q_host, after=read_done[(k + 1) % 2], out=dev_in[(k + 1) % 2])
             d2h_done = actx.to_numpy_async(res, out_host)         # D2H of step k's result (download stream)
         stream.wait_event(d2h_done)                               # the last result is on the host
         s1.record(stream)

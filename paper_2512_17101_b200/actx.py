@@ -303,20 +303,27 @@ class B200ArrayContext:
             self._copy_stream = _torch().cuda.Stream(device=self.device)
         return self._copy_stream
 
-    def from_numpy_async(self, value, after=None) -> DeviceArray:
+    def from_numpy_async(self, value, after=None, out: DeviceArray | None = None) -> DeviceArray:
         """Upload a PINNED host array on the copy stream.  ``after``: an event the copy must wait for
-        (e.g. the last kernel that read a buffer being recycled).  The result carries ``.ready``; call
-        ``actx.wait_for(arr)`` before using it on the compute stream."""
+        (e.g. the last kernel that read a buffer being recycled).  ``out``: an existing device array of
+        the same shape to upload into (a streaming caller ping-pongs two of them instead of allocating
+        per step; pass ``after`` = the event recorded after its last reader).  The result carries
+        ``.ready``; call ``actx.wait_for(arr)`` before using it on the compute stream."""
         torch = _torch()
         host = np.ascontiguousarray(value)
         if not self._is_pinned(host):
             raise errors.LazeError("from_numpy_async needs a page-locked buffer (actx.pinned_empty)")
         cs = self.copy_stream
-        with torch.cuda.stream(cs):
-            t = torch.empty(host.shape, dtype=_torch_dtype(_code_of_numpy(host.dtype)), device=self.device)
+        if out is None:
+            with torch.cuda.stream(cs):
+                t = torch.empty(host.shape, dtype=_torch_dtype(_code_of_numpy(host.dtype)), device=self.device)
+            out = DeviceArray(self, t)
+        else:
+            if tuple(out.shape) != tuple(host.shape) or out.dtype_code != _code_of_numpy(host.dtype):
+                raise errors.ShapeMismatch("from_numpy_async: `out` does not match the host array")
+            t = out.t
         if after is not None:
             cs.wait_event(after)
-        out = DeviceArray(self, t)
         _cabi.check(self.lib.dgb_memcpy_h2d(C.c_void_p(out.ptr), C.c_void_p(host.ctypes.data), host.nbytes,
                                             C.c_void_p(cs.cuda_stream)), "from_numpy_async")
         out.ready = torch.cuda.Event()
