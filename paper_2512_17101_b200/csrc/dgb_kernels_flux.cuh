@@ -21,13 +21,16 @@
 #include "dgb_kernels_warp.cuh"
 
 #ifndef DGB_FLUX_NB
-#define DGB_FLUX_NB 2
+#define DGB_FLUX_NB 4
 #endif
 #ifndef DGB_DIV_NB
 #define DGB_DIV_NB 2
 #endif
 #ifndef DGB_DIV_LAZY_EX
 #define DGB_DIV_LAZY_EX 0
+#endif
+#ifndef DGB_FLUX_PRODUCT_MAJOR
+#define DGB_FLUX_PRODUCT_MAJOR 0
 #endif
 #ifndef DGB_DIV4_NB
 #define DGB_DIV4_NB 2
@@ -212,11 +215,13 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
     ticket = draw_ticket(counter, lane);
 
     // ---- face averages q* (central flux, boundary states) -> Ss; metric coefficients ---------
+#if DGB_FLUX_PRODUCT_MAJOR
     for (int n = lane; n < nel * DIM * EL::NS; n += 32) {
       const int e = n / (DIM * EL::NS), xs = n - e * (DIM * EL::NS);
       const int x = xs / EL::NS, s = xs - x * EL::NS;
       W.coef[e][x][s] = s < DIM ? -geo.drdx[s * DIM + x][e] : geo.fsc[e][s - DIM] * geo.nrm[x][e][s - DIM];
     }
+#endif
     // the previous block left grad q in the q* rows: the K-padding columns must be zero again
     if (EL::NFPK != NFP) {
       for (int n = lane; n < WS::NCOLP * NF * (EL::NFPK - NFP); n += 32) {
@@ -273,45 +278,113 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
     }
     __syncwarp();
 
+#if DGB_FLUX_PRODUCT_MAJOR
+    // ---- tensor-core contractions, product by product over BOTH column tiles: every W fragment is
+    //      loaded once per block instead of once per tile (the L1/LSU data pipe is 68 % busy in this
+    //      kernel), each k-step issues 2*NI independent DMMAs, and a finished product is folded into
+    //      the gradient accumulators  v[x] += coef[x][s] * acc  while the next one runs.
+    {
+      const int k8 = lane >> 2;
+      double v[DIM][WS::NTILE][NI][2];
+#pragma unroll
+      for (int x = 0; x < DIM; ++x)
+#pragma unroll
+        for (int mt = 0; mt < WS::NTILE; ++mt)
+#pragma unroll
+          for (int ni = 0; ni < NI; ++ni) { v[x][mt][ni][0] = 0.0; v[x][mt][ni][1] = 0.0; }
+#pragma unroll
+      for (int s = 0; s < EL::NS; ++s) {
+        double acc[WS::NTILE][NI][2];
+#pragma unroll
+        for (int mt = 0; mt < WS::NTILE; ++mt)
+#pragma unroll
+          for (int ni = 0; ni < NI; ++ni) { acc[mt][ni][0] = 0.0; acc[mt][ni][1] = 0.0; }
+        if (s < DIM)
+          mma_block<NI, WS::NTILE>(acc, Qs, EL::LDQ, S.Wq + s * EL::NPR * EL::LDQ, EL::LDQ, EL::NPK / 4, lane);
+        else
+          mma_block<NI, WS::NTILE>(acc, W.Ss + (s - DIM) * EL::NFPK, LDSX, S.Wf + (s - DIM) * EL::NPR * EL::LDL,
+                                   EL::LDL, EL::NFPK / 4, lane);
+#pragma unroll
+        for (int mt = 0; mt < WS::NTILE; ++mt) {
+          const int e = (mt * 8 + k8) % KW;          // element of this lane's column (any value for padding columns)
+#pragma unroll
+          for (int x = 0; x < DIM; ++x) {
+            const double cf = W.coef[e][x][s];
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni) { v[x][mt][ni][0] += cf * acc[mt][ni][0]; v[x][mt][ni][1] += cf * acc[mt][ni][1]; }
+          }
+        }
+      }
+      __syncwarp();                       // every lane has read the q* rows: grad q may overwrite them
+#pragma unroll
+      for (int mt = 0; mt < WS::NTILE; ++mt) {
+        const int col = mt * 8 + k8;
+        const int c = col / KW, e = col - c * KW;
+        if (col < WS::NCOL && e < nel) {
+          double* sg = W.Ss + mt * 8 * LDSX;
+#pragma unroll
+          for (int x = 0; x < DIM; ++x)
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni) {
+              const int i = ni * 8 + 2 * (lane & 3);
+              if (NP % 2 == 0) {
+                if (i < NP) *reinterpret_cast<double2*>(sg + (x * 8 + k8) * NP + i) = make_double2(v[x][mt][ni][0], v[x][mt][ni][1]);
+              } else {
+                if (i < NP) sg[(x * 8 + k8) * NP + i] = v[x][mt][ni][0];
+                if (i + 1 < NP) sg[(x * 8 + k8) * NP + i + 1] = v[x][mt][ni][1];
+              }
+            }
+        }
+      }
+    }
+    __syncwarp();
+#else
     // ---- tensor-core contractions, one 8-column tile at a time; grad q of the tile -> its Ss rows ----
+    // On a simplex  fscale n_x (face f) = sum_r a[f][r] dr/dx[r][x]  with a[0][r] = 1, a[r+1][r] = -1, so
+    //   grad_x q = sum_f fscale n_x lift_f q*_f - sum_r dr/dx[r][x] Sw_r q
+    //            = -sum_r dr/dx[r][x] (Z_r - U_0),   Z_r = Sw_r q + lift_{r+1} q*_{r+1},  U_0 = lift_0 q*_0:
+    // DIM+1 accumulator sets instead of DIM+NF (Z_r simply continues its k-loop over the face-(r+1)
+    // operand rows) and DIM*DIM + DIM FP64 operations per value in the combination instead of
+    // DIM*(DIM+NF).
 #pragma unroll 1
     for (int tile = 0; tile < WS::NTILE; ++tile) {
-      double accT[DIM][1][NI][2], accU[NF][1][NI][2];
+      double accZ[DIM][1][NI][2], accU[1][NI][2];
 #pragma unroll
       for (int s = 0; s < DIM; ++s)
 #pragma unroll
-        for (int ni = 0; ni < NI; ++ni) { accT[s][0][ni][0] = 0.0; accT[s][0][ni][1] = 0.0; }
+        for (int ni = 0; ni < NI; ++ni) { accZ[s][0][ni][0] = 0.0; accZ[s][0][ni][1] = 0.0; }
 #pragma unroll
-      for (int s = 0; s < NF; ++s)
+      for (int ni = 0; ni < NI; ++ni) { accU[0][ni][0] = 0.0; accU[0][ni][1] = 0.0; }
 #pragma unroll
-        for (int ni = 0; ni < NI; ++ni) { accU[s][0][ni][0] = 0.0; accU[s][0][ni][1] = 0.0; }
-#pragma unroll
-      for (int r = 0; r < DIM; ++r)
-        mma_block<NI, 1>(accT[r], Qs + tile * 8 * EL::LDQ, EL::LDQ, S.Wq + r * EL::NPR * EL::LDQ, EL::LDQ,
+      for (int r = 0; r < DIM; ++r) {
+        mma_block<NI, 1>(accZ[r], Qs + tile * 8 * EL::LDQ, EL::LDQ, S.Wq + r * EL::NPR * EL::LDQ, EL::LDQ,
                          EL::NPK / 4, lane);
-#pragma unroll
-      for (int f = 0; f < NF; ++f)
-        mma_block<NI, 1>(accU[f], W.Ss + tile * 8 * LDSX + f * EL::NFPK, LDSX,
-                         S.Wf + f * EL::NPR * EL::LDL, EL::LDL, EL::NFPK / 4, lane);
+        mma_block<NI, 1>(accZ[r], W.Ss + tile * 8 * LDSX + (r + 1) * EL::NFPK, LDSX,
+                         S.Wf + (r + 1) * EL::NPR * EL::LDL, EL::LDL, EL::NFPK / 4, lane);
+      }
+      mma_block<NI, 1>(accU, W.Ss + tile * 8 * LDSX, LDSX, S.Wf, EL::LDL, EL::NFPK / 4, lane);
       __syncwarp();                       // every lane has read this tile's q* rows: they may be overwritten
       const int k8 = lane >> 2;
       const int col = tile * 8 + k8;
       const int c = col / KW, e = col - c * KW;
       if (col < WS::NCOL && e < nel) {
         double* sg = W.Ss + tile * 8 * LDSX;
+        double m[DIM][DIM];               // m[r][x] = -dr/dx[r][x]
 #pragma unroll
-        for (int x = 0; x < DIM; ++x) {
-          double cf[EL::NS];
+        for (int r = 0; r < DIM; ++r)
 #pragma unroll
-          for (int s = 0; s < EL::NS; ++s) cf[s] = W.coef[e][x][s];
+          for (int x = 0; x < DIM; ++x) m[r][x] = -geo.drdx[r * DIM + x][e];
 #pragma unroll
-          for (int ni = 0; ni < NI; ++ni) {
-            double v0 = 0.0, v1 = 0.0;
+        for (int ni = 0; ni < NI; ++ni) {
+          double z0[DIM], z1[DIM];
 #pragma unroll
-            for (int s = 0; s < DIM; ++s) { v0 += cf[s] * accT[s][0][ni][0]; v1 += cf[s] * accT[s][0][ni][1]; }
+          for (int r = 0; r < DIM; ++r) { z0[r] = accZ[r][0][ni][0] - accU[0][ni][0]; z1[r] = accZ[r][0][ni][1] - accU[0][ni][1]; }
+          const int i = ni * 8 + 2 * (lane & 3);
 #pragma unroll
-            for (int s = 0; s < NF; ++s) { v0 += cf[DIM + s] * accU[s][0][ni][0]; v1 += cf[DIM + s] * accU[s][0][ni][1]; }
-            const int i = ni * 8 + 2 * (lane & 3);
+          for (int x = 0; x < DIM; ++x) {
+            double v0 = m[0][x] * z0[0], v1 = m[0][x] * z1[0];
+#pragma unroll
+            for (int r = 1; r < DIM; ++r) { v0 += m[r][x] * z0[r]; v1 += m[r][x] * z1[r]; }
             if (NP % 2 == 0) {
               if (i < NP) *reinterpret_cast<double2*>(sg + (x * 8 + k8) * NP + i) = make_double2(v0, v1);
             } else {
@@ -323,6 +396,7 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
       }
     }
     __syncwarp();
+#endif
 
     // ---- pointwise: total flux at every node, contravariant + Jacobian-scaled, and the wave speed ----
 #pragma unroll

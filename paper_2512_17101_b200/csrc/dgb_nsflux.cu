@@ -8,7 +8,7 @@
 
 namespace {
 
-// Measured on B200 (profiles/r01_flux_variants.md): pass 1 is fastest with 12 warps (168 registers, two
+// Measured on B200 (profiles/r01_flux_variants.md): pass 1 is fastest with 12 warps (164 registers, four
 // face nodes per lane in flight), pass 2 with 8 warps (235 registers, no spills, NB = 2).
 #ifndef DGB_FLUX_WARPS
 #define DGB_FLUX_WARPS 12

@@ -14,12 +14,9 @@ sys.path.insert(0, ROOT)
 PKG = os.path.join(ROOT, "paper_2512_17101_b200")
 
 VARIANTS = {
-    "p8_nb2lazy": [],
-    "p8_nb1": ["DGB_DIV4_NB=1"],
-    "p8_nb2": ["DGB_DIV4_NB=2", "DGB_DIV4_LAZY_EX=0"],
-    "p6_nb2": ["DGB_DIV_PAIRS=6", "DGB_DIV4_NB=2", "DGB_DIV4_LAZY_EX=0"],
-    "p6_nb4lazy": ["DGB_DIV_PAIRS=6", "DGB_DIV4_NB=4", "DGB_DIV4_LAZY_EX=1"],
-    "p4_nb2": ["DGB_DIV_PAIRS=4", "DGB_DIV4_NB=2", "DGB_DIV4_LAZY_EX=0"],
+    "z_w12_nb2": [],
+    "z_w12_nb4": ["DGB_FLUX_NB=4"],
+    "z_w12_nb1": ["DGB_FLUX_NB=1"],
 }
 
 
