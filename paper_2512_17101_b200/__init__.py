@@ -6,6 +6,7 @@ Public surface:
 * ``DOFArray``, ``DGDiscretization``      -- element-major nodal data + per-mesh operators
 * ``EulerOperator``, ``NavierStokesOperator``, ``rk4_step`` -- the operator program (operators.py)
 * ``dg.mesh.box_mesh``                    -- conforming simplicial box meshes
+* ``DeviceRK4``                           -- device-resident RK4 driver, one CUDA graph per step (timestepper.py)
 """
 from .dofarray import DOFArray
 from .discretization import BC_FARFIELD, BC_NONE, BC_WALL, DGDiscretization
@@ -20,4 +21,7 @@ def __getattr__(name):
     if name in ("B200ArrayContext", "DeviceArray", "CompiledFunction"):
         from . import actx
         return getattr(actx, name)
+    if name == "DeviceRK4":
+        from .timestepper import DeviceRK4
+        return DeviceRK4
     raise AttributeError(name)

@@ -281,3 +281,29 @@ def test_full_size_properties(gpu):
     o1, o2 = op.rhs_rk(q, q, r, (1.0, 0.25, 0.5, -2.0))
     assert rel_err(d.to_numpy(o1), smooth_state(d.nodes()) + 0.25 * rh) <= 1e-13
     assert rel_err(d.to_numpy(o2), 0.5 * rh - 2.0 * rh) <= 1e-13
+
+
+@pytest.mark.parametrize("Op,kw,dim,order,n", [(NavierStokesOperator, {"mu": 1e-2}, 3, 3, 3), (EulerOperator, {}, 3, 3, 3),
+                                                (NavierStokesOperator, {"mu": 1e-2}, 2, 4, 3)])
+def test_device_rk4_driver(gpu, Op, kw, dim, order, n):
+    """DeviceRK4 (all stage storage owned, C ABI called directly, whole step captured in one CUDA
+    graph) == classical RK4 of the same operator program on the oracle, and graph replay == eager launches."""
+    from paper_2512_17101_b200 import DeviceRK4
+    cpu = NumpyArrayContext()
+    dc, dg = make_dcoll(cpu, dim, order, n, "periodic"), make_dcoll(gpu, dim, order, n, "periodic")
+    q0 = smooth_state(dc.nodes())
+    oc, og = Op(dc, **kw), Op(dg, **kw)
+    dt, nsteps = 2e-3, 25
+    qc, t = dc.from_numpy(q0), 0.0
+    for _ in range(nsteps):
+        qc = rk4_step(oc.rhs, qc, t, dt)
+        t += dt
+    ref = dc.to_numpy(qc)
+    launches0 = gpu.launch_count
+    graph = DeviceRK4(og, dg.from_numpy(q0), dt, use_graph=True).step(nsteps)
+    eager = DeviceRK4(og, dg.from_numpy(q0), dt, use_graph=False).step(nsteps)
+    got_g, got_e = dg.to_numpy(graph.state), dg.to_numpy(eager.state)
+    assert graph.graph is not None and abs(graph.time - nsteps * dt) < 1e-15
+    assert np.array_equal(got_g, got_e)
+    assert rel_err(got_g, ref) <= TOL_RK, rel_err(got_g, ref)
+    assert gpu.launch_count > launches0
