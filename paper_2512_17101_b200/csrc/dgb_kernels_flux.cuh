@@ -39,6 +39,15 @@
 #define DGB_DIV4_LAZY_EX 1
 #endif
 
+#ifdef DGB_PHASE_TIMING
+// warp 0 of every CTA accumulates the cycles it spends in each phase (scripts/phase_timing_flux.py)
+#define DGB_WTICK(k) do { if (warp == 0 && lane == 0) { long long t_ = clock64(); d.timing[blockIdx.x * 8 + (k)] += t_ - wtlast; wtlast = t_; } } while (0)
+#define DGB_WTICK_INIT long long wtlast = clock64();
+#else
+#define DGB_WTICK(k) do { } while (0)
+#define DGB_WTICK_INIT
+#endif
+
 namespace dgb {
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -61,14 +70,27 @@ __device__ __forceinline__ long long ticket_block(unsigned long long v, long lon
   return first_dynamic + (long long)__shfl_sync(0xffffffffu, v, 0);
 }
 
-// Face node n = lane + 32*k of a warp's block, decoded once per lane: bits 0-1 element, 2-3 face,
-// 4-7 node within the face, 8-15 own volume node, 16-23 f*NFP + m; negative = no such face node.
+// Face nodes of a warp's block are visited in rounds of WHOLE faces: round k, lane l handles node
+// l % NFP of face k*FPR + l / NFP (FPR = 32 / NFP faces per round; the last 32 - FPR*NFP lanes idle).
+// A face's nodes lie in one 8*Np-byte row of the neighbour, so one gather instruction then touches
+// each of its sectors once; with plain n = lane + 32*k a quarter of the faces straddled two rounds
+// and their sectors were requested twice.  Code: bits 0-1 element, 2-3 face, 4-7 node within the
+// face, 8-15 own volume node, 16-23 f*NFP + m; negative = idle lane.
+template <int DIM, int P, int KW>
+__host__ __device__ constexpr int face_rounds() {
+  using EL = ElemT<DIM, P>;
+  return (KW * EL::NF + (32 / EL::NFP) - 1) / (32 / EL::NFP);
+}
+
 template <int DIM, int P, int KW>
 __device__ __forceinline__ int face_lane_code(const int* fn, int n) {
   using EL = ElemT<DIM, P>;
-  if (n >= KW * EL::NFT) return -1;
-  const int e = n / EL::NFT, fm = n - e * EL::NFT;
-  const int f = fm / EL::NFP, m = fm - f * EL::NFP;
+  constexpr int FPR = 32 / EL::NFP;
+  const int k = n >> 5, l = n & 31;
+  const int g = k * FPR + l / EL::NFP, m = l % EL::NFP;
+  if (l >= FPR * EL::NFP || g >= KW * EL::NF) return -1;
+  const int e = g / EL::NF, f = g - e * EL::NF;
+  const int fm = f * EL::NFP + m;
   return e | (f << 2) | (m << 4) | (fn[fm] << 8) | (fm << 16);
 }
 
@@ -113,7 +135,7 @@ struct Flux3Smem {
   Flux3Warp<DIM, P, KW> w[NWARPS];
   int fn[EL::NF * EL::NFP];
   int perm[EL::NPERM * EL::NFP];
-  int flc[((KW * EL::NFT + 31) / 32) * 32];      // face_lane_code of every face node of a block
+  int flc[face_rounds<DIM, P, KW>() * 32];      // face_lane_code of every face node of a block
 };
 
 template <int DIM, int P, int KW>
@@ -168,7 +190,7 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
   constexpr int C = EL::C, NP = EL::NP, NF = EL::NF, NFP = EL::NFP, NFT = EL::NFT, NI = EL::NI;
   constexpr int LDSX = FluxT<DIM, P>::LDSX;
   constexpr int NT = NWARPS * 32;
-  constexpr int NR = (KW * NFT + 31) / 32;        // face-node rounds per block
+  constexpr int NR = face_rounds<DIM, P, KW>();        // face-node rounds per block
   constexpr int NBF = DGB_FLUX_NB;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   auto& S = *reinterpret_cast<Flux3Smem<DIM, P, KW, NWARPS>*>(smem_raw);
@@ -196,6 +218,7 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
   }
   cp_async_commit();
   unsigned long long ticket = draw_ticket(counter, lane);
+  DGB_WTICK_INIT
 
   while (wb < nwblocks) {
     const long long e0 = ebeg + wb * KW;
@@ -213,6 +236,7 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
     }
     cp_async_commit();
     ticket = draw_ticket(counter, lane);
+    DGB_WTICK(0);
 
     // ---- face averages q* (central flux, boundary states) -> Ss; metric coefficients ---------
 #if DGB_FLUX_PRODUCT_MAJOR
@@ -277,6 +301,7 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
       }
     }
     __syncwarp();
+    DGB_WTICK(1);
 
 #if DGB_FLUX_PRODUCT_MAJOR
     // ---- tensor-core contractions, product by product over BOTH column tiles: every W fragment is
@@ -397,6 +422,7 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
     }
     __syncwarp();
 #endif
+    DGB_WTICK(2);
 
     // ---- pointwise: total flux at every node, contravariant + Jacobian-scaled, and the wave speed ----
 #pragma unroll
@@ -441,6 +467,7 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
       }
     }
     __syncwarp();
+    DGB_WTICK(3);
     wb = wb_next;
     buf ^= 1;
   }
@@ -482,7 +509,7 @@ struct Div3Smem {
   Div3Warp<DIM, P, KW> w[NWARPS];
   int fn[EL::NF * EL::NFP];
   int perm[EL::NPERM * EL::NFP];
-  int flc[((KW * EL::NFT + 31) / 32) * 32];      // face_lane_code of every face node of a block
+  int flc[face_rounds<DIM, P, KW>() * 32];      // face_lane_code of every face node of a block
 };
 
 // chunk t of every plane of a block: CH doubles at element e, node j
@@ -598,7 +625,7 @@ __device__ __forceinline__ void div_face_phase(const int* flc, const int* fn, co
                                                const Phys& ph, long long e0, int nel, int lane) {
   using EL = ElemT<DIM, P>;
   constexpr int C = EL::C, NP = EL::NP, NF = EL::NF, NFP = EL::NFP, NFT = EL::NFT;
-  constexpr int NR = (KW * NFT + 31) / 32;
+  constexpr int NR = face_rounds<DIM, P, KW>();
   constexpr int NEX = LAZY ? C : (DIM - 1) * C;
   const long long E = d.E, G = d.G;
 #pragma unroll 1
@@ -714,7 +741,7 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
   using WS = Div3Warp<DIM, P, KW>;
   constexpr int C = EL::C, NP = EL::NP, NF = EL::NF, NFP = EL::NFP, NFT = EL::NFT;
   constexpr int NT = NWARPS * 32;
-  constexpr int NR = (KW * NFT + 31) / 32;        // face-node rounds per block
+  constexpr int NR = face_rounds<DIM, P, KW>();        // face-node rounds per block
   constexpr int NB = DGB_DIV_NB;                  // face nodes per lane whose gathers are in flight together
   extern __shared__ __align__(16) unsigned char smem_raw[];
   auto& S = *reinterpret_cast<Div3Smem<DIM, P, KW, NWARPS>*>(smem_raw);
@@ -751,6 +778,7 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
   unsigned long long ticket = draw_ticket(counter, lane);
 
   // cp.async groups retire in order: S(b), T(b), S(b+1), T(b+1), ...
+  DGB_WTICK_INIT
   while (wb < nwblocks) {
     const long long e0 = ebeg + wb * KW;
     const int nel = (int)((eend - e0) < (long long)KW ? (eend - e0) : (long long)KW);
@@ -763,14 +791,17 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
     cp_async_wait<2>();                  // S(b) has landed; T(b) and S(b+1) may still be in flight
     __syncwarp();
     const Div3Small<DIM, P, KW>& M = W.sm[buf];
+    DGB_WTICK(0);
 
     // ---- face gather + Rusanov.  The own-side flux is linear in the block's own T rows with
     //      constant coefficients and lives in the folded volume matrix, so this phase needs only
     //      q, lam and the connectivity of the block -- not its T rows, which are still landing.
     //      Fs = (nbr - sJ max(lam-, lam+) (q- - q+)) / 2,  nbr = sJ F+.n+ gathered from the neighbour.
     div_face_phase<DIM, P, KW, NB, (DGB_DIV_LAZY_EX != 0)>(S.flc, S.fn, S.perm, M, W.Fs, d, q, T, ghost, Tghost, ph, e0, nel, lane);
+    DGB_WTICK(1);
     cp_async_wait<1>();                  // T(b) has landed
     __syncwarp();
+    DGB_WTICK(2);
 
     // ---- tensor-core contraction -------------------------------------------------------------
     double acc[WS::NTILE][EL::NI][2];
@@ -784,6 +815,7 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
 #pragma unroll
     for (int mt = 0; mt < WS::NTILE; ++mt) rj[mt] = M.rj[(mt * 8 + (lane >> 2)) % KW];
     __syncwarp();                        // all operand rows consumed: the next block may land on them
+    DGB_WTICK(3);
     if (nel1 > 0) div_stage_rows<DIM, P, KW>(W.Ts, d, T, e1, nel1, lane);
     cp_async_commit();                   // T(b+1)
 
@@ -801,6 +833,7 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
         }
       }
     }
+    DGB_WTICK(4);
     wb = wb_next;
     buf ^= 1;
   }
@@ -857,7 +890,7 @@ struct Div4Smem {
   Div4Pair<DIM, P, KW> w[NPAIR];
   int fn[EL::NF * EL::NFP];
   int perm[EL::NPERM * EL::NFP];
-  int flc[((KW * EL::NFT + 31) / 32) * 32];
+  int flc[face_rounds<DIM, P, KW>() * 32];
 };
 
 template <int DIM, int P, int KW, int NPAIR>
@@ -870,7 +903,7 @@ k_nsdiv4(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
   using WS = Div4Pair<DIM, P, KW>;
   constexpr int C = EL::C, NP = EL::NP, NF = EL::NF, NFP = EL::NFP, NFT = EL::NFT;
   constexpr int NT = NPAIR * 64;
-  constexpr int NR = (KW * NFT + 31) / 32;
+  constexpr int NR = face_rounds<DIM, P, KW>();
   constexpr int NB = DGB_DIV_NB;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   auto& S = *reinterpret_cast<Div4Smem<DIM, P, KW, NPAIR>*>(smem_raw);
@@ -982,6 +1015,244 @@ k_nsdiv4(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
     }
     cp_async_wait<0>();
   }
+}
+
+// ------------------------------------------------------------------------------------------
+// pass 2, cross-block software pipeline (k_nsdiv5).
+//
+// Same data flow as k_nsdiv3, but the neighbour gathers of block i+1 are ISSUED (into registers)
+// just before the DMMA contraction of block i and CONSUMED after its store, so their L2/HBM latency
+// hides behind ~3 us of tensor-core work instead of stalling the warp twice per block.  The small
+// per-block inputs (q, lam, connectivity) are therefore needed one block earlier: triple-buffered,
+// staged two blocks ahead.  Register budget: NR*(2C+1) gather values live across the MMA phase
+// (44 doubles for tets p3) next to the 24 accumulator registers -- 8 warps x 255 registers.
+// ------------------------------------------------------------------------------------------
+template <int DIM, int P, int KW>
+struct FaceRegs {
+  using EL = ElemT<DIM, P>;
+  static constexpr int NR = face_rounds<DIM, P, KW>();
+  double qp[NR][EL::C], nbr[NR][EL::C], lam_p[NR];
+  long long cnk[NR];
+};
+
+template <int DIM, int P, int KW>
+__device__ __forceinline__ void face_issue(FaceRegs<DIM, P, KW>& R, const int* flc, const int* fn, const int* perm,
+                                           const Div3Small<DIM, P, KW>& M, const DiscDev& d,
+                                           const double* __restrict__ q, const double* __restrict__ T,
+                                           const double* __restrict__ ghost, const double* __restrict__ Tghost,
+                                           int nel, int lane) {
+  using EL = ElemT<DIM, P>;
+  constexpr int C = EL::C, NP = EL::NP, NFP = EL::NFP;
+  constexpr int NR = FaceRegs<DIM, P, KW>::NR;
+  const long long E = d.E, G = d.G;
+#pragma unroll
+  for (int k = 0; k < NR; ++k) {
+    R.cnk[k] = -1;
+    const int flk = flc[k * 32 + lane];
+    const int e = flk & 3, f = (flk >> 2) & 3, m = (flk >> 4) & 15;
+    if (flk >= 0 && e < nel) {
+      const long long cn = M.conn[e][f];
+      R.cnk[k] = cn;
+      const long long nb = DGB_CONN_NB(cn);
+      const int nf = DGB_CONN_NF(cn);
+      const int jp = fn[nf * NFP + perm[DGB_CONN_PERM(cn) * NFP + m]];
+      const bool in_ghost = nb >= E;
+      const long long pstride = (in_ghost ? G : E) * NP;
+      const long long off = (in_ghost ? nb - E : nb) * NP + jp;
+      const double* qbase = (in_ghost ? ghost : q) + off;
+      const double* tbase = (in_ghost ? Tghost : T) + off;
+      const int r0 = nf == 0 ? 0 : nf - 1;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        R.qp[k][c] = qbase[c * pstride];
+        R.nbr[k][c] = tbase[(r0 * C + c) * pstride];
+      }
+      R.lam_p[k] = tbase[(DIM * C) * pstride];
+    }
+  }
+}
+
+template <int DIM, int P, int KW>
+__device__ __forceinline__ void face_finish(FaceRegs<DIM, P, KW>& R, const int* flc, const int* fn, const int* perm,
+                                            const Div3Small<DIM, P, KW>& M, double* Fs, const DiscDev& d,
+                                            const double* __restrict__ T, const double* __restrict__ Tghost,
+                                            const Phys& ph, long long e0, int nel, int lane) {
+  using EL = ElemT<DIM, P>;
+  constexpr int C = EL::C, NP = EL::NP, NF = EL::NF, NFP = EL::NFP;
+  constexpr int NR = FaceRegs<DIM, P, KW>::NR;
+  const long long E = d.E, G = d.G;
+  // second wave: a neighbour's face 0 is the sum of its DIM rows; fetch the other DIM-1 now
+  double ex[NR][C];
+#pragma unroll
+  for (int k = 0; k < NR; ++k) {
+    if (R.cnk[k] >= 0 && DGB_CONN_NF(R.cnk[k]) == 0 && DGB_CONN_BC(R.cnk[k]) == 0) {
+      const int flk = flc[k * 32 + lane];
+      const long long nb = DGB_CONN_NB(R.cnk[k]);
+      const int m = (flk >> 4) & 15;
+      const int jp = fn[perm[DGB_CONN_PERM(R.cnk[k]) * NFP + m]];
+      const bool in_ghost = nb >= E;
+      const long long pstride = (in_ghost ? G : E) * NP;
+      const double* tbase = (in_ghost ? Tghost : T) + (in_ghost ? nb - E : nb) * NP + jp;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        double t = tbase[(C + c) * pstride];
+#pragma unroll
+        for (int r = 2; r < DIM; ++r) t += tbase[(r * C + c) * pstride];
+        ex[k][c] = t;
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NR; ++k) {
+    if (R.cnk[k] >= 0) {
+      const int flk = flc[k * 32 + lane];
+      const int e = flk & 3, f = (flk >> 2) & 3, jm = (flk >> 8) & 255, fm = (flk >> 16) & 255;
+      const int nf = DGB_CONN_NF(R.cnk[k]), bc = DGB_CONN_BC(R.cnk[k]);
+      const double sj = M.sj[e][f];
+      const double lam_m = M.Lam[e * NP + jm];
+      double qm[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) qm[c] = M.Qs[(c * KW + e) * NP + jm];
+      double* fs = Fs + e * EL::LDF + fm;
+      if (bc == 0) {
+        const double pen = sj * fmax(lam_m, R.lam_p[k]);
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          const double nb_ = nf == 0 ? R.nbr[k][c] + ex[k][c] : -R.nbr[k][c];
+          fs[c * (KW * EL::LDF)] = 0.5 * (nb_ - pen * (qm[c] - R.qp[k][c]));
+        }
+      } else {
+        VecC<DIM> a_;
+#pragma unroll
+        for (int c = 0; c < C; ++c) a_.v[c] = qm[c];
+        const VecC<DIM> fb = boundary_operand<DIM>(bc, f, a_, T + (e0 + e) * NP + jm, E * NP, lam_m, sj,
+                                                   d.normals + (e0 + e) * NF + f, E * NF, ph);
+#pragma unroll
+        for (int c = 0; c < C; ++c) fs[c * (KW * EL::LDF)] = fb.v[c];
+      }
+    }
+  }
+}
+
+template <int DIM, int P, int KW>
+struct alignas(16) Div5Warp {
+  using EL = ElemT<DIM, P>;
+  static constexpr int NCOL = EL::C * KW;
+  static constexpr int NTILE = (NCOL + 7) / 8;
+  double Ts[NCOL * EL::LDV];
+  double Fs[NCOL * EL::LDF];
+  Div3Small<DIM, P, KW> sm[3];
+};
+
+template <int DIM, int P, int KW, int NWARPS>
+struct Div5Smem {
+  using EL = ElemT<DIM, P>;
+  double Wv[EL::NPR * EL::LDV];
+  double Wl[EL::NPR * EL::LDF];
+  Div5Warp<DIM, P, KW> w[NWARPS];
+  int fn[EL::NF * EL::NFP];
+  int perm[EL::NPERM * EL::NFP];
+  int flc[face_rounds<DIM, P, KW>() * 32];
+};
+
+template <int DIM, int P, int KW, int NWARPS>
+__global__ void __launch_bounds__(NWARPS * 32, 1)
+k_nsdiv5(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
+         const double* __restrict__ ghost, const double* __restrict__ Tghost,
+         Epilogue ep, Phys ph, long long ebeg, long long eend, long long nwblocks,
+         unsigned long long* __restrict__ counter) {
+  using EL = ElemT<DIM, P>;
+  using WS = Div5Warp<DIM, P, KW>;
+  constexpr int C = EL::C, NP = EL::NP, NF = EL::NF, NFP = EL::NFP, NFT = EL::NFT;
+  constexpr int NT = NWARPS * 32;
+  constexpr int NR = face_rounds<DIM, P, KW>();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  auto& S = *reinterpret_cast<Div5Smem<DIM, P, KW, NWARPS>*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long E = d.E;
+
+  for (int n = tid; n < EL::NPR * EL::LDV; n += NT) S.Wv[n] = d.Wv2[n];
+  for (int n = tid; n < EL::NPR * EL::LDF; n += NT) S.Wl[n] = d.Wl[n];
+  for (int n = tid; n < NF * NFP; n += NT) S.fn[n] = d.tables[n];
+  for (int n = tid; n < EL::NPERM * NFP; n += NT) S.perm[n] = d.tables[NF * NFP + n];
+  WS& W = S.w[warp];
+  {
+    double* z = reinterpret_cast<double*>(&W);
+    for (int n = lane; n < (int)(sizeof(WS) / 8); n += 32) z[n] = 0.0;
+  }
+  __syncthreads();
+  for (int n = tid; n < NR * 32; n += NT) S.flc[n] = face_lane_code<DIM, P, KW>(S.fn, n);
+  __syncthreads();
+
+  auto nel_of = [&](long long wbx) -> int {
+    if (wbx >= nwblocks) return 0;
+    const long long e = ebeg + wbx * KW;
+    return (int)((eend - e) < (long long)KW ? (eend - e) : (long long)KW);
+  };
+  const long long wstride = (long long)gridDim.x * NWARPS;
+  long long wb = (long long)blockIdx.x * NWARPS + warp;           // block i
+  if (wb >= nwblocks) return;
+  // prologue: S(0), T(0), S(1); gathers of block 0 in flight
+  div_stage_small<DIM, P, KW>(W.sm[0], d, q, T, ebeg + wb * KW, nel_of(wb), lane);
+  cp_async_commit();
+  div_stage_rows<DIM, P, KW>(W.Ts, d, T, ebeg + wb * KW, nel_of(wb), lane);
+  cp_async_commit();
+  unsigned long long ticket = draw_ticket(counter, lane);
+  long long wb1 = ticket_block(ticket, wstride);                  // block i+1
+  ticket = draw_ticket(counter, lane);
+  if (nel_of(wb1) > 0) div_stage_small<DIM, P, KW>(W.sm[1], d, q, T, ebeg + wb1 * KW, nel_of(wb1), lane);
+  cp_async_commit();
+  cp_async_wait<2>();                                             // S(0)
+  __syncwarp();
+  FaceRegs<DIM, P, KW> R;
+  face_issue<DIM, P, KW>(R, S.flc, S.fn, S.perm, W.sm[0], d, q, T, ghost, Tghost, nel_of(wb), lane);
+
+  for (int i = 0;; ++i) {
+    const int b0 = i % 3, b1 = (i + 1) % 3, b2 = (i + 2) % 3;
+    const long long e0 = ebeg + wb * KW;
+    const int nel = nel_of(wb);
+    const long long wb2 = ticket_block(ticket, wstride);          // block i+2: its small inputs start now
+    ticket = draw_ticket(counter, lane);
+    if (nel_of(wb2) > 0) div_stage_small<DIM, P, KW>(W.sm[b2], d, q, T, ebeg + wb2 * KW, nel_of(wb2), lane);
+    cp_async_commit();                                            // S(i+2)
+    // face phase of block i from the gathers issued one block ago
+    face_finish<DIM, P, KW>(R, S.flc, S.fn, S.perm, W.sm[b0], W.Fs, d, T, Tghost, ph, e0, nel, lane);
+    cp_async_wait<1>();                                           // S(i+1) and T(i) have landed
+    __syncwarp();
+    // gathers of block i+1 fly during the contraction of block i
+    face_issue<DIM, P, KW>(R, S.flc, S.fn, S.perm, W.sm[b1], d, q, T, ghost, Tghost, nel_of(wb1), lane);
+
+    double acc[WS::NTILE][EL::NI][2];
+#pragma unroll
+    for (int mt = 0; mt < WS::NTILE; ++mt)
+#pragma unroll
+      for (int ni = 0; ni < EL::NI; ++ni) { acc[mt][ni][0] = 0.0; acc[mt][ni][1] = 0.0; }
+    mma_block<EL::NI, WS::NTILE>(acc, W.Ts, EL::LDV, S.Wv, EL::LDV, EL::KV / 4, lane);
+    mma_block<EL::NI, WS::NTILE>(acc, W.Fs, EL::LDF, S.Wl, EL::LDF, EL::KF / 4, lane);
+    double rj[WS::NTILE];
+#pragma unroll
+    for (int mt = 0; mt < WS::NTILE; ++mt) rj[mt] = W.sm[b0].rj[(mt * 8 + (lane >> 2)) % KW];
+    __syncwarp();                                                 // operand rows consumed
+    if (nel_of(wb1) > 0) div_stage_rows<DIM, P, KW>(W.Ts, d, T, ebeg + wb1 * KW, nel_of(wb1), lane);
+    cp_async_commit();                                            // T(i+1)
+#pragma unroll
+    for (int mt = 0; mt < WS::NTILE; ++mt) {
+      const int col = mt * 8 + (lane >> 2);
+      const int c = col / KW, e = col - c * KW;
+      if (col < WS::NCOL && e < nel) {
+        const long long rowbase = ((long long)c * E + e0 + e) * NP;
+#pragma unroll
+        for (int ni = 0; ni < EL::NI; ++ni) {
+          const int i2 = ni * 8 + 2 * (lane & 3);
+          store_pair<NP>(ep, rowbase + i2, i2, rj[mt] * acc[mt][ni][0], rj[mt] * acc[mt][ni][1]);
+        }
+      }
+    }
+    if (wb1 >= nwblocks) break;
+    wb = wb1;
+    wb1 = wb2;
+  }
+  cp_async_wait<0>();
 }
 
 }  // namespace dgb

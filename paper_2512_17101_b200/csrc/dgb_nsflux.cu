@@ -106,6 +106,34 @@ int launch_div4(const dgb_disc* d, const double* q, const double* T, const doubl
   return DGB_OK;
 }
 
+#ifndef DGB_DIV5_WARPS
+#define DGB_DIV5_WARPS 8
+#endif
+template <int DIM, int P> struct Cfg5 {
+  static constexpr int KW = DIM == 3 ? 3 : 4;
+  static constexpr size_t per = sizeof(dgb::Div5Warp<DIM, P, KW>);
+  static constexpr size_t fixed = sizeof(dgb::Div5Smem<DIM, P, KW, 1>) - per;
+  static constexpr int NW = fit_warps(fixed, per, DGB_DIV5_WARPS);
+};
+
+template <int DIM, int P>
+int launch_div5(const dgb_disc* d, const double* q, const double* T, const double* ghost, const double* Tghost,
+                const dgb::Epilogue& ep, const dgb::Phys& ph, long long ebeg, long long eend, cudaStream_t st) {
+  using C = Cfg5<DIM, P>;
+  auto kern = dgb::k_nsdiv5<DIM, P, C::KW, C::NW>;
+  const size_t smem = sizeof(dgb::Div5Smem<DIM, P, C::KW, C::NW>);
+  const long long nwb = (eend - ebeg + C::KW - 1) / C::KW;
+  if (nwb == 0) return DGB_OK;
+  static bool configured = false;
+  if (!configured) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured = true; }
+  const long long need = (nwb + C::NW - 1) / C::NW;
+  const int grid = (int)(need < dgb_num_sms() ? need : dgb_num_sms());
+  DGB_CUDA(cudaMemsetAsync(d->counters + 1, 0, sizeof(unsigned long long), st));
+  kern<<<grid, C::NW * 32, smem, st>>>(d->dev, q, T, ghost, Tghost, ep, ph, ebeg, eend, nwb, d->counters + 1);
+  DGB_CUDA(cudaGetLastError());
+  return DGB_OK;
+}
+
 #define DGB_FOR_EACH_ELEMENT(X) X(2, 1) X(2, 2) X(2, 3) X(2, 4) X(3, 1) X(3, 2) X(3, 3) X(3, 4)
 
 void make_phys(dgb::Phys& ph, int C, const double* qfar, const double* phys) {
@@ -187,7 +215,8 @@ static int ns_div_impl(const dgb_disc* d, const double* q, const double* T, cons
   dgb::Phys ph; make_phys(ph, d->dim + 2, qfar, phys);
 #define X(DIM, P) if (d->dim == DIM && d->order == P)                                                         \
     return div_kernel() == 3 ? launch_div<DIM, P>(d, q, T, ghost, Tghost, ep, ph, ebegin, eend, (cudaStream_t)stream)  \
-                             : launch_div4<DIM, P>(d, q, T, ghost, Tghost, ep, ph, ebegin, eend, (cudaStream_t)stream);
+         : div_kernel() == 4 ? launch_div4<DIM, P>(d, q, T, ghost, Tghost, ep, ph, ebegin, eend, (cudaStream_t)stream) \
+                             : launch_div5<DIM, P>(d, q, T, ghost, Tghost, ep, ph, ebegin, eend, (cudaStream_t)stream);
   DGB_FOR_EACH_ELEMENT(X)
 #undef X
   return dgb_fail(DGB_ERR_INVALID, "unsupported (dim, order)");

@@ -14,9 +14,7 @@ sys.path.insert(0, ROOT)
 PKG = os.path.join(ROOT, "paper_2512_17101_b200")
 
 VARIANTS = {
-    "z_w12_nb2": [],
-    "z_w12_nb4": ["DGB_FLUX_NB=4"],
-    "z_w12_nb1": ["DGB_FLUX_NB=1"],
+    "timing": ["DGB_PHASE_TIMING=1"],
 }
 
 
