@@ -14,7 +14,10 @@ sys.path.insert(0, ROOT)
 PKG = os.path.join(ROOT, "paper_2512_17101_b200")
 
 VARIANTS = {
-    "timing": ["DGB_PHASE_TIMING=1"],
+    "timing": ["DGB_PHASE_TIMING=1"],                 # scripts/phase_timing_flux.py
+    "experimental": ["DGB_EXPERIMENTAL=1"],           # + DGB_DIV_KERNEL=4|5|6 at run time
+    "flux_nb2": ["DGB_FLUX_NB=2"],
+    "div_w12_nb1": ["DGB_DIV_WARPS=12", "DGB_DIV_NB=1"],
 }
 
 
@@ -24,6 +27,7 @@ def lib(name):
 
 def main():
     names = [a for a in sys.argv[1:] if a in VARIANTS] or list(VARIANTS)
+    kernels = {"experimental": ["4", "5", "6"]}
     if "--build" in sys.argv:
         # only dgb_nsflux.cu depends on the knobs: compile the other translation units once
         from paper_2512_17101_b200.csrc.build import FLAGS, HERE
@@ -43,8 +47,11 @@ def main():
             print("built", lib(name), flush=True)
     if "--run" in sys.argv:
         n = sys.argv[sys.argv.index("--n") + 1] if "--n" in sys.argv else "64"
-        for name in names:
+        for name, kern in [(nm, k) for nm in names for k in kernels.get(nm, [None])]:
             env = dict(os.environ, DGB_LIB=lib(name))
+            if kern:
+                env["DGB_DIV_KERNEL"] = kern
+                name = f"{name}:k_nsdiv{kern}"
             res = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--no-e2e", "--no-cpu", "--n", n,
                                   "--steps", "10"], env=env, capture_output=True, text=True)
             try:
