@@ -48,7 +48,20 @@
 #define DGB_WTICK_INIT
 #endif
 
+#ifndef DGB_T_RECORD
+#define DGB_T_RECORD 0
+#endif
+
 namespace dgb {
+
+// Addressing of the flux planes T (pass 1 writes, pass 2 streams and gathers):
+//   plane-major   T[pl][e][j]  (DGB_T_RECORD 0): the (dim*C+1, E, Np) array of the operator program as is;
+//   record-major  T[e][pl][j]  (DGB_T_RECORD 1): all planes of an element in one (dim*C+1)*Np*8-byte
+//                 record, so a face gather (q excepted) and a block's rows touch one DRAM page.
+template <int NPL, int NP>
+__host__ __device__ __forceinline__ long long t_elem_stride() { return DGB_T_RECORD ? (long long)NPL * NP : (long long)NP; }
+template <int NPL, int NP>
+__host__ __device__ __forceinline__ long long t_plane_stride(long long nelem) { return DGB_T_RECORD ? (long long)NP : nelem * NP; }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -449,7 +462,9 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
 #pragma unroll
           for (int c = 1; c < C; ++c) F[x][c] -= Fv[x][c];
         const double J = geo.jac[e];
-        double* out = T + e0 * NP + n;
+        constexpr int NPLT = DIM * C + 1;
+        const long long t_ps = t_plane_stride<NPLT, NP>(E);
+        double* out = T + (e0 + e) * t_elem_stride<NPLT, NP>() + j;
 #pragma unroll
         for (int r = 0; r < DIM; ++r) {
           double m[DIM];
@@ -460,10 +475,10 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
             double acc = m[0] * F[0][c];
 #pragma unroll
             for (int x = 1; x < DIM; ++x) acc += m[x] * F[x][c];
-            out[(long long)(r * C + c) * E * NP] = acc;
+            out[(r * C + c) * t_ps] = acc;
           }
         }
-        out[(long long)(DIM * C) * E * NP] = wavespeed<DIM>(s, ph.gamma);
+        out[(DIM * C) * t_ps] = wavespeed<DIM>(s, ph.gamma);
       }
     }
     __syncwarp();
@@ -533,8 +548,9 @@ __device__ __forceinline__ void div_stage_small(Div3Small<DIM, P, KW>& M, const 
         if (CH == 2) cp_async16(qs + c * (KW * NP), qg + c * pstride);
         else cp_async8(qs + c * (KW * NP), qg + c * pstride);
       }
-      if (CH == 2) cp_async16(M.Lam + e * NP + j, T + g0 + (DIM * C) * pstride);
-      else cp_async8(M.Lam + e * NP + j, T + g0 + (DIM * C) * pstride);
+      const double* lg = T + (e0 + e) * t_elem_stride<DIM * C + 1, NP>() + j + (DIM * C) * t_plane_stride<DIM * C + 1, NP>(d.E);
+      if (CH == 2) cp_async16(M.Lam + e * NP + j, lg);
+      else cp_async8(M.Lam + e * NP + j, lg);
     }
   }
   if (lane < nel * NF) {
@@ -549,7 +565,7 @@ __device__ __forceinline__ void div_stage_rows(double* Ts, const DiscDev& d, con
                                                int lane) {
   using EL = ElemT<DIM, P>;
   constexpr int C = EL::C, NP = EL::NP;
-  const long long pstride = d.E * NP;
+  const long long pstride = t_plane_stride<DIM * C + 1, NP>(d.E);
   constexpr int CH = (NP % 2 == 0) ? 2 : 1, NPC = NP / CH;
 #pragma unroll
   for (int t0 = 0; t0 < KW * NPC; t0 += 32) {
@@ -557,7 +573,7 @@ __device__ __forceinline__ void div_stage_rows(double* Ts, const DiscDev& d, con
     const int e = t / NPC, j = CH * (t - e * NPC);
     if (t < KW * NPC && e < nel) {
       double* ts = Ts + e * EL::LDV + j;
-      const double* tg = T + (e0 + e) * NP + j;
+      const double* tg = T + (e0 + e) * t_elem_stride<DIM * C + 1, NP>() + j;
 #pragma unroll 1
       for (int r = 0; r < DIM; ++r) {
 #pragma unroll
@@ -627,6 +643,7 @@ __device__ __forceinline__ void div_face_phase(const int* flc, const int* fn, co
   constexpr int C = EL::C, NP = EL::NP, NF = EL::NF, NFP = EL::NFP, NFT = EL::NFT;
   constexpr int NR = face_rounds<DIM, P, KW>();
   constexpr int NEX = LAZY ? C : (DIM - 1) * C;
+  constexpr int NPLT = DIM * C + 1;
   const long long E = d.E, G = d.G;
 #pragma unroll 1
   for (int k0 = 0; k0 < NR; k0 += NB) {
@@ -646,20 +663,21 @@ __device__ __forceinline__ void div_face_phase(const int* flc, const int* fn, co
           const int nf = DGB_CONN_NF(cn);
           const int jp = fn[nf * NFP + perm[DGB_CONN_PERM(cn) * NFP + m]];
           const bool in_ghost = nb >= E;
+          const long long nbl = in_ghost ? nb - E : nb;
           const long long pstride = (in_ghost ? G : E) * NP;
-          const long long off = (in_ghost ? nb - E : nb) * NP + jp;
-          const double* qbase = (in_ghost ? ghost : q) + off;
-          const double* tbase = (in_ghost ? Tghost : T) + off;
+          const long long tps = t_plane_stride<NPLT, NP>(in_ghost ? G : E);
+          const double* qbase = (in_ghost ? ghost : q) + nbl * NP + jp;
+          const double* tbase = (in_ghost ? Tghost : T) + nbl * t_elem_stride<NPLT, NP>() + jp;
           const int r0 = nf == 0 ? 0 : nf - 1;
 #pragma unroll
           for (int c = 0; c < C; ++c) {
             qp[b][c] = qbase[c * pstride];
-            nbr[b][c] = tbase[(r0 * C + c) * pstride];
+            nbr[b][c] = tbase[(r0 * C + c) * tps];
           }
-          lam_p[b] = tbase[(DIM * C) * pstride];
+          lam_p[b] = tbase[(DIM * C) * tps];
           if (!LAZY && nf == 0) {
 #pragma unroll
-            for (int rc = 0; rc < (DIM - 1) * C; ++rc) ex[b][rc] = tbase[(C + rc) * pstride];
+            for (int rc = 0; rc < (DIM - 1) * C; ++rc) ex[b][rc] = tbase[(C + rc) * tps];
           }
         }
       }
@@ -674,13 +692,13 @@ __device__ __forceinline__ void div_face_phase(const int* flc, const int* fn, co
           const int m = (flk >> 4) & 15;
           const int jp = fn[perm[DGB_CONN_PERM(cnk[b]) * NFP + m]];
           const bool in_ghost = nb >= E;
-          const long long pstride = (in_ghost ? G : E) * NP;
-          const double* tbase = (in_ghost ? Tghost : T) + (in_ghost ? nb - E : nb) * NP + jp;
+          const long long tps = t_plane_stride<NPLT, NP>(in_ghost ? G : E);
+          const double* tbase = (in_ghost ? Tghost : T) + (in_ghost ? nb - E : nb) * t_elem_stride<NPLT, NP>() + jp;
 #pragma unroll
           for (int c = 0; c < C; ++c) {
-            double t = tbase[(C + c) * pstride];
+            double t = tbase[(C + c) * tps];
 #pragma unroll
-            for (int r = 2; r < DIM; ++r) t += tbase[(r * C + c) * pstride];
+            for (int r = 2; r < DIM; ++r) t += tbase[(r * C + c) * tps];
             ex[b][c] = t;
           }
         }
@@ -721,7 +739,8 @@ __device__ __forceinline__ void div_face_phase(const int* flc, const int* fn, co
           VecC<DIM> a_;
 #pragma unroll
           for (int c = 0; c < C; ++c) a_.v[c] = qm[c];
-          const VecC<DIM> fb = boundary_operand<DIM>(bc, f, a_, T + (e0 + e) * NP + jm, E * NP, lam_m, sj,
+          const VecC<DIM> fb = boundary_operand<DIM>(bc, f, a_, T + (e0 + e) * t_elem_stride<NPLT, NP>() + jm,
+                                                     t_plane_stride<NPLT, NP>(E), lam_m, sj,
                                                      d.normals + (e0 + e) * NF + f, E * NF, ph);
 #pragma unroll
           for (int c = 0; c < C; ++c) fs[c * (KW * EL::LDF)] = fb.v[c];

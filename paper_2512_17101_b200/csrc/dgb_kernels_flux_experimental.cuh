@@ -9,6 +9,9 @@
 //   k_nsdiv6  TMA bulk copies (cp.async.bulk, UBLKCP) for all staging   2.77 ms
 #pragma once
 #include "dgb_kernels_flux.cuh"
+#if DGB_T_RECORD
+#error "the experimental pass-2 kernels address the flux planes plane-major only"
+#endif
 
 namespace dgb {
 
