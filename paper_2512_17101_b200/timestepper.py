@@ -117,3 +117,27 @@ class DeviceRK4:
     @property
     def time(self) -> float:
         return self.nsteps * self.dt
+
+    # {{{ checkpoint / restart: .npz of the state + step counter + a mesh fingerprint
+    def _fingerprint(self) -> np.ndarray:
+        d = self.op.dcoll
+        vp = np.asarray(d.vmap_p_host).reshape(-1)
+        return np.array([d.dim, d.order, d.nelements, d.Np, int(vp.sum() % (1 << 61)), int(vp[::97].sum() % (1 << 61))],
+                        dtype=np.int64)
+
+    def save(self, path: str) -> None:
+        """Write ``q`` (host copy), the step counter and ``dt``; bit-exact restart with ``restore``."""
+        np.savez(path, q=self.actx.to_numpy(self.q), nsteps=np.int64(self.nsteps), dt=np.float64(self.dt),
+                 mesh=self._fingerprint(), equations="ns" if self.viscous else "euler")
+
+    @classmethod
+    def restore(cls, op, path: str, use_graph: bool = True) -> "DeviceRK4":
+        """Continue a run saved with ``save`` on the same discretisation (checked by fingerprint)."""
+        with np.load(path) as ck:
+            q, nsteps, dt, mesh, eq = ck["q"], int(ck["nsteps"]), float(ck["dt"]), ck["mesh"], str(ck["equations"])
+        stepper = cls(op, DOFArray(op.actx, op.actx.from_numpy(q)), dt, use_graph=use_graph)
+        if not np.array_equal(mesh, stepper._fingerprint()) or eq != ("ns" if stepper.viscous else "euler"):
+            raise errors.BindingMismatch("checkpoint was written for another mesh / order / equation set")
+        stepper.nsteps = nsteps
+        return stepper
+    # }}}

@@ -304,6 +304,17 @@ def test_device_rk4_driver(gpu, Op, kw, dim, order, n):
     eager = DeviceRK4(og, dg.from_numpy(q0), dt, use_graph=False).step(nsteps)
     got_g, got_e = dg.to_numpy(graph.state), dg.to_numpy(eager.state)
     assert graph.graph is not None and abs(graph.time - nsteps * dt) < 1e-15
+    # checkpoint at step 10, restart, continue: bit-identical to the uninterrupted run
+    import os
+    import tempfile
+    with tempfile.TemporaryDirectory() as tmp:
+        part = DeviceRK4(og, dg.from_numpy(q0), dt).step(10)
+        part.save(os.path.join(tmp, "ck.npz"))
+        cont = DeviceRK4.restore(og, os.path.join(tmp, "ck.npz")).step(nsteps - 10)
+        assert cont.nsteps == nsteps and np.array_equal(dg.to_numpy(cont.state), got_g)
+        other = Op(make_dcoll(gpu, dim, order, n + 1, "periodic"), **kw)
+        with pytest.raises(Exception):
+            DeviceRK4.restore(other, os.path.join(tmp, "ck.npz"))
     assert np.array_equal(got_g, got_e)
     assert rel_err(got_g, ref) <= TOL_RK, rel_err(got_g, ref)
     assert gpu.launch_count > launches0
