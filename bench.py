@@ -305,7 +305,7 @@ def run_b200(args):
         ms_grad = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
         ms_div = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
         if euler:
-            dom = ("k_rhs3<inviscid> (fused Euler RHS)", ms_div, 80.0)
+            dom = ("k_euler4 (fused Euler RHS)", ms_div, 80.0)
         else:
             names = ("k_rhs3<viscous> (flux + divergence pass)", "k_grad3 (BR1 gradient pass)") if grad_form else \
                     ("k_nsdiv3 (divergence + face pass)", "k_nsflux3 (BR1 gradient + flux pass)")

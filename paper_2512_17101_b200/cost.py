@@ -58,8 +58,8 @@ def cost_report(dim: int, order: int, nelements: int, equations: str = "ns", arr
 
     out = []
     if equations == "euler":
-        out.append(KernelCost("k_rhs3<inviscid>", f(C) + geo_grad, f(C), f(C), f(C),
-                              dmma(dim * npk + kf), N * 250))
+        out.append(KernelCost("k_euler4", f(C) + geo_grad, f(C), f(C), f(C),
+                              dmma(dim * npk + kf), N * 230))
     elif arrangement == "flux":
         npl = dim * C + 1
         out.append(KernelCost("k_nsflux3", f(C) + geo_grad, f(npl), f(C), f(npl),

@@ -279,6 +279,10 @@ int dispatch_rhs(const dgb_disc* d, bool viscous, const double* q, const double*
                  long long ebeg = 0, long long eend = -1) {
   if ((ebeg != 0 || eend >= 0) && variant() != 5)
     return fail(DGB_ERR_INVALID, "element ranges need the default kernels (DGB_VARIANT=5)");
+  // Euler: k_euler4 (dgb_kernels_flux.cuh) unless DGB_EULER_KERNEL=3 asks for k_rhs3<inviscid>
+  static int euler_kernel = -1;
+  if (euler_kernel < 0) { const char* e = getenv("DGB_EULER_KERNEL"); euler_kernel = e ? atoi(e) : 4; }
+  if (!viscous && variant() == 5 && euler_kernel == 4) return dgb_launch_euler4(d, q, ghost, ep, ph, ebeg, eend, st);
 #define X(DIM, P)                                                                              \
   if (d->dim == DIM && d->order == P) {                                                        \
     if (variant() == 5)                                                                        \

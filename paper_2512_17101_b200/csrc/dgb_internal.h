@@ -29,3 +29,6 @@ struct dgb_disc {
 
 // dgb_nsflux.cu
 int dgb_disc_free_jacobian(dgb_disc* d);
+// single-pass Euler kernel of the flux-arrangement family (k_euler4); eend < 0 = all elements
+int dgb_launch_euler4(const dgb_disc* d, const double* q, const double* ghost, const dgb::Epilogue& ep,
+                      const dgb::Phys& ph, long long ebeg, long long eend, cudaStream_t st);

@@ -859,4 +859,239 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
   cp_async_wait<0>();
 }
 
+// ------------------------------------------------------------------------------------------
+// Euler right-hand side in one pass, built like k_nsdiv3 (k_euler4).
+//
+// rows + geometry by cp.async (double-buffered, one block ahead) -> the neighbour gathers of ALL face
+// nodes of the block are issued first and fly while the volume flux is evaluated -> T[r][c] =
+// sum_x dr/dx[r][x] F[x][c] into the DMMA operand rows -> face phase from the gathered q+:
+// Fs = -(fscale F(q+).n + fscale max(lam-, lam+)(q- - q+)) / 2, the own-side half of the numerical flux
+// being linear in the T rows and folded into the volume matrix (Wv2, as in pass 2 of Navier-Stokes)
+// -> one DMMA contraction -> (RK-fused) store.  Boundary faces need no special path: the exterior
+// state replaces q+.
+// ------------------------------------------------------------------------------------------
+template <int DIM, int P, int KW>
+struct alignas(16) Euler4Small {
+  using EL = ElemT<DIM, P>;
+  double Qs[EL::C * KW * EL::NP];
+  double drdx[DIM * DIM][KW];
+  double nrm[DIM][KW][EL::NF];
+  double fsc[KW][EL::NF];
+  long long conn[KW][EL::NF];
+};
+
+template <int DIM, int P, int KW>
+struct alignas(16) Euler4Warp {
+  using EL = ElemT<DIM, P>;
+  static constexpr int NCOL = EL::C * KW;
+  static constexpr int NTILE = (NCOL + 7) / 8;
+  double Ts[NCOL * EL::LDV];
+  double Fs[NCOL * EL::LDF];
+  double Lam[KW * EL::NP];
+  Euler4Small<DIM, P, KW> sm[2];
+};
+
+template <int DIM, int P, int KW, int NWARPS>
+struct Euler4Smem {
+  using EL = ElemT<DIM, P>;
+  double Wv[EL::NPR * EL::LDV];
+  double Wl[EL::NPR * EL::LDF];
+  Euler4Warp<DIM, P, KW> w[NWARPS];
+  int fn[EL::NF * EL::NFP];
+  int perm[EL::NPERM * EL::NFP];
+  int flc[face_rounds<DIM, P, KW>() * 32];
+};
+
+template <int DIM, int P, int KW>
+__device__ __forceinline__ void euler4_stage(Euler4Small<DIM, P, KW>& M, const DiscDev& d, const double* q,
+                                             long long e0, int nel, int lane) {
+  using EL = ElemT<DIM, P>;
+  constexpr int C = EL::C, NP = EL::NP, NF = EL::NF;
+  const long long E = d.E;
+  constexpr int CH = (NP % 2 == 0) ? 2 : 1, NPC = NP / CH;
+#pragma unroll
+  for (int t0 = 0; t0 < KW * NPC; t0 += 32) {
+    const int t = t0 + lane;
+    const int e = t / NPC, j = CH * (t - e * NPC);
+    if (t < KW * NPC && e < nel) {
+      double* qs = M.Qs + e * NP + j;
+      const double* qg = q + (e0 + e) * NP + j;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        if (CH == 2) cp_async16(qs + c * (KW * NP), qg + c * E * NP);
+        else cp_async8(qs + c * (KW * NP), qg + c * E * NP);
+      }
+    }
+  }
+  for (int n = lane; n < DIM * DIM * KW; n += 32) {
+    const int rx = n / KW, e = n - rx * KW;
+    if (e < nel) cp_async8(&M.drdx[rx][e], d.drdx + (long long)rx * E + e0 + e);
+  }
+  if (lane < nel * NF) {
+#pragma unroll
+    for (int x = 0; x < DIM; ++x) cp_async8(&M.nrm[x][0][lane], d.normals + ((long long)x * E + e0) * NF + lane);
+    cp_async8(&M.fsc[0][lane], d.fscale + e0 * NF + lane);
+    cp_async8(&M.conn[0][lane], d.conn + e0 * NF + lane);
+  }
+}
+
+template <int DIM, int P, int KW, int NWARPS>
+__global__ void __launch_bounds__(NWARPS * 32, 1)
+k_euler4(DiscDev d, const double* __restrict__ q, const double* __restrict__ ghost,
+         Epilogue ep, Phys ph, long long ebeg, long long eend, long long nwblocks,
+         unsigned long long* __restrict__ counter) {
+  using EL = ElemT<DIM, P>;
+  using WS = Euler4Warp<DIM, P, KW>;
+  constexpr int C = EL::C, NP = EL::NP, NF = EL::NF, NFP = EL::NFP;
+  constexpr int NT = NWARPS * 32;
+  constexpr int NR = face_rounds<DIM, P, KW>();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  auto& S = *reinterpret_cast<Euler4Smem<DIM, P, KW, NWARPS>*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long E = d.E, G = d.G;
+
+  for (int n = tid; n < EL::NPR * EL::LDV; n += NT) S.Wv[n] = d.Wv2[n];
+  for (int n = tid; n < EL::NPR * EL::LDF; n += NT) S.Wl[n] = d.Wl[n];
+  for (int n = tid; n < NF * NFP; n += NT) S.fn[n] = d.tables[n];
+  for (int n = tid; n < EL::NPERM * NFP; n += NT) S.perm[n] = d.tables[NF * NFP + n];
+  WS& W = S.w[warp];
+  {
+    double* z = reinterpret_cast<double*>(&W);
+    for (int n = lane; n < (int)(sizeof(WS) / 8); n += 32) z[n] = 0.0;
+  }
+  __syncthreads();
+  for (int n = tid; n < NR * 32; n += NT) S.flc[n] = face_lane_code<DIM, P, KW>(S.fn, n);
+  __syncthreads();
+
+  auto nel_of = [&](long long wbx) -> int {
+    if (wbx >= nwblocks) return 0;
+    const long long e = ebeg + wbx * KW;
+    return (int)((eend - e) < (long long)KW ? (eend - e) : (long long)KW);
+  };
+  const long long wstride = (long long)gridDim.x * NWARPS;
+  long long wb = (long long)blockIdx.x * NWARPS + warp;
+  if (wb >= nwblocks) return;
+  euler4_stage<DIM, P, KW>(W.sm[0], d, q, ebeg + wb * KW, nel_of(wb), lane);
+  cp_async_commit();
+  unsigned long long ticket = draw_ticket(counter, lane);
+
+  for (int i = 0;; ++i) {
+    const int buf = i & 1;
+    const long long e0 = ebeg + wb * KW;
+    const int nel = nel_of(wb);
+    const long long wb_next = ticket_block(ticket, wstride);
+    const int nel1 = nel_of(wb_next);
+    if (nel1 > 0) euler4_stage<DIM, P, KW>(W.sm[buf ^ 1], d, q, ebeg + wb_next * KW, nel1, lane);
+    cp_async_commit();
+    ticket = draw_ticket(counter, lane);
+    cp_async_wait<1>();                  // this block's rows + geometry have landed
+    __syncwarp();
+    const Euler4Small<DIM, P, KW>& M = W.sm[buf];
+
+    // ---- neighbour states of every face node: in flight during the volume phase --------------
+    double qp[NR][C];
+    long long cnk[NR];
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+      cnk[k] = -1;
+      const int flk = S.flc[k * 32 + lane];
+      const int e = flk & 3, f = (flk >> 2) & 3, m = (flk >> 4) & 15;
+      if (flk >= 0 && e < nel) {
+        const long long cn = M.conn[e][f];
+        cnk[k] = cn;
+        const long long nb = DGB_CONN_NB(cn);
+        const int jp = S.fn[DGB_CONN_NF(cn) * NFP + S.perm[DGB_CONN_PERM(cn) * NFP + m]];
+        const bool in_ghost = nb >= E;
+        const long long pstride = (in_ghost ? G : E) * NP;
+        const double* pbase = (in_ghost ? ghost : q) + (in_ghost ? nb - E : nb) * NP + jp;
+#pragma unroll
+        for (int c = 0; c < C; ++c) qp[k][c] = pbase[c * pstride];
+      }
+    }
+
+    // ---- volume flux -> contravariant operand rows, wave speed ---------------------------------
+#pragma unroll
+    for (int n0 = 0; n0 < KW * NP; n0 += 32) {
+      const int n = n0 + lane;
+      const int e = n / NP, j = n - e * NP;
+      if (n < KW * NP && e < nel) {
+        double qq[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) qq[c] = M.Qs[(c * KW + e) * NP + j];
+        Prim<DIM> s;
+        make_prim<DIM>(qq, ph.gamma, s);
+        double F[DIM][C];
+        inviscid_flux<DIM>(s, F);
+#pragma unroll
+        for (int r = 0; r < DIM; ++r) {
+          double mm[DIM];
+#pragma unroll
+          for (int x = 0; x < DIM; ++x) mm[x] = M.drdx[r * DIM + x][e];
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            double acc = mm[0] * F[0][c];
+#pragma unroll
+            for (int x = 1; x < DIM; ++x) acc += mm[x] * F[x][c];
+            W.Ts[(c * KW + e) * EL::LDV + r * EL::NPK + j] = acc;
+          }
+        }
+        W.Lam[n] = wavespeed<DIM>(s, ph.gamma);
+      }
+    }
+    __syncwarp();
+
+    // ---- face phase from the gathered states ----------------------------------------------------
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+      if (cnk[k] >= 0) {
+        const int flk = S.flc[k * 32 + lane];
+        const int e = flk & 3, f = (flk >> 2) & 3, jm = (flk >> 8) & 255, fm = (flk >> 16) & 255;
+        const int bc = DGB_CONN_BC(cnk[k]);
+        double qm[C], nrm[DIM];
+#pragma unroll
+        for (int c = 0; c < C; ++c) qm[c] = M.Qs[(c * KW + e) * NP + jm];
+#pragma unroll
+        for (int x = 0; x < DIM; ++x) nrm[x] = M.nrm[x][e][f];
+        if (bc != 0) bc_state<DIM, false>(bc, qm, nrm, ph, qp[k]);
+        Prim<DIM> sp_;
+        make_prim<DIM>(qp[k], ph.gamma, sp_);
+        double fnp[C];
+        inviscid_normal_flux<DIM>(sp_, nrm, fnp);
+        const double fs_ = M.fsc[e][f];
+        const double pen = fmax(W.Lam[e * NP + jm], wavespeed<DIM>(sp_, ph.gamma));
+        double* fsrow = W.Fs + e * EL::LDF + fm;
+#pragma unroll
+        for (int c = 0; c < C; ++c) fsrow[c * (KW * EL::LDF)] = -0.5 * fs_ * (fnp[c] + pen * (qm[c] - qp[k][c]));
+      }
+    }
+    __syncwarp();
+
+    // ---- tensor-core contraction + (RK-fused) store ----------------------------------------------
+    double acc[WS::NTILE][EL::NI][2];
+#pragma unroll
+    for (int mt = 0; mt < WS::NTILE; ++mt)
+#pragma unroll
+      for (int ni = 0; ni < EL::NI; ++ni) { acc[mt][ni][0] = 0.0; acc[mt][ni][1] = 0.0; }
+    mma_block<EL::NI, WS::NTILE>(acc, W.Ts, EL::LDV, S.Wv, EL::LDV, EL::KV / 4, lane);
+    mma_block<EL::NI, WS::NTILE>(acc, W.Fs, EL::LDF, S.Wl, EL::LDF, EL::KF / 4, lane);
+#pragma unroll
+    for (int mt = 0; mt < WS::NTILE; ++mt) {
+      const int col = mt * 8 + (lane >> 2);
+      const int c = col / KW, e = col - c * KW;
+      if (col < WS::NCOL && e < nel) {
+        const long long rowbase = ((long long)c * E + e0 + e) * NP;
+#pragma unroll
+        for (int ni = 0; ni < EL::NI; ++ni) {
+          const int i2 = ni * 8 + 2 * (lane & 3);
+          store_pair<NP>(ep, rowbase + i2, i2, acc[mt][ni][0], acc[mt][ni][1]);
+        }
+      }
+    }
+    __syncwarp();                        // operand rows free for the next block
+    if (nel1 == 0) break;
+    wb = wb_next;
+  }
+  cp_async_wait<0>();
+}
+
 }  // namespace dgb

@@ -202,6 +202,46 @@ int check_flux_args(const dgb_disc* d, const void* ghost, const void* a, const v
 
 }  // namespace
 
+#ifndef DGB_EULER_WARPS
+#define DGB_EULER_WARPS 12
+#endif
+namespace {
+template <int DIM, int P> struct CfgE {
+  static constexpr int KW = DIM == 3 ? 3 : 4;
+  static constexpr size_t per = sizeof(dgb::Euler4Warp<DIM, P, KW>);
+  static constexpr size_t fixed = sizeof(dgb::Euler4Smem<DIM, P, KW, 1>) - per;
+  static constexpr int NW = fit_warps(fixed, per, DGB_EULER_WARPS);
+};
+
+template <int DIM, int P>
+int launch_euler4(const dgb_disc* d, const double* q, const double* ghost, const dgb::Epilogue& ep, const dgb::Phys& ph,
+                  long long ebeg, long long eend, cudaStream_t st) {
+  using C = CfgE<DIM, P>;
+  auto kern = dgb::k_euler4<DIM, P, C::KW, C::NW>;
+  const size_t smem = sizeof(dgb::Euler4Smem<DIM, P, C::KW, C::NW>);
+  const long long nwb = (eend - ebeg + C::KW - 1) / C::KW;
+  if (nwb == 0) return DGB_OK;
+  static bool configured = false;
+  if (!configured) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured = true; }
+  const long long need = (nwb + C::NW - 1) / C::NW;
+  const int grid = (int)(need < dgb_num_sms() ? need : dgb_num_sms());
+  DGB_CUDA(cudaMemsetAsync(d->counters + 1, 0, sizeof(unsigned long long), st));
+  kern<<<grid, C::NW * 32, smem, st>>>(d->dev, q, ghost, ep, ph, ebeg, eend, nwb, d->counters + 1);
+  DGB_CUDA(cudaGetLastError());
+  return DGB_OK;
+}
+}  // namespace
+
+int dgb_launch_euler4(const dgb_disc* d, const double* q, const double* ghost, const dgb::Epilogue& ep,
+                      const dgb::Phys& ph, long long ebeg, long long eend, cudaStream_t st) {
+  if (eend < 0) eend = d->dev.E;
+  if ((((uintptr_t)q) | ((uintptr_t)ep.out1)) & 15) return dgb_fail(DGB_ERR_INVALID, "device arrays must be 16-byte aligned");
+#define X(DIM, P) if (d->dim == DIM && d->order == P) return launch_euler4<DIM, P>(d, q, ghost, ep, ph, ebeg, eend, st);
+  DGB_FOR_EACH_ELEMENT(X)
+#undef X
+  return dgb_fail(DGB_ERR_INVALID, "unsupported (dim, order)");
+}
+
 int dgb_disc_free_jacobian(dgb_disc* d) {
   if (d) { cudaFree(d->sj); cudaFree(d->rj); d->sj = d->rj = nullptr; }
   return DGB_OK;

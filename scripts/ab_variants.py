@@ -17,6 +17,7 @@ VARIANTS = {
     "timing": ["DGB_PHASE_TIMING=1"],                 # scripts/phase_timing_flux.py
     "experimental": ["DGB_EXPERIMENTAL=1"],           # + DGB_DIV_KERNEL=4|5|6 at run time
     "trecord": ["DGB_T_RECORD=1"],                    # record-major flux planes (experiment: rhs only)
+    "euler_w8": ["DGB_EULER_WARPS=8"],
     "flux_nb2": ["DGB_FLUX_NB=2"],
     "div_w12_nb1": ["DGB_DIV_WARPS=12", "DGB_DIV_NB=1"],
 }
@@ -53,8 +54,9 @@ def main():
             if kern:
                 env["DGB_DIV_KERNEL"] = kern
                 name = f"{name}:k_nsdiv{kern}"
+            extra = sys.argv[sys.argv.index("--bench-args") + 1].split() if "--bench-args" in sys.argv else []
             res = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--no-e2e", "--no-cpu", "--n", n,
-                                  "--steps", "10"], env=env, capture_output=True, text=True)
+                                  "--steps", "10"] + extra, env=env, capture_output=True, text=True)
             try:
                 d = json.loads(res.stdout.strip().splitlines()[-1])
                 r = d["roofline"]
