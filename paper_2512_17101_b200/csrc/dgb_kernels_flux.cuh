@@ -29,6 +29,9 @@
 #ifndef DGB_DIV_LAZY_EX
 #define DGB_DIV_LAZY_EX 0
 #endif
+#ifndef DGB_DIV_SPLIT_MMA
+#define DGB_DIV_SPLIT_MMA 0
+#endif
 #ifndef DGB_FLUX_PRODUCT_MAJOR
 #define DGB_FLUX_PRODUCT_MAJOR 0
 #endif
@@ -750,6 +753,116 @@ __device__ __forceinline__ void div_face_phase(const int* flc, const int* fn, co
   }
 }
 
+// Split form of the face phase: face_issue() puts the first-wave gathers of ALL face nodes of a block
+// in flight (registers), face_finish() consumes them.  k_nsdiv3 (DGB_DIV_SPLIT_MMA) runs the volume
+// half of the DMMA contraction -- which does not depend on the face operand rows -- in between.
+template <int DIM, int P, int KW>
+struct FaceRegs {
+  using EL = ElemT<DIM, P>;
+  static constexpr int NR = face_rounds<DIM, P, KW>();
+  double qp[NR][EL::C], nbr[NR][EL::C], lam_p[NR];
+  long long cnk[NR];
+};
+
+template <int DIM, int P, int KW>
+__device__ __forceinline__ void face_issue(FaceRegs<DIM, P, KW>& R, const int* flc, const int* fn, const int* perm,
+                                           const Div3Small<DIM, P, KW>& M, const DiscDev& d,
+                                           const double* __restrict__ q, const double* __restrict__ T,
+                                           const double* __restrict__ ghost, const double* __restrict__ Tghost,
+                                           int nel, int lane) {
+  using EL = ElemT<DIM, P>;
+  constexpr int C = EL::C, NP = EL::NP, NFP = EL::NFP;
+  constexpr int NR = FaceRegs<DIM, P, KW>::NR;
+  const long long E = d.E, G = d.G;
+#pragma unroll
+  for (int k = 0; k < NR; ++k) {
+    R.cnk[k] = -1;
+    const int flk = flc[k * 32 + lane];
+    const int e = flk & 3, f = (flk >> 2) & 3, m = (flk >> 4) & 15;
+    if (flk >= 0 && e < nel) {
+      const long long cn = M.conn[e][f];
+      R.cnk[k] = cn;
+      const long long nb = DGB_CONN_NB(cn);
+      const int nf = DGB_CONN_NF(cn);
+      const int jp = fn[nf * NFP + perm[DGB_CONN_PERM(cn) * NFP + m]];
+      const bool in_ghost = nb >= E;
+      const long long pstride = (in_ghost ? G : E) * NP;
+      const long long off = (in_ghost ? nb - E : nb) * NP + jp;
+      const double* qbase = (in_ghost ? ghost : q) + off;
+      const double* tbase = (in_ghost ? Tghost : T) + off;
+      const int r0 = nf == 0 ? 0 : nf - 1;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        R.qp[k][c] = qbase[c * pstride];
+        R.nbr[k][c] = tbase[(r0 * C + c) * pstride];
+      }
+      R.lam_p[k] = tbase[(DIM * C) * pstride];
+    }
+  }
+}
+
+template <int DIM, int P, int KW>
+__device__ __forceinline__ void face_finish(FaceRegs<DIM, P, KW>& R, const int* flc, const int* fn, const int* perm,
+                                            const Div3Small<DIM, P, KW>& M, double* Fs, const DiscDev& d,
+                                            const double* __restrict__ T, const double* __restrict__ Tghost,
+                                            const Phys& ph, long long e0, int nel, int lane) {
+  using EL = ElemT<DIM, P>;
+  constexpr int C = EL::C, NP = EL::NP, NF = EL::NF, NFP = EL::NFP;
+  constexpr int NR = FaceRegs<DIM, P, KW>::NR;
+  const long long E = d.E, G = d.G;
+  // second wave: a neighbour's face 0 is the sum of its DIM rows; fetch the other DIM-1 now
+  double ex[NR][C];
+#pragma unroll
+  for (int k = 0; k < NR; ++k) {
+    if (R.cnk[k] >= 0 && DGB_CONN_NF(R.cnk[k]) == 0 && DGB_CONN_BC(R.cnk[k]) == 0) {
+      const int flk = flc[k * 32 + lane];
+      const long long nb = DGB_CONN_NB(R.cnk[k]);
+      const int m = (flk >> 4) & 15;
+      const int jp = fn[perm[DGB_CONN_PERM(R.cnk[k]) * NFP + m]];
+      const bool in_ghost = nb >= E;
+      const long long pstride = (in_ghost ? G : E) * NP;
+      const double* tbase = (in_ghost ? Tghost : T) + (in_ghost ? nb - E : nb) * NP + jp;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        double t = tbase[(C + c) * pstride];
+#pragma unroll
+        for (int r = 2; r < DIM; ++r) t += tbase[(r * C + c) * pstride];
+        ex[k][c] = t;
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NR; ++k) {
+    if (R.cnk[k] >= 0) {
+      const int flk = flc[k * 32 + lane];
+      const int e = flk & 3, f = (flk >> 2) & 3, jm = (flk >> 8) & 255, fm = (flk >> 16) & 255;
+      const int nf = DGB_CONN_NF(R.cnk[k]), bc = DGB_CONN_BC(R.cnk[k]);
+      const double sj = M.sj[e][f];
+      const double lam_m = M.Lam[e * NP + jm];
+      double qm[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) qm[c] = M.Qs[(c * KW + e) * NP + jm];
+      double* fs = Fs + e * EL::LDF + fm;
+      if (bc == 0) {
+        const double pen = sj * fmax(lam_m, R.lam_p[k]);
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          const double nb_ = nf == 0 ? R.nbr[k][c] + ex[k][c] : -R.nbr[k][c];
+          fs[c * (KW * EL::LDF)] = 0.5 * (nb_ - pen * (qm[c] - R.qp[k][c]));
+        }
+      } else {
+        VecC<DIM> a_;
+#pragma unroll
+        for (int c = 0; c < C; ++c) a_.v[c] = qm[c];
+        const VecC<DIM> fb = boundary_operand<DIM>(bc, f, a_, T + (e0 + e) * NP + jm, E * NP, lam_m, sj,
+                                                   d.normals + (e0 + e) * NF + f, E * NF, ph);
+#pragma unroll
+        for (int c = 0; c < C; ++c) fs[c * (KW * EL::LDF)] = fb.v[c];
+      }
+    }
+  }
+}
+
 template <int DIM, int P, int KW, int NWARPS>
 __global__ void __launch_bounds__(NWARPS * 32, 1)
 k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
@@ -816,6 +929,24 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
     //      constant coefficients and lives in the folded volume matrix, so this phase needs only
     //      q, lam and the connectivity of the block -- not its T rows, which are still landing.
     //      Fs = (nbr - sJ max(lam-, lam+) (q- - q+)) / 2,  nbr = sJ F+.n+ gathered from the neighbour.
+#if DGB_DIV_SPLIT_MMA
+    // gathers of the whole block in flight ... under the volume half of the contraction
+    FaceRegs<DIM, P, KW> R;
+    face_issue<DIM, P, KW>(R, S.flc, S.fn, S.perm, M, d, q, T, ghost, Tghost, nel, lane);
+    DGB_WTICK(1);
+    cp_async_wait<1>();                  // T(b) has landed
+    __syncwarp();
+    DGB_WTICK(2);
+    double acc[WS::NTILE][EL::NI][2];
+#pragma unroll
+    for (int mt = 0; mt < WS::NTILE; ++mt)
+#pragma unroll
+      for (int ni = 0; ni < EL::NI; ++ni) { acc[mt][ni][0] = 0.0; acc[mt][ni][1] = 0.0; }
+    mma_block<EL::NI, WS::NTILE>(acc, W.Ts, EL::LDV, S.Wv, EL::LDV, EL::KV / 4, lane);
+    face_finish<DIM, P, KW>(R, S.flc, S.fn, S.perm, M, W.Fs, d, T, Tghost, ph, e0, nel, lane);
+    __syncwarp();
+    mma_block<EL::NI, WS::NTILE>(acc, W.Fs, EL::LDF, S.Wl, EL::LDF, EL::KF / 4, lane);
+#else
     div_face_phase<DIM, P, KW, NB, (DGB_DIV_LAZY_EX != 0)>(S.flc, S.fn, S.perm, M, W.Fs, d, q, T, ghost, Tghost, ph, e0, nel, lane);
     DGB_WTICK(1);
     cp_async_wait<1>();                  // T(b) has landed
@@ -830,6 +961,7 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
       for (int ni = 0; ni < EL::NI; ++ni) { acc[mt][ni][0] = 0.0; acc[mt][ni][1] = 0.0; }
     mma_block<EL::NI, WS::NTILE>(acc, W.Ts, EL::LDV, S.Wv, EL::LDV, EL::KV / 4, lane);
     mma_block<EL::NI, WS::NTILE>(acc, W.Fs, EL::LDF, S.Wl, EL::LDF, EL::KF / 4, lane);
+#endif
     double rj[WS::NTILE];
 #pragma unroll
     for (int mt = 0; mt < WS::NTILE; ++mt) rj[mt] = M.rj[(mt * 8 + (lane >> 2)) % KW];

@@ -203,113 +203,6 @@ k_nsdiv4(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
 // (44 doubles for tets p3) next to the 24 accumulator registers -- 8 warps x 255 registers.
 // ------------------------------------------------------------------------------------------
 template <int DIM, int P, int KW>
-struct FaceRegs {
-  using EL = ElemT<DIM, P>;
-  static constexpr int NR = face_rounds<DIM, P, KW>();
-  double qp[NR][EL::C], nbr[NR][EL::C], lam_p[NR];
-  long long cnk[NR];
-};
-
-template <int DIM, int P, int KW>
-__device__ __forceinline__ void face_issue(FaceRegs<DIM, P, KW>& R, const int* flc, const int* fn, const int* perm,
-                                           const Div3Small<DIM, P, KW>& M, const DiscDev& d,
-                                           const double* __restrict__ q, const double* __restrict__ T,
-                                           const double* __restrict__ ghost, const double* __restrict__ Tghost,
-                                           int nel, int lane) {
-  using EL = ElemT<DIM, P>;
-  constexpr int C = EL::C, NP = EL::NP, NFP = EL::NFP;
-  constexpr int NR = FaceRegs<DIM, P, KW>::NR;
-  const long long E = d.E, G = d.G;
-#pragma unroll
-  for (int k = 0; k < NR; ++k) {
-    R.cnk[k] = -1;
-    const int flk = flc[k * 32 + lane];
-    const int e = flk & 3, f = (flk >> 2) & 3, m = (flk >> 4) & 15;
-    if (flk >= 0 && e < nel) {
-      const long long cn = M.conn[e][f];
-      R.cnk[k] = cn;
-      const long long nb = DGB_CONN_NB(cn);
-      const int nf = DGB_CONN_NF(cn);
-      const int jp = fn[nf * NFP + perm[DGB_CONN_PERM(cn) * NFP + m]];
-      const bool in_ghost = nb >= E;
-      const long long pstride = (in_ghost ? G : E) * NP;
-      const long long off = (in_ghost ? nb - E : nb) * NP + jp;
-      const double* qbase = (in_ghost ? ghost : q) + off;
-      const double* tbase = (in_ghost ? Tghost : T) + off;
-      const int r0 = nf == 0 ? 0 : nf - 1;
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        R.qp[k][c] = qbase[c * pstride];
-        R.nbr[k][c] = tbase[(r0 * C + c) * pstride];
-      }
-      R.lam_p[k] = tbase[(DIM * C) * pstride];
-    }
-  }
-}
-
-template <int DIM, int P, int KW>
-__device__ __forceinline__ void face_finish(FaceRegs<DIM, P, KW>& R, const int* flc, const int* fn, const int* perm,
-                                            const Div3Small<DIM, P, KW>& M, double* Fs, const DiscDev& d,
-                                            const double* __restrict__ T, const double* __restrict__ Tghost,
-                                            const Phys& ph, long long e0, int nel, int lane) {
-  using EL = ElemT<DIM, P>;
-  constexpr int C = EL::C, NP = EL::NP, NF = EL::NF, NFP = EL::NFP;
-  constexpr int NR = FaceRegs<DIM, P, KW>::NR;
-  const long long E = d.E, G = d.G;
-  // second wave: a neighbour's face 0 is the sum of its DIM rows; fetch the other DIM-1 now
-  double ex[NR][C];
-#pragma unroll
-  for (int k = 0; k < NR; ++k) {
-    if (R.cnk[k] >= 0 && DGB_CONN_NF(R.cnk[k]) == 0 && DGB_CONN_BC(R.cnk[k]) == 0) {
-      const int flk = flc[k * 32 + lane];
-      const long long nb = DGB_CONN_NB(R.cnk[k]);
-      const int m = (flk >> 4) & 15;
-      const int jp = fn[perm[DGB_CONN_PERM(R.cnk[k]) * NFP + m]];
-      const bool in_ghost = nb >= E;
-      const long long pstride = (in_ghost ? G : E) * NP;
-      const double* tbase = (in_ghost ? Tghost : T) + (in_ghost ? nb - E : nb) * NP + jp;
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        double t = tbase[(C + c) * pstride];
-#pragma unroll
-        for (int r = 2; r < DIM; ++r) t += tbase[(r * C + c) * pstride];
-        ex[k][c] = t;
-      }
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < NR; ++k) {
-    if (R.cnk[k] >= 0) {
-      const int flk = flc[k * 32 + lane];
-      const int e = flk & 3, f = (flk >> 2) & 3, jm = (flk >> 8) & 255, fm = (flk >> 16) & 255;
-      const int nf = DGB_CONN_NF(R.cnk[k]), bc = DGB_CONN_BC(R.cnk[k]);
-      const double sj = M.sj[e][f];
-      const double lam_m = M.Lam[e * NP + jm];
-      double qm[C];
-#pragma unroll
-      for (int c = 0; c < C; ++c) qm[c] = M.Qs[(c * KW + e) * NP + jm];
-      double* fs = Fs + e * EL::LDF + fm;
-      if (bc == 0) {
-        const double pen = sj * fmax(lam_m, R.lam_p[k]);
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-          const double nb_ = nf == 0 ? R.nbr[k][c] + ex[k][c] : -R.nbr[k][c];
-          fs[c * (KW * EL::LDF)] = 0.5 * (nb_ - pen * (qm[c] - R.qp[k][c]));
-        }
-      } else {
-        VecC<DIM> a_;
-#pragma unroll
-        for (int c = 0; c < C; ++c) a_.v[c] = qm[c];
-        const VecC<DIM> fb = boundary_operand<DIM>(bc, f, a_, T + (e0 + e) * NP + jm, E * NP, lam_m, sj,
-                                                   d.normals + (e0 + e) * NF + f, E * NF, ph);
-#pragma unroll
-        for (int c = 0; c < C; ++c) fs[c * (KW * EL::LDF)] = fb.v[c];
-      }
-    }
-  }
-}
-
-template <int DIM, int P, int KW>
 struct alignas(16) Div5Warp {
   using EL = ElemT<DIM, P>;
   static constexpr int NCOL = EL::C * KW;
