@@ -215,7 +215,17 @@ def run_b200(args):
     # weak scaling: every rank owns one periodic n^3 block of the same size (configs[2] per GPU)
     mesh = box_mesh((n,) * DIM, (-1.0,) * DIM, (1.0,) * DIM, periodic=(True,) * DIM)
     halo = None
-    if world > 1:
+    strong = args.scaling == "strong"
+    if world > 1 and strong:
+        # strong scaling (BASELINE configs[3]): ONE periodic n^3 box, recursive coordinate bisection into
+        # `world` parts, interior-first renumbering; every rank builds the global mesh once (host, setup only)
+        from paper_2512_17101_b200.dg.partition import interior_first, partition_elements, rank_mesh
+        from paper_2512_17101_b200.dg.simplex import simplex_element
+        from paper_2512_17101_b200.halo import HaloExchange, TorchCommunicator
+        part = partition_elements(mesh, world)
+        mesh, plan = interior_first(*rank_mesh(mesh, part, rank))
+        halo = HaloExchange(actx, plan, TorchCommunicator(), simplex_element(DIM, ORDER).Np)
+    elif world > 1:
         from paper_2512_17101_b200.halo import ring_slab_halo
         mesh, halo = ring_slab_halo(actx, mesh, n, rank, world, ORDER)
     d = DGDiscretization(actx, mesh, ORDER, ghost_elements=0 if halo is None else halo.nghost)
@@ -297,7 +307,12 @@ def run_b200(args):
         t = torch.tensor([ms_step], device="cpu" if share else "cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step = float(t.item())
-    value = world * ndof / (ms_step * 1e-3) / 1e9
+    total_dofs = ndof
+    if world > 1:
+        td = torch.tensor([float(ndof)], device="cpu" if share else "cuda", dtype=torch.float64)
+        dist.all_reduce(td, op=dist.ReduceOp.SUM)
+        total_dofs = int(td.item())
+    value = total_dofs / (ms_step * 1e-3) / 1e9
 
     peak, peak_src = measured_peaks()
     roofline = None
@@ -316,6 +331,8 @@ def run_b200(args):
         if os.path.exists(tpath):
             with open(tpath) as fh:
                 tj = json.load(fh)
+            if tj.get("n") == n and ORDER == 3 and euler and "k_euler4" in tj:
+                traffic = tj["k_euler4"]["dram_read_bytes"] + tj["k_euler4"]["dram_write_bytes"]
             if tj.get("n") == n and ORDER == 3 and not euler:      # ncu capture of exactly this workload (bytes per launch)
                 if grad_form:
                     key = "k_rhs3_viscous" if ms_div >= ms_grad else "k_grad3"
@@ -376,7 +393,7 @@ def run_b200(args):
             t = torch.tensor([ms_e2e], device="cpu" if share else "cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms_e2e = float(t.item())
-        e2e = {"value": world * ndof / (ms_e2e * 1e-3) / 1e9, "unit": "GDOF/s",
+        e2e = {"value": total_dofs / (ms_e2e * 1e-3) / 1e9, "unit": "GDOF/s",
                "h2d_bytes_per_step": int(q_host.nbytes), "d2h_bytes_per_step": int(out_host.nbytes),
                "ms_per_step": ms_e2e, "steps": Ke, "checksum": float(out_host[0, 0, 0])}
 
@@ -394,9 +411,10 @@ def run_b200(args):
         line = {
             "metric": "3D Navier-Stokes DG RHS throughput" if not euler else "3D Euler DG RHS throughput",
             "value": value, "unit": "GDOF/s", "n_gpus": world, "steps": K, "warmup": max(args.warmup, 3), "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic",
-            "config": {"workload": workload_name(n, args.workload),
+            "higher_is_better": True, "scaling": "strong" if (strong and world > 1) else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(n, args.workload) if not (strong and world > 1) else
+                       workload_name(n, args.workload).replace("per GPU", "in total"),
                        "elements_per_gpu": E, "dofs_per_gpu": ndof, "order": ORDER, "dim": DIM,
                        "l2_policy": "inputs larger than L2 (q 4.0 GB, grad q 12 GB per GPU vs 126 MB L2)"
                        if ndof * 40 > 126e6 * 4 else "inputs comparable to L2: reduced size, not the headline config",
@@ -429,6 +447,8 @@ def main():
     ap.add_argument("--order", type=int, default=3, help="polynomial order (headline: 3)")
     ap.add_argument("--form", default="flux", choices=["flux", "grad"],
                     help="arrangement of the NS scheme: flux (default; dg_ns_flux + dg_ns_div) or grad (dg_ns_grad + dg_ns_rhs)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N>1: weak = one n^3 box per GPU in a ring (default); strong = one n^3 box partitioned over the GPUs")
     ap.add_argument("--workload", default="ns", choices=["ns", "euler"],
                     help="ns = BASELINE configs[2] (headline); euler = configs[1] (3D Euler, read q + write rhs = 80 B/DOF)")
     args = ap.parse_args()
