@@ -82,6 +82,8 @@ def get_disc(actx, dim, q, nghost, Sw, drdx, lift, normals, fscale, vmap_m, vmap
     disc = _Disc(actx.lib, handle, keep)
     disc.dim, disc.order, disc.E, disc.Np, disc.Nf, disc.Nfp, disc.G = dim, order, E, Np, Nf, Nfp, nghost
     actx._discs[key] = disc
+    # dg_ns_div does not take drdx (the metric is already inside the flux planes): second index without it
+    actx._discs[("nodrdx",) + key[:3] + key[4:]] = disc
     return disc
 
 
@@ -268,14 +270,9 @@ def _div_common(actx, f, q, T, ghost, Tghost, Sw, jac, lift, normals, fscale, fa
     TG, tg, tgptr = _ghost_ptr(actx, Tghost, (npl,), q.shape[-1])
     if TG != G:
         raise errors.BindingMismatch("ghost arrays of q and of the flux planes disagree in size")
-    # the fused kernels take drdx only through the handle; dg_ns_div does not receive it, so the
-    # handle must already exist (dg_ns_flux of the same discretisation creates it)
-    disc = None
-    for key, cand in actx._discs.items():
-        if key[0] == dim and key[1] == G and key[4] == id(lift) and key[5] == id(normals) and key[6] == id(fscale) \
-                and key[7] == id(vmap_m) and key[8] == id(vmap_p) and key[9] == id(bc_kind) and key[2] == id(Sw):
-            disc = cand
-            break
+    # dg_ns_div does not receive drdx; the handle was created by dg_ns_flux of the same discretisation
+    disc = actx._discs.get(("nodrdx", dim, G, id(Sw), id(lift), id(normals), id(fscale), id(vmap_m), id(vmap_p),
+                            id(bc_kind)))
     if disc is None:
         raise errors.BindingMismatch("dg_ns_div: no discretisation handle for these arrays (call dg_ns_flux first)")
     _bind_jacobian(actx, disc, jac)
