@@ -6,12 +6,14 @@ Public surface:
 * ``DOFArray``, ``DGDiscretization``      -- element-major nodal data + per-mesh operators
 * ``EulerOperator``, ``NavierStokesOperator``, ``rk4_step`` -- the operator program (operators.py)
 * ``dg.mesh.box_mesh``                    -- conforming simplicial box meshes
+* ``MultispeciesOperator``, ``Mixture``     -- multi-species reactive NS (configs[4]), generic device ops (multispecies.py)
 * ``DeviceRK4``                           -- device-resident RK4 driver, one CUDA graph per step (timestepper.py)
 """
 from .dofarray import DOFArray
 from .discretization import BC_FARFIELD, BC_NONE, BC_WALL, DGDiscretization
 from .operators import EulerOperator, NavierStokesOperator, rk4_step, rk4_step_fused
 from .dg.mesh import box_mesh
+from .multispecies import Mixture, MultispeciesOperator
 from . import errors
 
 

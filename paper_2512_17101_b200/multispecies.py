@@ -1,0 +1,235 @@
+"""Multi-species reactive compressible Navier-Stokes (BASELINE.json configs[4]) -- array-context program.
+
+Nothing in the reference defines a mixture EOS, transport model or reaction mechanism (SURVEY.md §8c:
+"parity unpinned"; §8d c4: "a small builder-chosen mechanism"), so the model is fixed HERE and
+documented; like ``operators.py`` it is written once against the reference's array-context API
+(/root/reference/pkg/src/laze/frontend.py:257-302) and runs unchanged on ``laze.ArrayContext``
+(eager and lazy), on the NumPy oracle and on ``B200ArrayContext``.  On B200 it is NOT hand-fused in
+round 1: every op runs on the generic device kernels of the context (``dgb_einsum``, ``dgb_take``,
+``dgb_ew_*``) -- on the device, without a CPU fallback, but at a fraction of the fused path's speed
+(profiles/r01_multispecies.md).  It exists so that configs[4] has a parity-checked drop-in path.
+
+Model
+-----
+* conserved state ``q = [rho, rho E, rho u_1..rho u_d, rho Y_1..rho Y_ns]`` stored ``(C, E, Np)``,
+  ``C = d + 2 + ns``; ``rho`` is the mixture density and is transported itself;
+* thermally perfect mixture with constant species properties: gas constants ``R_k``, heat
+  capacities ``cv_k``, formation enthalpies ``h0_k``:
+  ``R = sum Y_k R_k``, ``cv = sum Y_k cv_k``,
+  ``T = (E/rho - |u|^2/2 - sum Y_k h0_k) / cv``, ``p = rho R T``, ``c^2 = (1 + R/cv) p / rho``;
+* transport: constant ``mu``, ``kappa``, species diffusivity ``D`` (Fick, ``J_k = -rho D grad Y_k``, with
+  the enthalpy flux ``sum h_k J_k``, ``h_k = h0_k + (cv_k + R_k) T``);
+* chemistry: one irreversible Arrhenius step ``species a -> species b``:
+  ``omega = A rho Y_a exp(-T_a / T)``, source ``-omega`` / ``+omega`` on ``rho Y_a`` / ``rho Y_b`` (the heat
+  release is in ``h0``; total energy needs no source);
+* discretisation = the single-species scheme: weak-form nodal DG, Rusanov inviscid flux with the
+  mixture wave speed, BR1 (gradient of the conserved variables AND of ``T``, central flux; viscous
+  flux central), periodic or prescribed far-field exterior state.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .discretization import BC_NONE, DGDiscretization
+from .dofarray import DOFArray
+from .operators import _traces
+
+
+class Mixture:
+    """Constant-property species set + one Arrhenius step (defaults: a 3-species toy mechanism
+    fuel -> product in an inert bath, non-dimensional)."""
+
+    def __init__(self, R=(1.0, 0.8, 1.2), cv=(2.5, 2.0, 3.0), h0=(0.5, -0.5, 0.0), reaction=(0, 1), A=5.0, Ta=2.0):
+        self.R, self.cv, self.h0 = (np.asarray(v, dtype=np.float64) for v in (R, cv, h0))
+        self.ns = self.R.size
+        if not (self.cv.size == self.ns == self.h0.size) or self.ns < 1:
+            raise ValueError("species property arrays must have one entry per species")
+        self.reaction, self.A, self.Ta = (int(reaction[0]), int(reaction[1])), float(A), float(Ta)
+
+
+def _thermo(actx, mix, q, dim):
+    """Velocity, mass fractions, temperature, pressure, mixture R and cv from conserved fields."""
+    rho, ener = q[0], q[1]
+    inv_rho = 1.0 / rho
+    vel = [q[2 + i] * inv_rho for i in range(dim)]
+    Y = [q[2 + dim + k] * inv_rho for k in range(mix.ns)]
+    ke = vel[0] * vel[0]
+    for i in range(1, dim):
+        ke = ke + vel[i] * vel[i]
+    R = float(mix.R[0]) * Y[0]
+    cv = float(mix.cv[0]) * Y[0]
+    hf = float(mix.h0[0]) * Y[0]
+    for k in range(1, mix.ns):
+        R = R + float(mix.R[k]) * Y[k]
+        cv = cv + float(mix.cv[k]) * Y[k]
+        hf = hf + float(mix.h0[k]) * Y[k]
+    T = (ener * inv_rho - 0.5 * ke - hf) / cv
+    p = rho * R * T
+    return vel, Y, T, p, R, cv
+
+
+def _inviscid(actx, mix, q, dim):
+    vel, Y, T, p, R, cv = _thermo(actx, mix, q, dim)
+    C = len(q)
+    flux = []
+    for x in range(dim):
+        fx = [q[2 + x], vel[x] * (q[1] + p)]
+        for i in range(dim):
+            mi = q[2 + i] * vel[x]
+            fx.append(mi + p if i == x else mi)
+        for k in range(mix.ns):
+            fx.append(q[2 + dim + k] * vel[x])
+        flux.append(fx)
+    v2 = vel[0] * vel[0]
+    for i in range(1, dim):
+        v2 = v2 + vel[i] * vel[i]
+    lam = actx.np.sqrt(v2) + actx.np.sqrt((1.0 + R / cv) * p / q[0])
+    assert len(flux[0]) == C
+    return flux, lam, (vel, Y, T)
+
+
+def _viscous(actx, mix, q, gq, gT, prim, transport, dim):
+    """``Fv[x][c]`` from the state, ``gq[x][c] = d q_c/dx_x`` and ``gT[x] = dT/dx_x``."""
+    mu, kappa, D = transport
+    vel, Y, T = prim
+    rho = q[0]
+    inv_rho = 1.0 / rho
+    du = [[(gq[x][2 + i] - vel[i] * gq[x][0]) * inv_rho for x in range(dim)] for i in range(dim)]
+    div = du[0][0]
+    for i in range(1, dim):
+        div = div + du[i][i]
+    dY = [[(gq[x][2 + dim + k] - Y[k] * gq[x][0]) * inv_rho for x in range(dim)] for k in range(mix.ns)]
+    flux = []
+    for x in range(dim):
+        tau = []
+        for i in range(dim):
+            t = mu * (du[i][x] + du[x][i])
+            if i == x:
+                t = t - (2.0 / 3.0) * mu * div
+            tau.append(t)
+        work = vel[0] * tau[0]
+        for i in range(1, dim):
+            work = work + vel[i] * tau[i]
+        heat = kappa * gT[x]
+        spec = []
+        for k in range(mix.ns):
+            jk = (rho * D) * dY[k][x]                       # = -J_k
+            hk = float(mix.h0[k]) + float(mix.cv[k] + mix.R[k]) * T
+            heat = heat + hk * jk
+            spec.append(jk)
+        flux.append([None, work + heat] + tau + spec)
+    return flux
+
+
+def _make_ms_rhs(dim, mix, with_ghost):
+    ns = mix.ns
+
+    def body(actx, q, ghost, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, transport):
+        C, E, Np = q.shape
+        Nf = dim + 1
+        Nfp = lift.shape[1] // Nf
+        tr = [transport[k] for k in range(3)]
+        nrm = [normals[x] for x in range(dim)]
+        is_bnd = actx.np.not_equal(bc_kind, BC_NONE)
+        qc = [q[c] for c in range(C)]
+        finv, lam, prim = _inviscid(actx, mix, qc, dim)
+
+        # ---- pass 1: BR1 gradient of [q, T] with the central flux --------------------------------
+        W = actx.np.concatenate([q, actx.np.reshape(prim[2], (1, E, Np))])                  # (C+1, E, Np)
+        Wg = None
+        if ghost is not None:
+            gprim = _thermo(actx, mix, [ghost[c] for c in range(C)], dim)
+            Wg = actx.np.concatenate([ghost, actx.np.reshape(gprim[2], (1,) + tuple(ghost.shape[1:]))])
+        vol = actx.np.einsum("rij,rxe,cej->xcei", Sw, drdx, W)
+        wm, wp = _traces(actx, W, Wg, vmap_m, vmap_p, C + 1, E, Np, Nf, Nfp)
+        far = [qfar[c] for c in range(C)]
+        far_T = _thermo(actx, mix, far, dim)[2]
+        ext = far + [far_T]
+        wpl = [actx.np.where(is_bnd, ext[c], wp[c]) for c in range(C + 1)]
+        wstar = [fscale * (0.5 * (wm[c] + wpl[c])) for c in range(C + 1)]
+        fs = actx.np.stack([actx.np.stack([nrm[x] * wstar[c] for c in range(C + 1)]) for x in range(dim)])
+        gW = actx.np.einsum("if,xcef->xcei", lift, actx.np.reshape(fs, (dim, C + 1, E, Nf * Nfp))) - vol
+
+        # ---- pass 2: total flux, divergence, Rusanov / central numerical flux ----------------------
+        gq = [[gW[x][c] for c in range(C)] for x in range(dim)]
+        gT = [gW[x][C] for x in range(dim)]
+        fvis = _viscous(actx, mix, qc, gq, gT, prim, tr, dim)
+        ftot = [[finv[x][c] if fvis[x][c] is None else finv[x][c] - fvis[x][c] for c in range(C)] for x in range(dim)]
+        fstack = actx.np.stack([actx.np.stack(fx) for fx in ftot])
+        volf = actx.np.einsum("rij,rxe,xcej->cei", Sw, drdx, fstack)
+        lamr = actx.np.reshape(lam, (1, E, Np))
+        planes = actx.np.concatenate([q, actx.np.reshape(fstack, (dim * C, E, Np)), lamr])  # q, F, lam
+        gplanes = None
+        if ghost is not None:
+            raise NotImplementedError("partitioned multispecies runs exchange [q, F, lam]; not wired in round 1")
+        L = C + dim * C + 1
+        tm, tp = _traces(actx, planes, gplanes, vmap_m, vmap_p, L, E, Np, Nf, Nfp)
+        qm = [tm[c] for c in range(C)]
+        qp = [actx.np.where(is_bnd, far[c], tp[c]) for c in range(C)]
+        # exterior flux on boundary faces: inviscid flux of the far-field state, viscous flux of the interior
+        ffar, lam_far, _ = _inviscid(actx, mix, far, dim)
+        fmi, _, _ = _inviscid(actx, mix, qm, dim)
+        fstar = []
+        lam_p = actx.np.where(is_bnd, lam_far, tp[L - 1])
+        lmax = actx.np.maximum(tm[L - 1], lam_p)
+        for c in range(C):
+            fnm = nrm[0] * tm[C + c]
+            fnp = nrm[0] * tp[C + c]
+            fnb = nrm[0] * (ffar[0][c] - fmi[0][c])
+            for x in range(1, dim):
+                fnm = fnm + nrm[x] * tm[C + x * C + c]
+                fnp = fnp + nrm[x] * tp[C + x * C + c]
+                fnb = fnb + nrm[x] * (ffar[x][c] - fmi[x][c])
+            fplus = actx.np.where(is_bnd, fnm + fnb, fnp)
+            fstar.append(fscale * (0.5 * (fnm + fplus) + 0.5 * lmax * (qm[c] - qp[c])))
+        fsx = actx.np.reshape(actx.np.stack(fstar), (C, E, Nf * Nfp))
+        rhs = volf - actx.np.einsum("if,cef->cei", lift, fsx)
+
+        # ---- chemistry: one Arrhenius step a -> b ---------------------------------------------------
+        a, b = mix.reaction
+        omega = mix.A * qc[2 + dim + a] * actx.np.exp((-mix.Ta) / prim[2])
+        zero = 0.0 * omega
+        src = [zero] * (2 + dim) + [(-1.0 * omega) if k == a else (omega if k == b else zero) for k in range(ns)]
+        return rhs + actx.np.stack(src)
+
+    def dg_ms_rhs(q, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, transport):
+        return body(dg_ms_rhs.actx, q, None, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, transport)
+    return dg_ms_rhs
+
+
+class MultispeciesOperator:
+    """``rhs(q)`` of the multi-species reactive Navier-Stokes equations; ``q``: ``DOFArray (C, E, Np)``.
+    Boundaries: periodic, or far-field (every tagged boundary face takes ``farfield`` as exterior state)."""
+
+    def __init__(self, dcoll: DGDiscretization, mixture: Mixture | None = None, mu=1e-2, kappa=2e-2, diffusivity=1e-2,
+                 farfield=None):
+        self.dcoll, self.actx, self.dim = dcoll, dcoll.actx, dcoll.dim
+        self.mix = mixture or Mixture()
+        self.ncomp = self.dim + 2 + self.mix.ns
+        if farfield is None:
+            farfield = self.state_from_primitive(1.0, np.zeros(self.dim), 1.0, np.full(self.mix.ns, 1.0 / self.mix.ns))
+        self.qfar_host = np.asarray(farfield, dtype=np.float64).reshape(self.ncomp)
+        self.qfar = self.actx.from_numpy(self.qfar_host.reshape(self.ncomp, 1, 1, 1))
+        self.transport = self.actx.from_numpy(np.array([mu, kappa, diffusivity], dtype=np.float64))
+        f = _make_ms_rhs(self.dim, self.mix, False)
+        f.actx = self.actx
+        f.dg_dim = self.dim
+        self._f = self.actx.outline(f)
+
+    def state_from_primitive(self, rho, vel, T, Y):
+        """Conserved state (any broadcastable shapes) from density, velocity, temperature, mass fractions."""
+        mix = self.mix
+        Y = [np.asarray(y, dtype=np.float64) for y in Y]
+        vel = [np.asarray(v, dtype=np.float64) for v in vel]
+        rho = np.asarray(rho, dtype=np.float64)
+        cv = sum(mix.cv[k] * Y[k] for k in range(mix.ns))
+        hf = sum(mix.h0[k] * Y[k] for k in range(mix.ns))
+        e = cv * T + hf + 0.5 * sum(v * v for v in vel)
+        parts = [rho, rho * e] + [rho * v for v in vel] + [rho * y for y in Y]
+        return np.stack(np.broadcast_arrays(*parts))
+
+    def rhs(self, q: DOFArray, t=0.0) -> DOFArray:
+        d = self.dcoll
+        out = self._f(q.data, d.Sw, d.drdx, d.lift, d.normals, d.fscale, d.vmap_m, d.vmap_p, d.bc_kind, self.qfar,
+                      self.transport)
+        return DOFArray(self.actx, out)

@@ -1,0 +1,94 @@
+"""Multi-species reactive Navier-Stokes (BASELINE configs[4]): the model is builder-chosen (nothing in
+the reference defines one), so it is pinned by reference-independent properties, by the reference's
+own contexts executing the same program, and by GPU-vs-oracle parity of the generic device ops."""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from oracle.laze_port import NumpyArrayContext, rel_err
+from paper_2512_17101_b200 import EulerOperator, Mixture, MultispeciesOperator
+from tests.common import make_dcoll, smooth_state
+
+REF = "/root/reference/pkg/src"
+
+
+def ms_state(op, nodes, seed=0):
+    """Smooth multispecies state on nodes (dim, E, Np)."""
+    dim = nodes.shape[0]
+    r2 = (nodes ** 2).sum(axis=0)
+    bump = np.exp(-r2 / (2 * 0.4 ** 2))
+    rho = 1.0 + 0.1 * bump
+    vel = [0.1 * np.sin(np.pi * nodes[(i + 1) % dim]) for i in range(dim)]
+    T = 1.0 + 0.2 * bump
+    ns = op.mix.ns
+    Y = [np.full_like(rho, 1.0 / ns) for _ in range(ns)]
+    if ns > 1:
+        Y[0] = Y[0] + 0.1 * bump
+        Y[-1] = Y[-1] - 0.1 * bump
+    return op.state_from_primitive(rho, vel, T, Y)
+
+
+def test_reduces_to_euler_for_one_inert_species():
+    """ns = 1, no transport, no reaction: the first dim+2 components are the single-species Euler RHS and
+    the species equation is the continuity equation."""
+    actx = NumpyArrayContext()
+    d = make_dcoll(actx, 3, 2, 3, "periodic")
+    mix = Mixture(R=(1.0,), cv=(2.5,), h0=(0.0,), reaction=(0, 0), A=0.0, Ta=1.0)
+    op = MultispeciesOperator(d, mix, mu=0.0, kappa=0.0, diffusivity=0.0)
+    q5 = smooth_state(d.nodes())
+    q = np.concatenate([q5, q5[:1]])
+    r = d.to_numpy(op.rhs(d.from_numpy(q)))
+    ref = d.to_numpy(EulerOperator(d, gamma=1.4).rhs(d.from_numpy(q5)))
+    assert rel_err(r[:5], ref) <= 1e-13
+    assert rel_err(r[5], ref[0]) <= 1e-13
+
+
+@pytest.mark.parametrize("dim,bc", [(3, "periodic"), (2, "farfield")])
+def test_free_stream_and_conservation(dim, bc):
+    actx = NumpyArrayContext()
+    d = make_dcoll(actx, dim, 3, 3, bc)
+    mix = Mixture()
+    far = None
+    op0 = MultispeciesOperator(d, Mixture(A=0.0), farfield=far)
+    qf = op0.state_from_primitive(1.1, [0.2, -0.1, 0.05][:dim], 1.3, [0.5, 0.2, 0.3])
+    op0 = MultispeciesOperator(d, Mixture(A=0.0), farfield=qf)
+    q = d.from_numpy(np.broadcast_to(qf.reshape(-1, 1, 1), (op0.ncomp, d.nelements, d.Np)))
+    assert np.abs(d.to_numpy(op0.rhs(q))).max() < 5e-12          # uniform inert state is steady
+    if bc == "periodic":
+        op = MultispeciesOperator(d, mix)
+        r = d.to_numpy(op.rhs(d.from_numpy(ms_state(op, d.nodes()))))
+        w = np.einsum("i,ij->j", np.ones(d.Np), d.element.mass)
+        total = np.einsum("cej,j,e->c", r, w, d.geo.jac)
+        assert np.abs(total[:2 + dim]).max() < 1e-11              # mass, energy, momentum
+        assert abs(total[2 + dim:].sum()) < 1e-11                 # the reaction moves mass between species only
+        assert total[2 + dim + mix.reaction[0]] < 0 < total[2 + dim + mix.reaction[1]]
+
+
+@pytest.mark.skipif(not os.path.isdir(REF), reason="reference not mounted")
+def test_program_runs_on_the_reference_contexts():
+    sys.path.insert(0, REF)
+    import laze
+    res = {}
+    for name, actx in [("port", NumpyArrayContext()), ("eager", laze.ArrayContext(mode="eager")),
+                       ("lazy", laze.ArrayContext(mode="lazy"))]:
+        d = make_dcoll(actx, 2, 2, 3, "farfield")
+        op = MultispeciesOperator(d, Mixture())
+        res[name] = np.asarray(actx.to_numpy(op.rhs(d.from_numpy(ms_state(op, d.nodes()))).data))
+    assert np.array_equal(res["port"], res["eager"])
+    assert rel_err(res["lazy"], res["eager"]) <= 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dim,order,n,bc", [(3, 3, 2, "periodic") if False else (3, 3, 3, "periodic"), (2, 3, 4, "farfield"), (3, 2, 2, "farfield")])
+def test_gpu_parity_multispecies(dim, order, n, bc):
+    """B200ArrayContext (generic device kernels, no fused dispatch for this program) vs the oracle."""
+    from paper_2512_17101_b200 import B200ArrayContext
+    gpu, cpu = B200ArrayContext(), NumpyArrayContext()
+    dc, dg = make_dcoll(cpu, dim, order, n, bc), make_dcoll(gpu, dim, order, n, bc)
+    oc, og = MultispeciesOperator(dc, Mixture()), MultispeciesOperator(dg, Mixture())
+    q0 = ms_state(oc, dc.nodes())
+    ref = dc.to_numpy(oc.rhs(dc.from_numpy(q0)))
+    got = dg.to_numpy(og.rhs(dg.from_numpy(q0)))
+    assert np.all(np.isfinite(got)) and rel_err(got, ref) <= 1e-12, rel_err(got, ref)
