@@ -224,10 +224,10 @@ def run_b200(args):
         from paper_2512_17101_b200.halo import HaloExchange, TorchCommunicator
         part = partition_elements(mesh, world)
         mesh, plan = interior_first(*rank_mesh(mesh, part, rank))
-        halo = HaloExchange(actx, plan, TorchCommunicator(), simplex_element(DIM, ORDER).Np)
+        halo = HaloExchange(actx, plan, TorchCommunicator(), simplex_element(DIM, ORDER).Np, transport=args.halo)
     elif world > 1:
         from paper_2512_17101_b200.halo import ring_slab_halo
-        mesh, halo = ring_slab_halo(actx, mesh, n, rank, world, ORDER)
+        mesh, halo = ring_slab_halo(actx, mesh, n, rank, world, ORDER, transport=args.halo)
     d = DGDiscretization(actx, mesh, ORDER, ghost_elements=0 if halo is None else halo.nghost)
     euler = args.workload == "euler"
     if euler:
@@ -420,7 +420,9 @@ def run_b200(args):
                        if ndof * 40 > 126e6 * 4 else "inputs comparable to L2: reduced size, not the headline config",
                        "arrangement": ("euler single pass" if euler else
                                        "gradient (dg_ns_grad + dg_ns_rhs)" if grad_form else "flux (dg_ns_flux + dg_ns_div)"),
-                       "parallelism": f"mesh partition x{world}, NCCL face-halo exchange" if world > 1 else "single GPU",
+                       "parallelism": (f"mesh partition x{world}, " + ("NCCL face-halo exchange" if args.halo == "nccl" else
+                                       "peer-memory face-halo exchange (pack kernel stores over NVLink)"))
+                       if world > 1 else "single GPU",
                        "setup_s": t_setup},
             "roofline": roofline,
             "rhs_roofline": {"bound": "hbm", "achieved": rhs_gbs, "peak": peak, "unit": "GB/s",
@@ -430,6 +432,8 @@ def run_b200(args):
         }
         print(json.dumps(line))
     if world > 1:
+        if halo is not None:
+            halo.close()
         dist.destroy_process_group()
 
 
@@ -447,6 +451,9 @@ def main():
     ap.add_argument("--order", type=int, default=3, help="polynomial order (headline: 3)")
     ap.add_argument("--form", default="flux", choices=["flux", "grad"],
                     help="arrangement of the NS scheme: flux (default; dg_ns_flux + dg_ns_div) or grad (dg_ns_grad + dg_ns_rhs)")
+    ap.add_argument("--halo", default="nccl", choices=["nccl", "peer"],
+                    help="N>1 halo transport: nccl = grouped send/recv on a communication stream (default); peer = the "
+                         "pack kernel stores into the neighbour's ghost array through CUDA-IPC peer memory (NVLink)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N>1: weak = one n^3 box per GPU in a ring (default); strong = one n^3 box partitioned over the GPUs")
     ap.add_argument("--workload", default="ns", choices=["ns", "euler"],

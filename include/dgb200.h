@@ -160,6 +160,21 @@ int dgb_ns_div_range(const dgb_disc* disc, const double* q_dev, const double* T_
 int dgb_pack_elements(double* dst_dev, const double* src_dev, const int64_t* elems_dev,
                       int64_t ncomp, int64_t nsrc_elems, int64_t nsel, int64_t ndofs, void* stream);
 
+/* ---- peer-memory halo transport (optional alternative to NCCL send/recv for the messages of
+ *      adfg.py:380-399,834-869): each rank allocates its ghost arrays with dgb_ipc_alloc and publishes the
+ *      64-byte handle; a neighbour maps it (dgb_ipc_open) and its pack kernel stores the halo rows
+ *      straight into it over NVLink -- pack and transfer are one kernel, no staging buffer, no
+ *      communication kernel competing for SMs.  Ordering: stream-ordered flags in peer-mapped memory
+ *      (signal = system-scope release after everything enqueued before it; wait holds the stream).   ---- */
+int dgb_ipc_alloc(void** dev, size_t bytes, void* handle64_out);         /* zero-filled */
+int dgb_ipc_open(void** dev, const void* handle64);
+int dgb_ipc_close(void* dev);
+int dgb_pack_elements_to(double* dst_dev, int64_t ndst_elems, int64_t dst_slot0, const double* src_dev,
+                         const int64_t* elems_dev, int64_t ncomp, int64_t nsrc_elems, int64_t nsel,
+                         int64_t ndofs, void* stream);
+int dgb_flag_signal(uint64_t* flag_dev, uint64_t value, void* stream);
+int dgb_flag_wait(const uint64_t* flag_dev, uint64_t value, void* stream);
+
 /* ---- generic array ops of the context (frontend.py:257-302), for glue outside the fused
  *      functions.  Shapes are given after broadcasting: `rank`, `shape[rank]`, and per-operand
  *      element strides (0 on broadcast axes).  Outputs are dense row-major.                 ---- */

@@ -102,6 +102,34 @@ __global__ void k_pack_elements(double* __restrict__ dst, const double* __restri
   }
 }
 
+// halo rows straight into a (peer-mapped) ghost array: dst[(c*ndst + slot0 + i)*ndofs + j] = src[(c*nsrc + elems[i])*ndofs + j]
+__global__ void k_pack_elements_to(double* __restrict__ dst, long long ndst, long long slot0,
+                                   const double* __restrict__ src, const long long* __restrict__ elems,
+                                   long long ncomp, long long nsrc, long long nsel, long long ndofs) {
+  const long long total = ncomp * nsel * ndofs;
+  for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < total;
+       n += (long long)gridDim.x * blockDim.x) {
+    const long long j = n % ndofs, ci = n / ndofs;
+    const long long i = ci % nsel, c = ci / nsel;
+    dst[(c * ndst + slot0 + i) * ndofs + j] = src[(c * nsrc + elems[i]) * ndofs + j];
+  }
+}
+
+// stream-ordered flags in (peer-mapped) device memory: everything enqueued before dgb_flag_signal on the
+// stream is visible system-wide before the flag takes its value; dgb_flag_wait holds the stream until then
+__global__ void k_flag_signal(unsigned long long* flag, unsigned long long value) {
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(value) : "memory");
+}
+
+__global__ void k_flag_wait(const unsigned long long* flag, unsigned long long value) {
+  unsigned long long v;
+  do {
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+    if (v < value) __nanosleep(200);
+  } while (v < value);
+}
+
 }  // namespace
 
 // }}}
@@ -587,6 +615,51 @@ int dgb_pack_elements(double* dst, const double* src, const int64_t* elems, int6
   if (blocks > 148 * 16) blocks = 148 * 16;
   k_pack_elements<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(dst, src, (const long long*)elems, ncomp,
                                                                        nsrc, nsel, ndofs);
+  DGB_CUDA(cudaGetLastError());
+  return DGB_OK;
+}
+
+int dgb_pack_elements_to(double* dst, int64_t ndst_elems, int64_t dst_slot0, const double* src, const int64_t* elems,
+                         int64_t ncomp, int64_t nsrc, int64_t nsel, int64_t ndofs, void* stream) {
+  const long long total = ncomp * nsel * ndofs;
+  if (total == 0) return DGB_OK;
+  if (dst_slot0 < 0 || dst_slot0 + nsel > ndst_elems) return fail(DGB_ERR_OUT_OF_BOUNDS, "halo slots outside the ghost array");
+  long long blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_pack_elements_to<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(dst, ndst_elems, dst_slot0, src,
+                                                                          (const long long*)elems, ncomp, nsrc, nsel, ndofs);
+  DGB_CUDA(cudaGetLastError());
+  return DGB_OK;
+}
+
+int dgb_ipc_alloc(void** dev, size_t bytes, void* handle64) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  DGB_CUDA(cudaMalloc(dev, bytes ? bytes : 8));
+  DGB_CUDA(cudaMemset(*dev, 0, bytes ? bytes : 8));
+  // the zero fill must have HAPPENED before a neighbour can map the array and store into it (cudaMemset
+  // is asynchronous and would queue behind this rank's pending kernels, wiping a flag set meanwhile)
+  DGB_CUDA(cudaDeviceSynchronize());
+  DGB_CUDA(cudaIpcGetMemHandle((cudaIpcMemHandle_t*)handle64, *dev));
+  return DGB_OK;
+}
+
+int dgb_ipc_open(void** dev, const void* handle64) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  DGB_CUDA(cudaIpcOpenMemHandle(dev, h, cudaIpcMemLazyEnablePeerAccess));
+  return DGB_OK;
+}
+
+int dgb_ipc_close(void* dev) { DGB_CUDA(cudaIpcCloseMemHandle(dev)); return DGB_OK; }
+
+int dgb_flag_signal(uint64_t* flag_dev, uint64_t value, void* stream) {
+  k_flag_signal<<<1, 1, 0, (cudaStream_t)stream>>>((unsigned long long*)flag_dev, (unsigned long long)value);
+  DGB_CUDA(cudaGetLastError());
+  return DGB_OK;
+}
+
+int dgb_flag_wait(const uint64_t* flag_dev, uint64_t value, void* stream) {
+  k_flag_wait<<<1, 1, 0, (cudaStream_t)stream>>>((const unsigned long long*)flag_dev, (unsigned long long)value);
   DGB_CUDA(cudaGetLastError());
   return DGB_OK;
 }

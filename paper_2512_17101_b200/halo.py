@@ -63,8 +63,15 @@ class TorchCommunicator:
 class HaloExchange:
     """Packs the elements a peer needs, exchanges, and returns the ghost array of a field."""
 
-    def __init__(self, actx, plan: HaloPlan, comm: TorchCommunicator | None, ndofs: int):
+    def __init__(self, actx, plan: HaloPlan, comm: TorchCommunicator | None, ndofs: int, transport: str = "nccl"):
+        """``transport``: "nccl" = torch.distributed send/recv (NCCL over NVLink; gloo in tests);
+        "peer" = the pack kernel stores the halo rows straight into the neighbour's ghost array through
+        CUDA-IPC peer-mapped memory (device contexts only; ``comm`` is then used once, for the handles)."""
         self.actx, self.plan, self.comm, self.ndofs = actx, plan, comm, ndofs
+        if transport not in ("nccl", "peer"):
+            raise ValueError("transport must be 'nccl' or 'peer'")
+        self.transport = transport
+        self._channels = {}
         self.nghost = plan.nghost
         self.on_device = hasattr(actx, "lib")
         self.send_tags = getattr(plan, "send_tags", plan.tags)
@@ -104,6 +111,14 @@ class HaloExchange:
             return None
         lead = tuple(data.shape[:-2])
         import torch
+        if self.on_device and self.transport == "peer":
+            from . import _cabi
+            ch = self._peer_begin(data)
+            shared = self._peer_end(ch)
+            ghost = self.actx.empty(lead + (plan.nghost, self.ndofs))       # private copy: the shared array is released at once
+            _cabi.check(self.actx.lib.dgb_memcpy_d2d(ghost.ptr, shared.ptr, ghost.size * 8, self.actx._st), "d2d")
+            self._peer_release(ch)
+            return ghost
         if self.on_device:
             actx = self.actx
             ghost = actx.empty(lead + (plan.nghost, self.ndofs))
@@ -182,6 +197,153 @@ class HaloExchange:
         return ghost
     # }}}
 
+    # {{{ peer-memory transport: pack kernel -> neighbour's ghost array over NVLink, flags for ordering
+    class _Channel:
+        pass
+
+    def _peer_channel(self, lead):
+        """Ghost array + flags of one message family (state halos, flux-plane halos), created on first use:
+        allocate, publish the IPC handles, map the neighbours' arrays, pair the plan entries."""
+        import ctypes as C
+        import math
+        import torch
+        from . import _cabi
+        key = tuple(lead)
+        ch = self._channels.get(key)
+        if ch is not None:
+            return ch
+        actx, plan, lib, dist = self.actx, self.plan, self.actx.lib, self.comm.dist
+        ncomp = math.prod(lead) if lead else 1
+        npeers = len(plan.peers)
+        ch = HaloExchange._Channel()
+        ch.lead, ch.ncomp, ch.epoch = key, ncomp, 0
+        gh, fl = C.c_void_p(), C.c_void_p()
+        hg, hf = C.create_string_buffer(64), C.create_string_buffer(64)
+        _cabi.check(lib.dgb_ipc_alloc(C.byref(gh), ncomp * max(plan.nghost, 1) * self.ndofs * 8, hg), "ipc alloc")
+        _cabi.check(lib.dgb_ipc_alloc(C.byref(fl), 16 * max(npeers, 1), hf), "ipc alloc")
+        ch.ghost_ptr, ch.flags_ptr = gh.value, fl.value            # flags: ready[npeers] then ack[npeers] (u64)
+
+        class _Raw:
+            __cuda_array_interface__ = {"shape": key + (plan.nghost, self.ndofs), "typestr": "<f8",
+                                        "data": (gh.value, False), "version": 3, "strides": None}
+        from .actx import DeviceArray
+        ch.ghost = DeviceArray(actx, torch.as_tensor(_Raw(), device=actx.device))
+        info = {"rank": plan.rank, "key": key, "ghost": hg.raw, "flags": hf.raw, "nghost": plan.nghost,
+                "peers": list(plan.peers), "tags": list(plan.tags), "send_tags": list(self.send_tags),
+                "recv_slots": [tuple(x) for x in plan.recv_slots]}
+        infos = [None] * self.comm.size
+        dist.all_gather_object(infos, info, group=self.comm.group)
+        by_rank = {i["rank"]: i for i in infos}
+        opened = {}
+
+        def peer_ptrs(r):
+            if r not in opened:
+                a, b = C.c_void_p(), C.c_void_p()
+                if r == plan.rank:
+                    a.value, b.value = ch.ghost_ptr, ch.flags_ptr
+                else:
+                    _cabi.check(lib.dgb_ipc_open(C.byref(a), by_rank[r]["ghost"]), "ipc open")
+                    _cabi.check(lib.dgb_ipc_open(C.byref(b), by_rank[r]["flags"]), "ipc open")
+                opened[r] = (a.value, b.value)
+            return opened[r]
+
+        ch.send = []      # per entry k: (peer ghost ptr, peer nghost, peer slot0, peer ready-flag ptr)
+        ch.ack_to = []    # per entry k: ack-flag ptr at the peer for the message RECEIVED through entry k
+        for k, peer in enumerate(plan.peers):
+            pi = by_rank[peer]
+            if pi["key"] != key:
+                raise errors.MismatchedCommunication(f"rank {peer} opened channel {pi['key']}, expected {key}")
+            np_ = len(pi["peers"])
+            j = [jj for jj in range(np_) if pi["peers"][jj] == plan.rank and pi["tags"][jj] == self.send_tags[k]]
+            jb = [jj for jj in range(np_) if pi["peers"][jj] == plan.rank and pi["send_tags"][jj] == plan.tags[k]]
+            if len(j) != 1 or len(jb) != 1:
+                raise errors.MismatchedCommunication(f"no unique partner entry at rank {peer}",
+                                                     keys=[(plan.rank, peer, self.send_tags[k])])
+            gp, fp = peer_ptrs(peer)
+            a, b = pi["recv_slots"][j[0]]
+            if b - a != len(plan.send_local[k]):
+                raise errors.MismatchedCommunication(f"message to rank {peer}: {len(plan.send_local[k])} elements sent, "
+                                                     f"{b - a} expected", keys=[(plan.rank, peer, self.send_tags[k])])
+            ch.send.append((gp, pi["nghost"], a, fp + 8 * j[0]))
+            ch.ack_to.append(fp + 8 * (np_ + jb[0]))
+        ch.keep = opened
+        dist.barrier(group=self.comm.group)
+        self._channels[key] = ch
+        return ch
+
+    def _peer_begin(self, data):
+        import math
+        from . import _cabi
+        actx, lib, plan = self.actx, self.actx.lib, self.plan
+        lead = tuple(data.shape[:-2])
+        ch = self._peer_channel(lead)
+        ch.epoch += 1
+        src = actx._contiguous(data)
+        npeers = len(plan.peers)
+        nbytes = 0
+        for k in range(npeers):
+            gp, ng, slot0, ready = ch.send[k]
+            # the neighbour has consumed what I stored there last time
+            _cabi.check(lib.dgb_flag_wait(ch.flags_ptr + 8 * (npeers + k), ch.epoch - 1, actx._st), "halo ack wait")
+            _cabi.check(lib.dgb_pack_elements_to(gp, ng, slot0, src.ptr, self._send_idx[k].ptr, ch.ncomp, src.shape[-2],
+                                                 len(plan.send_local[k]), self.ndofs, actx._st), "halo pack (peer)")
+            _cabi.check(lib.dgb_flag_signal(ready, ch.epoch, actx._st), "halo signal")
+            actx.launch_count += 3
+            nbytes += ch.ncomp * len(plan.send_local[k]) * self.ndofs * 8
+        self.bytes_per_exchange = nbytes
+        self._keep_src = src
+        return ch
+
+    def _peer_end(self, ch):
+        from . import _cabi
+        for k in range(len(self.plan.peers)):
+            _cabi.check(self.actx.lib.dgb_flag_wait(ch.flags_ptr + 8 * k, ch.epoch, self.actx._st), "halo wait")
+            self.actx.launch_count += 1
+        return ch.ghost
+
+    def _peer_release(self, ch):
+        """Everything enqueued so far has read the ghost array: let the neighbours overwrite it."""
+        from . import _cabi
+        for k in range(len(self.plan.peers)):
+            _cabi.check(self.actx.lib.dgb_flag_signal(ch.ack_to[k], ch.epoch, self.actx._st), "halo ack")
+            self.actx.launch_count += 1
+    # }}}
+
+    def close(self):
+        """Peer transport: wait until every rank is done with everybody's ghost arrays, then unmap and free
+        them.  (Call before the process group is destroyed; a no-op for the NCCL transport.)"""
+        if not self._channels:
+            return
+        from . import _cabi
+        self.actx.synchronize()
+        self.comm.dist.barrier(group=self.comm.group)
+        for ch in self._channels.values():
+            for r, (gp, fp) in ch.keep.items():
+                if r != self.plan.rank:
+                    _cabi.check(self.actx.lib.dgb_ipc_close(gp), "ipc close")
+                    _cabi.check(self.actx.lib.dgb_ipc_close(fp), "ipc close")
+        self.comm.dist.barrier(group=self.comm.group)        # nobody still maps what is freed next
+        for ch in self._channels.values():
+            ch.ghost = None
+            _cabi.check(self.actx.lib.dgb_free(ch.ghost_ptr), "free")
+            _cabi.check(self.actx.lib.dgb_free(ch.flags_ptr), "free")
+        self._channels = {}
+
+    # {{{ transport-independent begin / end / release
+    def _begin(self, data):
+        return self._peer_begin(data) if self.transport == "peer" else self.exchange_begin(data)
+
+    def _ghost_of(self, ticket):
+        return ticket.ghost if self.transport == "peer" else ticket[0]
+
+    def _end(self, ticket):
+        return self._peer_end(ticket) if self.transport == "peer" else self.exchange_end(ticket)
+
+    def _release(self, ticket):
+        if self.transport == "peer":
+            self._peer_release(ticket)
+    # }}}
+
     # {{{ partition-aware right-hand sides
     def _can_overlap(self):
         return (self.on_device and self.overlap and self.plan.nranks > 1 and bool(self.plan.peers)
@@ -192,11 +354,12 @@ class HaloExchange:
             return op.rhs(q, ghost=self.exchange(q.data))
         from . import fused
         actx, nI, E = self.actx, self.plan.n_interior, self.plan.nlocal
-        ticket = self.exchange_begin(q.data)                            # state halos in flight ...
+        t1 = self._begin(q.data)                                        # state halos in flight ...
         out = actx.empty(q.data.shape)
-        fused.euler_rhs_range(actx, op, q.data, ticket[0], out, 0, nI)  # ... under the interior elements
-        ghost = self.exchange_end(ticket)
+        fused.euler_rhs_range(actx, op, q.data, self._ghost_of(t1), out, 0, nI)   # ... under the interior elements
+        ghost = self._end(t1)
         fused.euler_rhs_range(actx, op, q.data, ghost, out, nI, E)
+        self._release(t1)
         return DOFArray(actx, out)
 
     def ns_rhs(self, op, q: DOFArray) -> DOFArray:
@@ -206,16 +369,18 @@ class HaloExchange:
         from . import fused
         actx, nI, E = self.actx, self.plan.n_interior, self.plan.nlocal
         dim = op.dim
-        t1 = self.exchange_begin(q.data)                                    # batch 1 in flight ...
+        t1 = self._begin(q.data)                                            # batch 1 in flight ...
         T = actx.empty((dim * (dim + 2) + 1,) + tuple(q.data.shape[1:]))
-        fused.ns_flux_range(actx, op, q.data, t1[0], T, 0, nI)              # ... under pass 1 of the interior
-        ghost = self.exchange_end(t1)
+        fused.ns_flux_range(actx, op, q.data, self._ghost_of(t1), T, 0, nI)  # ... under pass 1 of the interior
+        ghost = self._end(t1)
         fused.ns_flux_range(actx, op, q.data, ghost, T, nI, E)              # pass 1 next to the partition boundary
-        t2 = self.exchange_begin(T)                                         # batch 2 in flight ...
+        t2 = self._begin(T)                                                 # batch 2 in flight ...
         out = actx.empty(q.data.shape)
-        fused.ns_div_range(actx, op, q.data, T, ghost, t2[0], out, 0, nI)   # ... under pass 2 of the interior
-        tghost = self.exchange_end(t2)
+        fused.ns_div_range(actx, op, q.data, T, ghost, self._ghost_of(t2), out, 0, nI)   # ... under pass 2 of the interior
+        tghost = self._end(t2)
         fused.ns_div_range(actx, op, q.data, T, ghost, tghost, out, nI, E)
+        self._release(t1)
+        self._release(t2)
         return DOFArray(actx, out)
 
     def ns_rhs_grad_form(self, op, q: DOFArray) -> DOFArray:
@@ -224,7 +389,7 @@ class HaloExchange:
     # }}}
 
 
-def ring_slab_halo(actx, mesh, ncells_x, rank, nranks, order, lo_x=-1.0, hi_x=1.0):
+def ring_slab_halo(actx, mesh, ncells_x, rank, nranks, order, lo_x=-1.0, hi_x=1.0, transport="nccl"):
     """Weak-scaling helper for bench.py: local mesh + ``HaloExchange`` of one rank of a ring."""
     from .dg.partition import ring_slab
     from .dg.simplex import simplex_element
@@ -233,4 +398,4 @@ def ring_slab_halo(actx, mesh, ncells_x, rank, nranks, order, lo_x=-1.0, hi_x=1.
     if nranks > 1:
         local, plan = interior_first(local, plan)
     comm = TorchCommunicator() if nranks > 1 else None
-    return local, HaloExchange(actx, plan, comm, simplex_element(mesh.dim, order).Np)
+    return local, HaloExchange(actx, plan, comm, simplex_element(mesh.dim, order).Np, transport=transport)

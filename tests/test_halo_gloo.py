@@ -18,7 +18,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, mode, outq, device=False):
+def _worker(rank, world, port, mode, outq, device=False, transport="nccl"):
     sys.path.insert(0, ROOT)
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -51,30 +51,39 @@ def _worker(rank, world, port, mode, outq, device=False):
         else:
             ids = plan.global_ids
         d = DGDiscretization(actx, local, 2, ghost_elements=plan.nghost)
-        halo = HaloExchange(actx, plan, comm, d.Np)
+        halo = HaloExchange(actx, plan, comm, d.Np, transport=transport)
         assert halo._can_overlap() == device
         e = d.to_numpy(halo.euler_rhs(EulerOperator(d), d.from_numpy(q0)))
         v = d.to_numpy(halo.ns_rhs(NavierStokesOperator(d, mu=2e-2), d.from_numpy(q0)))
-        if device:      # the plain exchange-then-compute order gives the same bits
+        if device:      # the plain exchange-then-compute order gives the same bits, and so does a second evaluation
+            v3 = d.to_numpy(halo.ns_rhs(NavierStokesOperator(d, mu=2e-2), d.from_numpy(q0)))
+            assert np.array_equal(v, v3)
             halo.overlap = False
             v2 = d.to_numpy(halo.ns_rhs(NavierStokesOperator(d, mu=2e-2), d.from_numpy(q0)))
             assert np.array_equal(v, v2)
+        halo.close()
         outq.put((rank, ids, e, v, halo.messages_per_exchange, halo.bytes_per_exchange))
     finally:
         dist.destroy_process_group()
 
 
-def _run(mode, device=False):
+def _run(mode, device=False, transport="nccl"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, mode, q, device)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, mode, q, device, transport)) for r in range(2)]
     for p in procs:
         p.start()
-    res = sorted([q.get(timeout=180) for _ in procs], key=lambda t: t[0])
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    try:
+        res = sorted([q.get(timeout=180) for _ in procs], key=lambda t: t[0])
+        for p in procs:
+            p.join(timeout=60)
+            assert p.exitcode == 0
+    finally:
+        for p in procs:          # never leave a worker (and its kernels) behind
+            if p.is_alive():
+                p.kill()
+                p.join(timeout=10)
     return res
 
 
@@ -161,4 +170,42 @@ def test_two_ranks_one_gpu_overlapped_exchange():
     ref = d.to_numpy(NavierStokesOperator(d, mu=2e-2).rhs(d.from_numpy(q0)))
     for rank, perm, e, v, nmsg, nbytes in res:
         assert nmsg == 2
+        assert rel_err(v, ref[:, idx[rank][perm], :]) <= 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(600)
+def test_two_ranks_one_gpu_peer_memory_transport():
+    """transport="peer": the pack kernel of one rank stores the halo rows straight into the other rank's
+    ghost array through CUDA-IPC mapped memory (the two processes share the one GPU of the test box; on
+    a multi-GPU node the same mapping goes over NVLink), ordered by stream flags.  Same checks as above."""
+    sys.path.insert(0, ROOT)
+    from oracle.laze_port import NumpyArrayContext, rel_err
+    from paper_2512_17101_b200 import DGDiscretization, EulerOperator, NavierStokesOperator, box_mesh
+    from tests.common import random_state
+    actx = NumpyArrayContext()
+    res = _run("partition", device=True, transport="peer")
+    mesh = box_mesh((3,) * 3, (-1,) * 3, (1,) * 3, periodic=(True,) * 3)
+    d = DGDiscretization(actx, mesh, 2)
+    q0 = random_state(3, mesh.nelements, 10, seed=9)
+    ref_e = d.to_numpy(EulerOperator(d).rhs(d.from_numpy(q0)))
+    ref_v = d.to_numpy(NavierStokesOperator(d, mu=2e-2).rhs(d.from_numpy(q0)))
+    full_e, full_v = np.empty_like(ref_e), np.empty_like(ref_v)
+    for rank, ids, e, v, nmsg, nbytes in res:
+        full_e[:, ids, :], full_v[:, ids, :] = e, v
+        assert nbytes > 0
+    assert rel_err(full_e, ref_e) <= 1e-12 and rel_err(full_v, ref_v) <= 1e-12
+    res = _run("ring", device=True, transport="peer")
+    glob = box_mesh((6, 3, 3), (-1, -1, -1), (3, 1, 1), periodic=(True,) * 3)
+    base = box_mesh((3,) * 3, (-1,) * 3, (1,) * 3, periodic=(True,) * 3)
+    d = DGDiscretization(actx, glob, 2)
+    gkey = {tuple(np.round(c, 9)): e for e, c in enumerate(glob.vertices.mean(axis=1))}
+    q0 = np.empty((5, glob.nelements, 10))
+    idx = []
+    for r in range(2):
+        cent = base.vertices.mean(axis=1) + np.array([2.0 * r, 0, 0])
+        idx.append(np.array([gkey[tuple(np.round(c, 9))] for c in cent]))
+        q0[:, idx[r], :] = random_state(3, base.nelements, 10, seed=9 + r)
+    ref = d.to_numpy(NavierStokesOperator(d, mu=2e-2).rhs(d.from_numpy(q0)))
+    for rank, perm, e, v, nmsg, nbytes in res:
         assert rel_err(v, ref[:, idx[rank][perm], :]) <= 1e-12
