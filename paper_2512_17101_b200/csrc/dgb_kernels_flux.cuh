@@ -29,6 +29,15 @@
 #ifndef DGB_DIV_LAZY_EX
 #define DGB_DIV_LAZY_EX 0
 #endif
+#ifndef DGB_FLUX_EARLY_GATHER
+#define DGB_FLUX_EARLY_GATHER 1
+#endif
+#ifndef DGB_DIV_LATE_ISSUE
+#define DGB_DIV_LATE_ISSUE 0
+#endif
+#ifndef DGB_DIV_LATE_ROUNDS
+#define DGB_DIV_LATE_ROUNDS 99
+#endif
 #ifndef DGB_DIV_SPLIT_MMA
 #define DGB_DIV_SPLIT_MMA 0
 #endif
@@ -235,6 +244,38 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
   cp_async_commit();
   unsigned long long ticket = draw_ticket(counter, lane);
   DGB_WTICK_INIT
+#if DGB_FLUX_EARLY_GATHER
+  // Neighbour states of ALL face nodes of a block, issued one phase early (during the pointwise flux
+  // phase of the previous block, which is FP64 work and leaves the L1/LSU pipe to the gathers) and
+  // consumed at the top of the block's own iteration.
+  double qpE[NR][C];
+  long long cnkE[NR];
+  auto issue_gathers = [&](const FluxGeo<DIM, P, KW>& g, int nelx) {
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+      cnkE[k] = -1;
+      const int flk = S.flc[k * 32 + lane];
+      const int e = flk & 3, f = (flk >> 2) & 3, m = (flk >> 4) & 15;
+      if (flk >= 0 && e < nelx) {
+        const long long cn = g.conn[e][f];
+        cnkE[k] = cn;
+        const long long nb = DGB_CONN_NB(cn);
+        const int jp = S.fn[DGB_CONN_NF(cn) * NFP + S.perm[DGB_CONN_PERM(cn) * NFP + m]];
+        const bool in_ghost = nb >= E;
+        const long long pstride = (in_ghost ? G : E) * NP;
+        const double* pbase = (in_ghost ? ghost : q) + (in_ghost ? nb - E : nb) * NP + jp;
+#pragma unroll
+        for (int c = 0; c < C; ++c) qpE[k][c] = pbase[c * pstride];
+      }
+    }
+  };
+  if (wb < nwblocks) {
+    cp_async_wait<0>();
+    __syncwarp();
+    const long long e0 = ebeg + wb * KW;
+    issue_gathers(W.geo[0], (int)((eend - e0) < (long long)KW ? (eend - e0) : (long long)KW));
+  }
+#endif
 
   while (wb < nwblocks) {
     const long long e0 = ebeg + wb * KW;
@@ -270,6 +311,27 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
         W.Ss[col * LDSX + f * EL::NFPK + m] = 0.0;
       }
     }
+#if DGB_FLUX_EARLY_GATHER
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+      if (cnkE[k] >= 0) {
+        const int flk = S.flc[k * 32 + lane];
+        const int e = flk & 3, f = (flk >> 2) & 3, m = (flk >> 4) & 15, jm = (flk >> 8) & 255;
+        const int bc = DGB_CONN_BC(cnkE[k]);
+        double qm[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) qm[c] = Qs[(c * KW + e) * EL::LDQ + jm];
+        if (bc != 0) {
+          double nrm[DIM];
+#pragma unroll
+          for (int x = 0; x < DIM; ++x) nrm[x] = geo.nrm[x][e][f];
+          bc_state<DIM, true>(bc, qm, nrm, ph, qpE[k]);
+        }
+#pragma unroll
+        for (int c = 0; c < C; ++c) W.Ss[(c * KW + e) * LDSX + f * EL::NFPK + m] = 0.5 * (qm[c] + qpE[k][c]);
+      }
+    }
+#else
     // NBF face nodes per lane have their neighbour loads in flight together
 #pragma unroll 1
     for (int k0 = 0; k0 < NR; k0 += NBF) {
@@ -316,6 +378,7 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
         }
       }
     }
+#endif
     __syncwarp();
     DGB_WTICK(1);
 
@@ -439,6 +502,14 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
     __syncwarp();
 #endif
     DGB_WTICK(2);
+#if DGB_FLUX_EARLY_GATHER
+    if (wb_next < nwblocks) {             // rows + connectivity of the next block have landed by now
+      cp_async_wait<0>();
+      __syncwarp();
+      const long long e1 = ebeg + wb_next * KW;
+      issue_gathers(W.geo[buf ^ 1], (int)((eend - e1) < (long long)KW ? (eend - e1) : (long long)KW));
+    }
+#endif
 
     // ---- pointwise: total flux at every node, contravariant + Jacobian-scaled, and the wave speed ----
 #pragma unroll
@@ -636,7 +707,7 @@ __device__ __noinline__ VecC<DIM> boundary_operand(int bc, int f, VecC<DIM> qm_,
 // nbr = sJ F+.n+ (the own-side half lives in the folded volume matrix Wv2).  NB face nodes per
 // lane have their gathers in flight together; with LAZY the DIM-1 extra rows a neighbour's face 0
 // needs are fetched in a second wave (fewer live registers).
-template <int DIM, int P, int KW, int NB, bool LAZY>
+template <int DIM, int P, int KW, int NB, bool LAZY, int K0 = 0>
 __device__ __forceinline__ void div_face_phase(const int* flc, const int* fn, const int* perm,
                                                const Div3Small<DIM, P, KW>& M, double* Fs, const DiscDev& d,
                                                const double* __restrict__ q, const double* __restrict__ T,
@@ -649,7 +720,7 @@ __device__ __forceinline__ void div_face_phase(const int* flc, const int* fn, co
   constexpr int NPLT = DIM * C + 1;
   const long long E = d.E, G = d.G;
 #pragma unroll 1
-  for (int k0 = 0; k0 < NR; k0 += NB) {
+  for (int k0 = K0; k0 < NR; k0 += NB) {
     double qp[NB][C], nbr[NB][C], ex[NB][NEX], lam_p[NB];
     long long cnk[NB];
 #pragma unroll
@@ -764,7 +835,7 @@ struct FaceRegs {
   long long cnk[NR];
 };
 
-template <int DIM, int P, int KW>
+template <int DIM, int P, int KW, int NRE = FaceRegs<DIM, P, KW>::NR>
 __device__ __forceinline__ void face_issue(FaceRegs<DIM, P, KW>& R, const int* flc, const int* fn, const int* perm,
                                            const Div3Small<DIM, P, KW>& M, const DiscDev& d,
                                            const double* __restrict__ q, const double* __restrict__ T,
@@ -775,7 +846,7 @@ __device__ __forceinline__ void face_issue(FaceRegs<DIM, P, KW>& R, const int* f
   constexpr int NR = FaceRegs<DIM, P, KW>::NR;
   const long long E = d.E, G = d.G;
 #pragma unroll
-  for (int k = 0; k < NR; ++k) {
+  for (int k = 0; k < NRE; ++k) {
     R.cnk[k] = -1;
     const int flk = flc[k * 32 + lane];
     const int e = flk & 3, f = (flk >> 2) & 3, m = (flk >> 4) & 15;
@@ -801,7 +872,7 @@ __device__ __forceinline__ void face_issue(FaceRegs<DIM, P, KW>& R, const int* f
   }
 }
 
-template <int DIM, int P, int KW>
+template <int DIM, int P, int KW, int NRE = FaceRegs<DIM, P, KW>::NR>
 __device__ __forceinline__ void face_finish(FaceRegs<DIM, P, KW>& R, const int* flc, const int* fn, const int* perm,
                                             const Div3Small<DIM, P, KW>& M, double* Fs, const DiscDev& d,
                                             const double* __restrict__ T, const double* __restrict__ Tghost,
@@ -813,7 +884,7 @@ __device__ __forceinline__ void face_finish(FaceRegs<DIM, P, KW>& R, const int* 
   // second wave: a neighbour's face 0 is the sum of its DIM rows; fetch the other DIM-1 now
   double ex[NR][C];
 #pragma unroll
-  for (int k = 0; k < NR; ++k) {
+  for (int k = 0; k < NRE; ++k) {
     if (R.cnk[k] >= 0 && DGB_CONN_NF(R.cnk[k]) == 0 && DGB_CONN_BC(R.cnk[k]) == 0) {
       const int flk = flc[k * 32 + lane];
       const long long nb = DGB_CONN_NB(R.cnk[k]);
@@ -832,7 +903,7 @@ __device__ __forceinline__ void face_finish(FaceRegs<DIM, P, KW>& R, const int* 
     }
   }
 #pragma unroll
-  for (int k = 0; k < NR; ++k) {
+  for (int k = 0; k < NRE; ++k) {
     if (R.cnk[k] >= 0) {
       const int flk = flc[k * 32 + lane];
       const int e = flk & 3, f = (flk >> 2) & 3, jm = (flk >> 8) & 255, fm = (flk >> 16) & 255;
@@ -908,6 +979,20 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
     cp_async_commit();
   }
   unsigned long long ticket = draw_ticket(counter, lane);
+#if DGB_DIV_LATE_ISSUE
+  // The first-wave gathers of block b+1 are issued right AFTER the contraction of block b and fly
+  // during its store, the staging of the next rows and the top of the next iteration -- phases that
+  // leave the L1/LSU pipe mostly alone (issuing them before the contraction, k_nsdiv5, lost 35 %).
+  constexpr int NRL = DGB_DIV_LATE_ROUNDS < NR ? DGB_DIV_LATE_ROUNDS : NR;   // rounds gathered early
+  FaceRegs<DIM, P, KW> R;
+  if (wb < nwblocks) {
+    const long long e0 = ebeg + wb * KW;
+    cp_async_wait<1>();                  // S(0)
+    __syncwarp();
+    face_issue<DIM, P, KW, NRL>(R, S.flc, S.fn, S.perm, W.sm[0], d, q, T, ghost, Tghost,
+                                (int)((eend - e0) < (long long)KW ? (eend - e0) : (long long)KW), lane);
+  }
+#endif
 
   // cp.async groups retire in order: S(b), T(b), S(b+1), T(b+1), ...
   DGB_WTICK_INIT
@@ -947,7 +1032,13 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
     __syncwarp();
     mma_block<EL::NI, WS::NTILE>(acc, W.Fs, EL::LDF, S.Wl, EL::LDF, EL::KF / 4, lane);
 #else
+#if DGB_DIV_LATE_ISSUE
+    face_finish<DIM, P, KW, NRL>(R, S.flc, S.fn, S.perm, M, W.Fs, d, T, Tghost, ph, e0, nel, lane);
+    if (NRL < NR)                        // the remaining rounds are gathered in place
+      div_face_phase<DIM, P, KW, NB, (DGB_DIV_LAZY_EX != 0), NRL>(S.flc, S.fn, S.perm, M, W.Fs, d, q, T, ghost, Tghost, ph, e0, nel, lane);
+#else
     div_face_phase<DIM, P, KW, NB, (DGB_DIV_LAZY_EX != 0)>(S.flc, S.fn, S.perm, M, W.Fs, d, q, T, ghost, Tghost, ph, e0, nel, lane);
+#endif
     DGB_WTICK(1);
     cp_async_wait<1>();                  // T(b) has landed
     __syncwarp();
@@ -967,6 +1058,13 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
     for (int mt = 0; mt < WS::NTILE; ++mt) rj[mt] = M.rj[(mt * 8 + (lane >> 2)) % KW];
     __syncwarp();                        // all operand rows consumed: the next block may land on them
     DGB_WTICK(3);
+#if DGB_DIV_LATE_ISSUE
+    if (nel1 > 0) {
+      cp_async_wait<0>();                // S(b+1) has landed (staged a whole face phase + contraction ago)
+      __syncwarp();
+      face_issue<DIM, P, KW, NRL>(R, S.flc, S.fn, S.perm, W.sm[buf ^ 1], d, q, T, ghost, Tghost, nel1, lane);
+    }
+#endif
     if (nel1 > 0) div_stage_rows<DIM, P, KW>(W.Ts, d, T, e1, nel1, lane);
     cp_async_commit();                   // T(b+1)
 

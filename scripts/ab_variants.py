@@ -17,6 +17,10 @@ VARIANTS = {
     "timing": ["DGB_PHASE_TIMING=1"],                 # scripts/phase_timing_flux.py
     "experimental": ["DGB_EXPERIMENTAL=1"],           # + DGB_DIV_KERNEL=4|5|6 at run time
     "trecord": ["DGB_T_RECORD=1"],                    # record-major flux planes (experiment: rhs only)
+    "div_late": ["DGB_DIV_LATE_ISSUE=1"],
+    "div_late1": ["DGB_DIV_LATE_ISSUE=1", "DGB_DIV_LATE_ROUNDS=1"],
+    "div_late2": ["DGB_DIV_LATE_ISSUE=1", "DGB_DIV_LATE_ROUNDS=2"],
+    "flux_noearly": ["DGB_FLUX_EARLY_GATHER=0"],
     "div_split": ["DGB_DIV_SPLIT_MMA=1"],
     "euler_w8": ["DGB_EULER_WARPS=8"],
     "flux_nb2": ["DGB_FLUX_NB=2"],
