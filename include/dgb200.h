@@ -204,6 +204,11 @@ int dgb_copy_scatter(void* out_dev, int out_dtype, const int64_t* out_strides, c
  * every index is range-checked, DGB_ERR_OUT_OF_BOUNDS otherwise (frontend.py:121-136) */
 int dgb_take(void* out_dev, const void* a_dev, int dtype, const int64_t* idx_dev,
              int64_t outer, int64_t extent, int64_t inner, int64_t nidx, void* stream);
+/* the same gather for use inside a captured CUDA graph (CompiledFunction(graph=True)): no host
+ * synchronisation; an out-of-range index sets *err_dev != 0, which the context checks at its next
+ * synchronisation point */
+int dgb_take_deferred(void* out_dev, const void* a_dev, int dtype, const int64_t* idx_dev,
+                      int64_t outer, int64_t extent, int64_t inner, int64_t nidx, int* err_dev, void* stream);
 /* einsum with up to 3 FP64 operands: loop extents `ext[nletters]` (output letters first, then
  * summed letters, ascending accumulation like expr.py:344-364), per-operand strides per letter */
 int dgb_einsum(double* out_dev, int nops, const double* const* ops_dev, const int64_t* op_strides,

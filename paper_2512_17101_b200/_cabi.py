@@ -23,7 +23,7 @@ SYMBOLS = [
     "dgb_euler_rhs_range", "dgb_ns_flux_range", "dgb_ns_div_range",
     "dgb_pack_elements", "dgb_pack_elements_to", "dgb_ipc_alloc", "dgb_ipc_open", "dgb_ipc_close",
     "dgb_flag_signal", "dgb_flag_wait",
-    "dgb_ew_binary", "dgb_ew_unary", "dgb_ew_where", "dgb_copy_strided", "dgb_copy_scatter", "dgb_take",
+    "dgb_ew_binary", "dgb_ew_unary", "dgb_ew_where", "dgb_copy_strided", "dgb_copy_scatter", "dgb_take", "dgb_take_deferred",
     "dgb_einsum",
 ]
 
@@ -97,6 +97,7 @@ def load():
     lib.dgb_copy_strided.argtypes = [dp, C.c_int, dp, C.c_int, vp, C.c_int, vp, vp]
     lib.dgb_copy_scatter.argtypes = [dp, C.c_int, vp, dp, C.c_int, vp, C.c_int, vp, vp]
     lib.dgb_take.argtypes = [dp, dp, C.c_int, dp, i64, i64, i64, i64, vp]
+    lib.dgb_take_deferred.argtypes = [dp, dp, C.c_int, dp, i64, i64, i64, i64, vp, vp]
     lib.dgb_einsum.argtypes = [dp, C.c_int, vp, vp, C.c_int, C.c_int, vp, vp]
     _LIB = lib
     return lib

@@ -530,6 +530,11 @@ class B200ArrayContext:
         node = self._contiguous(node)
         return DeviceArray(self, node.t.view(newshape))
 
+    def _copy_d2d(self, dst: DeviceArray, src: DeviceArray):
+        if dst.size:
+            nbytes = dst.size * _NP_OF[dst.dtype_code].itemsize
+            _cabi.check(self.lib.dgb_memcpy_d2d(C.c_void_p(dst.ptr), C.c_void_p(src.ptr), nbytes, self._st), "d2d")
+
     def _scatter_into(self, out: DeviceArray, view, src: DeviceArray):
         """Copy ``src`` into the (strided) torch view ``view`` of ``out``."""
         if not src.size:
@@ -591,10 +596,31 @@ class B200ArrayContext:
         outer = math.prod(shape[:axis])
         inner = math.prod(shape[axis + 1:])
         out = self.empty(shape[:axis] + idx.shape + shape[axis + 1:], arr.dtype_code)
-        _cabi.check(self.lib.dgb_take(out.ptr, arr.ptr, arr.dtype_code, idx.ptr, outer, shape[axis], inner,
-                                      idx.size, self._st), "index array")
+        if getattr(self, "_capturing", False):
+            # inside a CUDA-graph capture: no host synchronisation; a bad index raises the context's
+            # device-side flag, checked after every replay (the eager warm-up run has range-checked
+            # this very gather already)
+            _cabi.check(self.lib.dgb_take_deferred(out.ptr, arr.ptr, arr.dtype_code, idx.ptr, outer, shape[axis], inner,
+                                                   idx.size, C.c_void_p(self._err_flag().data_ptr()), self._st),
+                        "index array")
+        else:
+            _cabi.check(self.lib.dgb_take(out.ptr, arr.ptr, arr.dtype_code, idx.ptr, outer, shape[axis], inner,
+                                          idx.size, self._st), "index array")
         self.launch_count += 1
         return out
+
+    def _err_flag(self):
+        if getattr(self, "_err", None) is None:
+            torch = _torch()
+            with torch.cuda.stream(self.stream):
+                self._err = torch.zeros(1, dtype=torch.int32, device=self.device)
+        return self._err
+
+    def check_deferred_errors(self):
+        """Raise ``OutOfBoundsIndex`` if a gather inside a replayed graph left its range (synchronises)."""
+        if getattr(self, "_err", None) is not None and int(self._err.item()) != 0:
+            self._err.zero_()
+            raise errors.OutOfBoundsIndex("index array leaves [0, extent) (detected in a captured graph)")
 
     def _einsum(self, subscripts, args):
         nodes = [self._node_of(a) for a in args]
@@ -663,8 +689,14 @@ class B200ArrayContext:
     # }}}
 
     # {{{ compile / outline (frontend.py:485-519, 606-679)
-    def compile(self, f: Callable) -> "CompiledFunction":
-        return CompiledFunction(self, f)
+    def compile(self, f: Callable, graph: bool = False) -> "CompiledFunction":
+        """``graph=True``: per signature, the first call runs ``f`` eagerly (validating it and warming
+        every cache), the second captures it into ONE CUDA graph over static argument buffers, and
+        later calls copy the arguments in and replay the graph -- the B200 counterpart of the
+        reference's trace-once / execute-many ``CompiledFunction`` (frontend.py:606-679) for glue
+        that is not hand-fused: same kernels, no per-op Python dispatch and no launch gaps.
+        Only for functions of device arrays whose control flow does not depend on array values."""
+        return CompiledFunction(self, f, graph=graph)
 
     def outline(self, f: Callable) -> Callable:
         """Named call boundary.  DG functions known to ``fused.FUSED`` run as fused kernels; any
@@ -703,12 +735,69 @@ class CompiledFunction:
     the function body runs on the stream.  ndarray arguments are uploaded and ndarray results
     returned; ``DeviceArray`` arguments stay on the device and so do the results."""
 
-    def __init__(self, actx, f):
+    def __init__(self, actx, f, graph: bool = False):
         self.actx, self.f = actx, f
         self.signatures: set = set()
         self.trace_count = 0
         self.execution_count = 0
         self.cache_hits = 0
+        self.use_graph = graph
+        self._graphs: dict = {}          # signature -> (CUDAGraph, static inputs, static outputs)
+        self._seen: dict = {}            # signature -> number of eager calls so far
+        self.replays = 0
+
+    # {{{ CUDA-graph path
+    def _graph_call(self, sig, call_args):
+        torch = _torch()
+        actx = self.actx
+        names = list(call_args)
+        if any(hasattr(v, "data") and not isinstance(v, DeviceArray) for v in call_args.values()):
+            return None                   # containers (DOFArray ...) are not flattened here: eager
+        dev = dict(call_args)
+        # scalars are arguments, not baked constants (frontend.py:665-668): a graph is keyed on their values
+        sig = (sig, tuple(v for v in call_args.values() if not isinstance(v, DeviceArray)))
+        entry = self._graphs.get(sig)
+        if entry is None:
+            if self._seen.get(sig, 0) < 1:          # first call of this signature: plain eager run
+                self._seen[sig] = self._seen.get(sig, 0) + 1
+                return None
+            static = {n: (actx.empty(v.shape, v.dtype_code) if isinstance(v, DeviceArray) else v) for n, v in dev.items()}
+            for n in names:
+                if isinstance(dev[n], DeviceArray):
+                    actx._copy_d2d(static[n], actx._contiguous(dev[n]))
+            actx.synchronize()
+            g = torch.cuda.CUDAGraph()
+            cap = torch.cuda.Stream(device=actx.device)
+            cap.wait_stream(actx.stream)
+            home, actx.stream = actx.stream, cap
+            actx._capturing = True
+            try:
+                with torch.cuda.graph(g, stream=cap):
+                    out = self.f(**static)
+            finally:
+                actx._capturing = False
+                actx.stream = home
+            home.wait_stream(cap)
+            entry = (g, static, out)
+            self._graphs[sig] = entry
+        g, static, out = entry
+        for n in names:
+            if isinstance(dev[n], DeviceArray):
+                actx._copy_d2d(static[n], actx._contiguous(dev[n]))
+        with torch.cuda.stream(actx.stream):
+            g.replay()
+        self.replays += 1
+
+        def fresh(a):                     # results live in the graph's pool: hand out copies
+            if isinstance(a, DeviceArray):
+                c = actx.empty(a.shape, a.dtype_code)
+                actx._copy_d2d(c, a)
+                return c
+            return a
+        if isinstance(out, dict):
+            return {k: fresh(v) for k, v in out.items()}
+        return fresh(out)
+    # }}}
 
     def __call__(self, *args, **kwargs):
         bound = inspect.signature(self.f).bind(*args, **kwargs)
@@ -738,6 +827,10 @@ class CompiledFunction:
             self.signatures.add(sig)
             self.trace_count += 1
         self.execution_count += 1
+        if self.use_graph and on_device and not kwargs:
+            res = self._graph_call(sig, call_args)
+            if res is not None:
+                return res
         out = self.f(**call_args)
         if on_device:
             return out

@@ -306,6 +306,24 @@ int dgb_take(void* out, const void* a, int dtype, const int64_t* idx, int64_t ou
   return h ? DGB_ERR_OUT_OF_BOUNDS : DGB_OK;
 }
 
+int dgb_take_deferred(void* out, const void* a, int dtype, const int64_t* idx, int64_t outer, int64_t extent,
+                      int64_t inner, int64_t nidx, int* err_dev, void* stream) {
+  // same gather, but an out-of-range index only raises *err_dev (checked by the caller at its next
+  // synchronisation point): no allocation, no host synchronisation, capturable in a CUDA graph
+  const long long total = outer * nidx * inner;
+  if (total == 0) return DGB_OK;
+  if (!err_dev) return DGB_ERR_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == DGB_BOOL)
+    k_take<unsigned char><<<grid_for(total), 256, 0, st>>>((unsigned char*)out, (const unsigned char*)a,
+                                                           (const long long*)idx, outer, extent, inner, nidx, err_dev);
+  else
+    k_take<long long><<<grid_for(total), 256, 0, st>>>((long long*)out, (const long long*)a, (const long long*)idx,
+                                                       outer, extent, inner, nidx, err_dev);
+  DGB_CHECK_LAUNCH();
+  return DGB_OK;
+}
+
 int dgb_einsum(double* out, int nops, const double* const* ops, const int64_t* op_strides, int nout, int nletters,
                const int64_t* ext, void* stream) {
   if (nops < 1 || nops > 3 || nletters > 8 || nout > nletters) return DGB_ERR_INVALID;

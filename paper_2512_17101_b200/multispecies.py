@@ -202,7 +202,10 @@ class MultispeciesOperator:
     Boundaries: periodic, or far-field (every tagged boundary face takes ``farfield`` as exterior state)."""
 
     def __init__(self, dcoll: DGDiscretization, mixture: Mixture | None = None, mu=1e-2, kappa=2e-2, diffusivity=1e-2,
-                 farfield=None):
+                 farfield=None, graph: bool | None = None):
+        """``graph`` (device contexts only; default on): evaluate the right-hand side through
+        ``actx.compile(f, graph=True)`` -- first call eager, second call captured into one CUDA graph,
+        later calls replayed -- instead of ~800 separately dispatched kernels."""
         self.dcoll, self.actx, self.dim = dcoll, dcoll.actx, dcoll.dim
         self.mix = mixture or Mixture()
         self.ncomp = self.dim + 2 + self.mix.ns
@@ -215,6 +218,10 @@ class MultispeciesOperator:
         f.actx = self.actx
         f.dg_dim = self.dim
         self._f = self.actx.outline(f)
+        if graph is None:
+            graph = hasattr(self.actx, "lib")
+        if graph:
+            self._f = self.actx.compile(self._f, graph=True)
 
     def state_from_primitive(self, rho, vel, T, Y):
         """Conserved state (any broadcastable shapes) from density, velocity, temperature, mass fractions."""
