@@ -17,6 +17,9 @@ VARIANTS = {
     "timing": ["DGB_PHASE_TIMING=1"],                 # scripts/phase_timing_flux.py
     "experimental": ["DGB_EXPERIMENTAL=1"],           # + DGB_DIV_KERNEL=4|5|6 at run time
     "trecord": ["DGB_T_RECORD=1"],                    # record-major flux planes (experiment: rhs only)
+    "pf600": ["DGB_L2_PREFETCH_BLOCKS=600"],
+    "pf2400": ["DGB_L2_PREFETCH_BLOCKS=2400"],
+    "pf8000": ["DGB_L2_PREFETCH_BLOCKS=8000"],
     "div_late": ["DGB_DIV_LATE_ISSUE=1"],
     "div_late1": ["DGB_DIV_LATE_ISSUE=1", "DGB_DIV_LATE_ROUNDS=1"],
     "div_late2": ["DGB_DIV_LATE_ISSUE=1", "DGB_DIV_LATE_ROUNDS=2"],
