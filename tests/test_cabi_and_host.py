@@ -94,3 +94,23 @@ def test_cost_report_matches_measured_dram_traffic():
     per_dof = sum(k.bytes_field_read + k.bytes_field_written for k in ns) / (E * 20)
     assert per_dof == 376.0          # 360 B/DOF of SURVEY §8d + the wave-speed plane written and read once
     assert sum(k.bytes_field_read + k.bytes_field_written for k in cost_report(3, 3, E, "ns", "grad")) / (E * 20) == 360.0
+
+
+def test_bench_reference_arm_contract():
+    """`bench.py --impl reference` (the CPU arm the driver runs first) prints one JSON line with the
+    contract's keys; tiny sample so the CPU suite stays fast."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "0", "--cpu-n", "3"], capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    line = json.loads(res.stdout.strip().splitlines()[-1])
+    for key in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert key in line, key
+    assert line["impl"] == "reference" and line["unit"] == "GDOF/s" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
