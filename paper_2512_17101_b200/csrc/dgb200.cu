@@ -123,11 +123,15 @@ __global__ void k_flag_signal(unsigned long long* flag, unsigned long long value
 }
 
 __global__ void k_flag_wait(const unsigned long long* flag, unsigned long long value) {
+  // bounded: a neighbour that never signals (crashed rank) must not wedge the GPU -- after ~20 s of
+  // polling the kernel traps and the stream reports an error instead of hanging
   unsigned long long v;
-  do {
+  for (long long it = 0;; ++it) {
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
-    if (v < value) __nanosleep(200);
-  } while (v < value);
+    if (v >= value) return;
+    if (it > 40000000LL) __trap();
+    __nanosleep(500);
+  }
 }
 
 }  // namespace
