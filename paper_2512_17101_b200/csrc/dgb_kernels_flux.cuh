@@ -1142,9 +1142,8 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
 // state replaces q+.
 // ------------------------------------------------------------------------------------------
 template <int DIM, int P, int KW>
-struct alignas(16) Euler4Small {
+struct alignas(16) Euler4Geo {
   using EL = ElemT<DIM, P>;
-  double Qs[EL::C * KW * EL::NP];
   double drdx[DIM * DIM][KW];
   double nrm[DIM][KW][EL::NF];
   double fsc[KW][EL::NF];
@@ -1159,7 +1158,8 @@ struct alignas(16) Euler4Warp {
   double Ts[NCOL * EL::LDV];
   double Fs[NCOL * EL::LDF];
   double Lam[KW * EL::NP];
-  Euler4Small<DIM, P, KW> sm[2];
+  double Qs[EL::C * KW * EL::NP];        // single buffer: the next block's rows are staged once the face phase has read these
+  Euler4Geo<DIM, P, KW> geo[2];
 };
 
 template <int DIM, int P, int KW, int NWARPS>
@@ -1174,7 +1174,7 @@ struct Euler4Smem {
 };
 
 template <int DIM, int P, int KW>
-__device__ __forceinline__ void euler4_stage(Euler4Small<DIM, P, KW>& M, const DiscDev& d, const double* q,
+__device__ __forceinline__ void euler4_stage(double* Qs, Euler4Geo<DIM, P, KW>& M, const DiscDev& d, const double* q,
                                              long long e0, int nel, int lane) {
   using EL = ElemT<DIM, P>;
   constexpr int C = EL::C, NP = EL::NP, NF = EL::NF;
@@ -1185,7 +1185,7 @@ __device__ __forceinline__ void euler4_stage(Euler4Small<DIM, P, KW>& M, const D
     const int t = t0 + lane;
     const int e = t / NPC, j = CH * (t - e * NPC);
     if (t < KW * NPC && e < nel) {
-      double* qs = M.Qs + e * NP + j;
+      double* qs = Qs + e * NP + j;
       const double* qg = q + (e0 + e) * NP + j;
 #pragma unroll
       for (int c = 0; c < C; ++c) {
@@ -1242,7 +1242,7 @@ k_euler4(DiscDev d, const double* __restrict__ q, const double* __restrict__ gho
   const long long wstride = (long long)gridDim.x * NWARPS;
   long long wb = (long long)blockIdx.x * NWARPS + warp;
   if (wb >= nwblocks) return;
-  euler4_stage<DIM, P, KW>(W.sm[0], d, q, ebeg + wb * KW, nel_of(wb), lane);
+  euler4_stage<DIM, P, KW>(W.Qs, W.geo[0], d, q, ebeg + wb * KW, nel_of(wb), lane);
   cp_async_commit();
   unsigned long long ticket = draw_ticket(counter, lane);
 
@@ -1252,20 +1252,10 @@ k_euler4(DiscDev d, const double* __restrict__ q, const double* __restrict__ gho
     const int nel = nel_of(wb);
     const long long wb_next = ticket_block(ticket, wstride);
     const int nel1 = nel_of(wb_next);
-    if (nel1 > 0) euler4_stage<DIM, P, KW>(W.sm[buf ^ 1], d, q, ebeg + wb_next * KW, nel1, lane);
-    cp_async_commit();
     ticket = draw_ticket(counter, lane);
-    if (DGB_L2_PREFETCH_BLOCKS > 0) {
-      const long long wbp = wb_next + DGB_L2_PREFETCH_BLOCKS;
-      if (wbp < nwblocks) {
-        const long long ep = ebeg + wbp * KW;
-        prefetch_block_rows<NP, KW>(q, C, E * NP, q, 0, 0, ep,
-                                    (int)((eend - ep) < (long long)KW ? (eend - ep) : (long long)KW), lane);
-      }
-    }
-    cp_async_wait<1>();                  // this block's rows + geometry have landed
+    cp_async_wait<0>();                  // this block's rows + geometry have landed (staged during the previous contraction)
     __syncwarp();
-    const Euler4Small<DIM, P, KW>& M = W.sm[buf];
+    const Euler4Geo<DIM, P, KW>& M = W.geo[buf];
 
     // ---- neighbour states of every face node: in flight during the volume phase --------------
     double qp[NR][C];
@@ -1296,7 +1286,7 @@ k_euler4(DiscDev d, const double* __restrict__ q, const double* __restrict__ gho
       if (n < KW * NP && e < nel) {
         double qq[C];
 #pragma unroll
-        for (int c = 0; c < C; ++c) qq[c] = M.Qs[(c * KW + e) * NP + j];
+        for (int c = 0; c < C; ++c) qq[c] = W.Qs[(c * KW + e) * NP + j];
         Prim<DIM> s;
         make_prim<DIM>(qq, ph.gamma, s);
         double F[DIM][C];
@@ -1328,7 +1318,7 @@ k_euler4(DiscDev d, const double* __restrict__ q, const double* __restrict__ gho
         const int bc = DGB_CONN_BC(cnk[k]);
         double qm[C], nrm[DIM];
 #pragma unroll
-        for (int c = 0; c < C; ++c) qm[c] = M.Qs[(c * KW + e) * NP + jm];
+        for (int c = 0; c < C; ++c) qm[c] = W.Qs[(c * KW + e) * NP + jm];
 #pragma unroll
         for (int x = 0; x < DIM; ++x) nrm[x] = M.nrm[x][e][f];
         if (bc != 0) bc_state<DIM, false>(bc, qm, nrm, ph, qp[k]);
@@ -1343,7 +1333,19 @@ k_euler4(DiscDev d, const double* __restrict__ q, const double* __restrict__ gho
         for (int c = 0; c < C; ++c) fsrow[c * (KW * EL::LDF)] = -0.5 * fs_ * (fnp[c] + pen * (qm[c] - qp[k][c]));
       }
     }
-    __syncwarp();
+    __syncwarp();                        // Qs and this block's geometry are no longer needed ...
+
+    // ... so the next block's rows start their trip now and land during the contraction
+    if (nel1 > 0) euler4_stage<DIM, P, KW>(W.Qs, W.geo[buf ^ 1], d, q, ebeg + wb_next * KW, nel1, lane);
+    cp_async_commit();
+    if (DGB_L2_PREFETCH_BLOCKS > 0) {
+      const long long wbp = wb_next + DGB_L2_PREFETCH_BLOCKS;
+      if (wbp < nwblocks) {
+        const long long epf = ebeg + wbp * KW;
+        prefetch_block_rows<NP, KW>(q, C, E * NP, q, 0, 0, epf,
+                                    (int)((eend - epf) < (long long)KW ? (eend - epf) : (long long)KW), lane);
+      }
+    }
 
     // ---- tensor-core contraction + (RK-fused) store ----------------------------------------------
     double acc[WS::NTILE][EL::NI][2];
