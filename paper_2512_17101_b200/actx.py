@@ -264,6 +264,9 @@ class B200ArrayContext:
 
     def synchronize(self):
         _cabi.check(self.lib.dgb_stream_sync(self._st), "synchronize")
+        if getattr(self, "_err", None) is not None and getattr(self, "_err_armed", False):
+            self._err_armed = False
+            self.check_deferred_errors()      # gathers inside replayed graphs report here (to_numpy / freeze call this)
 
     def pinned_empty(self, shape, dtype=np.float64) -> np.ndarray:
         """Page-locked host staging buffer as a NumPy array (async H2D / D2H copies)."""
@@ -787,6 +790,8 @@ class CompiledFunction:
         with torch.cuda.stream(actx.stream):
             g.replay()
         self.replays += 1
+        if getattr(actx, "_err", None) is not None:
+            actx._err_armed = True        # the next synchronisation point looks at the device-side error flag
 
         def fresh(a):                     # results live in the graph's pool: hand out copies
             if isinstance(a, DeviceArray):

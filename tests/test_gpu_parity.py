@@ -318,3 +318,36 @@ def test_device_rk4_driver(gpu, Op, kw, dim, order, n):
     assert np.array_equal(got_g, got_e)
     assert rel_err(got_g, ref) <= TOL_RK, rel_err(got_g, ref)
     assert gpu.launch_count > launches0
+
+
+def test_graph_compiled_function_semantics(gpu):
+    """actx.compile(f, graph=True): scalars stay arguments (a new value is a new graph, never a stale
+    constant), shapes key the cache, results of consecutive calls do not alias, and an out-of-range
+    gather inside a replayed graph is reported at the next check."""
+    from paper_2512_17101_b200 import errors
+
+    def f(x, a, idx):
+        y = gpu.np.sqrt(x * x + a)
+        return {"y": y, "picked": y[idx] * 2.0}
+
+    cf = gpu.compile(f, graph=True)
+    rng = np.random.default_rng(0)
+    idx_h = np.array([3, 0, 7, 7, 2], dtype=np.int64)
+    idx = gpu.from_numpy(idx_h)
+    outs = []
+    for call, a in enumerate([1.5, 1.5, 1.5, 2.5, 2.5, 2.5]):
+        xh = rng.standard_normal(11)
+        out = cf(gpu.from_numpy(xh), a, idx)
+        ref = np.sqrt(xh * xh + a)
+        assert np.array_equal(gpu.to_numpy(out["y"]), ref), (call, a)
+        assert np.array_equal(gpu.to_numpy(out["picked"]), ref[idx_h] * 2.0)
+        outs.append((out["y"], ref))
+    for y, ref in outs:                                   # earlier results were not overwritten by later replays
+        assert np.array_equal(gpu.to_numpy(y), ref)
+    assert cf.replays == 4 and len(cf._graphs) == 2       # per scalar value: eager, capture + replay, replay
+    bad = gpu.from_numpy(np.array([3, 0, 11, 7, 2], dtype=np.int64))
+    out = cf(gpu.from_numpy(rng.standard_normal(11)), 1.5, bad)       # same signature: replayed, no host check ...
+    with pytest.raises(errors.OutOfBoundsIndex):          # ... the device-side flag is raised at the next synchronisation
+        gpu.to_numpy(out["picked"])
+    ok = cf(gpu.from_numpy(np.ones(11)), 1.5, idx)        # the flag is cleared once reported
+    assert np.array_equal(gpu.to_numpy(ok["y"]), np.sqrt(np.ones(11) + 1.5))
