@@ -190,17 +190,32 @@ __global__ void k_einsum(double* __restrict__ out, const double* a, const double
       o0 += i * d.stride[0][k]; o1 += i * d.stride[1][k]; o2 += i * d.stride[2][k];
     }
     double acc = 0.0;
-    // ascending, outer-letter-first accumulation (expr.py:344-364)
+    // ascending, outer-letter-first accumulation (expr.py:344-364).  The reduced letters are walked
+    // with an odometer (last letter fastest) and incremental offsets -- the same order of terms as
+    // decoding r by division, without two 64-bit divisions per letter and term.
+    int idx[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) idx[k] = 0;
+    long long p0 = o0, p1 = o1, p2 = o2;
     for (long long r = 0; r < nred_total; ++r) {
-      long long p0 = o0, p1 = o1, p2 = o2, rr = r;
-      for (int k = d.nletters - 1; k >= d.nout; --k) {
-        const long long i = rr % d.ext[k]; rr /= d.ext[k];
-        p0 += i * d.stride[0][k]; p1 += i * d.stride[1][k]; p2 += i * d.stride[2][k];
-      }
       double v = a[p0];
       if (d.nops > 1) v *= b[p1];
       if (d.nops > 2) v *= c[p2];
       acc += v;
+      bool carry = true;
+#pragma unroll
+      for (int k = 7; k >= 0; --k) {
+        if (carry && k >= d.nout && k < d.nletters) {
+          ++idx[k];
+          p0 += d.stride[0][k]; p1 += d.stride[1][k]; p2 += d.stride[2][k];
+          if (idx[k] < d.ext[k]) {
+            carry = false;
+          } else {
+            p0 -= d.ext[k] * d.stride[0][k]; p1 -= d.ext[k] * d.stride[1][k]; p2 -= d.ext[k] * d.stride[2][k];
+            idx[k] = 0;
+          }
+        }
+      }
     }
     out[n] = acc;
   }
