@@ -14,6 +14,7 @@ thread_local std::string g_err2;
 
 struct Dims {
   int rank;
+  int ma, mb, mc;          // per operand: 0 = general strides, 1 = dense (offset == flat index), 2 = scalar (offset 0)
   long long ext[8];
   long long sa[8], sb[8], sc[8];
 };
@@ -41,6 +42,12 @@ __device__ __forceinline__ void st_any(void* p, int dt, long long off, double fv
 }
 
 __device__ __forceinline__ void offsets(const Dims& d, long long n, long long& oa, long long& ob, long long& oc) {
+  // most elementwise ops of an array program combine same-shape dense arrays and scalars: no index decoding
+  if (d.ma && d.mb && d.mc) {
+    oa = d.ma == 1 ? n : 0; ob = d.mb == 1 ? n : 0; oc = d.mc == 1 ? n : 0;
+    return;
+  }
+  const long long n0 = n;
   oa = ob = oc = 0;
 #pragma unroll 1
   for (int k = d.rank - 1; k >= 0; --k) {
@@ -48,6 +55,9 @@ __device__ __forceinline__ void offsets(const Dims& d, long long n, long long& o
     n /= d.ext[k];
     oa += i * d.sa[k]; ob += i * d.sb[k]; oc += i * d.sc[k];
   }
+  if (d.ma) oa = d.ma == 1 ? n0 : 0;
+  if (d.mb) ob = d.mb == 1 ? n0 : 0;
+  if (d.mc) oc = d.mc == 1 ? n0 : 0;
 }
 
 __device__ __forceinline__ long long floordiv_i(long long a, long long b) {
@@ -239,6 +249,22 @@ int fill_dims(Dims& d, int rank, const int64_t* shape, const int64_t* sa, const 
     if (k < rank) t *= shape[k];
   }
   *total = t;
+  // classify each operand: dense (strides of a row-major array of this shape; extent-1 axes are free),
+  // scalar (all strides 0), or general
+  auto mode = [&](const long long* st, bool present) -> int {
+    if (!present) return 2;
+    bool dense = true, scalar = true;
+    long long run = 1;
+    for (int k = rank - 1; k >= 0; --k) {
+      if (d.ext[k] != 1) {
+        if (st[k] != run) dense = false;
+        if (st[k] != 0) scalar = false;
+      }
+      run *= d.ext[k];
+    }
+    return dense ? 1 : (scalar ? 2 : 0);
+  };
+  d.ma = mode(d.sa, sa != nullptr); d.mb = mode(d.sb, sb != nullptr); d.mc = mode(d.sc, sc != nullptr);
   return DGB_OK;
 }
 
