@@ -383,6 +383,11 @@ class HaloExchange:
         self._release(t2)
         return DOFArray(actx, out)
 
+    def ms_rhs(self, op, q: DOFArray) -> DOFArray:
+        """Multispecies operator (array program on the generic ops): state halos, then flux-plane halos."""
+        ghost = self.exchange(q.data)
+        return op.rhs(q, ghost=ghost, halo_fn=lambda FL: self.exchange(FL.data))
+
     def ns_rhs_grad_form(self, op, q: DOFArray) -> DOFArray:
         ghost = self.exchange(q.data)
         return op.rhs_grad_form(q, ghost=ghost, halo_fn=lambda gq: self.exchange(gq.data))

@@ -24,7 +24,8 @@ Model
   release is in ``h0``; total energy needs no source);
 * discretisation = the single-species scheme: weak-form nodal DG, Rusanov inviscid flux with the
   mixture wave speed, BR1 (gradient of the conserved variables AND of ``T``, central flux; viscous
-  flux central), periodic or prescribed far-field exterior state.
+  flux central), periodic or prescribed far-field exterior state; partitioned meshes through ghost
+  arrays (``rhs(q, ghost, halo_fn)``, ``HaloExchange.ms_rhs``).
 """
 from __future__ import annotations
 
@@ -121,80 +122,101 @@ def _viscous(actx, mix, q, gq, gT, prim, transport, dim):
     return flux
 
 
-def _make_ms_rhs(dim, mix, with_ghost):
+def _ms_pass1(actx, mix, dim, q, ghost, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, transport):
+    """BR1 gradient of [q, T] (central flux), then the total flux at every node.  Returns the planes
+    ``[F_x[c] (x-major, dim*C planes), lam]``, shape ``(dim*C + 1, E, Np)`` -- what pass 2 gathers and, on a
+    partitioned mesh, what the second halo exchange carries."""
+    C, E, Np = q.shape
+    Nf = dim + 1
+    Nfp = lift.shape[1] // Nf
+    tr = [transport[k] for k in range(3)]
+    nrm = [normals[x] for x in range(dim)]
+    is_bnd = actx.np.not_equal(bc_kind, BC_NONE)
+    qc = [q[c] for c in range(C)]
+    finv, lam, prim = _inviscid(actx, mix, qc, dim)
+    W = actx.np.concatenate([q, actx.np.reshape(prim[2], (1, E, Np))])                  # (C+1, E, Np)
+    Wg = None
+    if ghost is not None:
+        gprim = _thermo(actx, mix, [ghost[c] for c in range(C)], dim)
+        Wg = actx.np.concatenate([ghost, actx.np.reshape(gprim[2], (1,) + tuple(ghost.shape[1:]))])
+    vol = actx.np.einsum("rij,rxe,cej->xcei", Sw, drdx, W)
+    wm, wp = _traces(actx, W, Wg, vmap_m, vmap_p, C + 1, E, Np, Nf, Nfp)
+    far = [qfar[c] for c in range(C)]
+    far_T = _thermo(actx, mix, far, dim)[2]
+    ext = far + [far_T]
+    wpl = [actx.np.where(is_bnd, ext[c], wp[c]) for c in range(C + 1)]
+    wstar = [fscale * (0.5 * (wm[c] + wpl[c])) for c in range(C + 1)]
+    fs = actx.np.stack([actx.np.stack([nrm[x] * wstar[c] for c in range(C + 1)]) for x in range(dim)])
+    gW = actx.np.einsum("if,xcef->xcei", lift, actx.np.reshape(fs, (dim, C + 1, E, Nf * Nfp))) - vol
+    gq = [[gW[x][c] for c in range(C)] for x in range(dim)]
+    gT = [gW[x][C] for x in range(dim)]
+    fvis = _viscous(actx, mix, qc, gq, gT, prim, tr, dim)
+    ftot = [[finv[x][c] if fvis[x][c] is None else finv[x][c] - fvis[x][c] for c in range(C)] for x in range(dim)]
+    fstack = actx.np.stack([actx.np.stack(fx) for fx in ftot])
+    return actx.np.concatenate([actx.np.reshape(fstack, (dim * C, E, Np)), actx.np.reshape(lam, (1, E, Np))])
+
+
+def _ms_pass2(actx, mix, dim, q, FL, ghost, gFL, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar):
+    """Divergence of the stored flux, Rusanov / central numerical flux from gathered neighbour planes,
+    Arrhenius source."""
+    C, E, Np = q.shape
+    Nf = dim + 1
+    Nfp = lift.shape[1] // Nf
     ns = mix.ns
+    nrm = [normals[x] for x in range(dim)]
+    is_bnd = actx.np.not_equal(bc_kind, BC_NONE)
+    far = [qfar[c] for c in range(C)]
+    volf = actx.np.einsum("rij,rxe,xcej->cei", Sw, drdx, actx.np.reshape(FL[0:dim * C], (dim, C, E, Np)))
+    planes = actx.np.concatenate([q, FL])                                               # q, F, lam
+    gplanes = None if ghost is None else actx.np.concatenate([ghost, gFL])
+    L = C + dim * C + 1
+    tm, tp = _traces(actx, planes, gplanes, vmap_m, vmap_p, L, E, Np, Nf, Nfp)
+    qm = [tm[c] for c in range(C)]
+    qp = [actx.np.where(is_bnd, far[c], tp[c]) for c in range(C)]
+    # exterior flux on boundary faces: inviscid flux of the far-field state, viscous flux of the interior
+    ffar, lam_far, _ = _inviscid(actx, mix, far, dim)
+    fmi, _, _ = _inviscid(actx, mix, qm, dim)
+    fstar = []
+    lam_p = actx.np.where(is_bnd, lam_far, tp[L - 1])
+    lmax = actx.np.maximum(tm[L - 1], lam_p)
+    for c in range(C):
+        fnm = nrm[0] * tm[C + c]
+        fnp = nrm[0] * tp[C + c]
+        fnb = nrm[0] * (ffar[0][c] - fmi[0][c])
+        for x in range(1, dim):
+            fnm = fnm + nrm[x] * tm[C + x * C + c]
+            fnp = fnp + nrm[x] * tp[C + x * C + c]
+            fnb = fnb + nrm[x] * (ffar[x][c] - fmi[x][c])
+        fplus = actx.np.where(is_bnd, fnm + fnb, fnp)
+        fstar.append(fscale * (0.5 * (fnm + fplus) + 0.5 * lmax * (qm[c] - qp[c])))
+    fsx = actx.np.reshape(actx.np.stack(fstar), (C, E, Nf * Nfp))
+    rhs = volf - actx.np.einsum("if,cef->cei", lift, fsx)
+    # chemistry: one Arrhenius step a -> b
+    qc = [q[c] for c in range(C)]
+    T = _thermo(actx, mix, qc, dim)[2]
+    a, b = mix.reaction
+    omega = mix.A * qc[2 + dim + a] * actx.np.exp((-mix.Ta) / T)
+    zero = 0.0 * omega
+    src = [zero] * (2 + dim) + [(-1.0 * omega) if k == a else (omega if k == b else zero) for k in range(ns)]
+    return rhs + actx.np.stack(src)
 
-    def body(actx, q, ghost, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, transport):
-        C, E, Np = q.shape
-        Nf = dim + 1
-        Nfp = lift.shape[1] // Nf
-        tr = [transport[k] for k in range(3)]
-        nrm = [normals[x] for x in range(dim)]
-        is_bnd = actx.np.not_equal(bc_kind, BC_NONE)
-        qc = [q[c] for c in range(C)]
-        finv, lam, prim = _inviscid(actx, mix, qc, dim)
 
-        # ---- pass 1: BR1 gradient of [q, T] with the central flux --------------------------------
-        W = actx.np.concatenate([q, actx.np.reshape(prim[2], (1, E, Np))])                  # (C+1, E, Np)
-        Wg = None
-        if ghost is not None:
-            gprim = _thermo(actx, mix, [ghost[c] for c in range(C)], dim)
-            Wg = actx.np.concatenate([ghost, actx.np.reshape(gprim[2], (1,) + tuple(ghost.shape[1:]))])
-        vol = actx.np.einsum("rij,rxe,cej->xcei", Sw, drdx, W)
-        wm, wp = _traces(actx, W, Wg, vmap_m, vmap_p, C + 1, E, Np, Nf, Nfp)
-        far = [qfar[c] for c in range(C)]
-        far_T = _thermo(actx, mix, far, dim)[2]
-        ext = far + [far_T]
-        wpl = [actx.np.where(is_bnd, ext[c], wp[c]) for c in range(C + 1)]
-        wstar = [fscale * (0.5 * (wm[c] + wpl[c])) for c in range(C + 1)]
-        fs = actx.np.stack([actx.np.stack([nrm[x] * wstar[c] for c in range(C + 1)]) for x in range(dim)])
-        gW = actx.np.einsum("if,xcef->xcei", lift, actx.np.reshape(fs, (dim, C + 1, E, Nf * Nfp))) - vol
-
-        # ---- pass 2: total flux, divergence, Rusanov / central numerical flux ----------------------
-        gq = [[gW[x][c] for c in range(C)] for x in range(dim)]
-        gT = [gW[x][C] for x in range(dim)]
-        fvis = _viscous(actx, mix, qc, gq, gT, prim, tr, dim)
-        ftot = [[finv[x][c] if fvis[x][c] is None else finv[x][c] - fvis[x][c] for c in range(C)] for x in range(dim)]
-        fstack = actx.np.stack([actx.np.stack(fx) for fx in ftot])
-        volf = actx.np.einsum("rij,rxe,xcej->cei", Sw, drdx, fstack)
-        lamr = actx.np.reshape(lam, (1, E, Np))
-        planes = actx.np.concatenate([q, actx.np.reshape(fstack, (dim * C, E, Np)), lamr])  # q, F, lam
-        gplanes = None
-        if ghost is not None:
-            raise NotImplementedError("partitioned multispecies runs exchange [q, F, lam]; not wired in round 1")
-        L = C + dim * C + 1
-        tm, tp = _traces(actx, planes, gplanes, vmap_m, vmap_p, L, E, Np, Nf, Nfp)
-        qm = [tm[c] for c in range(C)]
-        qp = [actx.np.where(is_bnd, far[c], tp[c]) for c in range(C)]
-        # exterior flux on boundary faces: inviscid flux of the far-field state, viscous flux of the interior
-        ffar, lam_far, _ = _inviscid(actx, mix, far, dim)
-        fmi, _, _ = _inviscid(actx, mix, qm, dim)
-        fstar = []
-        lam_p = actx.np.where(is_bnd, lam_far, tp[L - 1])
-        lmax = actx.np.maximum(tm[L - 1], lam_p)
-        for c in range(C):
-            fnm = nrm[0] * tm[C + c]
-            fnp = nrm[0] * tp[C + c]
-            fnb = nrm[0] * (ffar[0][c] - fmi[0][c])
-            for x in range(1, dim):
-                fnm = fnm + nrm[x] * tm[C + x * C + c]
-                fnp = fnp + nrm[x] * tp[C + x * C + c]
-                fnb = fnb + nrm[x] * (ffar[x][c] - fmi[x][c])
-            fplus = actx.np.where(is_bnd, fnm + fnb, fnp)
-            fstar.append(fscale * (0.5 * (fnm + fplus) + 0.5 * lmax * (qm[c] - qp[c])))
-        fsx = actx.np.reshape(actx.np.stack(fstar), (C, E, Nf * Nfp))
-        rhs = volf - actx.np.einsum("if,cef->cei", lift, fsx)
-
-        # ---- chemistry: one Arrhenius step a -> b ---------------------------------------------------
-        a, b = mix.reaction
-        omega = mix.A * qc[2 + dim + a] * actx.np.exp((-mix.Ta) / prim[2])
-        zero = 0.0 * omega
-        src = [zero] * (2 + dim) + [(-1.0 * omega) if k == a else (omega if k == b else zero) for k in range(ns)]
-        return rhs + actx.np.stack(src)
-
+def _make_ms_functions(dim, mix):
+    """The outlined functions: ``dg_ms_rhs`` (single domain, both passes), and for partitioned meshes
+    ``dg_ms_flux`` / ``dg_ms_div`` with ghost arrays (the halo of the flux planes is exchanged in between)."""
     def dg_ms_rhs(q, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, transport):
-        return body(dg_ms_rhs.actx, q, None, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, transport)
-    return dg_ms_rhs
+        actx = dg_ms_rhs.actx
+        FL = _ms_pass1(actx, mix, dim, q, None, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, transport)
+        return _ms_pass2(actx, mix, dim, q, FL, None, None, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar)
+
+    def dg_ms_flux(q, ghost, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, transport):
+        return _ms_pass1(dg_ms_flux.actx, mix, dim, q, ghost, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind,
+                         qfar, transport)
+
+    def dg_ms_div(q, FL, ghost, gFL, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar):
+        return _ms_pass2(dg_ms_div.actx, mix, dim, q, FL, ghost, gFL, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p,
+                         bc_kind, qfar)
+    return dg_ms_rhs, dg_ms_flux, dg_ms_div
 
 
 class MultispeciesOperator:
@@ -214,14 +236,15 @@ class MultispeciesOperator:
         self.qfar_host = np.asarray(farfield, dtype=np.float64).reshape(self.ncomp)
         self.qfar = self.actx.from_numpy(self.qfar_host.reshape(self.ncomp, 1, 1, 1))
         self.transport = self.actx.from_numpy(np.array([mu, kappa, diffusivity], dtype=np.float64))
-        f = _make_ms_rhs(self.dim, self.mix, False)
-        f.actx = self.actx
-        f.dg_dim = self.dim
-        self._f = self.actx.outline(f)
         if graph is None:
             graph = hasattr(self.actx, "lib")
-        if graph:
-            self._f = self.actx.compile(self._f, graph=True)
+        fns = []
+        for f in _make_ms_functions(self.dim, self.mix):
+            f.actx = self.actx
+            f.dg_dim = self.dim
+            g = self.actx.outline(f)
+            fns.append(self.actx.compile(g, graph=True) if graph else g)
+        self._f, self._flux, self._div = fns
 
     def state_from_primitive(self, rho, vel, T, Y):
         """Conserved state (any broadcastable shapes) from density, velocity, temperature, mass fractions."""
@@ -235,8 +258,14 @@ class MultispeciesOperator:
         parts = [rho, rho * e] + [rho * v for v in vel] + [rho * y for y in Y]
         return np.stack(np.broadcast_arrays(*parts))
 
-    def rhs(self, q: DOFArray, t=0.0) -> DOFArray:
+    def _geo(self):
         d = self.dcoll
-        out = self._f(q.data, d.Sw, d.drdx, d.lift, d.normals, d.fscale, d.vmap_m, d.vmap_p, d.bc_kind, self.qfar,
-                      self.transport)
-        return DOFArray(self.actx, out)
+        return (d.Sw, d.drdx, d.lift, d.normals, d.fscale, d.vmap_m, d.vmap_p, d.bc_kind, self.qfar)
+
+    def rhs(self, q: DOFArray, t=0.0, ghost=None, halo_fn=None) -> DOFArray:
+        """Single domain: ``rhs(q)``.  Partitioned: ``ghost`` = halo of ``q`` and ``halo_fn(DOFArray of the flux
+        planes) -> their halo`` (second exchange), like ``NavierStokesOperator.rhs``."""
+        if ghost is None:
+            return DOFArray(self.actx, self._f(q.data, *self._geo(), self.transport))
+        FL = self._flux(q.data, ghost, *self._geo(), self.transport)
+        return DOFArray(self.actx, self._div(q.data, FL, ghost, halo_fn(DOFArray(self.actx, FL)), *self._geo()))

@@ -115,3 +115,86 @@ def test_gpu_graph_compiled_rhs():
             assert gpu.launch_count == n0          # replay: no per-op dispatch (copies in/out are memcpys)
     assert fast._f.replays == 3 and fast._f.trace_count == 1
     gpu.check_deferred_errors()
+
+
+@pytest.mark.parametrize("dim,n,per,nparts", [(3, 3, True, 2), (2, 4, False, 3)])
+def test_partitioned_multispecies_equals_single_domain(dim, n, per, nparts):
+    """Partitioned mesh with looped-back halos (state, then flux planes) == the single-domain right-hand side."""
+    from paper_2512_17101_b200 import DGDiscretization, box_mesh
+    from paper_2512_17101_b200.dg.partition import partition_elements, rank_mesh
+    from paper_2512_17101_b200.discretization import BC_FARFIELD
+    actx = NumpyArrayContext()
+    mesh = box_mesh((n,) * dim, (-1,) * dim, (1,) * dim, periodic=(per,) * dim)
+    bc = None if per else {k: BC_FARFIELD for k in range(1, 2 * dim + 1)}
+    d = DGDiscretization(actx, mesh, 2, bc_map=bc)
+    op = MultispeciesOperator(d, Mixture())
+    q0 = ms_state(op, d.nodes())
+    ref = d.to_numpy(op.rhs(d.from_numpy(q0)))
+    part = partition_elements(mesh, nparts)
+    locs = [rank_mesh(mesh, part, r) for r in range(nparts)]
+    ds = [DGDiscretization(actx, m, 2, bc_map=bc, ghost_elements=p.nghost) for m, p in locs]
+    ops = [MultispeciesOperator(dd, Mixture()) for dd in ds]
+    qs = [q0[:, p.global_ids, :] for _, p in locs]
+
+    def loopback(fields):
+        out = []
+        for r, (m, p) in enumerate(locs):
+            g = np.empty(fields[r].shape[:-2] + (p.nghost, d.Np))
+            for k, peer in enumerate(p.peers):
+                pp = locs[peer][1]
+                a, b = p.recv_slots[k]
+                g[..., a:b, :] = fields[peer][..., pp.send_local[pp.peers.index(r)], :]
+            out.append(g)
+        return out
+
+    gh = loopback(qs)
+    FLs = [np.asarray(ops[r]._flux(qs[r], gh[r], *ops[r]._geo(), ops[r].transport)) for r in range(nparts)]
+    gFL = loopback(FLs)
+    full = np.empty_like(ref)
+    for r, (m, p) in enumerate(locs):
+        out = ops[r].rhs(ds[r].from_numpy(qs[r]), ghost=gh[r], halo_fn=lambda FL, r=r: gFL[r])
+        full[:, p.global_ids, :] = ds[r].to_numpy(out)
+    assert rel_err(full, ref) <= 1e-13
+
+
+@pytest.mark.gpu
+def test_gpu_partitioned_multispecies():
+    """Partitioned multispecies on the device (ghost arrays through the generic gather, device pack kernel,
+    exchange looped back on the host: this box has one GPU) against the single-domain oracle."""
+    from paper_2512_17101_b200 import B200ArrayContext, DGDiscretization, box_mesh
+    from paper_2512_17101_b200.dg.partition import partition_elements, rank_mesh
+    from paper_2512_17101_b200.halo import HaloExchange
+    gpu, cpu = B200ArrayContext(), NumpyArrayContext()
+    mesh = box_mesh((3,) * 3, (-1,) * 3, (1,) * 3, periodic=(True,) * 3)
+    d = DGDiscretization(cpu, mesh, 2)
+    opc = MultispeciesOperator(d, Mixture())
+    q0 = ms_state(opc, d.nodes())
+    ref = d.to_numpy(opc.rhs(d.from_numpy(q0)))
+    part = partition_elements(mesh, 2)
+    locs = [rank_mesh(mesh, part, r) for r in range(2)]
+    ds = [DGDiscretization(gpu, m, 2, ghost_elements=p.nghost) for m, p in locs]
+    ops = [MultispeciesOperator(dd, Mixture()) for dd in ds]
+    qs = [ds[r].from_numpy(q0[:, p.global_ids, :]) for r, (_, p) in enumerate(locs)]
+    halos = [HaloExchange(gpu, p, object(), d.Np) for _, p in locs]
+
+    def exchange(fields):
+        packed = {(r, peer): gpu.to_numpy(halos[r]._pack(fields[r], k))
+                  for r, (_, p) in enumerate(locs) for k, peer in enumerate(p.peers)}
+        out = []
+        for r, (_, p) in enumerate(locs):
+            g = np.empty(tuple(fields[r].shape[:-2]) + (p.nghost, d.Np))
+            for k, peer in enumerate(p.peers):
+                a, b = p.recv_slots[k]
+                g[..., a:b, :] = packed[(peer, r)]
+            out.append(gpu.from_numpy(g))
+        return out
+
+    for rep in range(3):                  # eager, captured, replayed
+        gh = exchange([q.data for q in qs])
+        FLs = [ops[r]._flux(qs[r].data, gh[r], *ops[r]._geo(), ops[r].transport) for r in range(2)]
+        gFL = exchange(FLs)
+        full = np.empty_like(ref)
+        for r, (_, p) in enumerate(locs):
+            out = ops[r].rhs(qs[r], ghost=gh[r], halo_fn=lambda FL, r=r: gFL[r])
+            full[:, p.global_ids, :] = ds[r].to_numpy(out)
+        assert rel_err(full, ref) <= 1e-12, rep
