@@ -37,6 +37,10 @@ CPU_REPS = 16          # RHS evaluations per process in one CPU sample (~10-15 s
 
 def workload_name(n, workload="ns"):
     E = 6 * n ** 3
+    if workload == "multispecies":
+        return (f"3D multi-species reactive Navier-Stokes DG RHS (3 species, 1 Arrhenius step; generic device ops, one CUDA "
+                f"graph per RHS), Kuhn tets order {ORDER}, periodic {n}^3 box per GPU: {E} elements, {E * NP} DOFs per GPU "
+                f"(BASELINE configs[4], single GPU)")
     if workload == "euler":
         return (f"3D compressible Euler DG RHS, Kuhn tets order {ORDER}, periodic {n}^3 box per GPU: {E} elements, "
                 f"{E * NP} DOFs per GPU (BASELINE configs[1])")
@@ -230,21 +234,34 @@ def run_b200(args):
         mesh, halo = ring_slab_halo(actx, mesh, n, rank, world, ORDER, transport=args.halo)
     d = DGDiscretization(actx, mesh, ORDER, ghost_elements=0 if halo is None else halo.nghost)
     euler = args.workload == "euler"
-    if euler:
+    multi = args.workload == "multispecies"
+    if multi:
+        if world > 1:
+            raise SystemExit("--workload multispecies is a single-GPU line in round 1")
+        from paper_2512_17101_b200 import Mixture, MultispeciesOperator
+        op = MultispeciesOperator(d, Mixture())
+    elif euler:
         from paper_2512_17101_b200 import EulerOperator
         op = EulerOperator(d, gamma=PHYS["gamma"])
     else:
         op = NavierStokesOperator(d, **PHYS)
     E, Np = d.nelements, d.Np
     ndof = E * Np
-    q_host = actx.pinned_empty((DIM + 2, E, Np))
-    q_host[...] = state_for((E, Np), 20251217 + rank)
-    out_host = actx.pinned_empty((DIM + 2, E, Np))
+    ncomp = op.ncomp if multi else DIM + 2
+    q_host = actx.pinned_empty((ncomp, E, Np))
+    if multi:       # smooth seeded state: rho, u, T perturbed, three mass fractions
+        rng = np.random.default_rng(20251217 + rank)
+        Y = rng.uniform(0.2, 0.4, (3, E, Np)); Y /= Y.sum(axis=0)
+        q_host[...] = op.state_from_primitive(rng.uniform(0.9, 1.1, (E, Np)), rng.uniform(-0.1, 0.1, (DIM, E, Np)),
+                                              rng.uniform(0.9, 1.1, (E, Np)), Y)
+    else:
+        q_host[...] = state_for((E, Np), 20251217 + rank)
+    out_host = actx.pinned_empty((ncomp, E, Np))
     q = DOFArray(actx, actx.from_numpy(q_host))
     actx.synchronize()
     t_setup = time.perf_counter() - t_setup
 
-    grad_form = args.form == "grad" and not euler
+    grad_form = args.form == "grad" and not euler and not multi
 
     def rhs_step(qarr):
         if halo is None:
@@ -263,7 +280,12 @@ def run_b200(args):
         after pass 2.  Warm-up and timed steps run this same code, so the caching allocator sees the
         same request pattern and never calls cudaMalloc inside the timed region."""
         rec = (lambda i: marks[i].record(stream)) if marks is not None else (lambda i: None)
-        if halo is None and not euler and grad_form:
+        if multi:
+            rec(0)
+            rec(1)
+            op.rhs(q)
+            rec(2)
+        elif halo is None and not euler and grad_form:
             rec(0)
             gq = op.grad(q)
             rec(1)
@@ -319,7 +341,9 @@ def run_b200(args):
     if halo is None:
         ms_grad = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
         ms_div = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
-        if euler:
+        if multi:
+            dom = ("generic device ops, one CUDA graph per RHS (not hand-fused)", ms_div, 72.0 * ncomp)
+        elif euler:
             dom = ("k_euler4 (fused Euler RHS)", ms_div, 80.0)
         else:
             names = ("k_rhs3<viscous> (flux + divergence pass)", "k_grad3 (BR1 gradient pass)") if grad_form else \
@@ -347,7 +371,7 @@ def run_b200(args):
                     "ms_grad_pass": ms_grad, "ms_div_pass": ms_div,
                     "ms_step_min_median_max": [float(np.min(per_step)), float(np.median(per_step)),
                                                float(np.max(per_step))]}
-    b_alg = 80.0 if euler else B_ALG_RHS
+    b_alg = 72.0 * ncomp if multi else (80.0 if euler else B_ALG_RHS)      # (3C + 2Cd) * 8 = 72 C for NS-type two-pass schemes
     rhs_gbs = ndof * b_alg / (ms_step * 1e-3) / 1e9
     if roofline is None:
         # partitioned run: the passes interleave with the halo exchange, so the roofline entry is the
@@ -409,7 +433,8 @@ def run_b200(args):
 
     if rank == 0:
         line = {
-            "metric": "3D Navier-Stokes DG RHS throughput" if not euler else "3D Euler DG RHS throughput",
+            "metric": ("3D multispecies reactive Navier-Stokes DG RHS throughput" if multi else
+                       "3D Navier-Stokes DG RHS throughput" if not euler else "3D Euler DG RHS throughput"),
             "value": value, "unit": "GDOF/s", "n_gpus": world, "steps": K, "warmup": max(args.warmup, 3), "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong" if (strong and world > 1) else "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
@@ -418,7 +443,8 @@ def run_b200(args):
                        "elements_per_gpu": E, "dofs_per_gpu": ndof, "order": ORDER, "dim": DIM,
                        "l2_policy": "inputs larger than L2 (q 4.0 GB, grad q 12 GB per GPU vs 126 MB L2)"
                        if ndof * 40 > 126e6 * 4 else "inputs comparable to L2: reduced size, not the headline config",
-                       "arrangement": ("euler single pass" if euler else
+                       "arrangement": ("array program on generic device ops (not fused)" if multi else
+                                       "euler single pass" if euler else
                                        "gradient (dg_ns_grad + dg_ns_rhs)" if grad_form else "flux (dg_ns_flux + dg_ns_div)"),
                        "parallelism": (f"mesh partition x{world}, " + ("NCCL face-halo exchange" if args.halo == "nccl" else
                                        "peer-memory face-halo exchange (pack kernel stores over NVLink)"))
@@ -456,7 +482,7 @@ def main():
                          "pack kernel stores into the neighbour's ghost array through CUDA-IPC peer memory (NVLink)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N>1: weak = one n^3 box per GPU in a ring (default); strong = one n^3 box partitioned over the GPUs")
-    ap.add_argument("--workload", default="ns", choices=["ns", "euler"],
+    ap.add_argument("--workload", default="ns", choices=["ns", "euler", "multispecies"],
                     help="ns = BASELINE configs[2] (headline); euler = configs[1] (3D Euler, read q + write rhs = 80 B/DOF)")
     args = ap.parse_args()
     global ORDER, NP
