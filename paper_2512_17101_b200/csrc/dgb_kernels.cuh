@@ -18,6 +18,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#ifndef DGB_STREAMING_STORES
+#define DGB_STREAMING_STORES 0
+#endif
+
 namespace dgb {
 
 constexpr int ceil_to(int x, int m) { return (x + m - 1) / m * m; }
@@ -349,11 +353,19 @@ __device__ __forceinline__ void store_pair(const Epilogue& ep, long long idx, in
       double2 o;
       if (ep.x1) { double2 x = *reinterpret_cast<const double2*>(ep.x1 + idx); o.x = ep.a1 * x.x + ep.b1 * v0; o.y = ep.a1 * x.y + ep.b1 * v1; }
       else { o.x = ep.b1 * v0; o.y = ep.b1 * v1; }
+#if DGB_STREAMING_STORES
+      __stcs(reinterpret_cast<double2*>(ep.out1 + idx), o);      // written once, not re-read by this kernel: keep L2 for the gathers
+#else
       *reinterpret_cast<double2*>(ep.out1 + idx) = o;
+#endif
       if (ep.out2) {
         double2 x = *reinterpret_cast<const double2*>(ep.x2 + idx);
         double2 o2; o2.x = ep.a2 * x.x + ep.b2 * v0; o2.y = ep.a2 * x.y + ep.b2 * v1;
+#if DGB_STREAMING_STORES
+        __stcs(reinterpret_cast<double2*>(ep.out2 + idx), o2);
+#else
         *reinterpret_cast<double2*>(ep.out2 + idx) = o2;
+#endif
       }
     }
   } else {

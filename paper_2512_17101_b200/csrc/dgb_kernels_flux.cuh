@@ -582,10 +582,18 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
             double acc = m[0] * F[0][c];
 #pragma unroll
             for (int x = 1; x < DIM; ++x) acc += m[x] * F[x][c];
+#if DGB_STREAMING_STORES
+            __stcs(out + (r * C + c) * t_ps, acc);
+#else
             out[(r * C + c) * t_ps] = acc;
+#endif
           }
         }
+#if DGB_STREAMING_STORES
+        __stcs(out + (DIM * C) * t_ps, wavespeed<DIM>(s, ph.gamma));
+#else
         out[(DIM * C) * t_ps] = wavespeed<DIM>(s, ph.gamma);
+#endif
       }
     }
     __syncwarp();

@@ -21,6 +21,7 @@ VARIANTS = {
     "pf2400": ["DGB_L2_PREFETCH_BLOCKS=2400"],
     "pf8000": ["DGB_L2_PREFETCH_BLOCKS=8000"],
     "flux_w14": ["DGB_FLUX_WARPS=16"],
+    "stcs": ["DGB_STREAMING_STORES=1"],
     "div_late": ["DGB_DIV_LATE_ISSUE=1"],
     "div_late1": ["DGB_DIV_LATE_ISSUE=1", "DGB_DIV_LATE_ROUNDS=1"],
     "div_late2": ["DGB_DIV_LATE_ISSUE=1", "DGB_DIV_LATE_ROUNDS=2"],
