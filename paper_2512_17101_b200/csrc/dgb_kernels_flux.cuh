@@ -230,7 +230,7 @@ __device__ __forceinline__ void flux_stage_async(double* Qs, FluxGeo<DIM, P, KW>
   if (lane < nel) cp_async8(&g.jac[lane], d.jac + e0 + lane);
 }
 
-template <int DIM, int P, int KW, int NWARPS>
+template <int DIM, int P, int KW, int NWARPS, bool GH>
 __global__ void __launch_bounds__(NWARPS * 32, 1)
 k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ ghost,
           double* __restrict__ T, Phys ph, long long ebeg, long long eend, long long nwblocks,
@@ -286,7 +286,7 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
         cnkE[k] = cn;
         const long long nb = DGB_CONN_NB(cn);
         const int jp = S.fn[DGB_CONN_NF(cn) * NFP + S.perm[DGB_CONN_PERM(cn) * NFP + m]];
-        const bool in_ghost = nb >= E;
+        const bool in_ghost = GH && nb >= E;
         const long long pstride = (in_ghost ? G : E) * NP;
         const double* pbase = (in_ghost ? ghost : q) + (in_ghost ? nb - E : nb) * NP + jp;
 #pragma unroll
@@ -382,7 +382,7 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
             cnk[b] = cn;
             const long long nb = DGB_CONN_NB(cn);
             const int jp = S.fn[DGB_CONN_NF(cn) * NFP + S.perm[DGB_CONN_PERM(cn) * NFP + m]];
-            const bool in_ghost = nb >= E;
+            const bool in_ghost = GH && nb >= E;
             const long long pstride = (in_ghost ? G : E) * NP;
             const double* pbase = (in_ghost ? ghost : q) + (in_ghost ? nb - E : nb) * NP + jp;
 #pragma unroll
@@ -748,7 +748,7 @@ __device__ __noinline__ VecC<DIM> boundary_operand(int bc, int f, VecC<DIM> qm_,
 // nbr = sJ F+.n+ (the own-side half lives in the folded volume matrix Wv2).  NB face nodes per
 // lane have their gathers in flight together; with LAZY the DIM-1 extra rows a neighbour's face 0
 // needs are fetched in a second wave (fewer live registers).
-template <int DIM, int P, int KW, int NB, bool LAZY, int K0 = 0>
+template <int DIM, int P, int KW, int NB, bool LAZY, int K0 = 0, bool GH = true>
 __device__ __forceinline__ void div_face_phase(const int* flc, const int* fn, const int* perm,
                                                const Div3Small<DIM, P, KW>& M, double* Fs, const DiscDev& d,
                                                const double* __restrict__ q, const double* __restrict__ T,
@@ -777,7 +777,7 @@ __device__ __forceinline__ void div_face_phase(const int* flc, const int* fn, co
           const long long nb = DGB_CONN_NB(cn);
           const int nf = DGB_CONN_NF(cn);
           const int jp = fn[nf * NFP + perm[DGB_CONN_PERM(cn) * NFP + m]];
-          const bool in_ghost = nb >= E;
+          const bool in_ghost = GH && nb >= E;
           const long long nbl = in_ghost ? nb - E : nb;
           const long long pstride = (in_ghost ? G : E) * NP;
           const long long tps = t_plane_stride<NPLT, NP>(in_ghost ? G : E);
@@ -806,7 +806,7 @@ __device__ __forceinline__ void div_face_phase(const int* flc, const int* fn, co
           const long long nb = DGB_CONN_NB(cnk[b]);
           const int m = (flk >> 4) & 15;
           const int jp = fn[perm[DGB_CONN_PERM(cnk[b]) * NFP + m]];
-          const bool in_ghost = nb >= E;
+          const bool in_ghost = GH && nb >= E;
           const long long tps = t_plane_stride<NPLT, NP>(in_ghost ? G : E);
           const double* tbase = (in_ghost ? Tghost : T) + (in_ghost ? nb - E : nb) * t_elem_stride<NPLT, NP>() + jp;
 #pragma unroll
@@ -975,7 +975,7 @@ __device__ __forceinline__ void face_finish(FaceRegs<DIM, P, KW>& R, const int* 
   }
 }
 
-template <int DIM, int P, int KW, int NWARPS>
+template <int DIM, int P, int KW, int NWARPS, bool GH>
 __global__ void __launch_bounds__(NWARPS * 32, 1)
 k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
          const double* __restrict__ ghost, const double* __restrict__ Tghost,
@@ -1084,9 +1084,9 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
 #if DGB_DIV_LATE_ISSUE
     face_finish<DIM, P, KW, NRL>(R, S.flc, S.fn, S.perm, M, W.Fs, d, T, Tghost, ph, e0, nel, lane);
     if (NRL < NR)                        // the remaining rounds are gathered in place
-      div_face_phase<DIM, P, KW, NB, (DGB_DIV_LAZY_EX != 0), NRL>(S.flc, S.fn, S.perm, M, W.Fs, d, q, T, ghost, Tghost, ph, e0, nel, lane);
+      div_face_phase<DIM, P, KW, NB, (DGB_DIV_LAZY_EX != 0), NRL, GH>(S.flc, S.fn, S.perm, M, W.Fs, d, q, T, ghost, Tghost, ph, e0, nel, lane);
 #else
-    div_face_phase<DIM, P, KW, NB, (DGB_DIV_LAZY_EX != 0)>(S.flc, S.fn, S.perm, M, W.Fs, d, q, T, ghost, Tghost, ph, e0, nel, lane);
+    div_face_phase<DIM, P, KW, NB, (DGB_DIV_LAZY_EX != 0), 0, GH>(S.flc, S.fn, S.perm, M, W.Fs, d, q, T, ghost, Tghost, ph, e0, nel, lane);
 #endif
     DGB_WTICK(1);
     cp_async_wait<1>();                  // T(b) has landed
@@ -1214,7 +1214,7 @@ __device__ __forceinline__ void euler4_stage(double* Qs, Euler4Geo<DIM, P, KW>& 
   }
 }
 
-template <int DIM, int P, int KW, int NWARPS>
+template <int DIM, int P, int KW, int NWARPS, bool GH>
 __global__ void __launch_bounds__(NWARPS * 32, 1)
 k_euler4(DiscDev d, const double* __restrict__ q, const double* __restrict__ ghost,
          Epilogue ep, Phys ph, long long ebeg, long long eend, long long nwblocks,
@@ -1278,7 +1278,7 @@ k_euler4(DiscDev d, const double* __restrict__ q, const double* __restrict__ gho
         cnk[k] = cn;
         const long long nb = DGB_CONN_NB(cn);
         const int jp = S.fn[DGB_CONN_NF(cn) * NFP + S.perm[DGB_CONN_PERM(cn) * NFP + m]];
-        const bool in_ghost = nb >= E;
+        const bool in_ghost = GH && nb >= E;
         const long long pstride = (in_ghost ? G : E) * NP;
         const double* pbase = (in_ghost ? ghost : q) + (in_ghost ? nb - E : nb) * NP + jp;
 #pragma unroll

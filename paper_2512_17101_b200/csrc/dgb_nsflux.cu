@@ -41,12 +41,13 @@ template <int DIM, int P>
 int launch_flux(const dgb_disc* d, const double* q, const double* ghost, double* T, const dgb::Phys& ph,
                 long long ebeg, long long eend, cudaStream_t st) {
   using C = CfgF<DIM, P>;
-  auto kern = dgb::k_nsflux3<DIM, P, C::KW, C::NWF>;
+  // GH = false: no ghost elements (single partition): the ghost/owned selects vanish from the gathers
+  auto kern = d->dev.G > 0 ? dgb::k_nsflux3<DIM, P, C::KW, C::NWF, true> : dgb::k_nsflux3<DIM, P, C::KW, C::NWF, false>;
   const size_t smem = sizeof(dgb::Flux3Smem<DIM, P, C::KW, C::NWF>);
   const long long nwb = (eend - ebeg + C::KW - 1) / C::KW;
   if (nwb == 0) return DGB_OK;
-  static bool configured = false;
-  if (!configured) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured = true; }
+  static bool configured[2] = {false, false};
+  if (!configured[d->dev.G > 0]) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured[d->dev.G > 0] = true; }
   const long long need = (nwb + C::NWF - 1) / C::NWF;
   const int grid = (int)(need < dgb_num_sms() ? need : dgb_num_sms());
   DGB_CUDA(cudaMemsetAsync(d->counters, 0, sizeof(unsigned long long), st));
@@ -59,12 +60,12 @@ template <int DIM, int P>
 int launch_div(const dgb_disc* d, const double* q, const double* T, const double* ghost, const double* Tghost,
                const dgb::Epilogue& ep, const dgb::Phys& ph, long long ebeg, long long eend, cudaStream_t st) {
   using C = CfgF<DIM, P>;
-  auto kern = dgb::k_nsdiv3<DIM, P, C::KW, C::NWD>;
+  auto kern = d->dev.G > 0 ? dgb::k_nsdiv3<DIM, P, C::KW, C::NWD, true> : dgb::k_nsdiv3<DIM, P, C::KW, C::NWD, false>;
   const size_t smem = sizeof(dgb::Div3Smem<DIM, P, C::KW, C::NWD>);
   const long long nwb = (eend - ebeg + C::KW - 1) / C::KW;
   if (nwb == 0) return DGB_OK;
-  static bool configured = false;
-  if (!configured) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured = true; }
+  static bool configured[2] = {false, false};
+  if (!configured[d->dev.G > 0]) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured[d->dev.G > 0] = true; }
   const long long need = (nwb + C::NWD - 1) / C::NWD;
   const int grid = (int)(need < dgb_num_sms() ? need : dgb_num_sms());
   DGB_CUDA(cudaMemsetAsync(d->counters + 1, 0, sizeof(unsigned long long), st));
@@ -217,12 +218,12 @@ template <int DIM, int P>
 int launch_euler4(const dgb_disc* d, const double* q, const double* ghost, const dgb::Epilogue& ep, const dgb::Phys& ph,
                   long long ebeg, long long eend, cudaStream_t st) {
   using C = CfgE<DIM, P>;
-  auto kern = dgb::k_euler4<DIM, P, C::KW, C::NW>;
+  auto kern = d->dev.G > 0 ? dgb::k_euler4<DIM, P, C::KW, C::NW, true> : dgb::k_euler4<DIM, P, C::KW, C::NW, false>;
   const size_t smem = sizeof(dgb::Euler4Smem<DIM, P, C::KW, C::NW>);
   const long long nwb = (eend - ebeg + C::KW - 1) / C::KW;
   if (nwb == 0) return DGB_OK;
-  static bool configured = false;
-  if (!configured) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured = true; }
+  static bool configured[2] = {false, false};
+  if (!configured[d->dev.G > 0]) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured[d->dev.G > 0] = true; }
   const long long need = (nwb + C::NW - 1) / C::NW;
   const int grid = (int)(need < dgb_num_sms() ? need : dgb_num_sms());
   DGB_CUDA(cudaMemsetAsync(d->counters + 1, 0, sizeof(unsigned long long), st));
