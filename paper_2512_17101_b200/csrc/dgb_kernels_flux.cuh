@@ -32,6 +32,9 @@
 #ifndef DGB_FLUX_EARLY_GATHER
 #define DGB_FLUX_EARLY_GATHER 1
 #endif
+#ifndef DGB_TICKET_BLOCKS
+#define DGB_TICKET_BLOCKS 1
+#endif
 #ifndef DGB_L2_PREFETCH_BLOCKS
 #define DGB_L2_PREFETCH_BLOCKS 0
 #endif
@@ -96,6 +99,33 @@ __device__ __forceinline__ unsigned long long draw_ticket(unsigned long long* co
 }
 __device__ __forceinline__ long long ticket_block(unsigned long long v, long long first_dynamic) {
   return first_dynamic + (long long)__shfl_sync(0xffffffffu, v, 0);
+}
+
+// Tickets in batches of DGB_TICKET_BLOCKS consecutive blocks: one atomic on the (single, hot) work counter
+// per batch instead of per block.  With ~1200 warps drawing a ticket every ~6 us the counter's L2 slice
+// serialises ~200 same-address atomics per microsecond and a ticket drawn a whole block earlier was
+// still not back when it was needed (19 % of a pass-2 warp's time sat in the shuffle that reads it).
+struct TicketStream {
+  unsigned long long pending;   // raw result of the last draw (valid on lane 0)
+  long long cur;                // block most recently handed out
+  int left;                     // blocks left in the current batch
+};
+__device__ __forceinline__ unsigned long long draw_tickets(unsigned long long* counter, int lane, int count) {
+  unsigned long long v;
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.eq.s32 p, %2, 0;\n\t@p atom.global.add.u64 %0, [%1], %3;\n\t}"
+               : "=l"(v) : "l"(counter), "r"(lane), "l"((unsigned long long)count) : "memory");
+  return v;
+}
+__device__ __forceinline__ void tickets_init(TicketStream& ts, long long first_block, unsigned long long* counter, int lane) {
+  ts.cur = first_block; ts.left = 0;
+  ts.pending = draw_tickets(counter, lane, DGB_TICKET_BLOCKS);
+}
+__device__ __forceinline__ long long tickets_next(TicketStream& ts, long long first_dynamic, unsigned long long* counter, int lane) {
+  if (ts.left > 0) { --ts.left; return ++ts.cur; }
+  ts.cur = ticket_block(ts.pending, first_dynamic);
+  ts.left = DGB_TICKET_BLOCKS - 1;
+  ts.pending = draw_tickets(counter, lane, DGB_TICKET_BLOCKS);     // the next batch, a whole batch of blocks early
+  return ts.cur;
 }
 
 // Face nodes of a warp's block are visited in rounds of WHOLE faces: round k, lane l handles node
@@ -267,7 +297,8 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
     flux_stage_async<DIM, P, KW>(W.Qs[0], W.geo[0], d, q, e0, (int)((eend - e0) < (long long)KW ? (eend - e0) : (long long)KW), lane);
   }
   cp_async_commit();
-  unsigned long long ticket = draw_ticket(counter, lane);
+  TicketStream tks;
+  tickets_init(tks, wb, counter, lane);
   DGB_WTICK_INIT
 #if DGB_FLUX_EARLY_GATHER
   // Neighbour states of ALL face nodes of a block, issued one phase early (during the pointwise flux
@@ -306,7 +337,7 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
     const long long e0 = ebeg + wb * KW;
     const int nel = (int)((eend - e0) < (long long)KW ? (eend - e0) : (long long)KW);
     // the next block (its ticket was drawn one block ago) starts its trip from HBM now
-    const long long wb_next = ticket_block(ticket, wstride);
+    const long long wb_next = tickets_next(tks, wstride, counter, lane);
     cp_async_wait<0>();
     __syncwarp();
     const double* Qs = W.Qs[buf];
@@ -317,7 +348,6 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
                                    (int)((eend - e1) < (long long)KW ? (eend - e1) : (long long)KW), lane);
     }
     cp_async_commit();
-    ticket = draw_ticket(counter, lane);
     if (DGB_L2_PREFETCH_BLOCKS > 0) {
       const long long wbp = wb_next + DGB_L2_PREFETCH_BLOCKS;
       if (wbp < nwblocks) {
@@ -1019,7 +1049,8 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
     cp_async_commit();
     cp_async_commit();
   }
-  unsigned long long ticket = draw_ticket(counter, lane);
+  TicketStream tks;
+  tickets_init(tks, wb, counter, lane);
 #if DGB_DIV_LATE_ISSUE
   // The first-wave gathers of block b+1 are issued right AFTER the contraction of block b and fly
   // during its store, the staging of the next rows and the top of the next iteration -- phases that
@@ -1040,7 +1071,7 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
   while (wb < nwblocks) {
     const long long e0 = ebeg + wb * KW;
     const int nel = (int)((eend - e0) < (long long)KW ? (eend - e0) : (long long)KW);
-    const long long wb_next = ticket_block(ticket, wstride);
+    const long long wb_next = tickets_next(tks, wstride, counter, lane);
     const long long e1 = ebeg + wb_next * KW;
     const int nel1 = wb_next < nwblocks ? (int)((eend - e1) < (long long)KW ? (eend - e1) : (long long)KW) : 0;
     if (nel1 > 0) div_stage_small<DIM, P, KW>(W.sm[buf ^ 1], d, q, T, e1, nel1, lane);
@@ -1053,7 +1084,7 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
                                     (int)((eend - ep) < (long long)KW ? (eend - ep) : (long long)KW), lane);
       }
     }
-    ticket = draw_ticket(counter, lane);
+    DGB_WTICK(5);
     cp_async_wait<2>();                  // S(b) has landed; T(b) and S(b+1) may still be in flight
     __syncwarp();
     const Div3Small<DIM, P, KW>& M = W.sm[buf];
@@ -1252,15 +1283,15 @@ k_euler4(DiscDev d, const double* __restrict__ q, const double* __restrict__ gho
   if (wb >= nwblocks) return;
   euler4_stage<DIM, P, KW>(W.Qs, W.geo[0], d, q, ebeg + wb * KW, nel_of(wb), lane);
   cp_async_commit();
-  unsigned long long ticket = draw_ticket(counter, lane);
+  TicketStream tks;
+  tickets_init(tks, wb, counter, lane);
 
   for (int i = 0;; ++i) {
     const int buf = i & 1;
     const long long e0 = ebeg + wb * KW;
     const int nel = nel_of(wb);
-    const long long wb_next = ticket_block(ticket, wstride);
+    const long long wb_next = tickets_next(tks, wstride, counter, lane);
     const int nel1 = nel_of(wb_next);
-    ticket = draw_ticket(counter, lane);
     cp_async_wait<0>();                  // this block's rows + geometry have landed (staged during the previous contraction)
     __syncwarp();
     const Euler4Geo<DIM, P, KW>& M = W.geo[buf];

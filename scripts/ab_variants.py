@@ -22,6 +22,9 @@ VARIANTS = {
     "pf8000": ["DGB_L2_PREFETCH_BLOCKS=8000"],
     "flux_w14": ["DGB_FLUX_WARPS=16"],
     "stcs": ["DGB_STREAMING_STORES=1"],
+    "tk2": ["DGB_TICKET_BLOCKS=2"],
+    "tk4": ["DGB_TICKET_BLOCKS=4"],
+    "tk8": ["DGB_TICKET_BLOCKS=8"],
     "div_late": ["DGB_DIV_LATE_ISSUE=1"],
     "div_late1": ["DGB_DIV_LATE_ISSUE=1", "DGB_DIV_LATE_ROUNDS=1"],
     "div_late2": ["DGB_DIV_LATE_ISSUE=1", "DGB_DIV_LATE_ROUNDS=2"],

@@ -28,6 +28,7 @@ print("k_nsflux3, warp 0 of each CTA, share of its time per phase:")
 for k in range(4): print(f"  {names[k]:34s} {100 * v[k] / v[:4].sum():5.1f} %   {v[k] / reps / 148 / 1.965e3:9.1f} us per CTA-warp and launch")
 for _ in range(reps): op._div(q.data, T, *op._div_args())
 v = read()
-names = ["ticket + stage small + wait small", "face phase (gathers)", "wait T rows", "DMMA", "stage rows + store"]
+names = ["wait for q/lam/conn of this block", "face phase (gathers)", "wait T rows", "DMMA", "stage rows + store",
+         "ticket + stage q/lam/conn of next block"]
 print("k_nsdiv3:")
-for k in range(5): print(f"  {names[k]:34s} {100 * v[k] / v[:5].sum():5.1f} %   {v[k] / reps / 148 / 1.965e3:9.1f} us per CTA-warp and launch")
+for k in (5, 0, 1, 2, 3, 4): print(f"  {names[k]:40s} {100 * v[k] / v[:6].sum():5.1f} %   {v[k] / reps / 148 / 1.965e3:9.1f} us per CTA-warp and launch")
