@@ -35,6 +35,9 @@
 #ifndef DGB_TICKET_BLOCKS
 #define DGB_TICKET_BLOCKS 1
 #endif
+#ifndef DGB_TICKET_DEPTH
+#define DGB_TICKET_DEPTH 2
+#endif
 #ifndef DGB_L2_PREFETCH_BLOCKS
 #define DGB_L2_PREFETCH_BLOCKS 0
 #endif
@@ -106,7 +109,10 @@ __device__ __forceinline__ long long ticket_block(unsigned long long v, long lon
 // serialises ~200 same-address atomics per microsecond and a ticket drawn a whole block earlier was
 // still not back when it was needed (19 % of a pass-2 warp's time sat in the shuffle that reads it).
 struct TicketStream {
-  unsigned long long pending;   // raw result of the last draw (valid on lane 0)
+  unsigned long long pending;   // raw result of the oldest outstanding draw (valid on lane 0)
+#if DGB_TICKET_DEPTH > 1
+  unsigned long long pending2;  // second outstanding draw: every ticket gets two block times to come back
+#endif
   long long cur;                // block most recently handed out
   int left;                     // blocks left in the current batch
 };
@@ -119,12 +125,20 @@ __device__ __forceinline__ unsigned long long draw_tickets(unsigned long long* c
 __device__ __forceinline__ void tickets_init(TicketStream& ts, long long first_block, unsigned long long* counter, int lane) {
   ts.cur = first_block; ts.left = 0;
   ts.pending = draw_tickets(counter, lane, DGB_TICKET_BLOCKS);
+#if DGB_TICKET_DEPTH > 1
+  ts.pending2 = draw_tickets(counter, lane, DGB_TICKET_BLOCKS);
+#endif
 }
 __device__ __forceinline__ long long tickets_next(TicketStream& ts, long long first_dynamic, unsigned long long* counter, int lane) {
   if (ts.left > 0) { --ts.left; return ++ts.cur; }
   ts.cur = ticket_block(ts.pending, first_dynamic);
   ts.left = DGB_TICKET_BLOCKS - 1;
+#if DGB_TICKET_DEPTH > 1
+  ts.pending = ts.pending2;
+  ts.pending2 = draw_tickets(counter, lane, DGB_TICKET_BLOCKS);
+#else
   ts.pending = draw_tickets(counter, lane, DGB_TICKET_BLOCKS);     // the next batch, a whole batch of blocks early
+#endif
   return ts.cur;
 }
 

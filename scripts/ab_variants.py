@@ -22,6 +22,7 @@ VARIANTS = {
     "pf8000": ["DGB_L2_PREFETCH_BLOCKS=8000"],
     "flux_w14": ["DGB_FLUX_WARPS=16"],
     "stcs": ["DGB_STREAMING_STORES=1"],
+    "tkd2": ["DGB_TICKET_DEPTH=2"],
     "tk2": ["DGB_TICKET_BLOCKS=2"],
     "tk4": ["DGB_TICKET_BLOCKS=4"],
     "tk8": ["DGB_TICKET_BLOCKS=8"],
