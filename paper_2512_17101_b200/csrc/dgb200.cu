@@ -142,19 +142,6 @@ __global__ void k_flag_wait(const unsigned long long* flag, unsigned long long v
 
 namespace {
 
-// V = tuning variant (env DGB_VARIANT, default 0): block size K, warps NW, column tiles per warp MT,
-// minimum resident CTAs per SM MINB (register cap)
-template <int DIM, int P, int V> struct Cfg { static constexpr int K = 16, NW = DIM == 3 ? 5 : 4, MT = 2, MINB = 2, KG = 16, NWG = DIM == 3 ? 5 : 4, MINBG = 2; };
-template <int DIM, int P> struct Cfg<DIM, P, 1> { static constexpr int K = 16, NW = DIM == 3 ? 10 : 8, MT = 1, MINB = 2, KG = 16, NWG = DIM == 3 ? 10 : 8, MINBG = 2; };
-template <int DIM, int P> struct Cfg<DIM, P, 2> { static constexpr int K = 8, NW = DIM == 3 ? 5 : 4, MT = 1, MINB = 4, KG = 8, NWG = DIM == 3 ? 5 : 4, MINBG = 4; };
-template <int DIM, int P> struct Cfg<DIM, P, 3> { static constexpr int K = 8, NW = DIM == 3 ? 5 : 4, MT = 1, MINB = 3, KG = 16, NWG = DIM == 3 ? 5 : 4, MINBG = 3; };
-template <> struct Cfg<3, 4, 0> { static constexpr int K = 8, NW = 5, MT = 1, MINB = 1, KG = 8, NWG = 5, MINBG = 1; };
-template <> struct Cfg<3, 4, 1> { static constexpr int K = 8, NW = 10, MT = 1, MINB = 1, KG = 8, NWG = 10, MINBG = 1; };
-
-// launch configuration of the asynchronous-pipeline kernels (dgb_kernels_async.cuh), the default path
-template <int DIM, int P> struct Cfg2 { static constexpr int K = 8, NW = 8, MINB = 2, KG = 8, NWG = DIM == 3 ? 5 : 4, MINBG = 3; };
-template <> struct Cfg2<3, 4> { static constexpr int K = 8, NW = 8, MINB = 1, KG = 8, NWG = 5, MINBG = 1; };
-
 // launch configuration of the warp-autonomous kernels (dgb_kernels_warp.cuh), the default path:
 // KW elements per warp (C*KW columns padded to whole 8-column tiles), as many warps per SM as fit
 #ifndef DGB_GRAD_WARPS
@@ -177,55 +164,6 @@ template <int DIM, int P> struct Cfg3 {
   static constexpr size_t grad_fixed = sizeof(dgb::Grad3Smem<DIM, P, KW, 1>) - grad_per;
   static constexpr int NWG = fit_warps(grad_fixed, grad_per, DGB_GRAD_WARPS);
 };
-
-// DGB_VARIANT: 5 (default) = warp-autonomous; 4 = CTA-phased asynchronous pipeline; 0..3 = first
-// generation CTA-phased kernels (kept for A/B measurements, see profiles/)
-int variant() {
-  static int v = -1;
-  if (v < 0) { const char* e = getenv("DGB_VARIANT"); v = e ? atoi(e) : 5; if (v < 0 || v > 5) v = 5; }
-  return v;
-}
-
-template <typename Kern>
-int persistent_grid(Kern kern, int threads, size_t smem, int nblocks, int* grid) {
-  DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int occ = 0;
-  DGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
-  if (occ < 1) return fail(DGB_ERR_INVALID, "kernel does not fit on an SM");
-  long long g = (long long)occ * num_sms();
-  *grid = (int)(g < nblocks ? g : nblocks);
-  return DGB_OK;
-}
-
-template <int DIM, int P, bool VISCOUS, int V>
-int launch_rhs(const dgb_disc* d, const double* q, const double* gq, const double* ghost, const double* gghost,
-               const dgb::Epilogue& ep, const dgb::Phys& ph, cudaStream_t st) {
-  using C = Cfg<DIM, P, V>;
-  auto kern = dgb::k_rhs<DIM, P, C::K, C::NW, C::MT, VISCOUS, C::MINB>;
-  const size_t smem = sizeof(dgb::RhsSmem<DIM, P, C::K, C::NW, C::MT, VISCOUS>);
-  const long long nb = (d->dev.E + C::K - 1) / C::K;
-  if (nb == 0) return DGB_OK;
-  static int grid_cache = 0; static long long nb_cache = -1;
-  if (nb_cache != nb) { int rc = persistent_grid(kern, C::NW * 32, smem, (int)nb, &grid_cache); if (rc) return rc; nb_cache = nb; }
-  kern<<<grid_cache, C::NW * 32, smem, st>>>(d->dev, q, gq, ghost, gghost, ep, ph, (int)nb);
-  DGB_CUDA(cudaGetLastError());
-  return DGB_OK;
-}
-
-template <int DIM, int P, bool VISCOUS>
-int launch_rhs2(const dgb_disc* d, const double* q, const double* gq, const double* ghost, const double* gghost,
-                const dgb::Epilogue& ep, const dgb::Phys& ph, cudaStream_t st) {
-  using C = Cfg2<DIM, P>;
-  auto kern = dgb::k_rhs2<DIM, P, C::K, C::NW, VISCOUS, C::MINB>;
-  const size_t smem = sizeof(dgb::Rhs2Smem<DIM, P, C::K, VISCOUS>);
-  const long long nb = (d->dev.E + C::K - 1) / C::K;
-  if (nb == 0) return DGB_OK;
-  static int grid_cache = 0; static long long nb_cache = -1;
-  if (nb_cache != nb) { int rc = persistent_grid(kern, C::NW * 32, smem, (int)nb, &grid_cache); if (rc) return rc; nb_cache = nb; }
-  kern<<<grid_cache, C::NW * 32, smem, st>>>(d->dev, q, gq, ghost, gghost, ep, ph, (int)nb);
-  DGB_CUDA(cudaGetLastError());
-  return DGB_OK;
-}
 
 template <int DIM, int P, bool VISCOUS>
 int launch_rhs3(const dgb_disc* d, const double* q, const double* gq, const double* ghost, const double* gghost,
@@ -274,69 +212,23 @@ int launch_grad3(const dgb_disc* d, const double* q, const double* ghost, double
   return DGB_OK;
 }
 
-template <int DIM, int P>
-int launch_grad2(const dgb_disc* d, const double* q, const double* ghost, double* grad, const dgb::Phys& ph,
-                 cudaStream_t st) {
-  using C = Cfg2<DIM, P>;
-  auto kern = dgb::k_grad2<DIM, P, C::KG, C::NWG, C::MINBG>;
-  const size_t smem = sizeof(dgb::Grad2Smem<DIM, P, C::KG>);
-  const long long nb = (d->dev.E + C::KG - 1) / C::KG;
-  if (nb == 0) return DGB_OK;
-  static int grid_cache = 0; static long long nb_cache = -1;
-  if (nb_cache != nb) { int rc = persistent_grid(kern, C::NWG * 32, smem, (int)nb, &grid_cache); if (rc) return rc; nb_cache = nb; }
-  kern<<<grid_cache, C::NWG * 32, smem, st>>>(d->dev, q, ghost, grad, ph, (int)nb);
-  DGB_CUDA(cudaGetLastError());
-  return DGB_OK;
-}
-
-template <int DIM, int P, int V>
-int launch_grad(const dgb_disc* d, const double* q, const double* ghost, double* grad, const dgb::Phys& ph,
-                cudaStream_t st) {
-  using C = Cfg<DIM, P, V>;
-  auto kern = dgb::k_grad<DIM, P, C::KG, C::NWG, C::MINBG>;
-  const size_t smem = sizeof(dgb::GradSmem<DIM, P, C::KG>);
-  const long long nb = (d->dev.E + C::KG - 1) / C::KG;
-  if (nb == 0) return DGB_OK;
-  static int grid_cache = 0; static long long nb_cache = -1;
-  if (nb_cache != nb) { int rc = persistent_grid(kern, C::NWG * 32, smem, (int)nb, &grid_cache); if (rc) return rc; nb_cache = nb; }
-  kern<<<grid_cache, C::NWG * 32, smem, st>>>(d->dev, q, ghost, grad, ph, (int)nb);
-  DGB_CUDA(cudaGetLastError());
-  return DGB_OK;
-}
-
+#ifdef DGB_ONLY_3D_P3   // fast kernel-tuning builds (scripts/ab_variants.py)
+#define DGB_FOR_EACH_ELEMENT(X) X(3, 3)
+#else
 #define DGB_FOR_EACH_ELEMENT(X) X(2, 1) X(2, 2) X(2, 3) X(2, 4) X(3, 1) X(3, 2) X(3, 3) X(3, 4)
+#endif
 
 int dispatch_rhs(const dgb_disc* d, bool viscous, const double* q, const double* gq, const double* ghost,
                  const double* gghost, const dgb::Epilogue& ep, const dgb::Phys& ph, cudaStream_t st,
                  long long ebeg = 0, long long eend = -1) {
-  if ((ebeg != 0 || eend >= 0) && variant() != 5)
-    return fail(DGB_ERR_INVALID, "element ranges need the default kernels (DGB_VARIANT=5)");
   // Euler: k_euler4 (dgb_kernels_flux.cuh) unless DGB_EULER_KERNEL=3 asks for k_rhs3<inviscid>
   static int euler_kernel = -1;
   if (euler_kernel < 0) { const char* e = getenv("DGB_EULER_KERNEL"); euler_kernel = e ? atoi(e) : 4; }
-  if (!viscous && variant() == 5 && euler_kernel == 4) return dgb_launch_euler4(d, q, ghost, ep, ph, ebeg, eend, st);
+  if (!viscous && euler_kernel == 4) return dgb_launch_euler4(d, q, ghost, ep, ph, ebeg, eend, st);
 #define X(DIM, P)                                                                              \
-  if (d->dim == DIM && d->order == P) {                                                        \
-    if (variant() == 5)                                                                        \
-      return viscous ? launch_rhs3<DIM, P, true>(d, q, gq, ghost, gghost, ep, ph, st, ebeg, eend)   \
-                     : launch_rhs3<DIM, P, false>(d, q, gq, ghost, gghost, ep, ph, st, ebeg, eend); \
-    if (variant() == 4)                                                                        \
-      return viscous ? launch_rhs2<DIM, P, true>(d, q, gq, ghost, gghost, ep, ph, st)          \
-                     : launch_rhs2<DIM, P, false>(d, q, gq, ghost, gghost, ep, ph, st);        \
-    if (DIM == 3 && P == 3) {                                                                  \
-      switch (variant()) {                                                                     \
-        case 1: return viscous ? launch_rhs<3, 3, true, 1>(d, q, gq, ghost, gghost, ep, ph, st) \
-                               : launch_rhs<3, 3, false, 1>(d, q, gq, ghost, gghost, ep, ph, st); \
-        case 2: return viscous ? launch_rhs<3, 3, true, 2>(d, q, gq, ghost, gghost, ep, ph, st) \
-                               : launch_rhs<3, 3, false, 2>(d, q, gq, ghost, gghost, ep, ph, st); \
-        case 3: return viscous ? launch_rhs<3, 3, true, 3>(d, q, gq, ghost, gghost, ep, ph, st) \
-                               : launch_rhs<3, 3, false, 3>(d, q, gq, ghost, gghost, ep, ph, st); \
-        default: break;                                                                        \
-      }                                                                                        \
-    }                                                                                          \
-    return viscous ? launch_rhs<DIM, P, true, 0>(d, q, gq, ghost, gghost, ep, ph, st)          \
-                   : launch_rhs<DIM, P, false, 0>(d, q, gq, ghost, gghost, ep, ph, st);        \
-  }
+  if (d->dim == DIM && d->order == P)                                                          \
+    return viscous ? launch_rhs3<DIM, P, true>(d, q, gq, ghost, gghost, ep, ph, st, ebeg, eend)   \
+                   : launch_rhs3<DIM, P, false>(d, q, gq, ghost, gghost, ep, ph, st, ebeg, eend);
   DGB_FOR_EACH_ELEMENT(X)
 #undef X
   return fail(DGB_ERR_INVALID, "unsupported (dim, order)");
@@ -344,20 +236,7 @@ int dispatch_rhs(const dgb_disc* d, bool viscous, const double* q, const double*
 
 int dispatch_grad(const dgb_disc* d, const double* q, const double* ghost, double* grad, const dgb::Phys& ph,
                   cudaStream_t st) {
-#define X(DIM, P)                                                              \
-  if (d->dim == DIM && d->order == P) {                                        \
-    if (variant() == 5) return launch_grad3<DIM, P>(d, q, ghost, grad, ph, st); \
-    if (variant() == 4) return launch_grad2<DIM, P>(d, q, ghost, grad, ph, st); \
-    if (DIM == 3 && P == 3) {                                                  \
-      switch (variant()) {                                                     \
-        case 1: return launch_grad<3, 3, 1>(d, q, ghost, grad, ph, st);        \
-        case 2: return launch_grad<3, 3, 2>(d, q, ghost, grad, ph, st);        \
-        case 3: return launch_grad<3, 3, 3>(d, q, ghost, grad, ph, st);        \
-        default: break;                                                        \
-      }                                                                        \
-    }                                                                          \
-    return launch_grad<DIM, P, 0>(d, q, ghost, grad, ph, st);                  \
-  }
+#define X(DIM, P) if (d->dim == DIM && d->order == P) return launch_grad3<DIM, P>(d, q, ghost, grad, ph, st);
   DGB_FOR_EACH_ELEMENT(X)
 #undef X
   return fail(DGB_ERR_INVALID, "unsupported (dim, order)");

@@ -20,17 +20,11 @@
 #include "dgb_kernels_async.cuh"
 #include "dgb_kernels_warp.cuh"
 
-#ifndef DGB_FLUX_NB
-#define DGB_FLUX_NB 4
-#endif
 #ifndef DGB_DIV_NB
 #define DGB_DIV_NB 2
 #endif
 #ifndef DGB_DIV_LAZY_EX
 #define DGB_DIV_LAZY_EX 0
-#endif
-#ifndef DGB_FLUX_EARLY_GATHER
-#define DGB_FLUX_EARLY_GATHER 1
 #endif
 #ifndef DGB_TICKET_BLOCKS
 #define DGB_TICKET_BLOCKS 1
@@ -40,24 +34,6 @@
 #endif
 #ifndef DGB_L2_PREFETCH_BLOCKS
 #define DGB_L2_PREFETCH_BLOCKS 0
-#endif
-#ifndef DGB_DIV_LATE_ISSUE
-#define DGB_DIV_LATE_ISSUE 0
-#endif
-#ifndef DGB_DIV_LATE_ROUNDS
-#define DGB_DIV_LATE_ROUNDS 99
-#endif
-#ifndef DGB_DIV_SPLIT_MMA
-#define DGB_DIV_SPLIT_MMA 0
-#endif
-#ifndef DGB_FLUX_PRODUCT_MAJOR
-#define DGB_FLUX_PRODUCT_MAJOR 0
-#endif
-#ifndef DGB_DIV4_NB
-#define DGB_DIV4_NB 2
-#endif
-#ifndef DGB_DIV4_LAZY_EX
-#define DGB_DIV4_LAZY_EX 1
 #endif
 
 #ifdef DGB_PHASE_TIMING
@@ -285,7 +261,6 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
   constexpr int LDSX = FluxT<DIM, P>::LDSX;
   constexpr int NT = NWARPS * 32;
   constexpr int NR = face_rounds<DIM, P, KW>();        // face-node rounds per block
-  constexpr int NBF = DGB_FLUX_NB;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   auto& S = *reinterpret_cast<Flux3Smem<DIM, P, KW, NWARPS>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -314,7 +289,6 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
   TicketStream tks;
   tickets_init(tks, wb, counter, lane);
   DGB_WTICK_INIT
-#if DGB_FLUX_EARLY_GATHER
   // Neighbour states of ALL face nodes of a block, issued one phase early (during the pointwise flux
   // phase of the previous block, which is FP64 work and leaves the L1/LSU pipe to the gathers) and
   // consumed at the top of the block's own iteration.
@@ -345,7 +319,6 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
     const long long e0 = ebeg + wb * KW;
     issue_gathers(W.geo[0], (int)((eend - e0) < (long long)KW ? (eend - e0) : (long long)KW));
   }
-#endif
 
   while (wb < nwblocks) {
     const long long e0 = ebeg + wb * KW;
@@ -373,13 +346,6 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
     DGB_WTICK(0);
 
     // ---- face averages q* (central flux, boundary states) -> Ss; metric coefficients ---------
-#if DGB_FLUX_PRODUCT_MAJOR
-    for (int n = lane; n < nel * DIM * EL::NS; n += 32) {
-      const int e = n / (DIM * EL::NS), xs = n - e * (DIM * EL::NS);
-      const int x = xs / EL::NS, s = xs - x * EL::NS;
-      W.coef[e][x][s] = s < DIM ? -geo.drdx[s * DIM + x][e] : geo.fsc[e][s - DIM] * geo.nrm[x][e][s - DIM];
-    }
-#endif
     // the previous block left grad q in the q* rows: the K-padding columns must be zero again
     if (EL::NFPK != NFP) {
       for (int n = lane; n < WS::NCOLP * NF * (EL::NFPK - NFP); n += 32) {
@@ -388,7 +354,6 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
         W.Ss[col * LDSX + f * EL::NFPK + m] = 0.0;
       }
     }
-#if DGB_FLUX_EARLY_GATHER
 #pragma unroll
     for (int k = 0; k < NR; ++k) {
       if (cnkE[k] >= 0) {
@@ -408,118 +373,9 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
         for (int c = 0; c < C; ++c) W.Ss[(c * KW + e) * LDSX + f * EL::NFPK + m] = 0.5 * (qm[c] + qpE[k][c]);
       }
     }
-#else
-    // NBF face nodes per lane have their neighbour loads in flight together
-#pragma unroll 1
-    for (int k0 = 0; k0 < NR; k0 += NBF) {
-      double qp[NBF][C];
-      long long cnk[NBF];
-#pragma unroll
-      for (int b = 0; b < NBF; ++b) {
-        const int k = k0 + b;
-        cnk[b] = -1;
-        if (k < NR) {
-          const int flk = S.flc[k * 32 + lane];
-          const int e = flk & 3, f = (flk >> 2) & 3, m = (flk >> 4) & 15;
-          if (flk >= 0 && e < nel) {
-            const long long cn = geo.conn[e][f];
-            cnk[b] = cn;
-            const long long nb = DGB_CONN_NB(cn);
-            const int jp = S.fn[DGB_CONN_NF(cn) * NFP + S.perm[DGB_CONN_PERM(cn) * NFP + m]];
-            const bool in_ghost = GH && nb >= E;
-            const long long pstride = (in_ghost ? G : E) * NP;
-            const double* pbase = (in_ghost ? ghost : q) + (in_ghost ? nb - E : nb) * NP + jp;
-#pragma unroll
-            for (int c = 0; c < C; ++c) qp[b][c] = pbase[c * pstride];
-          }
-        }
-      }
-#pragma unroll
-      for (int b = 0; b < NBF; ++b) {
-        const int k = k0 + b;
-        if (k < NR && cnk[b] >= 0) {
-          const int flk = S.flc[k * 32 + lane];
-          const int e = flk & 3, f = (flk >> 2) & 3, m = (flk >> 4) & 15, jm = (flk >> 8) & 255;
-          const int bc = DGB_CONN_BC(cnk[b]);
-          double qm[C];
-#pragma unroll
-          for (int c = 0; c < C; ++c) qm[c] = Qs[(c * KW + e) * EL::LDQ + jm];
-          if (bc != 0) {
-            double nrm[DIM];
-#pragma unroll
-            for (int x = 0; x < DIM; ++x) nrm[x] = geo.nrm[x][e][f];
-            bc_state<DIM, true>(bc, qm, nrm, ph, qp[b]);
-          }
-#pragma unroll
-          for (int c = 0; c < C; ++c) W.Ss[(c * KW + e) * LDSX + f * EL::NFPK + m] = 0.5 * (qm[c] + qp[b][c]);
-        }
-      }
-    }
-#endif
     __syncwarp();
     DGB_WTICK(1);
 
-#if DGB_FLUX_PRODUCT_MAJOR
-    // ---- tensor-core contractions, product by product over BOTH column tiles: every W fragment is
-    //      loaded once per block instead of once per tile (the L1/LSU data pipe is 68 % busy in this
-    //      kernel), each k-step issues 2*NI independent DMMAs, and a finished product is folded into
-    //      the gradient accumulators  v[x] += coef[x][s] * acc  while the next one runs.
-    {
-      const int k8 = lane >> 2;
-      double v[DIM][WS::NTILE][NI][2];
-#pragma unroll
-      for (int x = 0; x < DIM; ++x)
-#pragma unroll
-        for (int mt = 0; mt < WS::NTILE; ++mt)
-#pragma unroll
-          for (int ni = 0; ni < NI; ++ni) { v[x][mt][ni][0] = 0.0; v[x][mt][ni][1] = 0.0; }
-#pragma unroll
-      for (int s = 0; s < EL::NS; ++s) {
-        double acc[WS::NTILE][NI][2];
-#pragma unroll
-        for (int mt = 0; mt < WS::NTILE; ++mt)
-#pragma unroll
-          for (int ni = 0; ni < NI; ++ni) { acc[mt][ni][0] = 0.0; acc[mt][ni][1] = 0.0; }
-        if (s < DIM)
-          mma_block<NI, WS::NTILE>(acc, Qs, EL::LDQ, S.Wq + s * EL::NPR * EL::LDQ, EL::LDQ, EL::NPK / 4, lane);
-        else
-          mma_block<NI, WS::NTILE>(acc, W.Ss + (s - DIM) * EL::NFPK, LDSX, S.Wf + (s - DIM) * EL::NPR * EL::LDL,
-                                   EL::LDL, EL::NFPK / 4, lane);
-#pragma unroll
-        for (int mt = 0; mt < WS::NTILE; ++mt) {
-          const int e = (mt * 8 + k8) % KW;          // element of this lane's column (any value for padding columns)
-#pragma unroll
-          for (int x = 0; x < DIM; ++x) {
-            const double cf = W.coef[e][x][s];
-#pragma unroll
-            for (int ni = 0; ni < NI; ++ni) { v[x][mt][ni][0] += cf * acc[mt][ni][0]; v[x][mt][ni][1] += cf * acc[mt][ni][1]; }
-          }
-        }
-      }
-      __syncwarp();                       // every lane has read the q* rows: grad q may overwrite them
-#pragma unroll
-      for (int mt = 0; mt < WS::NTILE; ++mt) {
-        const int col = mt * 8 + k8;
-        const int c = col / KW, e = col - c * KW;
-        if (col < WS::NCOL && e < nel) {
-          double* sg = W.Ss + mt * 8 * LDSX;
-#pragma unroll
-          for (int x = 0; x < DIM; ++x)
-#pragma unroll
-            for (int ni = 0; ni < NI; ++ni) {
-              const int i = ni * 8 + 2 * (lane & 3);
-              if (NP % 2 == 0) {
-                if (i < NP) *reinterpret_cast<double2*>(sg + (x * 8 + k8) * NP + i) = make_double2(v[x][mt][ni][0], v[x][mt][ni][1]);
-              } else {
-                if (i < NP) sg[(x * 8 + k8) * NP + i] = v[x][mt][ni][0];
-                if (i + 1 < NP) sg[(x * 8 + k8) * NP + i + 1] = v[x][mt][ni][1];
-              }
-            }
-        }
-      }
-    }
-    __syncwarp();
-#else
     // ---- tensor-core contractions, one 8-column tile at a time; grad q of the tile -> its Ss rows ----
     // On a simplex  fscale n_x (face f) = sum_r a[f][r] dr/dx[r][x]  with a[0][r] = 1, a[r+1][r] = -1, so
     //   grad_x q = sum_f fscale n_x lift_f q*_f - sum_r dr/dx[r][x] Sw_r q
@@ -577,16 +433,13 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
       }
     }
     __syncwarp();
-#endif
     DGB_WTICK(2);
-#if DGB_FLUX_EARLY_GATHER
     if (wb_next < nwblocks) {             // rows + connectivity of the next block have landed by now
       cp_async_wait<0>();
       __syncwarp();
       const long long e1 = ebeg + wb_next * KW;
       issue_gathers(W.geo[buf ^ 1], (int)((eend - e1) < (long long)KW ? (eend - e1) : (long long)KW));
     }
-#endif
 
     // ---- pointwise: total flux at every node, contravariant + Jacobian-scaled, and the wave speed ----
 #pragma unroll
@@ -909,116 +762,6 @@ __device__ __forceinline__ void div_face_phase(const int* flc, const int* fn, co
   }
 }
 
-// Split form of the face phase: face_issue() puts the first-wave gathers of ALL face nodes of a block
-// in flight (registers), face_finish() consumes them.  k_nsdiv3 (DGB_DIV_SPLIT_MMA) runs the volume
-// half of the DMMA contraction -- which does not depend on the face operand rows -- in between.
-template <int DIM, int P, int KW>
-struct FaceRegs {
-  using EL = ElemT<DIM, P>;
-  static constexpr int NR = face_rounds<DIM, P, KW>();
-  double qp[NR][EL::C], nbr[NR][EL::C], lam_p[NR];
-  long long cnk[NR];
-};
-
-template <int DIM, int P, int KW, int NRE = FaceRegs<DIM, P, KW>::NR>
-__device__ __forceinline__ void face_issue(FaceRegs<DIM, P, KW>& R, const int* flc, const int* fn, const int* perm,
-                                           const Div3Small<DIM, P, KW>& M, const DiscDev& d,
-                                           const double* __restrict__ q, const double* __restrict__ T,
-                                           const double* __restrict__ ghost, const double* __restrict__ Tghost,
-                                           int nel, int lane) {
-  using EL = ElemT<DIM, P>;
-  constexpr int C = EL::C, NP = EL::NP, NFP = EL::NFP;
-  constexpr int NR = FaceRegs<DIM, P, KW>::NR;
-  const long long E = d.E, G = d.G;
-#pragma unroll
-  for (int k = 0; k < NRE; ++k) {
-    R.cnk[k] = -1;
-    const int flk = flc[k * 32 + lane];
-    const int e = flk & 3, f = (flk >> 2) & 3, m = (flk >> 4) & 15;
-    if (flk >= 0 && e < nel) {
-      const long long cn = M.conn[e][f];
-      R.cnk[k] = cn;
-      const long long nb = DGB_CONN_NB(cn);
-      const int nf = DGB_CONN_NF(cn);
-      const int jp = fn[nf * NFP + perm[DGB_CONN_PERM(cn) * NFP + m]];
-      const bool in_ghost = nb >= E;
-      const long long pstride = (in_ghost ? G : E) * NP;
-      const long long off = (in_ghost ? nb - E : nb) * NP + jp;
-      const double* qbase = (in_ghost ? ghost : q) + off;
-      const double* tbase = (in_ghost ? Tghost : T) + off;
-      const int r0 = nf == 0 ? 0 : nf - 1;
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        R.qp[k][c] = qbase[c * pstride];
-        R.nbr[k][c] = tbase[(r0 * C + c) * pstride];
-      }
-      R.lam_p[k] = tbase[(DIM * C) * pstride];
-    }
-  }
-}
-
-template <int DIM, int P, int KW, int NRE = FaceRegs<DIM, P, KW>::NR>
-__device__ __forceinline__ void face_finish(FaceRegs<DIM, P, KW>& R, const int* flc, const int* fn, const int* perm,
-                                            const Div3Small<DIM, P, KW>& M, double* Fs, const DiscDev& d,
-                                            const double* __restrict__ T, const double* __restrict__ Tghost,
-                                            const Phys& ph, long long e0, int nel, int lane) {
-  using EL = ElemT<DIM, P>;
-  constexpr int C = EL::C, NP = EL::NP, NF = EL::NF, NFP = EL::NFP;
-  constexpr int NR = FaceRegs<DIM, P, KW>::NR;
-  const long long E = d.E, G = d.G;
-  // second wave: a neighbour's face 0 is the sum of its DIM rows; fetch the other DIM-1 now
-  double ex[NR][C];
-#pragma unroll
-  for (int k = 0; k < NRE; ++k) {
-    if (R.cnk[k] >= 0 && DGB_CONN_NF(R.cnk[k]) == 0 && DGB_CONN_BC(R.cnk[k]) == 0) {
-      const int flk = flc[k * 32 + lane];
-      const long long nb = DGB_CONN_NB(R.cnk[k]);
-      const int m = (flk >> 4) & 15;
-      const int jp = fn[perm[DGB_CONN_PERM(R.cnk[k]) * NFP + m]];
-      const bool in_ghost = nb >= E;
-      const long long pstride = (in_ghost ? G : E) * NP;
-      const double* tbase = (in_ghost ? Tghost : T) + (in_ghost ? nb - E : nb) * NP + jp;
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        double t = tbase[(C + c) * pstride];
-#pragma unroll
-        for (int r = 2; r < DIM; ++r) t += tbase[(r * C + c) * pstride];
-        ex[k][c] = t;
-      }
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < NRE; ++k) {
-    if (R.cnk[k] >= 0) {
-      const int flk = flc[k * 32 + lane];
-      const int e = flk & 3, f = (flk >> 2) & 3, jm = (flk >> 8) & 255, fm = (flk >> 16) & 255;
-      const int nf = DGB_CONN_NF(R.cnk[k]), bc = DGB_CONN_BC(R.cnk[k]);
-      const double sj = M.sj[e][f];
-      const double lam_m = M.Lam[e * NP + jm];
-      double qm[C];
-#pragma unroll
-      for (int c = 0; c < C; ++c) qm[c] = M.Qs[(c * KW + e) * NP + jm];
-      double* fs = Fs + e * EL::LDF + fm;
-      if (bc == 0) {
-        const double pen = sj * fmax(lam_m, R.lam_p[k]);
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-          const double nb_ = nf == 0 ? R.nbr[k][c] + ex[k][c] : -R.nbr[k][c];
-          fs[c * (KW * EL::LDF)] = 0.5 * (nb_ - pen * (qm[c] - R.qp[k][c]));
-        }
-      } else {
-        VecC<DIM> a_;
-#pragma unroll
-        for (int c = 0; c < C; ++c) a_.v[c] = qm[c];
-        const VecC<DIM> fb = boundary_operand<DIM>(bc, f, a_, T + (e0 + e) * NP + jm, E * NP, lam_m, sj,
-                                                   d.normals + (e0 + e) * NF + f, E * NF, ph);
-#pragma unroll
-        for (int c = 0; c < C; ++c) fs[c * (KW * EL::LDF)] = fb.v[c];
-      }
-    }
-  }
-}
-
 template <int DIM, int P, int KW, int NWARPS, bool GH>
 __global__ void __launch_bounds__(NWARPS * 32, 1)
 k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
@@ -1065,20 +808,6 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
   }
   TicketStream tks;
   tickets_init(tks, wb, counter, lane);
-#if DGB_DIV_LATE_ISSUE
-  // The first-wave gathers of block b+1 are issued right AFTER the contraction of block b and fly
-  // during its store, the staging of the next rows and the top of the next iteration -- phases that
-  // leave the L1/LSU pipe mostly alone (issuing them before the contraction, k_nsdiv5, lost 35 %).
-  constexpr int NRL = DGB_DIV_LATE_ROUNDS < NR ? DGB_DIV_LATE_ROUNDS : NR;   // rounds gathered early
-  FaceRegs<DIM, P, KW> R;
-  if (wb < nwblocks) {
-    const long long e0 = ebeg + wb * KW;
-    cp_async_wait<1>();                  // S(0)
-    __syncwarp();
-    face_issue<DIM, P, KW, NRL>(R, S.flc, S.fn, S.perm, W.sm[0], d, q, T, ghost, Tghost,
-                                (int)((eend - e0) < (long long)KW ? (eend - e0) : (long long)KW), lane);
-  }
-#endif
 
   // cp.async groups retire in order: S(b), T(b), S(b+1), T(b+1), ...
   DGB_WTICK_INIT
@@ -1108,31 +837,7 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
     //      constant coefficients and lives in the folded volume matrix, so this phase needs only
     //      q, lam and the connectivity of the block -- not its T rows, which are still landing.
     //      Fs = (nbr - sJ max(lam-, lam+) (q- - q+)) / 2,  nbr = sJ F+.n+ gathered from the neighbour.
-#if DGB_DIV_SPLIT_MMA
-    // gathers of the whole block in flight ... under the volume half of the contraction
-    FaceRegs<DIM, P, KW> R;
-    face_issue<DIM, P, KW>(R, S.flc, S.fn, S.perm, M, d, q, T, ghost, Tghost, nel, lane);
-    DGB_WTICK(1);
-    cp_async_wait<1>();                  // T(b) has landed
-    __syncwarp();
-    DGB_WTICK(2);
-    double acc[WS::NTILE][EL::NI][2];
-#pragma unroll
-    for (int mt = 0; mt < WS::NTILE; ++mt)
-#pragma unroll
-      for (int ni = 0; ni < EL::NI; ++ni) { acc[mt][ni][0] = 0.0; acc[mt][ni][1] = 0.0; }
-    mma_block<EL::NI, WS::NTILE>(acc, W.Ts, EL::LDV, S.Wv, EL::LDV, EL::KV / 4, lane);
-    face_finish<DIM, P, KW>(R, S.flc, S.fn, S.perm, M, W.Fs, d, T, Tghost, ph, e0, nel, lane);
-    __syncwarp();
-    mma_block<EL::NI, WS::NTILE>(acc, W.Fs, EL::LDF, S.Wl, EL::LDF, EL::KF / 4, lane);
-#else
-#if DGB_DIV_LATE_ISSUE
-    face_finish<DIM, P, KW, NRL>(R, S.flc, S.fn, S.perm, M, W.Fs, d, T, Tghost, ph, e0, nel, lane);
-    if (NRL < NR)                        // the remaining rounds are gathered in place
-      div_face_phase<DIM, P, KW, NB, (DGB_DIV_LAZY_EX != 0), NRL, GH>(S.flc, S.fn, S.perm, M, W.Fs, d, q, T, ghost, Tghost, ph, e0, nel, lane);
-#else
     div_face_phase<DIM, P, KW, NB, (DGB_DIV_LAZY_EX != 0), 0, GH>(S.flc, S.fn, S.perm, M, W.Fs, d, q, T, ghost, Tghost, ph, e0, nel, lane);
-#endif
     DGB_WTICK(1);
     cp_async_wait<1>();                  // T(b) has landed
     __syncwarp();
@@ -1146,19 +851,11 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
       for (int ni = 0; ni < EL::NI; ++ni) { acc[mt][ni][0] = 0.0; acc[mt][ni][1] = 0.0; }
     mma_block<EL::NI, WS::NTILE>(acc, W.Ts, EL::LDV, S.Wv, EL::LDV, EL::KV / 4, lane);
     mma_block<EL::NI, WS::NTILE>(acc, W.Fs, EL::LDF, S.Wl, EL::LDF, EL::KF / 4, lane);
-#endif
     double rj[WS::NTILE];
 #pragma unroll
     for (int mt = 0; mt < WS::NTILE; ++mt) rj[mt] = M.rj[(mt * 8 + (lane >> 2)) % KW];
     __syncwarp();                        // all operand rows consumed: the next block may land on them
     DGB_WTICK(3);
-#if DGB_DIV_LATE_ISSUE
-    if (nel1 > 0) {
-      cp_async_wait<0>();                // S(b+1) has landed (staged a whole face phase + contraction ago)
-      __syncwarp();
-      face_issue<DIM, P, KW, NRL>(R, S.flc, S.fn, S.perm, W.sm[buf ^ 1], d, q, T, ghost, Tghost, nel1, lane);
-    }
-#endif
     if (nel1 > 0) div_stage_rows<DIM, P, KW>(W.Ts, d, T, e1, nel1, lane);
     cp_async_commit();                   // T(b+1)
 

@@ -2,9 +2,6 @@
 // launch configuration.  Kernels: dgb_kernels_flux.cuh.
 #include "dgb_internal.h"
 #include "dgb_kernels_flux.cuh"
-#if DGB_EXPERIMENTAL
-#include "dgb_kernels_flux_experimental.cuh"
-#endif
 
 #include <cstdlib>
 #include <string>
@@ -74,109 +71,11 @@ int launch_div(const dgb_disc* d, const double* q, const double* T, const double
   return DGB_OK;
 }
 
-// DGB_DIV_KERNEL selects the pass-2 kernel: 3 = k_nsdiv3 (default).  4 / 5 / 6 = the experimental
-// variants of dgb_kernels_flux_experimental.cuh (producer/consumer pairs, cross-block gather pipeline,
-// TMA bulk staging): correct, measured slower, only in builds with -DDGB_EXPERIMENTAL=1.
-int div_kernel() {
-  static int v = -1;
-  if (v < 0) v = env_int("DGB_DIV_KERNEL", 3);
-  return v;
-}
-
-#if DGB_EXPERIMENTAL
-#ifndef DGB_DIV_PAIRS
-#define DGB_DIV_PAIRS 8
-#endif
-template <int DIM, int P> struct CfgP {
-  static constexpr int KW = DIM == 3 ? 3 : 4;
-  static constexpr size_t per = sizeof(dgb::Div4Pair<DIM, P, KW>);
-  static constexpr size_t fixed = sizeof(dgb::Div4Smem<DIM, P, KW, 1>) - per;
-  static constexpr int NPAIR = fit_warps(fixed, per, DGB_DIV_PAIRS);
-};
-
-template <int DIM, int P>
-int launch_div4(const dgb_disc* d, const double* q, const double* T, const double* ghost, const double* Tghost,
-                const dgb::Epilogue& ep, const dgb::Phys& ph, long long ebeg, long long eend, cudaStream_t st) {
-  using C = CfgP<DIM, P>;
-  auto kern = dgb::k_nsdiv4<DIM, P, C::KW, C::NPAIR>;
-  const size_t smem = sizeof(dgb::Div4Smem<DIM, P, C::KW, C::NPAIR>);
-  const long long nwb = (eend - ebeg + C::KW - 1) / C::KW;
-  if (nwb == 0) return DGB_OK;
-  static bool configured = false;
-  if (!configured) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured = true; }
-  const long long need = (nwb + C::NPAIR - 1) / C::NPAIR;
-  const int grid = (int)(need < dgb_num_sms() ? need : dgb_num_sms());
-  DGB_CUDA(cudaMemsetAsync(d->counters + 1, 0, sizeof(unsigned long long), st));
-  kern<<<grid, C::NPAIR * 64, smem, st>>>(d->dev, q, T, ghost, Tghost, ep, ph, ebeg, eend, nwb, d->counters + 1);
-  DGB_CUDA(cudaGetLastError());
-  return DGB_OK;
-}
-
-#ifndef DGB_DIV5_WARPS
-#define DGB_DIV5_WARPS 8
-#endif
-template <int DIM, int P> struct Cfg5 {
-  static constexpr int KW = DIM == 3 ? 3 : 4;
-  static constexpr size_t per = sizeof(dgb::Div5Warp<DIM, P, KW>);
-  static constexpr size_t fixed = sizeof(dgb::Div5Smem<DIM, P, KW, 1>) - per;
-  static constexpr int NW = fit_warps(fixed, per, DGB_DIV5_WARPS);
-};
-
-template <int DIM, int P>
-int launch_div5(const dgb_disc* d, const double* q, const double* T, const double* ghost, const double* Tghost,
-                const dgb::Epilogue& ep, const dgb::Phys& ph, long long ebeg, long long eend, cudaStream_t st) {
-  using C = Cfg5<DIM, P>;
-  auto kern = dgb::k_nsdiv5<DIM, P, C::KW, C::NW>;
-  const size_t smem = sizeof(dgb::Div5Smem<DIM, P, C::KW, C::NW>);
-  const long long nwb = (eend - ebeg + C::KW - 1) / C::KW;
-  if (nwb == 0) return DGB_OK;
-  static bool configured = false;
-  if (!configured) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured = true; }
-  const long long need = (nwb + C::NW - 1) / C::NW;
-  const int grid = (int)(need < dgb_num_sms() ? need : dgb_num_sms());
-  DGB_CUDA(cudaMemsetAsync(d->counters + 1, 0, sizeof(unsigned long long), st));
-  kern<<<grid, C::NW * 32, smem, st>>>(d->dev, q, T, ghost, Tghost, ep, ph, ebeg, eend, nwb, d->counters + 1);
-  DGB_CUDA(cudaGetLastError());
-  return DGB_OK;
-}
-
-#ifndef DGB_DIV6_WARPS
-#define DGB_DIV6_WARPS 8
-#endif
-template <int DIM, int P> struct Cfg6 {
-  static constexpr int KW = DIM == 3 ? 3 : 4;
-  static constexpr size_t per = sizeof(dgb::Div6Warp<DIM, P, KW>);
-  static constexpr size_t fixed = sizeof(dgb::Div6Smem<DIM, P, KW, 1>) - per;
-  static constexpr int NW = fit_warps(fixed, per, DGB_DIV6_WARPS);
-};
-
-template <int DIM, int P>
-int launch_div6(const dgb_disc* d, const double* q, const double* T, const double* ghost, const double* Tghost,
-                const dgb::Epilogue& ep, const dgb::Phys& ph, long long ebeg, long long eend, cudaStream_t st) {
-  if constexpr (dgb::ElemT<DIM, P>::NP % 2 != 0 || DIM != 3) {
-    // bulk copies need 16-byte multiples: odd Np rows are not, nor are the 24-byte per-element
-    // geometry records of triangles
-    return launch_div<DIM, P>(d, q, T, ghost, Tghost, ep, ph, ebeg, eend, st);
-  } else {
-    using C = Cfg6<DIM, P>;
-    auto kern = dgb::k_nsdiv6<DIM, P, C::KW, C::NW>;
-    const size_t smem = sizeof(dgb::Div6Smem<DIM, P, C::KW, C::NW>);
-    const long long nwb = (eend - ebeg + C::KW - 1) / C::KW;
-    if (nwb == 0) return DGB_OK;
-    static bool configured = false;
-    if (!configured) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured = true; }
-    const long long need = (nwb + C::NW - 1) / C::NW;
-    const int grid = (int)(need < dgb_num_sms() ? need : dgb_num_sms());
-    DGB_CUDA(cudaMemsetAsync(d->counters + 1, 0, sizeof(unsigned long long), st));
-    kern<<<grid, C::NW * 32, smem, st>>>(d->dev, q, T, ghost, Tghost, ep, ph, ebeg, eend, nwb, d->counters + 1);
-    DGB_CUDA(cudaGetLastError());
-    return DGB_OK;
-  }
-}
-
-#endif  // DGB_EXPERIMENTAL
-
+#ifdef DGB_ONLY_3D_P3   // fast kernel-tuning builds (scripts/ab_variants.py)
+#define DGB_FOR_EACH_ELEMENT(X) X(3, 3)
+#else
 #define DGB_FOR_EACH_ELEMENT(X) X(2, 1) X(2, 2) X(2, 3) X(2, 4) X(3, 1) X(3, 2) X(3, 3) X(3, 4)
+#endif
 
 void make_phys(dgb::Phys& ph, int C, const double* qfar, const double* phys) {
   ph.gamma = phys ? phys[0] : 1.4; ph.mu = phys ? phys[1] : 0.0; ph.kappa = phys ? phys[2] : 0.0;
@@ -295,17 +194,8 @@ static int ns_div_impl(const dgb_disc* d, const double* q, const double* T, cons
   if ((rc = check_range(d, ebegin, eend))) return rc;
   if (d->dev.G > 0 && !Tghost) return dgb_fail(DGB_ERR_INVALID, "ghost elements need the ghost flux planes");
   dgb::Phys ph; make_phys(ph, d->dim + 2, qfar, phys);
-#if DGB_EXPERIMENTAL
-#define X(DIM, P) if (d->dim == DIM && d->order == P)                                                         \
-    return div_kernel() == 4 ? launch_div4<DIM, P>(d, q, T, ghost, Tghost, ep, ph, ebegin, eend, (cudaStream_t)stream) \
-         : div_kernel() == 5 ? launch_div5<DIM, P>(d, q, T, ghost, Tghost, ep, ph, ebegin, eend, (cudaStream_t)stream) \
-         : div_kernel() == 6 ? launch_div6<DIM, P>(d, q, T, ghost, Tghost, ep, ph, ebegin, eend, (cudaStream_t)stream) \
-                             : launch_div<DIM, P>(d, q, T, ghost, Tghost, ep, ph, ebegin, eend, (cudaStream_t)stream);
-#else
-  if (div_kernel() != 3) return dgb_fail(DGB_ERR_INVALID, "DGB_DIV_KERNEL != 3 needs a library built with -DDGB_EXPERIMENTAL=1");
 #define X(DIM, P) if (d->dim == DIM && d->order == P)                                                         \
     return launch_div<DIM, P>(d, q, T, ghost, Tghost, ep, ph, ebegin, eend, (cudaStream_t)stream);
-#endif
   DGB_FOR_EACH_ELEMENT(X)
 #undef X
   return dgb_fail(DGB_ERR_INVALID, "unsupported (dim, order)");

@@ -139,6 +139,35 @@ def test_out_of_bounds_map_rejected(gpu):
         EulerOperator(d, farfield=FARFIELD[3]).rhs(d.from_numpy(random_state(3, d.nelements, d.Np)))
 
 
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("order,n,bc", [(3, 16, "periodic"), (3, 24, "mixed"), (4, 16, "mixed")])
+def test_midsize_parity(gpu, order, n, bc):
+    """Direct oracle comparison at sizes where the persistent-kernel machinery is exercised: 24.6 k /
+    82.9 k elements = 5-23 blocks per warp of a full grid (work tickets two deep, double-buffered
+    staging across blocks, early gathers of the next block), mixed boundaries, and the odd-Np order-4
+    path.  Same 1e-12 bar as the small cases."""
+    cpu = NumpyArrayContext()
+    dc, dg = make_dcoll(cpu, 3, order, n, bc), make_dcoll(gpu, 3, order, n, bc)
+    q0 = random_state(3, dc.nelements, dc.Np, seed=11)
+    q0s = smooth_state(dc.nodes())
+    for Op, kw, qq in [(NavierStokesOperator, {"mu": 2e-2}, q0), (EulerOperator, {}, q0),
+                       (NavierStokesOperator, {"mu": 1e-3}, q0s)]:
+        oc = Op(dc, farfield=FARFIELD[3], **kw)
+        og = Op(dg, farfield=FARFIELD[3], **kw)
+        ref = dc.to_numpy(oc.rhs(dc.from_numpy(qq)))
+        got = dg.to_numpy(og.rhs(dg.from_numpy(qq)))
+        assert rel_err(got, ref) <= TOL_RHS, (Op.__name__, rel_err(got, ref))
+        if Op is NavierStokesOperator and qq is q0:
+            tref = np.asarray(cpu.to_numpy(oc.flux(dc.from_numpy(qq))))
+            tgot = np.asarray(gpu.to_numpy(og.flux(dg.from_numpy(qq))))
+            assert rel_err(tgot, tref) <= TOL_RHS, ("flux planes", rel_err(tgot, tref))
+            # RK-fused epilogue at this size: out1 = a1*x1 + b1*rhs, out2 = a2*x2 + b2*rhs
+            qd = dg.from_numpy(qq)
+            o1, o2 = og.rhs_rk(qd, qd, qd, (1.0, 0.25, 0.5, -2.0))
+            assert rel_err(dg.to_numpy(o1), qq + 0.25 * ref) <= TOL_RHS
+            assert rel_err(dg.to_numpy(o2), 0.5 * qq - 2.0 * ref) <= TOL_RHS
+
+
 def test_run_to_run_bitwise(gpu):
     """No atomics anywhere on the path: two evaluations are bitwise identical."""
     d = make_dcoll(gpu, 3, 3, 3, "periodic")
@@ -194,8 +223,9 @@ def test_fused_rk_stage(gpu, dim, order, n, Op, kw):
         assert rel_err(dg.to_numpy(b2), dg.to_numpy(a2)) <= 1e-12
 
 
-@pytest.mark.parametrize("dim,n,per,nparts", [(3, 3, True, 2), (2, 4, False, 3)])
-def test_ghost_elements_on_device(gpu, dim, n, per, nparts):
+@pytest.mark.parametrize("dim,order,n,per,nparts", [(3, 3, 3, True, 2), (2, 3, 4, False, 3), (3, 3, 4, True, 4), (3, 3, 4, False, 8),
+                                                         (3, 4, 3, True, 2), (3, 4, 4, False, 4), (3, 4, 4, True, 8)])
+def test_ghost_elements_on_device(gpu, dim, order, n, per, nparts):
     """Partitioned meshes on the device: halo packing kernel + ghost-element gathers in the fused
     kernels, with the exchange itself looped back on the host (this box has one GPU)."""
     from paper_2512_17101_b200 import DGDiscretization, box_mesh
@@ -205,12 +235,12 @@ def test_ghost_elements_on_device(gpu, dim, n, per, nparts):
     cpu = NumpyArrayContext()
     mesh = box_mesh((n,) * dim, (-1,) * dim, (1,) * dim, periodic=(per,) * dim)
     bc = None if per else {k: (BC_WALL if k % 2 else BC_FARFIELD) for k in range(1, 2 * dim + 1)}
-    d = DGDiscretization(cpu, mesh, 3, bc_map=bc)
+    d = DGDiscretization(cpu, mesh, order, bc_map=bc)
     q0 = random_state(dim, d.nelements, d.Np, seed=5)
     ref = d.to_numpy(NavierStokesOperator(d, farfield=FARFIELD[dim], mu=2e-2).rhs(d.from_numpy(q0)))
     part = partition_elements(mesh, nparts)
     locs = [rank_mesh(mesh, part, r) for r in range(nparts)]
-    ds = [DGDiscretization(gpu, m, 3, bc_map=bc, ghost_elements=p.nghost) for m, p in locs]
+    ds = [DGDiscretization(gpu, m, order, bc_map=bc, ghost_elements=p.nghost) for m, p in locs]
     ops = [NavierStokesOperator(dd, farfield=FARFIELD[dim], mu=2e-2) for dd in ds]
     qs = [ds[r].from_numpy(q0[:, p.global_ids, :]) for r, (_, p) in enumerate(locs)]
     halos = [HaloExchange(gpu, p, object(), d.Np) for _, p in locs]
