@@ -25,6 +25,18 @@
 #pragma once
 #include "dgb_kernels_flux.cuh"
 
+#ifndef DGB_DIV7_LAZY_EX
+#define DGB_DIV7_LAZY_EX 0
+#endif
+#ifdef DGB_PHASE_TIMING
+// consumer warp 0 and producer warp 4 of every CTA accumulate the cycles they spend per phase
+#define DGB_T7(k) do { if (lane == 0 && (warp == 0 || warp == 4)) { long long t_ = clock64(); d.timing[blockIdx.x * 8 + (k)] += t_ - t7last; t7last = t_; } } while (0)
+#define DGB_T7_INIT long long t7last = clock64();
+#else
+#define DGB_T7(k) do { } while (0)
+#define DGB_T7_INIT
+#endif
+
 namespace dgb {
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -53,9 +65,17 @@ struct alignas(16) Div7Stage {
   // the rows that follow it in this struct; its accumulators are never stored and DMMA rows do not mix
   double Ts[NCOL * EL::LDV];          // T rows; the consumer leaves the contraction result in [col][0..NPR)
   double Fs[NCOL * EL::LDF];
-  Div3Small<DIM, P, KW> sm;           // producer-private small inputs of the block
   unsigned long long full, done;      // mbarriers: producer -> consumer, consumer -> producer
   long long more;                     // 0 = the producer has no further blocks (published with `full`)
+  long long pad_;
+};
+
+// A producer owns two operand stages (it runs the face phase of block b+1 while its consumer contracts
+// block b) and one private buffer of small inputs.
+template <int DIM, int P, int KW>
+struct alignas(16) Div7Prod {
+  Div7Stage<DIM, P, KW> st[2];
+  Div3Small<DIM, P, KW> sm;
 };
 
 template <int DIM, int P, int KW, int NPROD, int NIR>
@@ -64,7 +84,7 @@ struct Div7Smem {
   static constexpr bool WSM = NIR < EL::NI;             // some node tiles come from shared memory
   double Wv[WSM ? EL::NPR * EL::LDV : 2];
   double Wl[WSM ? EL::NPR * EL::LDF : 2];
-  Div7Stage<DIM, P, KW> st[NPROD];
+  Div7Prod<DIM, P, KW> pr[NPROD];
   int fn[EL::NF * EL::NFP];
   int perm[EL::NPERM * EL::NFP];
   int flc[face_rounds<DIM, P, KW>() * 32];
@@ -104,10 +124,10 @@ k_nsdiv7(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
   }
   for (int n = tid; n < NF * NFP; n += NT) S.fn[n] = d.tables[n];
   for (int n = tid; n < EL::NPERM * NFP; n += NT) S.perm[n] = d.tables[NF * NFP + n];
-  for (int n = tid; n < NPROD * (int)(sizeof(ST) / 8); n += NT) reinterpret_cast<double*>(&S.st[0])[n] = 0.0;
+  for (int n = tid; n < NPROD * (int)(sizeof(Div7Prod<DIM, P, KW>) / 8); n += NT) reinterpret_cast<double*>(&S.pr[0])[n] = 0.0;
   __syncthreads();
   for (int n = tid; n < NR * 32; n += NT) S.flc[n] = face_lane_code<DIM, P, KW>(S.fn, n);
-  if (tid < NPROD) { mbar_init(&S.st[tid].full, 1); mbar_init(&S.st[tid].done, 1); }
+  if (tid < 2 * NPROD) { mbar_init(&S.pr[tid >> 1].st[tid & 1].full, 1); mbar_init(&S.pr[tid >> 1].st[tid & 1].done, 1); }
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
 
@@ -126,17 +146,21 @@ k_nsdiv7(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
     }
     const double* wvs = S.Wv + r * EL::LDV + kq;     // shared-memory tiles NIR..NI-1
     const double* wls = S.Wl + r * EL::LDF + kq;
-    unsigned fin = 0, par = 0;                       // per-producer bit masks: finished / expected parity of `full`
+    // per-producer bit masks: finished / stage the producer fills next / expected parity of `full` per stage
+    unsigned fin = 0, cur = 0, par = 0;
     const int ng = (NPROD - warp + 3) / 4;           // this consumer's producers: stages warp, warp + 4, ...
     int alive = ng, g = 0;
+    DGB_T7_INIT
     while (alive > 0) {
       ST* st;
       for (;;) {
-        st = &S.st[g * 4 + warp];
-        if (!((fin >> g) & 1) && mbar_test(&st->full, (par >> g) & 1)) break;
+        const int sidx = (cur >> g) & 1;
+        st = &S.pr[g * 4 + warp].st[sidx];
+        if (!((fin >> g) & 1) && mbar_test(&st->full, (par >> (2 * g + sidx)) & 1)) break;
         g = g + 1 >= ng ? 0 : g + 1;
       }
       if (st->more == 0) { fin |= 1u << g; --alive; continue; }
+      DGB_T7(0);
       double acc[MT][NI][2];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
@@ -185,15 +209,17 @@ k_nsdiv7(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&st->done);
-      par ^= 1u << g;
+      DGB_T7(1);
+      par ^= 1u << (2 * g + ((cur >> g) & 1));
+      cur ^= 1u << g;
       g = g + 1 >= ng ? 0 : g + 1;
     }
   } else {
     // ======================================= producer =======================================
     if (RG::PROD > 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(RG::PROD > 0 ? RG::PROD : 24));
-    const int p = warp - 4;                          // stage index; consumer = p & 3
+    const int p = warp - 4;                          // producer index; its consumer is warp p & 3
     if (p >= NPROD) return;
-    ST& W = S.st[p];
+    Div7Prod<DIM, P, KW>& W = S.pr[p];
     const long long wstride = (long long)gridDim.x * NPROD;
     long long wb = (long long)blockIdx.x * NPROD + p;
     auto nel_of = [&](long long wbx) -> int {
@@ -201,21 +227,62 @@ k_nsdiv7(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
       const long long e = ebeg + wbx * KW;
       return (int)((eend - e) < (long long)KW ? (eend - e) : (long long)KW);
     };
+    DGB_T7_INIT
+    // 1/J and the (RK-fused) store of a finished block, straight from its result rows: KW*Np consecutive
+    // doubles per field in global memory, so every store instruction is fully coalesced
+    auto retire = [&](ST& st, int parity, long long e0, int nelx, const double (&rj)[KW]) {
+      mbar_wait(&st.done, parity);
+      DGB_T7(5);
+      constexpr int CH = (NP % 2 == 0) ? 2 : 1, NPC = NP / CH;
+#pragma unroll
+      for (int t0 = 0; t0 < KW * NPC; t0 += 32) {
+        const int t = t0 + lane;
+        const int e = t / NPC, j = CH * (t - e * NPC);
+        if (t < KW * NPC && e < nelx) {
+          double s = rj[0];
+#pragma unroll
+          for (int k = 1; k < KW; ++k) s = e == k ? rj[k] : s;
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            const long long idx = ((long long)c * E + e0 + e) * NP + j;
+            if (CH == 2) {
+              const double2 v = *reinterpret_cast<const double2*>(st.Ts + (c * KW + e) * EL::LDV + j);
+              store_pair<NP>(ep, idx, j, s * v.x, s * v.y);
+            } else {
+              const double v = s * st.Ts[(c * KW + e) * EL::LDV + j];
+              ep.out1[idx] = ep.x1 ? ep.a1 * ep.x1[idx] + ep.b1 * v : ep.b1 * v;
+              if (ep.out2) ep.out2[idx] = ep.a2 * ep.x2[idx] + ep.b2 * v;
+            }
+          }
+        }
+      }
+      __syncwarp();                                  // result rows consumed: this stage may be refilled
+      DGB_T7(6);
+    };
     int nel = nel_of(wb);
     if (nel > 0) div_stage_small<DIM, P, KW>(W.sm, d, q, T, ebeg + wb * KW, nel, lane);
     cp_async_commit();                               // S(b)
     TicketStream tks;
     tickets_init(tks, wb, counter, lane);
     int it = 0;
+    long long e0_prev = 0;
+    int nel_prev = 0;
+    double rj_prev[KW];
+#pragma unroll
+    for (int e = 0; e < KW; ++e) rj_prev[e] = 0.0;
+    // cp.async groups retire in order: S(b), T(b), S(b+1), T(b+1), ...
     while (nel > 0) {
+      ST& st = W.st[it & 1];                         // free: the block that used it two iterations ago has been retired
       const long long e0 = ebeg + wb * KW;
-      div_stage_rows<DIM, P, KW>(W.Ts, d, T, e0, nel, lane);
+      div_stage_rows<DIM, P, KW>(st.Ts, d, T, e0, nel, lane);
       cp_async_commit();                             // T(b)
       const long long wb_next = tickets_next(tks, wstride, counter, lane);
       const int nel1 = nel_of(wb_next);
       cp_async_wait<1>();                            // S(b) has landed; T(b) may still be in flight
       __syncwarp();
-      div_face_phase<DIM, P, KW, NB, false, 0, GH>(S.flc, S.fn, S.perm, W.sm, W.Fs, d, q, T, ghost, Tghost, ph, e0, nel, lane);
+      DGB_T7(2);
+      div_face_phase<DIM, P, KW, NB, (DGB_DIV7_LAZY_EX != 0), 0, GH, (DGB_DIV_INBLOCK != 0), 0>(S.flc, S.fn, S.perm, W.sm, st.Fs, d, q, T, ghost, Tghost, ph, e0, nel, lane, st.Ts);
+      DGB_T7(3);
       double rj[KW];
 #pragma unroll
       for (int e = 0; e < KW; ++e) rj[e] = W.sm.rj[e];
@@ -223,56 +290,27 @@ k_nsdiv7(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
       if (nel1 > 0) div_stage_small<DIM, P, KW>(W.sm, d, q, T, ebeg + wb_next * KW, nel1, lane);
       cp_async_commit();                             // S(b+1)
       cp_async_wait<1>();                            // T(b) has landed
-      if (lane == 0) W.more = 1;
+      if (lane == 0) st.more = 1;
       __syncwarp();
-      if (lane == 0) mbar_arrive(&W.full);
-      mbar_wait(&W.done, it & 1);
-      // ---- 1/J and the (RK-fused) store, straight from the result rows: KW*Np consecutive doubles per field ----
-      if (NP % 2 == 0) {
-        constexpr int NPC = NP / 2;
+      if (lane == 0) mbar_arrive(&st.full);
+      DGB_T7(4);
+      // the previous block went to the consumer a whole face phase ago: retire it now
+      if (it > 0) retire(W.st[(it - 1) & 1], ((it - 1) >> 1) & 1, e0_prev, nel_prev, rj_prev);
+      e0_prev = e0; nel_prev = nel;
 #pragma unroll
-        for (int t0 = 0; t0 < KW * NPC; t0 += 32) {
-          const int t = t0 + lane;
-          const int e = t / NPC, j = 2 * (t - e * NPC);
-          if (t < KW * NPC && e < nel) {
-            double s = rj[0];
-#pragma unroll
-            for (int k = 1; k < KW; ++k) s = e == k ? rj[k] : s;
-#pragma unroll
-            for (int c = 0; c < C; ++c) {
-              const double2 v = *reinterpret_cast<const double2*>(W.Ts + (c * KW + e) * EL::LDV + j);
-              store_pair<NP>(ep, ((long long)c * E + e0 + e) * NP + j, j, s * v.x, s * v.y);
-            }
-          }
-        }
-      } else {
-#pragma unroll
-        for (int t0 = 0; t0 < KW * NP; t0 += 32) {
-          const int t = t0 + lane;
-          const int e = t / NP, j = t - e * NP;
-          if (t < KW * NP && e < nel) {
-            double s = rj[0];
-#pragma unroll
-            for (int k = 1; k < KW; ++k) s = e == k ? rj[k] : s;
-#pragma unroll
-            for (int c = 0; c < C; ++c) {
-              const long long idx = ((long long)c * E + e0 + e) * NP + j;
-              const double v = s * W.Ts[(c * KW + e) * EL::LDV + j];
-              ep.out1[idx] = ep.x1 ? ep.a1 * ep.x1[idx] + ep.b1 * v : ep.b1 * v;
-              if (ep.out2) ep.out2[idx] = ep.a2 * ep.x2[idx] + ep.b2 * v;
-            }
-          }
-        }
-      }
-      __syncwarp();                                  // result rows consumed: the next block's T rows may land
+      for (int e = 0; e < KW; ++e) rj_prev[e] = rj[e];
       wb = wb_next;
       nel = nel1;
       ++it;
     }
     cp_async_wait<0>();
-    if (lane == 0) W.more = 0;
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&W.full);
+    if (it > 0) retire(W.st[(it - 1) & 1], ((it - 1) >> 1) & 1, e0_prev, nel_prev, rj_prev);
+    {
+      ST& st = W.st[it & 1];                         // end marker on the stage the consumer looks at next
+      if (lane == 0) st.more = 0;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&st.full);
+    }
   }
 }
 

@@ -23,6 +23,9 @@
 #ifndef DGB_DIV_NB
 #define DGB_DIV_NB 2
 #endif
+#ifndef DGB_DIV_INBLOCK
+#define DGB_DIV_INBLOCK 0
+#endif
 #ifndef DGB_DIV_LAZY_EX
 #define DGB_DIV_LAZY_EX 0
 #endif
@@ -645,12 +648,21 @@ __device__ __noinline__ VecC<DIM> boundary_operand(int bc, int f, VecC<DIM> qm_,
 // nbr = sJ F+.n+ (the own-side half lives in the folded volume matrix Wv2).  NB face nodes per
 // lane have their gathers in flight together; with LAZY the DIM-1 extra rows a neighbour's face 0
 // needs are fetched in a second wave (fewer live registers).
-template <int DIM, int P, int KW, int NB, bool LAZY, int K0 = 0, bool GH = true>
+//
+// INB: a neighbour inside the warp's own block is read from SHARED memory (its q, lam and T rows are
+// staged there anyway) instead of being gathered from L2.  ncu (profiles/r02_pass2_lsu.md): pass 2 is
+// bound by the L1/LSU wavefront queue, and two thirds of its wavefronts are these gathers -- every
+// (face, plane) row costs two 128-byte lines whatever the lane mapping.  With the Kuhn ordering of the
+// box meshes a third of all face sides are in-block.  `Ts_own` = the block's operand rows; the caller's
+// T rows are the cp.async group with TW younger groups behind it (waited for here, after the first
+// batch of global gathers has been issued).
+template <int DIM, int P, int KW, int NB, bool LAZY, int K0 = 0, bool GH = true, bool INB = false, int TW = 1>
 __device__ __forceinline__ void div_face_phase(const int* flc, const int* fn, const int* perm,
                                                const Div3Small<DIM, P, KW>& M, double* Fs, const DiscDev& d,
                                                const double* __restrict__ q, const double* __restrict__ T,
                                                const double* __restrict__ ghost, const double* __restrict__ Tghost,
-                                               const Phys& ph, long long e0, int nel, int lane) {
+                                               const Phys& ph, long long e0, int nel, int lane,
+                                               const double* Ts_own = nullptr) {
   using EL = ElemT<DIM, P>;
   constexpr int C = EL::C, NP = EL::NP, NF = EL::NF, NFP = EL::NFP, NFT = EL::NFT;
   constexpr int NR = face_rounds<DIM, P, KW>();
@@ -674,22 +686,67 @@ __device__ __forceinline__ void div_face_phase(const int* flc, const int* fn, co
           const long long nb = DGB_CONN_NB(cn);
           const int nf = DGB_CONN_NF(cn);
           const int jp = fn[nf * NFP + perm[DGB_CONN_PERM(cn) * NFP + m]];
-          const bool in_ghost = GH && nb >= E;
-          const long long nbl = in_ghost ? nb - E : nb;
-          const long long pstride = (in_ghost ? G : E) * NP;
-          const long long tps = t_plane_stride<NPLT, NP>(in_ghost ? G : E);
-          const double* qbase = (in_ghost ? ghost : q) + nbl * NP + jp;
-          const double* tbase = (in_ghost ? Tghost : T) + nbl * t_elem_stride<NPLT, NP>() + jp;
-          const int r0 = nf == 0 ? 0 : nf - 1;
+          // boundary faces take nothing from the neighbour slot (it names the element itself)
+          const bool skip = INB && (DGB_CONN_BC(cn) != 0 || (nb >= e0 && nb < e0 + nel));
+          if (!skip) {
+            const bool in_ghost = GH && nb >= E;
+            const long long nbl = in_ghost ? nb - E : nb;
+            const long long pstride = (in_ghost ? G : E) * NP;
+            const long long tps = t_plane_stride<NPLT, NP>(in_ghost ? G : E);
+            const double* qbase = (in_ghost ? ghost : q) + nbl * NP + jp;
+            const double* tbase = (in_ghost ? Tghost : T) + nbl * t_elem_stride<NPLT, NP>() + jp;
+            const int r0 = nf == 0 ? 0 : nf - 1;
 #pragma unroll
-          for (int c = 0; c < C; ++c) {
-            qp[b][c] = qbase[c * pstride];
-            nbr[b][c] = tbase[(r0 * C + c) * tps];
+            for (int c = 0; c < C; ++c) {
+              qp[b][c] = qbase[c * pstride];
+              nbr[b][c] = tbase[(r0 * C + c) * tps];
+            }
+            lam_p[b] = tbase[(DIM * C) * tps];
+            if (!LAZY && nf == 0) {
+#pragma unroll
+              for (int rc = 0; rc < (DIM - 1) * C; ++rc) ex[b][rc] = tbase[(C + rc) * tps];
+            }
           }
-          lam_p[b] = tbase[(DIM * C) * tps];
-          if (!LAZY && nf == 0) {
+        }
+      }
+    }
+    if (INB) {
+      if (k0 == K0) { cp_async_wait<TW>(); __syncwarp(); }      // the block's own T rows have landed
 #pragma unroll
-            for (int rc = 0; rc < (DIM - 1) * C; ++rc) ex[b][rc] = tbase[(C + rc) * tps];
+      for (int b = 0; b < NB; ++b) {
+        const int k = k0 + b;
+        if (k < NR && cnk[b] >= 0 && DGB_CONN_BC(cnk[b]) == 0) {
+          const long long nb = DGB_CONN_NB(cnk[b]);
+          if (nb >= e0 && nb < e0 + nel) {
+            const int eb = (int)(nb - e0);
+            const int flk = flc[k * 32 + lane];
+            const int m = (flk >> 4) & 15;
+            const int nf = DGB_CONN_NF(cnk[b]);
+            const int jp = fn[nf * NFP + perm[DGB_CONN_PERM(cnk[b]) * NFP + m]];
+            const int r0 = nf == 0 ? 0 : nf - 1;
+            const double* trow = Ts_own + eb * EL::LDV + jp;
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+              qp[b][c] = M.Qs[(c * KW + eb) * NP + jp];
+              nbr[b][c] = trow[c * (KW * EL::LDV) + r0 * EL::NPK];
+            }
+            lam_p[b] = M.Lam[eb * NP + jp];
+            if (nf == 0) {
+              if (LAZY) {
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                  double t = trow[c * (KW * EL::LDV) + EL::NPK];
+#pragma unroll
+                  for (int r = 2; r < DIM; ++r) t += trow[c * (KW * EL::LDV) + r * EL::NPK];
+                  ex[b][c] = t;
+                }
+              } else {
+#pragma unroll
+                for (int r = 1; r < DIM; ++r)
+#pragma unroll
+                  for (int c = 0; c < C; ++c) ex[b][(r - 1) * C + c] = trow[c * (KW * EL::LDV) + r * EL::NPK];
+              }
+            }
           }
         }
       }
@@ -698,7 +755,8 @@ __device__ __forceinline__ void div_face_phase(const int* flc, const int* fn, co
 #pragma unroll
       for (int b = 0; b < NB; ++b) {
         const int k = k0 + b;
-        if (k < NR && cnk[b] >= 0 && DGB_CONN_NF(cnk[b]) == 0 && DGB_CONN_BC(cnk[b]) == 0) {
+        const bool inblk = INB && cnk[b] >= 0 && DGB_CONN_NB(cnk[b]) >= e0 && DGB_CONN_NB(cnk[b]) < e0 + nel;
+        if (k < NR && cnk[b] >= 0 && !inblk && DGB_CONN_NF(cnk[b]) == 0 && DGB_CONN_BC(cnk[b]) == 0) {
           const int flk = flc[k * 32 + lane];
           const long long nb = DGB_CONN_NB(cnk[b]);
           const int m = (flk >> 4) & 15;
@@ -837,7 +895,7 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
     //      constant coefficients and lives in the folded volume matrix, so this phase needs only
     //      q, lam and the connectivity of the block -- not its T rows, which are still landing.
     //      Fs = (nbr - sJ max(lam-, lam+) (q- - q+)) / 2,  nbr = sJ F+.n+ gathered from the neighbour.
-    div_face_phase<DIM, P, KW, NB, (DGB_DIV_LAZY_EX != 0), 0, GH>(S.flc, S.fn, S.perm, M, W.Fs, d, q, T, ghost, Tghost, ph, e0, nel, lane);
+    div_face_phase<DIM, P, KW, NB, (DGB_DIV_LAZY_EX != 0), 0, GH, (DGB_DIV_INBLOCK != 0), 1>(S.flc, S.fn, S.perm, M, W.Fs, d, q, T, ghost, Tghost, ph, e0, nel, lane, W.Ts);
     DGB_WTICK(1);
     cp_async_wait<1>();                  // T(b) has landed
     __syncwarp();

@@ -2,6 +2,7 @@
 // launch configuration.  Kernels: dgb_kernels_flux.cuh.
 #include "dgb_internal.h"
 #include "dgb_kernels_flux.cuh"
+#include "dgb_kernels_div7.cuh"
 
 #include <cstdlib>
 #include <string>
@@ -10,6 +11,9 @@ namespace {
 
 // Measured on B200 (profiles/r01_flux_variants.md): pass 1 is fastest with 12 warps (164 registers, four
 // face nodes per lane in flight), pass 2 with 8 warps (235 registers, no spills, NB = 2).
+#ifndef DGB_DIV_KERNEL_DEFAULT
+#define DGB_DIV_KERNEL_DEFAULT 3
+#endif
 #ifndef DGB_FLUX_WARPS
 #define DGB_FLUX_WARPS 12
 #endif
@@ -70,6 +74,49 @@ int launch_div(const dgb_disc* d, const double* q, const double* T, const double
   DGB_CUDA(cudaGetLastError());
   return DGB_OK;
 }
+
+
+// ---- role-split pass 2 (k_nsdiv7, dgb_kernels_div7.cuh): 4 consumer warps + NPROD producer warps ----
+#ifndef DGB_DIV7_PRODUCERS
+#define DGB_DIV7_PRODUCERS 8
+#endif
+#ifndef DGB_DIV7_NB
+#define DGB_DIV7_NB 1
+#endif
+#ifndef DGB_DIV7_WREGS
+#define DGB_DIV7_WREGS 76          // doubles of W fragments a consumer lane may keep in registers
+#endif
+template <int DIM, int P> struct Cfg7 {
+  using EL = dgb::ElemT<DIM, P>;
+  static constexpr int KW = DIM == 3 ? 3 : 4;
+  static constexpr int per_tile = EL::KV / 4 + EL::KF / 4;
+  static constexpr int NIR = DGB_DIV7_WREGS / per_tile < EL::NI ? DGB_DIV7_WREGS / per_tile : EL::NI;
+  static constexpr size_t per = sizeof(dgb::Div7Prod<DIM, P, KW>);
+  static constexpr size_t fixed = sizeof(dgb::Div7Smem<DIM, P, KW, 1, NIR>) - per;
+  static constexpr int NPROD = fit_warps(fixed, per, DGB_DIV7_PRODUCERS);
+};
+
+template <int DIM, int P>
+int launch_div7(const dgb_disc* d, const double* q, const double* T, const double* ghost, const double* Tghost,
+                const dgb::Epilogue& ep, const dgb::Phys& ph, long long ebeg, long long eend, cudaStream_t st) {
+  using C = Cfg7<DIM, P>;
+  auto kern = d->dev.G > 0 ? dgb::k_nsdiv7<DIM, P, C::KW, C::NPROD, C::NIR, DGB_DIV7_NB, true>
+                           : dgb::k_nsdiv7<DIM, P, C::KW, C::NPROD, C::NIR, DGB_DIV7_NB, false>;
+  const size_t smem = sizeof(dgb::Div7Smem<DIM, P, C::KW, C::NPROD, C::NIR>);
+  const long long nwb = (eend - ebeg + C::KW - 1) / C::KW;
+  if (nwb == 0) return DGB_OK;
+  static bool configured[2] = {false, false};
+  if (!configured[d->dev.G > 0]) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured[d->dev.G > 0] = true; }
+  const long long need = (nwb + C::NPROD - 1) / C::NPROD;
+  const int grid = (int)(need < dgb_num_sms() ? need : dgb_num_sms());
+  DGB_CUDA(cudaMemsetAsync(d->counters + 1, 0, sizeof(unsigned long long), st));
+  kern<<<grid, 128 + 128 * ((C::NPROD + 3) / 4), smem, st>>>(d->dev, q, T, ghost, Tghost, ep, ph, ebeg, eend, nwb, d->counters + 1);
+  DGB_CUDA(cudaGetLastError());
+  return DGB_OK;
+}
+
+// DGB_DIV_KERNEL selects the pass-2 kernel at run time: 7 = role-split k_nsdiv7, 3 = warp-autonomous k_nsdiv3
+int div_kernel() { return env_int("DGB_DIV_KERNEL", DGB_DIV_KERNEL_DEFAULT); }   // read per launch: tests toggle it
 
 #ifdef DGB_ONLY_3D_P3   // fast kernel-tuning builds (scripts/ab_variants.py)
 #define DGB_FOR_EACH_ELEMENT(X) X(3, 3)
@@ -195,7 +242,8 @@ static int ns_div_impl(const dgb_disc* d, const double* q, const double* T, cons
   if (d->dev.G > 0 && !Tghost) return dgb_fail(DGB_ERR_INVALID, "ghost elements need the ghost flux planes");
   dgb::Phys ph; make_phys(ph, d->dim + 2, qfar, phys);
 #define X(DIM, P) if (d->dim == DIM && d->order == P)                                                         \
-    return launch_div<DIM, P>(d, q, T, ghost, Tghost, ep, ph, ebegin, eend, (cudaStream_t)stream);
+    return div_kernel() == 7 ? launch_div7<DIM, P>(d, q, T, ghost, Tghost, ep, ph, ebegin, eend, (cudaStream_t)stream) \
+                             : launch_div<DIM, P>(d, q, T, ghost, Tghost, ep, ph, ebegin, eend, (cudaStream_t)stream);
   DGB_FOR_EACH_ELEMENT(X)
 #undef X
   return dgb_fail(DGB_ERR_INVALID, "unsupported (dim, order)");

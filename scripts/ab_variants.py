@@ -15,24 +15,20 @@ PKG = os.path.join(ROOT, "paper_2512_17101_b200")
 
 VARIANTS = {
     "timing": ["DGB_PHASE_TIMING=1"],                 # scripts/phase_timing_flux.py
-    "experimental": ["DGB_EXPERIMENTAL=1"],           # + DGB_DIV_KERNEL=4|5|6 at run time
+    "timing7": ["DGB_PHASE_TIMING=1", "DGB_DIV_KERNEL_DEFAULT=7"],   # scripts/phase_timing_div7.py
+    "base": [],
+    "noinb": ["DGB_DIV_INBLOCK=0"],
+    "div7": ["DGB_DIV_KERNEL_DEFAULT=7"],
+    "div7_nb2": ["DGB_DIV_KERNEL_DEFAULT=7", "DGB_DIV7_NB=2"],
+    "div7_nb2_lazy": ["DGB_DIV_KERNEL_DEFAULT=7", "DGB_DIV7_NB=2", "DGB_DIV7_LAZY_EX=1"],
+    "div7_lazy": ["DGB_DIV_KERNEL_DEFAULT=7", "DGB_DIV7_LAZY_EX=1"],
+    "div7_p7": ["DGB_DIV_KERNEL_DEFAULT=7", "DGB_DIV7_PRODUCERS=7"],
+    "div7_p6": ["DGB_DIV_KERNEL_DEFAULT=7", "DGB_DIV7_PRODUCERS=6"],
     "trecord": ["DGB_T_RECORD=1"],                    # record-major flux planes (experiment: rhs only)
-    "pf600": ["DGB_L2_PREFETCH_BLOCKS=600"],
-    "pf2400": ["DGB_L2_PREFETCH_BLOCKS=2400"],
-    "pf8000": ["DGB_L2_PREFETCH_BLOCKS=8000"],
     "flux_w14": ["DGB_FLUX_WARPS=16"],
     "stcs": ["DGB_STREAMING_STORES=1"],
-    "tkd2": ["DGB_TICKET_DEPTH=2"],
     "tk2": ["DGB_TICKET_BLOCKS=2"],
-    "tk4": ["DGB_TICKET_BLOCKS=4"],
-    "tk8": ["DGB_TICKET_BLOCKS=8"],
-    "div_late": ["DGB_DIV_LATE_ISSUE=1"],
-    "div_late1": ["DGB_DIV_LATE_ISSUE=1", "DGB_DIV_LATE_ROUNDS=1"],
-    "div_late2": ["DGB_DIV_LATE_ISSUE=1", "DGB_DIV_LATE_ROUNDS=2"],
-    "flux_noearly": ["DGB_FLUX_EARLY_GATHER=0"],
-    "div_split": ["DGB_DIV_SPLIT_MMA=1"],
     "euler_w8": ["DGB_EULER_WARPS=8"],
-    "flux_nb2": ["DGB_FLUX_NB=2"],
     "div_w12_nb1": ["DGB_DIV_WARPS=12", "DGB_DIV_NB=1"],
 }
 
@@ -43,11 +39,11 @@ def lib(name):
 
 def main():
     names = [a for a in sys.argv[1:] if a in VARIANTS] or list(VARIANTS)
-    kernels = {"experimental": ["4", "5", "6"]}
+    kernels = {}
     if "--build" in sys.argv:
         # only dgb_nsflux.cu depends on the knobs: compile the other translation units once
         from paper_2512_17101_b200.csrc.build import FLAGS, HERE
-        cflags = [f for f in FLAGS if f != "-shared"]
+        cflags = [f for f in FLAGS if f != "-shared"] + (["-DDGB_ONLY_3D_P3"] if "--p3only" in sys.argv else [])
         objs = []
         for src in ("dgb200.cu", "dgb_arrayops.cu"):
             obj = os.path.join("/tmp", src.replace(".cu", ".o"))
