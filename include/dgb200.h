@@ -194,6 +194,32 @@ int dgb_ew_where(void* out_dev, int out_dtype,
                  const void* a_dev, int a_dtype, const int64_t* a_strides,
                  const void* b_dev, int b_dtype, const int64_t* b_strides,
                  int rank, const int64_t* shape, void* stream);
+
+/* Fused elementwise program: a chain of the elementwise operations above evaluated in ONE pass --
+ * the hand-written counterpart of the reference's loop fusion + array contraction for pointwise
+ * chains (ir_passes.py:189-284: fuse_loops, contract_arrays).  `ins` is a register program in issue
+ * order; LOAD reads leaf `a` (trailing-aligned broadcast strides over `ext`, like dgb_ew_binary), CONST
+ * reads `consts[a]` (raw 64-bit pattern of a double / int64 / 0-1 bool), BINARY / UNARY / WHERE apply
+ * `op` to registers a, b, c (WHERE: a if c else b) with the operand dtypes adt / bdt / cdt and the
+ * result dtype odt exactly as dgb_ew_binary / dgb_ew_unary / dgb_ew_where would (fcomp: the binary
+ * operation is carried out in f64).  Outputs are dense arrays of `total` elements.  Results are
+ * bit-identical to issuing the operations one by one. */
+enum { DGB_EW_MAX_INS = 96, DGB_EW_MAX_REGS = 32, DGB_EW_MAX_LEAVES = 12, DGB_EW_MAX_OUTS = 4, DGB_EW_MAX_CONSTS = 24 };
+typedef enum { DGB_EW_LOAD = 0, DGB_EW_CONST = 1, DGB_EW_BINARY = 2, DGB_EW_UNARY = 3, DGB_EW_WHERE = 4 } dgb_ew_kind;
+typedef struct { uint8_t kind, op, dst, a, b, c, adt, bdt, cdt, odt, fcomp, pad_; } dgb_ew_ins;
+typedef struct { const void* dev; int32_t dtype; int32_t mode; /* 0 strided, 1 dense, 2 scalar */ int64_t stride[8]; } dgb_ew_leaf;
+typedef struct { void* dev; int32_t dtype; int32_t reg; } dgb_ew_out;
+typedef struct {
+  int32_t nins, nleaves, nouts, rank, need_index, pad_;
+  int64_t total;
+  int64_t ext[8];
+  uint64_t consts[DGB_EW_MAX_CONSTS];
+  dgb_ew_leaf leaf[DGB_EW_MAX_LEAVES];
+  dgb_ew_out out[DGB_EW_MAX_OUTS];
+  dgb_ew_ins ins[DGB_EW_MAX_INS];
+} dgb_ew_prog;
+int dgb_ew_program(const dgb_ew_prog* prog, void* stream);
+
 /* strided copy / cast (reshape of views, slices, stack, concatenate): out dense */
 int dgb_copy_strided(void* out_dev, int out_dtype, const void* a_dev, int a_dtype,
                      const int64_t* a_strides, int rank, const int64_t* shape, void* stream);

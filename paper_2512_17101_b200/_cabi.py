@@ -24,7 +24,7 @@ SYMBOLS = [
     "dgb_pack_elements", "dgb_pack_elements_to", "dgb_ipc_alloc", "dgb_ipc_open", "dgb_ipc_close",
     "dgb_flag_signal", "dgb_flag_wait",
     "dgb_ew_binary", "dgb_ew_unary", "dgb_ew_where", "dgb_copy_strided", "dgb_copy_scatter", "dgb_take", "dgb_take_deferred",
-    "dgb_einsum",
+    "dgb_einsum", "dgb_ew_program",
 ]
 
 DGB_OK, DGB_ERR_CUDA, DGB_ERR_INVALID, DGB_ERR_OUT_OF_BOUNDS, DGB_ERR_BAD_MAP, DGB_ERR_DTYPE = range(6)
@@ -40,6 +40,30 @@ _STATUS_TO_EXC = {
 BINOPS = {name: k for k, name in enumerate(
     ["add", "sub", "mul", "truediv", "floordiv", "mod", "pow", "min", "max", "lt", "le", "gt", "ge", "eq", "ne"])}
 UNOPS = {name: k for k, name in enumerate(["neg", "abs", "sqrt", "exp", "log"])}
+
+
+# dgb_ew_program (include/dgb200.h)
+EW_MAX_INS, EW_MAX_REGS, EW_MAX_LEAVES, EW_MAX_OUTS, EW_MAX_CONSTS = 96, 32, 12, 4, 24
+EW_LOAD, EW_CONST, EW_BINARY, EW_UNARY, EW_WHERE = range(5)
+
+
+class EwIns(C.Structure):
+    _fields_ = [(n, C.c_uint8) for n in ("kind", "op", "dst", "a", "b", "c", "adt", "bdt", "cdt", "odt", "fcomp", "pad_")]
+
+
+class EwLeaf(C.Structure):
+    _fields_ = [("dev", C.c_void_p), ("dtype", C.c_int32), ("mode", C.c_int32), ("stride", C.c_int64 * 8)]
+
+
+class EwOut(C.Structure):
+    _fields_ = [("dev", C.c_void_p), ("dtype", C.c_int32), ("reg", C.c_int32)]
+
+
+class EwProg(C.Structure):
+    _fields_ = [("nins", C.c_int32), ("nleaves", C.c_int32), ("nouts", C.c_int32), ("rank", C.c_int32),
+                ("need_index", C.c_int32), ("pad_", C.c_int32), ("total", C.c_int64), ("ext", C.c_int64 * 8),
+                ("consts", C.c_uint64 * EW_MAX_CONSTS), ("leaf", EwLeaf * EW_MAX_LEAVES), ("out", EwOut * EW_MAX_OUTS),
+                ("ins", EwIns * EW_MAX_INS)]
 
 
 def load():
@@ -99,6 +123,7 @@ def load():
     lib.dgb_take.argtypes = [dp, dp, C.c_int, dp, i64, i64, i64, i64, vp]
     lib.dgb_take_deferred.argtypes = [dp, dp, C.c_int, dp, i64, i64, i64, i64, vp, vp]
     lib.dgb_einsum.argtypes = [dp, C.c_int, vp, vp, C.c_int, C.c_int, vp, vp]
+    lib.dgb_ew_program.argtypes = [C.POINTER(EwProg), vp]
     _LIB = lib
     return lib
 

@@ -196,6 +196,58 @@ class DeviceArray:
         return self.actx._take(view, axis, idx)
 
 
+class DeferredArray(DeviceArray):
+    """Result of an elementwise operation that has not been evaluated yet.
+
+    With ``actx.fuse_elementwise`` on, ``_binary_op / _unary_op / _where`` return one of these instead of
+    launching a kernel; a chain of them is evaluated by ONE ``dgb_ew_program`` launch when the value is
+    first needed by anything that is not elementwise (``.t`` / ``.ptr``: a fused DG kernel, an einsum, a
+    gather, a copy to the host, a graph output).  This is the hand-written counterpart of the reference's
+    ``fuse_loops`` + ``contract_arrays`` (ir_passes.py:189-284) for pointwise chains: the intermediate
+    arrays of the chain never exist.  Shape and element type are known without evaluating."""
+
+    _next_seq = 0
+
+    def __init__(self, actx, shape, code, kind, op, args, fcomp=False):
+        self.actx = actx
+        self._shape = tuple(int(e) for e in shape)
+        self._code = code
+        self._kind, self._op, self._args, self._fcomp = kind, op, args, fcomp
+        self._t = None
+        self._host = None
+        self._seq = DeferredArray._next_seq
+        DeferredArray._next_seq += 1
+        # upper bound of the chain below this node (shared nodes counted once per use): long chains are cut
+        # here, at creation, so that a program always fits the interpreter and evaluation never recurses deeply
+        self._n = 1 + sum(a._n for a in args if isinstance(a, DeferredArray) and a.pending)
+        while self._n > 48:
+            big = max((a for a in args if isinstance(a, DeferredArray) and a.pending), key=lambda a: a._n)
+            actx._materialize(big)
+            self._n = 1 + sum(a._n for a in args if isinstance(a, DeferredArray) and a.pending)
+
+    @property
+    def t(self):
+        if self._t is None:
+            self.actx._materialize(self)
+        return self._t
+
+    @property
+    def pending(self) -> bool:
+        return self._t is None
+
+    @property
+    def shape(self):
+        return self._shape
+
+    @property
+    def dtype_code(self) -> int:
+        return self._code
+
+    @property
+    def size(self) -> int:
+        return math.prod(self._shape)
+
+
 class _OpNamespace:
     """``actx.np`` (frontend.py:257-302)."""
 
@@ -233,8 +285,9 @@ class B200ArrayContext:
 
     mode = "eager"
 
-    def __init__(self, device: int | None = None, stream=None, comm=None):
+    def __init__(self, device: int | None = None, stream=None, comm=None, fuse_elementwise: bool = True):
         torch = _torch()
+        self.fuse_elementwise = fuse_elementwise       # chains of elementwise ops -> one dgb_ew_program launch
         self.lib = _cabi.load()                       # raises ExtensionMissing: no CPU fallback
         if not torch.cuda.is_available():
             raise errors.ExtensionMissing("B200ArrayContext needs a CUDA device; there is no CPU fallback")
@@ -245,6 +298,8 @@ class B200ArrayContext:
         self.comm = comm                               # optional paper_2512_17101_b200.halo.Communicator
         self.launch_count = 0                          # kernels launched through this context
         self._scalars: dict = {}
+        self._pending_sends: list = []
+        self._pending_recvs: list = []
         self._discs: dict = {}
         self._keepalive: list = []
         self._pinned: list = []
@@ -263,6 +318,8 @@ class B200ArrayContext:
         return DeviceArray(self, t)
 
     def synchronize(self):
+        if self._pending_sends or self._pending_recvs:
+            self.flush_communication()
         _cabi.check(self.lib.dgb_stream_sync(self._st), "synchronize")
         if getattr(self, "_err", None) is not None and getattr(self, "_err_armed", False):
             self._err_armed = False
@@ -388,13 +445,24 @@ class B200ArrayContext:
 
     # {{{ operands
     def _scalar(self, value, code) -> DeviceArray:
+        """Rank-0 device array holding a literal.  Outside a graph capture the arrays are cached (LRU,
+        4096 entries).  Inside a capture the cache is neither read nor written: the array is created by a
+        captured fill kernel in the graph's own memory pool, so a graph never holds the address of a
+        cache entry that a later eviction could free, and nothing synchronises the capturing stream."""
+        torch = _torch()
+        if getattr(self, "_capturing", False):
+            with torch.cuda.stream(self.stream):
+                t = torch.full((), float(value) if code == F64 else (bool(value) if code == BOOL else int(value)),
+                               dtype=_torch_dtype(code), device=self.device)
+            self.launch_count += 1
+            return DeviceArray(self, t)
         key = (code, float(value) if code == F64 else int(value))
-        arr = self._scalars.get(key)
+        arr = self._scalars.pop(key, None)
         if arr is None:
-            if len(self._scalars) > 4096:
-                self._scalars.clear()
+            while len(self._scalars) >= 4096:
+                self._scalars.pop(next(iter(self._scalars)))      # least recently used first
             arr = self.from_numpy(np.asarray(value, dtype=_NP_OF[code]))
-            self._scalars[key] = arr
+        self._scalars[key] = arr                                   # (re)insert as most recently used
         return arr
 
     def _as_operand(self, value):
@@ -436,6 +504,167 @@ class B200ArrayContext:
         return ops
     # }}}
 
+    # {{{ fused elementwise programs (ir_passes.py:189-284: fuse_loops + contract_arrays, for pointwise chains)
+    class _Literal:
+        """A literal operand of a deferred elementwise operation: an immediate of the program."""
+        __slots__ = ("value", "dtype_code")
+        shape = ()
+
+        def __init__(self, value, code):
+            self.value, self.dtype_code = value, code
+
+    def _literal(self, value, code):
+        if self.fuse_elementwise:
+            return B200ArrayContext._Literal(value, code)
+        return self._scalar(value, code)
+
+    def _pending_dag(self, root):
+        """Pending nodes reachable from ``root`` in issue order, and the number of references each gets
+        from inside that set."""
+        seen, stack, inner = {}, [root], {}
+        while stack:
+            x = stack.pop()
+            if id(x) in seen:
+                continue
+            seen[id(x)] = x
+            for a in x._args:
+                if isinstance(a, DeferredArray) and a.pending:
+                    inner[id(a)] = inner.get(id(a), 0) + 1
+                    stack.append(a)
+        return sorted(seen.values(), key=lambda n: n._seq), inner
+
+    def _materialize(self, root: "DeferredArray"):
+        """Evaluate ``root`` (and every pending node below it) with ONE interpreter launch; pending nodes
+        of the same shape that something else still refers to are written out by the same launch."""
+        import struct
+        import sys
+        while True:
+            order, inner = self._pending_dag(root)
+            # leaves, immediates, instructions
+            leaves, leaf_of, consts, const_of = [], {}, [], {}
+            prog = []                          # (kind, op, node-or-None, [operand keys], fcomp)
+            val_dtype = {}
+
+            def key_of(a):
+                if isinstance(a, B200ArrayContext._Literal):
+                    bits = (struct.unpack("<Q", struct.pack("<d", float(a.value)))[0] if a.dtype_code == F64
+                            else (int(bool(a.value)) if a.dtype_code == BOOL else int(a.value) & 0xFFFFFFFFFFFFFFFF))
+                    k = ("c", bits, a.dtype_code)
+                    if k not in const_of:
+                        const_of[k] = len(consts)
+                        consts.append(bits)
+                        prog.append((_cabi.EW_CONST, 0, k, [const_of[k]], False))
+                        val_dtype[k] = a.dtype_code
+                    return k
+                if isinstance(a, DeferredArray) and a.pending:
+                    return ("n", id(a))
+                k = ("l", id(a))
+                if k not in leaf_of:
+                    leaf_of[k] = len(leaves)
+                    leaves.append(a)
+                    prog.append((_cabi.EW_LOAD, 0, k, [leaf_of[k]], False))
+                    val_dtype[k] = a.dtype_code
+                return k
+
+            for node in order:
+                ops = [key_of(a) for a in node._args]
+                k = ("n", id(node))
+                prog.append((node._kind, node._op, k, ops, node._fcomp))
+                val_dtype[k] = node._code
+            # extra outputs: pending nodes of root's shape that are referenced from outside this DAG
+            outs = [root]
+            for node in order:
+                if node is root or node._shape != root._shape or len(outs) >= _cabi.EW_MAX_OUTS:
+                    continue
+                if sys.getrefcount(node) - 3 - inner.get(id(node), 0) > 0:     # `order`, `node`, getrefcount's argument
+                    outs.append(node)
+            # registers by liveness (values die after their last use; outputs live to the end)
+            last = {}
+            for i, (_, _, k, ops, _) in enumerate(prog):
+                if prog[i][0] not in (_cabi.EW_LOAD, _cabi.EW_CONST):
+                    for o in ops:
+                        last[o] = i
+            for o in outs:
+                last[("n", id(o))] = len(prog)
+            free, reg, ins, ok = list(range(_cabi.EW_MAX_REGS - 1, -1, -1)), {}, [], True
+            for i, (kind, op, k, ops, fcomp) in enumerate(prog):
+                srcs = [] if kind in (_cabi.EW_LOAD, _cabi.EW_CONST) else ops
+                for o in set(srcs):
+                    if last.get(o) == i:
+                        free.append(reg[o])            # the destination may reuse a dying source register
+                if k not in last:
+                    last[k] = i                        # value never used (cannot happen for DAG nodes)
+                if not free:
+                    ok = False
+                    break
+                reg[k] = free.pop()
+                if kind in (_cabi.EW_LOAD, _cabi.EW_CONST):
+                    ins.append((kind, op, reg[k], ops[0], 0, 0, 0, 0, 0, val_dtype[k], 0))
+                else:
+                    r = [reg[o] for o in srcs] + [0] * (3 - len(srcs))
+                    dt = [val_dtype[o] for o in srcs] + [0] * (3 - len(srcs))
+                    ins.append((kind, op, reg[k], r[0], r[1], r[2], dt[0], dt[1], dt[2], val_dtype[k], int(fcomp)))
+            if ok and len(ins) <= _cabi.EW_MAX_INS and len(leaves) <= _cabi.EW_MAX_LEAVES and len(consts) <= _cabi.EW_MAX_CONSTS:
+                break
+            # too large for one program: evaluate the pending operands of the root first, then retry
+            pend = [a for a in root._args if isinstance(a, DeferredArray) and a.pending]
+            if not pend:
+                raise errors.LazeError("elementwise program does not fit the interpreter limits")
+            for a in pend:
+                self._materialize(a)
+        shape = root._shape
+        total = math.prod(shape)
+        results = [self.empty(shape, o._code) for o in outs]
+        if total:
+            pg = _cabi.EwProg()
+            pg.nins, pg.nleaves, pg.nouts, pg.rank, pg.total = len(ins), len(leaves), len(outs), len(shape), total
+            need_index = 0
+            for k, e in enumerate(shape):
+                pg.ext[k] = e
+            for k, bits in enumerate(consts):
+                pg.consts[k] = bits
+            for k, lf in enumerate(leaves):
+                st = self._bstrides(lf, shape)
+                dense, scalar, run = True, True, 1
+                for ax in range(len(shape) - 1, -1, -1):
+                    if shape[ax] != 1:
+                        dense = dense and st[ax] == run
+                        scalar = scalar and st[ax] == 0
+                    run *= shape[ax]
+                mode = 1 if dense else (2 if scalar else 0)
+                need_index |= int(mode == 0)
+                pg.leaf[k].dev, pg.leaf[k].dtype, pg.leaf[k].mode = lf.ptr, lf.dtype_code, mode
+                for ax, v in enumerate(st):
+                    pg.leaf[k].stride[ax] = v
+            pg.need_index = need_index
+            for k, (o, res) in enumerate(zip(outs, results)):
+                pg.out[k].dev, pg.out[k].dtype, pg.out[k].reg = res.ptr, o._code, reg[("n", id(o))]
+            for k, f in enumerate(ins):
+                (pg.ins[k].kind, pg.ins[k].op, pg.ins[k].dst, pg.ins[k].a, pg.ins[k].b, pg.ins[k].c, pg.ins[k].adt,
+                 pg.ins[k].bdt, pg.ins[k].cdt, pg.ins[k].odt, pg.ins[k].fcomp) = f
+            _cabi.check(self.lib.dgb_ew_program(C.byref(pg), self._st), "elementwise program")
+            self.launch_count += 1
+            self.fused_programs = getattr(self, "fused_programs", 0) + 1
+            self.fused_ops = getattr(self, "fused_ops", 0) + len(order)
+        for o, res in zip(outs, results):
+            o._t = res.t
+            o._args = ()                       # the chain below is no longer needed
+
+    def materialize(self, value):
+        """Force the evaluation of deferred elementwise results inside ``value`` (array, DOFArray, dict, sequence)."""
+        if isinstance(value, DeferredArray):
+            value.t
+        elif isinstance(value, dict):
+            for v in value.values():
+                self.materialize(v)
+        elif isinstance(value, (list, tuple)):
+            for v in value:
+                self.materialize(v)
+        elif hasattr(value, "data") and isinstance(getattr(value, "data"), DeviceArray):
+            self.materialize(value.data)
+        return value
+    # }}}
+
     # {{{ elementwise (frontend.py:374-410)
     @staticmethod
     def _bstrides(arr: DeviceArray, out_shape):
@@ -458,12 +687,15 @@ class B200ArrayContext:
         else:
             out_code = both
         if na is None:
-            na = self._scalar(la[0], F64 if both == F64 else la[1])
+            na = self._literal(la[0], F64 if both == F64 else la[1])
         if nb is None:
-            nb = self._scalar(lb[0], F64 if both == F64 else lb[1])
+            nb = self._literal(lb[0], F64 if both == F64 else lb[1])
         out_shape = broadcast_shapes([na.shape, nb.shape])
         if len(out_shape) > 8:
             raise errors.ShapeMismatch(f"rank {len(out_shape)} exceeds the maximum of 8")
+        if self.fuse_elementwise:
+            return DeferredArray(self, out_shape, out_code, _cabi.EW_BINARY, _cabi.BINOPS[op], [na, nb],
+                                 fcomp=(na.dtype_code == F64 or nb.dtype_code == F64))
         out = self.empty(out_shape, out_code)
         sa, sb = self._bstrides(na, out_shape), self._bstrides(nb, out_shape)
         _cabi.check(self.lib.dgb_ew_binary(
@@ -477,8 +709,10 @@ class B200ArrayContext:
         node, lit = self._as_operand(a)
         if node is None:
             raise errors.LazeError("at least one operand must be an array")
-        node = self._contiguous(node)
         out_code = F64 if op in ("sqrt", "exp", "log") else node.dtype_code
+        if self.fuse_elementwise:
+            return DeferredArray(self, node.shape, out_code, _cabi.EW_UNARY, _cabi.UNOPS[op], [node])
+        node = self._contiguous(node)
         out = self.empty(node.shape, out_code)
         _cabi.check(self.lib.dgb_ew_unary(_cabi.UNOPS[op], out.ptr, out_code, node.ptr, node.dtype_code,
                                           node.size, self._st), op)
@@ -491,12 +725,16 @@ class B200ArrayContext:
         tb = (nb.dtype_code, False) if nb is not None else (lb[1], True)
         out_code, _ = self._combine(ta, tb)
         if nc is None:
-            nc = self._scalar(lc[0], lc[1])
+            nc = self._literal(lc[0], lc[1])
         if na is None:
-            na = self._scalar(la[0], F64 if out_code == F64 else la[1])
+            na = self._literal(la[0], F64 if out_code == F64 else la[1])
         if nb is None:
-            nb = self._scalar(lb[0], F64 if out_code == F64 else lb[1])
+            nb = self._literal(lb[0], F64 if out_code == F64 else lb[1])
         out_shape = broadcast_shapes([nc.shape, na.shape, nb.shape])
+        if self.fuse_elementwise:
+            if len(out_shape) > 8:
+                raise errors.ShapeMismatch(f"rank {len(out_shape)} exceeds the maximum of 8")
+            return DeferredArray(self, out_shape, out_code, _cabi.EW_WHERE, 0, [na, nb, nc])
         out = self.empty(out_shape, out_code)
         _cabi.check(self.lib.dgb_ew_where(
             out.ptr, out_code, nc.ptr, nc.dtype_code, _cabi.i64_array(self._bstrides(nc, out_shape)),
@@ -717,20 +955,81 @@ class B200ArrayContext:
         return fused_call
     # }}}
 
-    # {{{ communication (frontend.py:469-478): executed immediately through the communicator
+    # {{{ communication (frontend.py:469-478)
+    # The reference records Send / Receive nodes and its distributed executor posts every receive of a
+    # batch up front, then the sends (distpart.py:168-196).  Here ``receive`` hands out an array whose
+    # transfer is posted lazily and ``send`` queues its payload; the first use of any received array (or
+    # ``actx.synchronize()``) posts everything queued so far as ONE batch of point-to-point operations
+    # (an NCCL group: no ordering deadlock between ranks that both receive first), on the context's stream.
+    @staticmethod
+    def _code_of_any(dtype) -> int:
+        if dtype is None:
+            return F64
+        if isinstance(dtype, (int, np.integer)) and int(dtype) in _NP_OF:
+            return int(dtype)
+        name = getattr(dtype, "value", None)                      # the reference's DType enum (adfg.py:39-45)
+        if isinstance(name, str):
+            table = {"f64": F64, "i64": I64, "bool": BOOL}
+            if name not in table:
+                raise errors.DTypeMismatch(f"unsupported element type: {name}")
+            return table[name]
+        return _code_of_numpy(dtype)
+
     def receive(self, source: int, tag: int, shape: Sequence[int], dtype=None) -> DeviceArray:
         if self.comm is None:
             raise errors.CommunicationInSingleProcessGraph(
                 f"receive (source={source}, tag={tag}) on a context without a communicator")
-        return self.comm.receive(self, source, tag, tuple(shape))
+        return ReceivedArray(self, int(source), int(tag), tuple(int(e) for e in shape), self._code_of_any(dtype))
 
     def send(self, value, dest: int, tag: int, *, stapled_to):
         if self.comm is None:
             raise errors.CommunicationInSingleProcessGraph(
                 f"send (dest={dest}, tag={tag}) on a context without a communicator")
-        self.comm.send(self, self._node_of(value), dest, tag)
+        self._pending_sends.append((self._contiguous(self._node_of(value)), int(dest), int(tag)))
         return stapled_to
+
+    def flush_communication(self):
+        """Post every queued send and receive as one batch and wait for it on the context's stream."""
+        sends, recvs = self._pending_sends, self._pending_recvs
+        if not sends and not recvs:
+            return
+        self._pending_sends, self._pending_recvs = [], []
+        torch = _torch()
+        with torch.cuda.stream(self.stream):
+            self.comm.exchange([(a.t, dest, tag) for a, dest, tag in sends],
+                               [(r._buf.t, r._source, r._tag) for r in recvs])
+        for r in recvs:
+            r._arrived = True
     # }}}
+
+
+class ReceivedArray(DeviceArray):
+    """Result of ``actx.receive``: the buffer exists at once, the transfer is posted with the next batch."""
+
+    def __init__(self, actx, source, tag, shape, code):
+        self.actx = actx
+        self._buf = actx.empty(shape, code)
+        self._source, self._tag, self._arrived = source, tag, False
+        self._host = None
+        actx._pending_recvs.append(self)
+
+    @property
+    def t(self):
+        if not self._arrived:
+            self.actx.flush_communication()
+        return self._buf.t
+
+    @property
+    def shape(self):
+        return self._buf.shape
+
+    @property
+    def dtype_code(self) -> int:
+        return self._buf.dtype_code
+
+    @property
+    def size(self) -> int:
+        return self._buf.size
 
 
 class CompiledFunction:
@@ -776,7 +1075,7 @@ class CompiledFunction:
             actx._capturing = True
             try:
                 with torch.cuda.graph(g, stream=cap):
-                    out = self.f(**static)
+                    out = actx.materialize(self.f(**static))
             finally:
                 actx._capturing = False
                 actx.stream = home

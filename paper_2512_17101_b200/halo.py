@@ -48,6 +48,9 @@ class TorchCommunicator:
                 t.copy_(h)
             return
         ops = []
+        if self.backend == "gloo":
+            # gloo matches messages by tag only within a (source, destination) pair and needs dense CPU tensors
+            sends = [(t.contiguous(), peer, tag) for t, peer, tag in sends]
         # a deterministic global order keeps NCCL's paired send/recv matching happy: receives and
         # sends are sorted by (tag, peer)
         for t, peer, tag in sorted(recvs, key=lambda x: (x[2], x[1])):
@@ -132,8 +135,10 @@ class HaloExchange:
                 recvs.append((buf.t, peer, tag)); keep.append((buf, a, b))
                 packed = self._pack(data, k)
                 sends.append((packed.t, peer, self.send_tags[k]))
-            actx.synchronize()                 # packed payloads complete before NCCL reads them
-            self.comm.exchange(sends, recvs)
+            # NCCL enqueues on torch's current stream: make that the context's stream, so that the pack
+            # kernels before it and the scatter kernels after it are ordered with the transfer
+            with torch.cuda.stream(actx.stream):
+                self.comm.exchange(sends, recvs)
             for buf, a, b in keep:
                 actx._scatter_into(ghost, ghost.t[..., a:b, :], buf)
             self.bytes_per_exchange = sum(t.numel() * 8 for t, _, _ in sends)
