@@ -82,7 +82,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=self.file, stderr=subprocess.DEVNULL)
+                 "-lms", "20"], stdout=self.file, stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
 
@@ -122,11 +122,28 @@ class ClockSampler:
 
 # {{{ CPU reference arm (oracle port = the reference's eager NumPy context, oracle/laze_port.py)
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")     # pip install --target of /root/reference/pkg
+
+
+def reference_context():
+    """(array context, kind): the UNMODIFIED reference's own eager context when `laze` is installed under
+    baseline/_ref (it travels to the GPU box with the repository), else its restatement oracle/laze_port.py."""
+    if os.path.isdir(os.path.join(REF_DIR, "laze")):
+        if REF_DIR not in sys.path:
+            sys.path.insert(0, REF_DIR)
+        try:
+            import laze
+            return laze.ArrayContext(mode="eager"), "reference"
+        except Exception:
+            pass
+    from oracle.laze_port import NumpyArrayContext
+    return NumpyArrayContext(), "port"
+
+
 def _cpu_worker(args):
     n, reps, seed = args
-    from oracle.laze_port import NumpyArrayContext
     from paper_2512_17101_b200 import DGDiscretization, NavierStokesOperator, box_mesh
-    actx = NumpyArrayContext()
+    actx, _ = reference_context()
     mesh = box_mesh((n,) * DIM, (-1.0,) * DIM, (1.0,) * DIM, periodic=(True,) * DIM)
     d = DGDiscretization(actx, mesh, ORDER)
     op = NavierStokesOperator(d, **PHYS)
@@ -172,21 +189,80 @@ def run_reference(args):
         busy += b
     wall = time.perf_counter() - t0
     value = dofs / busy / 1e9
+    kind = reference_context()[1]
+    ctx_name = ("laze.ArrayContext(mode='eager') from baseline/_ref (the unmodified reference)" if kind == "reference"
+                else "NumPy eager context (oracle/laze_port.py, the reference's restatement)")
     sample = (f"{cores} processes x NS p3 RHS on a periodic {n}^3 Kuhn mesh ({6 * n ** 3} elements, "
-              f"{6 * n ** 3 * NP} DOFs each), {reps} evaluation(s) per step; NumPy eager context (oracle/laze_port.py)")
+              f"{6 * n ** 3 * NP} DOFs each), {reps} evaluation(s) per step; {ctx_name}")
     line = {
         "impl": "reference", "metric": "3D Navier-Stokes DG RHS throughput", "value": value, "unit": "GDOF/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * busy / max(args.steps, 1), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_name(args.n), "sample": sample},
-        "cpu_baseline": {"value": value, "unit": "GDOF/s", "cores": cores, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "GDOF/s", "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": wall,
     }
     print(json.dumps(line))
 
 # }}}
+
+
+FP64_PEAK_TFLOPS = 37.15   # DMMA.8x8x4, registers only, measured on B200 at 1965 MHz (profiles/r01_fp64_peak.txt)
+
+
+def fp64_ceiling(args, ndof, ms_step, hbm_frac, multi, euler, grad_form, world):
+    """the FP64 ceiling next to the HBM roofline.  Lane-operations per DOF are the ISSUED
+    FP64 work of the kernels (cost.py: tensor-core FMAs incl. padding + pointwise), so
+    `frac` = the share of the measured FP64 datapath peak the path sustains; `min_frac` = its position under
+    min(HBM roofline, FP64 ceiling)."""
+    if multi or ORDER != 3 or DIM != 3:
+        return None
+    ops = 896.0 if euler else (1920.0 if grad_form else 1720.0)
+    tflops = 2.0 * ops * ndof / (ms_step * 1e-3) / 1e12
+    peak_gdofs = FP64_PEAK_TFLOPS * 1e12 / (2.0 * ops) / 1e9
+    return {"fp64_lane_ops_per_dof": ops, "achieved": tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+            "frac": tflops / FP64_PEAK_TFLOPS, "ceiling_gdofs_per_gpu": peak_gdofs,
+            "peak_source": "measured DMMA register-only microbenchmark (profiles/r01_fp64_peak.txt)",
+            "min_frac": max(hbm_frac, tflops / FP64_PEAK_TFLOPS),
+            "note": "the path is FP64-bound: its distance to min(HBM roofline, FP64 ceiling) is the larger of the two fractions"}
+
+
+def gpu_numa_cpus(device_index: int):
+    """CPUs of the NUMA node the GPU hangs off (sysfs), or (None, node) when that cannot be determined."""
+    try:
+        import torch
+        pr = torch.cuda.get_device_properties(device_index)
+        addr = f"{pr.pci_domain_id:04x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        with open(f"/sys/bus/pci/devices/{addr}/numa_node") as fh:
+            node = int(fh.read().strip())
+        if node < 0:
+            return None, node
+        with open(f"/sys/devices/system/node/node{node}/cpulist") as fh:
+            spec = fh.read().strip()
+        cpus = set()
+        for part in spec.split(","):
+            a, _, b = part.partition("-")
+            cpus.update(range(int(a), int(b or a) + 1))
+        cpus &= os.sched_getaffinity(0)
+        return (cpus or None), node
+    except Exception:
+        return None, None
+
+
+def bind_to_gpu_numa_node(device_index: int):
+    """Pinned staging buffers are first-touched by this process: run it on the CPUs next to the GPU so that
+    host<->device copies do not cross the socket interconnect (the r01 driver box reached 58 GB/s for
+    H2D + D2H together where the builder box reached 82 GB/s).  Returns the node or None."""
+    cpus, node = gpu_numa_cpus(device_index)
+    if cpus:
+        try:
+            os.sched_setaffinity(0, cpus)
+            return node
+        except OSError:
+            return None
+    return None
 
 
 def run_b200(args):
@@ -205,10 +281,14 @@ def run_b200(args):
     if share:
         local_rank = 0
     torch.cuda.set_device(local_rank)
+    numa_node = bind_to_gpu_numa_node(local_rank)
     if world > 1:
         if share:
             dist.init_process_group("gloo")
         else:
+            # NCCL's init lines (communicator, nranks, transports: NVLS / P2P) on stderr, for the record of an N-GPU run
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     if world != args.gpus and rank == 0:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
@@ -351,7 +431,10 @@ def run_b200(args):
             dom = (names[0], ms_div, B_ALG_DIV) if ms_div >= ms_grad else (names[1], ms_grad, B_ALG_GRAD)
         achieved = ndof * dom[2] / (dom[1] * 1e-3) / 1e9
         traffic = None
-        tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
+        traffic_source = None
+        tpath = os.path.join(ROOT, "profiles", "r02_traffic.json")
+        if not os.path.exists(tpath):
+            tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
         if os.path.exists(tpath):
             with open(tpath) as fh:
                 tj = json.load(fh)
@@ -364,13 +447,17 @@ def run_b200(args):
                     key = "k_nsdiv3" if ms_div >= ms_grad else "k_nsflux3"
                 if key in tj:
                     traffic = tj[key]["dram_read_bytes"] + tj[key]["dram_write_bytes"]
+        if traffic is not None:
+            traffic_source = (f"static: dram__bytes_read.sum + dram__bytes_write.sum of one `ncu --set full` capture of this "
+                              f"kernel on this workload ({os.path.relpath(tpath, ROOT)}); not measured in this run")
         per_step = [e[0].elapsed_time(e[2]) for e in ev]
         roofline = {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                    "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_source, "peak_source": peak_src,
                     "algorithmic_bytes_per_dof": dom[2], "ms_per_launch": dom[1],
                     "ms_grad_pass": ms_grad, "ms_div_pass": ms_div,
                     "ms_step_min_median_max": [float(np.min(per_step)), float(np.median(per_step)),
-                                               float(np.max(per_step))]}
+                                               float(np.max(per_step))],
+                    "value_at_median_step": ndof / (float(np.median(per_step)) * 1e-3) / 1e9}
     b_alg = 72.0 * ncomp if multi else (80.0 if euler else B_ALG_RHS)      # (3C + 2Cd) * 8 = 72 C for NS-type two-pass schemes
     rhs_gbs = ndof * b_alg / (ms_step * 1e-3) / 1e9
     if roofline is None:
@@ -395,23 +482,34 @@ def run_b200(args):
         # host memory and downloads its full result; both are inside the timed region.
         # two device input buffers, ping-ponged (a streaming caller allocates them once)
         dev_in = [actx.empty(q_host.shape), actx.empty(q_host.shape)]
-        read_done = [None, None]
-        actx.synchronize()
-        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s0.record(stream)
-        actx.copy_stream.wait_event(s0)
-        nxt = actx.from_numpy_async(q_host, out=dev_in[0])
-        for k in range(Ke):
-            cur = actx.wait_for(nxt)
-            res = rhs_step(DOFArray(actx, cur)).data
-            read_done[k % 2] = torch.cuda.Event()
-            read_done[k % 2].record(stream)                       # step k no longer reads dev_in[k % 2]
-            if k + 1 < Ke:                                        # H2D of step k+1 into the other buffer
-                nxt = actx.from_numpy_async(q_host, after=read_done[(k + 1) % 2], out=dev_in[(k + 1) % 2])
-            d2h_done = actx.to_numpy_async(res, out_host)         # D2H of step k's result (download stream)
-        stream.wait_event(d2h_done)                               # the last result is on the host
-        s1.record(stream)
-        torch.cuda.synchronize()
+
+        def pipeline(nsteps):
+            """nsteps streamed evaluations; returns the events bracketing them on the compute stream."""
+            read_done = [None, None]
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            actx.copy_stream.wait_event(s0)
+            nxt = actx.from_numpy_async(q_host, out=dev_in[0])
+            d2h_done = None
+            for k in range(nsteps):
+                cur = actx.wait_for(nxt)
+                res = rhs_step(DOFArray(actx, cur)).data
+                read_done[k % 2] = torch.cuda.Event()
+                read_done[k % 2].record(stream)                       # step k no longer reads dev_in[k % 2]
+                if k + 1 < nsteps:                                    # H2D of step k+1 into the other buffer
+                    nxt = actx.from_numpy_async(q_host, after=read_done[(k + 1) % 2], out=dev_in[(k + 1) % 2])
+                d2h_done = actx.to_numpy_async(res, out_host)         # D2H of step k's result (download stream)
+            stream.wait_event(d2h_done)                               # the last result is on the host
+            s1.record(stream)
+            torch.cuda.synchronize()
+            return s0, s1
+
+        # warm-up THROUGH THE SAME PIPELINE: the result blocks are held by the download stream while they are
+        # copied out, so the caching allocator needs a third and fourth result block before its request pattern
+        # repeats; a cudaMalloc inside the timed region synchronises the device and serialises the copies
+        # (r01: 138 ms per step on the driver box where the link does 85 ms)
+        pipeline(4)
+        s0, s1 = pipeline(Ke)
         ms_e2e = s0.elapsed_time(s1) / Ke
         if world > 1:
             t = torch.tensor([ms_e2e], device="cpu" if share else "cuda", dtype=torch.float64)
@@ -426,10 +524,12 @@ def run_b200(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         cores = os.cpu_count() or 1
         v, dofs, busy, wall = cpu_throughput(cores, args.cpu_n, CPU_REPS)
-        cpu = {"value": v, "unit": "GDOF/s", "cores": cores, "kind": "port",
+        kind = reference_context()[1]
+        cpu = {"value": v, "unit": "GDOF/s", "cores": cores, "kind": kind,
                "sample": f"{cores} processes x {CPU_REPS} NS p3 RHS on a periodic {args.cpu_n}^3 Kuhn mesh "
-                         f"({6 * args.cpu_n ** 3 * NP} DOFs each), oracle/laze_port.py NumPy eager context; "
-                         f"{busy:.1f} s busy"}
+                         f"({6 * args.cpu_n ** 3 * NP} DOFs each), "
+                         + ("laze.ArrayContext(mode='eager') from baseline/_ref (the unmodified reference); " if kind == "reference"
+                            else "oracle/laze_port.py NumPy eager context; ") + f"{busy:.1f} s busy"}
 
     if rank == 0:
         line = {
@@ -438,7 +538,8 @@ def run_b200(args):
             "value": value, "unit": "GDOF/s", "n_gpus": world, "steps": K, "warmup": max(args.warmup, 3), "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong" if (strong and world > 1) else "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name(n, args.workload) if not (strong and world > 1) else
+            "config": {"numa_node_bound": numa_node,
+                       "workload": workload_name(n, args.workload) if not (strong and world > 1) else
                        workload_name(n, args.workload).replace("per GPU", "in total"),
                        "elements_per_gpu": E, "dofs_per_gpu": ndof, "order": ORDER, "dim": DIM,
                        "l2_policy": "inputs larger than L2 (q 4.0 GB, grad q 12 GB per GPU vs 126 MB L2)"
@@ -454,20 +555,23 @@ def run_b200(args):
             "rhs_roofline": {"bound": "hbm", "achieved": rhs_gbs, "peak": peak, "unit": "GB/s",
                              "frac": rhs_gbs / peak, "algorithmic_bytes_per_dof": b_alg,
                              "peak_source": peak_src},
+            "fp64_ceiling": fp64_ceiling(args, ndof, ms_step, rhs_gbs / peak, multi, euler, grad_form, world),
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         }
-        print(json.dumps(line))
     if world > 1:
         if halo is not None:
             halo.close()
         dist.destroy_process_group()
+    if rank == 0:
+        sys.stdout.flush()
+        print(json.dumps(line), flush=True)          # last line of stdout, after NCCL's own log lines
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--n", "--cells", dest="n", type=int, default=94, help="cells per axis per GPU (94 -> 4,983,504 elements, 99.67M DOFs)")
     ap.add_argument("--cpu-n", type=int, default=10, help="cells per axis of each CPU-baseline sample mesh")

@@ -172,6 +172,11 @@ int dgb_ipc_close(void* dev);
 int dgb_pack_elements_to(double* dst_dev, int64_t ndst_elems, int64_t dst_slot0, const double* src_dev,
                          const int64_t* elems_dev, int64_t ncomp, int64_t nsrc_elems, int64_t nsel,
                          int64_t ndofs, void* stream);
+/* Leave `nsm` SMs free in every persistent kernel launched from now on (0 = use all).  halo.py sets it while a
+ * halo batch is in flight on the communication stream, so that the transport's own kernels (NCCL send/recv)
+ * start at once and the exchange overlaps the interior range -- the reference's executor has no overlap
+ * (distpart.py:430-560 runs the batches back to back). */
+int dgb_set_sm_reserve(int nsm);
 int dgb_flag_signal(uint64_t* flag_dev, uint64_t value, void* stream);
 int dgb_flag_wait(const uint64_t* flag_dev, uint64_t value, void* stream);
 

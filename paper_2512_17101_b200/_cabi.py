@@ -24,7 +24,7 @@ SYMBOLS = [
     "dgb_pack_elements", "dgb_pack_elements_to", "dgb_ipc_alloc", "dgb_ipc_open", "dgb_ipc_close",
     "dgb_flag_signal", "dgb_flag_wait",
     "dgb_ew_binary", "dgb_ew_unary", "dgb_ew_where", "dgb_copy_strided", "dgb_copy_scatter", "dgb_take", "dgb_take_deferred",
-    "dgb_einsum", "dgb_ew_program",
+    "dgb_einsum", "dgb_ew_program", "dgb_set_sm_reserve",
 ]
 
 DGB_OK, DGB_ERR_CUDA, DGB_ERR_INVALID, DGB_ERR_OUT_OF_BOUNDS, DGB_ERR_BAD_MAP, DGB_ERR_DTYPE = range(6)
@@ -123,6 +123,7 @@ def load():
     lib.dgb_take.argtypes = [dp, dp, C.c_int, dp, i64, i64, i64, i64, vp]
     lib.dgb_take_deferred.argtypes = [dp, dp, C.c_int, dp, i64, i64, i64, i64, vp, vp]
     lib.dgb_einsum.argtypes = [dp, C.c_int, vp, vp, C.c_int, C.c_int, vp, vp]
+    lib.dgb_set_sm_reserve.argtypes = [C.c_int]
     lib.dgb_ew_program.argtypes = [C.POINTER(EwProg), vp]
     _LIB = lib
     return lib

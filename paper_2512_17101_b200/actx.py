@@ -940,10 +940,17 @@ class B200ArrayContext:
         return CompiledFunction(self, f, graph=graph)
 
     def outline(self, f: Callable) -> Callable:
-        """Named call boundary.  DG functions known to ``fused.FUSED`` run as fused kernels; any
-        other function runs its body op by op (the reference's eager behaviour, :494-495)."""
+        """Named call boundary.  DG functions known to ``fused.FUSED`` whose body is the one the kernels
+        implement (source fingerprint, ``fused.body_matches``) run as fused kernels; any other function
+        runs its body op by op on the device (the reference's eager behaviour, :494-495)."""
         impl = self._fused.get(f.__name__)
         if impl is None:
+            return f
+        from . import fused
+        if not fused.body_matches(f):
+            # same name, different body (another EOS, another flux ...): the hand-written kernel would
+            # silently compute the built-in physics.  Run the body itself, op by op, on the device.
+            fused.warn_mismatch(f.__name__)
             return f
         actx = self
 

@@ -17,9 +17,21 @@ thread_local std::string g_err;
 int dgb_fail(int code, const std::string& msg) { g_err = msg; return code; }
 
 int dgb_num_sms() {
-  static int n = 0;
-  if (!n) { int dev = 0; cudaGetDevice(&dev); cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev); }
-  return n;
+  static int n[64] = {};
+  int dev = 0; cudaGetDevice(&dev);
+  int& v = n[dev & 63];
+  if (!v) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  return v;
+}
+
+// SMs left free by the persistent kernels while a halo exchange is in flight, so that the NCCL send/recv
+// kernel on the communication stream can start at once instead of waiting for a CTA to retire
+static int g_sm_reserve = 0;
+int dgb_grid_sms() { const int n = dgb_num_sms() - g_sm_reserve; return n < 1 ? 1 : n; }
+extern "C" int dgb_set_sm_reserve(int nsm) {
+  if (nsm < 0 || nsm >= dgb_num_sms()) return dgb_fail(DGB_ERR_INVALID, "SM reserve outside [0, number of SMs)");
+  g_sm_reserve = nsm;
+  return DGB_OK;
 }
 
 namespace {
@@ -174,10 +186,10 @@ int launch_rhs3(const dgb_disc* d, const double* q, const double* gq, const doub
   if (eend < 0) eend = d->dev.E;
   const long long nwb = (eend - ebeg + C::KW - 1) / C::KW;
   if (nwb == 0) return DGB_OK;
-  static bool configured = false;
-  if (!configured) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured = true; }
+  static DgbPerDevice configured;
+  if (!configured()) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured() = true; }
   const long long need = (nwb + C::NW - 1) / C::NW;
-  const int grid = (int)(need < num_sms() ? need : num_sms());
+  const int grid = (int)(need < dgb_grid_sms() ? need : dgb_grid_sms());
   DGB_CUDA(cudaMemsetAsync(d->counters + 1, 0, sizeof(unsigned long long), st));
   kern<<<grid, C::NW * 32, smem, st>>>(d->dev, q, gq, ghost, gghost, ep, ph, nwb, d->counters + 1, ebeg, eend);
   {
@@ -202,10 +214,10 @@ int launch_grad3(const dgb_disc* d, const double* q, const double* ghost, double
   const size_t smem = sizeof(dgb::Grad3Smem<DIM, P, C::KW, C::NWG>);
   const long long nwb = (d->dev.E + C::KW - 1) / C::KW;
   if (nwb == 0) return DGB_OK;
-  static bool configured = false;
-  if (!configured) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured = true; }
+  static DgbPerDevice configured;
+  if (!configured()) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured() = true; }
   const long long need = (nwb + C::NWG - 1) / C::NWG;
-  const int grid = (int)(need < num_sms() ? need : num_sms());
+  const int grid = (int)(need < dgb_grid_sms() ? need : dgb_grid_sms());
   DGB_CUDA(cudaMemsetAsync(d->counters, 0, sizeof(unsigned long long), st));
   kern<<<grid, C::NWG * 32, smem, st>>>(d->dev, q, ghost, grad, ph, nwb, d->counters);
   DGB_CUDA(cudaGetLastError());
@@ -467,6 +479,9 @@ static int make_epilogue(dgb::Epilogue& ep, const double* q, const double* x1, d
   if (out1 == q || (out2 && out2 == q) || (x2 && out1 == x2))
     return fail(DGB_ERR_INVALID, "RK outputs must not alias the stage input q (neighbours still read it)");
   if (out2 && !x2) return fail(DGB_ERR_INVALID, "out2 needs x2");
+  // the epilogue loads and stores node pairs (double2) when Np is even
+  if ((((uintptr_t)x1) | ((uintptr_t)out1) | ((uintptr_t)x2) | ((uintptr_t)out2)) & 15)
+    return fail(DGB_ERR_INVALID, "RK operands and outputs must be 16-byte aligned");
   ep = dgb::Epilogue{x1, out1, x2, out2, rk[0], rk[1], rk[2], rk[3]};
   return DGB_OK;
 }

@@ -6,7 +6,14 @@
 #include <string>
 
 int dgb_fail(int code, const std::string& msg);   // records the message for dgb_last_error()
-int dgb_num_sms();
+int dgb_num_sms();                                // SMs of the CURRENT device
+int dgb_grid_sms();                               // SMs a persistent kernel may occupy: dgb_num_sms() minus the reserve (dgb_set_sm_reserve)
+
+// "done once" flags of the launch configuration (cudaFuncSetAttribute) are per DEVICE, not per process
+struct DgbPerDevice {
+  bool done[64] = {};
+  bool& operator()() { int dev = 0; cudaGetDevice(&dev); return done[dev & 63]; }
+};
 
 #define DGB_CUDA(expr)                                                                          \
   do {                                                                                          \

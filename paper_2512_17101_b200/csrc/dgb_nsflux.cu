@@ -47,10 +47,10 @@ int launch_flux(const dgb_disc* d, const double* q, const double* ghost, double*
   const size_t smem = sizeof(dgb::Flux3Smem<DIM, P, C::KW, C::NWF>);
   const long long nwb = (eend - ebeg + C::KW - 1) / C::KW;
   if (nwb == 0) return DGB_OK;
-  static bool configured[2] = {false, false};
-  if (!configured[d->dev.G > 0]) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured[d->dev.G > 0] = true; }
+  static DgbPerDevice configured[2];
+  if (!configured[d->dev.G > 0]()) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured[d->dev.G > 0]() = true; }
   const long long need = (nwb + C::NWF - 1) / C::NWF;
-  const int grid = (int)(need < dgb_num_sms() ? need : dgb_num_sms());
+  const int grid = (int)(need < dgb_grid_sms() ? need : dgb_grid_sms());
   DGB_CUDA(cudaMemsetAsync(d->counters, 0, sizeof(unsigned long long), st));
   kern<<<grid, C::NWF * 32, smem, st>>>(d->dev, q, ghost, T, ph, ebeg, eend, nwb, d->counters);
   DGB_CUDA(cudaGetLastError());
@@ -65,10 +65,10 @@ int launch_div(const dgb_disc* d, const double* q, const double* T, const double
   const size_t smem = sizeof(dgb::Div3Smem<DIM, P, C::KW, C::NWD>);
   const long long nwb = (eend - ebeg + C::KW - 1) / C::KW;
   if (nwb == 0) return DGB_OK;
-  static bool configured[2] = {false, false};
-  if (!configured[d->dev.G > 0]) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured[d->dev.G > 0] = true; }
+  static DgbPerDevice configured[2];
+  if (!configured[d->dev.G > 0]()) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured[d->dev.G > 0]() = true; }
   const long long need = (nwb + C::NWD - 1) / C::NWD;
-  const int grid = (int)(need < dgb_num_sms() ? need : dgb_num_sms());
+  const int grid = (int)(need < dgb_grid_sms() ? need : dgb_grid_sms());
   DGB_CUDA(cudaMemsetAsync(d->counters + 1, 0, sizeof(unsigned long long), st));
   kern<<<grid, C::NWD * 32, smem, st>>>(d->dev, q, T, ghost, Tghost, ep, ph, ebeg, eend, nwb, d->counters + 1);
   DGB_CUDA(cudaGetLastError());
@@ -105,10 +105,10 @@ int launch_div7(const dgb_disc* d, const double* q, const double* T, const doubl
   const size_t smem = sizeof(dgb::Div7Smem<DIM, P, C::KW, C::NPROD, C::NIR>);
   const long long nwb = (eend - ebeg + C::KW - 1) / C::KW;
   if (nwb == 0) return DGB_OK;
-  static bool configured[2] = {false, false};
-  if (!configured[d->dev.G > 0]) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured[d->dev.G > 0] = true; }
+  static DgbPerDevice configured[2];
+  if (!configured[d->dev.G > 0]()) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured[d->dev.G > 0]() = true; }
   const long long need = (nwb + C::NPROD - 1) / C::NPROD;
-  const int grid = (int)(need < dgb_num_sms() ? need : dgb_num_sms());
+  const int grid = (int)(need < dgb_grid_sms() ? need : dgb_grid_sms());
   DGB_CUDA(cudaMemsetAsync(d->counters + 1, 0, sizeof(unsigned long long), st));
   kern<<<grid, 128 + 128 * ((C::NPROD + 3) / 4), smem, st>>>(d->dev, q, T, ghost, Tghost, ep, ph, ebeg, eend, nwb, d->counters + 1);
   DGB_CUDA(cudaGetLastError());
@@ -168,10 +168,10 @@ int launch_euler4(const dgb_disc* d, const double* q, const double* ghost, const
   const size_t smem = sizeof(dgb::Euler4Smem<DIM, P, C::KW, C::NW>);
   const long long nwb = (eend - ebeg + C::KW - 1) / C::KW;
   if (nwb == 0) return DGB_OK;
-  static bool configured[2] = {false, false};
-  if (!configured[d->dev.G > 0]) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured[d->dev.G > 0] = true; }
+  static DgbPerDevice configured[2];
+  if (!configured[d->dev.G > 0]()) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured[d->dev.G > 0]() = true; }
   const long long need = (nwb + C::NW - 1) / C::NW;
-  const int grid = (int)(need < dgb_num_sms() ? need : dgb_num_sms());
+  const int grid = (int)(need < dgb_grid_sms() ? need : dgb_grid_sms());
   DGB_CUDA(cudaMemsetAsync(d->counters + 1, 0, sizeof(unsigned long long), st));
   kern<<<grid, C::NW * 32, smem, st>>>(d->dev, q, ghost, ep, ph, ebeg, eend, nwb, d->counters + 1);
   DGB_CUDA(cudaGetLastError());
@@ -270,6 +270,8 @@ int dgb_ns_div_rk(const dgb_disc* d, const double* q, const double* T, const dou
   if (out1 == q || (out2 && out2 == q) || (x2 && out1 == x2))
     return dgb_fail(DGB_ERR_INVALID, "RK outputs must not alias the stage input q (neighbours still read it)");
   if (out2 && !x2) return dgb_fail(DGB_ERR_INVALID, "out2 needs x2");
+  if ((((uintptr_t)x1) | ((uintptr_t)out1) | ((uintptr_t)x2) | ((uintptr_t)out2)) & 15)
+    return dgb_fail(DGB_ERR_INVALID, "RK operands and outputs must be 16-byte aligned");
   dgb::Epilogue ep{x1, out1, x2, out2, rk[0], rk[1], rk[2], rk[3]};
   return ns_div_impl(d, q, T, ghost, Tghost, ep, qfar, phys, stream);
 }

@@ -10,7 +10,15 @@ the int64 face maps on the device (range check + conformity) exactly once.
 """
 from __future__ import annotations
 
+import ast
 import ctypes as C
+import hashlib
+import inspect
+import json
+import os
+import textwrap
+import types
+import warnings
 
 import numpy as np
 
@@ -357,3 +365,75 @@ def ns_div_range(actx, op, q, T, ghost, Tghost, out, lo, hi):
 
 FUSED = {"dg_ns_flux": dg_ns_flux, "dg_ns_div": dg_ns_div, "dg_ns_div_rk": dg_ns_div_rk, "dg_euler_rhs": dg_euler_rhs, "dg_ns_grad": dg_ns_grad, "dg_ns_rhs": dg_ns_rhs,
          "dg_euler_rhs_rk": dg_euler_rhs_rk, "dg_ns_rhs_rk": dg_ns_rhs_rk}
+
+
+# {{{ guard of the by-name dispatch: the body must be the one the kernels implement
+
+_FP_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "fused_fingerprints.json")
+_FP_CACHE: dict = {}
+
+
+def fingerprint(f) -> str:
+    """SHA-256 over the normalised source (``ast.unparse``: comments and layout do not count) of ``f`` and
+    of every Python function it reaches through its closure cells and through global names of its own
+    module -- the physics helpers included, so that editing ``inviscid_flux`` or ``_bc_state`` changes the
+    fingerprint of every outlined function that uses them."""
+    seen, stack = {}, [f]
+    while stack:
+        g = inspect.unwrap(stack.pop())
+        code = getattr(g, "__code__", None)
+        if code is None or id(code) in seen:
+            continue
+        try:
+            text = ast.unparse(ast.parse(textwrap.dedent(inspect.getsource(g))))
+        except (OSError, TypeError, SyntaxError):
+            text = code.co_code.hex() + repr(code.co_consts)
+        seen[id(code)] = (g.__qualname__, text)
+        names, codes = set(), [code]
+        while codes:
+            c = codes.pop()
+            names.update(c.co_names)
+            codes.extend(k for k in c.co_consts if isinstance(k, types.CodeType))
+        for n in names:
+            v = g.__globals__.get(n)
+            if isinstance(v, types.FunctionType) and v.__module__ == g.__module__:
+                stack.append(v)
+        for cell in g.__closure__ or ():
+            try:
+                v = cell.cell_contents
+            except ValueError:
+                continue
+            if isinstance(v, types.FunctionType):
+                stack.append(v)
+    h = hashlib.sha256()
+    for name, text in sorted(seen.values()):
+        h.update(name.encode() + b"\0" + text.encode() + b"\0")
+    return h.hexdigest()
+
+
+def pinned_fingerprints() -> dict:
+    if "pinned" not in _FP_CACHE:
+        with open(_FP_PATH) as fh:
+            _FP_CACHE["pinned"] = {k: set(v) for k, v in json.load(fh)["functions"].items()}
+    return _FP_CACHE["pinned"]
+
+
+def body_matches(f) -> bool:
+    """True if the outlined function ``f`` is (source-identical to) the body the fused kernel named
+    ``f.__name__`` was written for (fused_fingerprints.json, regenerated by scripts/make_fingerprints.py)."""
+    ok = getattr(f, "_dgb_body_ok", None)           # per function object: closures of one factory share a code object
+    if ok is None:
+        ok = fingerprint(f) in pinned_fingerprints().get(f.__name__, ())
+        try:
+            f._dgb_body_ok = ok
+        except AttributeError:
+            pass
+    return ok
+
+
+def warn_mismatch(name: str) -> None:
+    warnings.warn(f"outlined function {name!r} does not match the body its fused B200 kernel implements: "
+                  "executing it op by op on the device instead (regenerate fused_fingerprints.json only if the "
+                  "kernels were changed accordingly)", RuntimeWarning, stacklevel=3)
+
+# }}}

@@ -87,6 +87,10 @@ class HaloExchange:
         # interior elements first + a communication stream: the exchange hides behind the interior
         # range of each pass (set ``overlap = False`` for the plain exchange-then-compute order)
         self.overlap = True
+        # SMs the persistent kernels leave free while a halo is in flight, so that NCCL's send/recv kernel can
+        # start at once on the communication stream instead of waiting for a CTA of the interior range to
+        # retire (the peer transport has no communication kernel: its pack kernels run on the compute stream)
+        self.sm_reserve = 8 if transport == "nccl" else 0
 
     # {{{ packing
     def _pack(self, data, k):
@@ -123,26 +127,9 @@ class HaloExchange:
             self._peer_release(ch)
             return ghost
         if self.on_device:
-            actx = self.actx
-            ghost = actx.empty(lead + (plan.nghost, self.ndofs))
-            gview = ghost.t.view(-1, plan.nghost, self.ndofs)
-            sends, recvs, keep = [], [], []
-            for k, (peer, tag) in enumerate(zip(plan.peers, plan.tags)):
-                a, b = plan.recv_slots[k]
-                # ghosts of one peer are a strided slab of the ghost array: receive into a dense
-                # buffer, scatter afterwards
-                buf = actx.empty(lead + (b - a, self.ndofs))
-                recvs.append((buf.t, peer, tag)); keep.append((buf, a, b))
-                packed = self._pack(data, k)
-                sends.append((packed.t, peer, self.send_tags[k]))
-            # NCCL enqueues on torch's current stream: make that the context's stream, so that the pack
-            # kernels before it and the scatter kernels after it are ordered with the transfer
-            with torch.cuda.stream(actx.stream):
-                self.comm.exchange(sends, recvs)
-            for buf, a, b in keep:
-                actx._scatter_into(ghost, ghost.t[..., a:b, :], buf)
-            self.bytes_per_exchange = sum(t.numel() * 8 for t, _, _ in sends)
-            return ghost
+            # same transfers as the overlapped path, posted on the context's own stream (the NCCL
+            # operations, the pack kernels before them and the consumers after them are then stream-ordered)
+            return self.exchange_end(self.exchange_begin(data, stream=self.actx.stream))
         ghost = np.empty(lead + (plan.nghost, self.ndofs))
         sends, recvs, bufs = [], [], []
         for k, (peer, tag) in enumerate(zip(plan.peers, plan.tags)):
@@ -164,41 +151,55 @@ class HaloExchange:
             self._comm_stream = torch.cuda.Stream(device=self.actx.device)
         return self._comm_stream
 
-    def exchange_begin(self, data):
+    # components of a message travel as separate transfers of one batch (one NCCL group): for component c the
+    # rows [a, b) of a peer are contiguous both in the packed send buffer (lead, n_k, Np) and in the ghost
+    # array (lead, G, Np), so the payload is received IN PLACE -- no staging buffer, no scatter kernel
+    _COMP_TAGS = 64
+
+    def exchange_begin(self, data, stream=None):
         """Pack on the compute stream, then post the whole batch on the communication stream
         (NCCL group of sends and receives over NVLink).  Returns a ticket for ``exchange_end``;
         kernels enqueued on the compute stream in between overlap the transfer."""
+        import math
         import torch
         plan, actx = self.plan, self.actx
         lead = tuple(data.shape[:-2])
+        ncomp = math.prod(lead) if lead else 1
+        if ncomp > self._COMP_TAGS:
+            raise errors.ShapeMismatch(f"halo messages carry at most {self._COMP_TAGS} components, got {ncomp}")
         ghost = actx.empty(lead + (plan.nghost, self.ndofs))
+        gview = ghost.t.view(ncomp, plan.nghost, self.ndofs)
         sends, recvs, keep = [], [], []
         for k, (peer, tag) in enumerate(zip(plan.peers, plan.tags)):
             a, b = plan.recv_slots[k]
-            buf = actx.empty(lead + (b - a, self.ndofs))
-            recvs.append((buf.t, peer, tag)); keep.append((buf, a, b))
             packed = self._pack(data, k)
-            sends.append((packed.t, peer, self.send_tags[k]))
-        packed_ready = torch.cuda.Event()
-        packed_ready.record(actx.stream)
-        cs = self.comm_stream
-        cs.wait_event(packed_ready)
+            keep.append(packed)
+            pview = packed.t.view(ncomp, -1, self.ndofs)
+            for c in range(ncomp):
+                recvs.append((gview[c, a:b], peer, tag * self._COMP_TAGS + c))
+                sends.append((pview[c], peer, self.send_tags[k] * self._COMP_TAGS + c))
+        cs = self.comm_stream if stream is None else stream
+        if cs is not actx.stream:
+            packed_ready = torch.cuda.Event()
+            packed_ready.record(actx.stream)
+            cs.wait_event(packed_ready)
         with torch.cuda.stream(cs):
-            for t, _, _ in sends + recvs:
-                t.record_stream(cs)
+            if cs is not actx.stream:
+                ghost.t.record_stream(cs)
+                for pk in keep:
+                    pk.t.record_stream(cs)
             self.comm.exchange(sends, recvs)
             done = torch.cuda.Event()
             done.record(cs)
-        self.bytes_per_exchange = sum(t.numel() * 8 for t, _, _ in sends)
-        return ghost, keep, done, sends
+        self.bytes_per_exchange = sum(pk.size * 8 for pk in keep)
+        self.transfers_per_exchange = len(sends)
+        return ghost, keep, done, cs
 
     def exchange_end(self, ticket):
-        """Make the compute stream wait for the transfer and place the received slabs in the ghost array."""
-        ghost, keep, done, _sends = ticket
-        actx = self.actx
-        actx.stream.wait_event(done)
-        for buf, a, b in keep:
-            actx._scatter_into(ghost, ghost.t[..., a:b, :], buf)
+        """Make the compute stream wait for the transfer; the ghost array was filled in place."""
+        ghost, _keep, done, cs = ticket
+        if cs is not self.actx.stream:
+            self.actx.stream.wait_event(done)
         return ghost
     # }}}
 
@@ -338,6 +339,11 @@ class HaloExchange:
     def _begin(self, data):
         return self._peer_begin(data) if self.transport == "peer" else self.exchange_begin(data)
 
+    def _reserve(self, on: bool):
+        if self.on_device and self.sm_reserve:
+            from . import _cabi
+            _cabi.check(self.actx.lib.dgb_set_sm_reserve(self.sm_reserve if on else 0), "dgb_set_sm_reserve")
+
     def _ghost_of(self, ticket):
         return ticket.ghost if self.transport == "peer" else ticket[0]
 
@@ -361,7 +367,9 @@ class HaloExchange:
         actx, nI, E = self.actx, self.plan.n_interior, self.plan.nlocal
         t1 = self._begin(q.data)                                        # state halos in flight ...
         out = actx.empty(q.data.shape)
+        self._reserve(True)
         fused.euler_rhs_range(actx, op, q.data, self._ghost_of(t1), out, 0, nI)   # ... under the interior elements
+        self._reserve(False)
         ghost = self._end(t1)
         fused.euler_rhs_range(actx, op, q.data, ghost, out, nI, E)
         self._release(t1)
@@ -376,12 +384,16 @@ class HaloExchange:
         dim = op.dim
         t1 = self._begin(q.data)                                            # batch 1 in flight ...
         T = actx.empty((dim * (dim + 2) + 1,) + tuple(q.data.shape[1:]))
+        self._reserve(True)
         fused.ns_flux_range(actx, op, q.data, self._ghost_of(t1), T, 0, nI)  # ... under pass 1 of the interior
+        self._reserve(False)
         ghost = self._end(t1)
         fused.ns_flux_range(actx, op, q.data, ghost, T, nI, E)              # pass 1 next to the partition boundary
         t2 = self._begin(T)                                                 # batch 2 in flight ...
         out = actx.empty(q.data.shape)
+        self._reserve(True)
         fused.ns_div_range(actx, op, q.data, T, ghost, self._ghost_of(t2), out, 0, nI)   # ... under pass 2 of the interior
+        self._reserve(False)
         tghost = self._end(t2)
         fused.ns_div_range(actx, op, q.data, T, ghost, tghost, out, nI, E)
         self._release(t1)

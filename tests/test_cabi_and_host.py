@@ -112,5 +112,32 @@ def test_bench_reference_arm_contract():
                 "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
         assert key in line, key
     assert line["impl"] == "reference" and line["unit"] == "GDOF/s" and line["value"] > 0
-    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert line["cpu_baseline"]["kind"] in ("reference", "port") and line["cpu_baseline"]["cores"] >= 1
+    # "reference" when the unmodified package is installed under baseline/_ref, else the port
+    assert (line["cpu_baseline"]["kind"] == "reference") == os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "laze"))
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def test_fused_fingerprints_in_sync():
+    """The by-name dispatch of B200ArrayContext.outline is guarded by a source fingerprint of the outlined
+    function and every helper it reaches; the pinned fingerprints must be those of the shipped operator
+    program, and an edited helper must change them."""
+    import importlib
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "scripts"))
+    mk = importlib.import_module("make_fingerprints")
+    from paper_2512_17101_b200 import fused, operators
+    pinned = fused.pinned_fingerprints()
+    assert {k: set(v) for k, v in mk.compute().items()} == pinned
+    f = operators._make_ns_flux(3, False)
+    assert fused.body_matches(f)
+    saved = operators._pressure
+    try:
+        def _pressure(actx, gamma, rho, ener, mom, vel):          # another equation of state
+            return (gamma - 1.0) * ener
+        _pressure.__module__ = operators.__name__
+        operators._pressure = _pressure
+        g = operators._make_ns_flux(3, False)
+        assert g.__name__ == "dg_ns_flux" and not fused.body_matches(g)
+    finally:
+        operators._pressure = saved

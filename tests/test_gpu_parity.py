@@ -381,3 +381,63 @@ def test_graph_compiled_function_semantics(gpu):
         gpu.to_numpy(out["picked"])
     ok = cf(gpu.from_numpy(np.ones(11)), 1.5, idx)        # the flag is cleared once reported
     assert np.array_equal(gpu.to_numpy(ok["y"]), np.sqrt(np.ones(11) + 1.5))
+
+
+def test_edited_outlined_body_is_not_dispatched_by_name(gpu):
+    """A function NAMED like a fused kernel but with a different body (here: another wave-speed estimate in
+    the helpers of dg_euler_rhs) must not silently run the built-in physics: the context executes the body
+    op by op on the device, and the result matches the oracle running the same edited body."""
+    from paper_2512_17101_b200 import operators
+    cpu = NumpyArrayContext()
+    saved = operators._wavespeed
+    try:
+        def _wavespeed(actx, gamma, q, vel, p, dim):               # edited helper: a cruder bound
+            return actx.np.sqrt(gamma * p / q[0]) * 2.0
+        _wavespeed.__module__ = operators.__name__
+        operators._wavespeed = _wavespeed
+        dc, dg = make_dcoll(cpu, 3, 2, 3, "mixed"), make_dcoll(gpu, 3, 2, 3, "mixed")
+        q0 = random_state(3, dc.nelements, dc.Np, seed=4)
+        n_fused0 = gpu.launch_count
+        with pytest.warns(RuntimeWarning, match="does not match the body"):
+            og = EulerOperator(dg, farfield=FARFIELD[3])
+        assert not getattr(og._f, "fused", False)
+        ref = dc.to_numpy(EulerOperator(dc, farfield=FARFIELD[3]).rhs(dc.from_numpy(q0)))
+        got = dg.to_numpy(og.rhs(dg.from_numpy(q0)))
+        assert rel_err(got, ref) <= TOL_RHS
+        assert gpu.launch_count - n_fused0 > 10                    # op by op, not one fused kernel
+    finally:
+        operators._wavespeed = saved
+    # the unedited program dispatches to the fused kernel again and differs from the edited physics
+    og2 = EulerOperator(dg, farfield=FARFIELD[3])
+    assert getattr(og2._f, "fused", False)
+    got2 = dg.to_numpy(og2.rhs(dg.from_numpy(q0)))
+    assert rel_err(got2, ref) > 1e-6
+
+
+def test_integration_stub_executes(gpu):
+    """the reference-side ctypes binding (integration/laze_backend_b200.py) runs the
+    CallSteps of dg_ns_flux / dg_ns_div on NumPy arrays exactly as the reference's interpreter would bind
+    them, and reproduces the oracle."""
+    import importlib.util
+    import os
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "integration", "laze_backend_b200.py")
+    spec = importlib.util.spec_from_file_location("laze_backend_b200", path)
+    stub = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(stub)
+    cpu = NumpyArrayContext()
+    d = make_dcoll(cpu, 3, 3, 3, "mixed")
+    op = NavierStokesOperator(d, farfield=FARFIELD[3], mu=2e-2)
+    q0 = random_state(3, d.nelements, d.Np, seed=6)
+    q = d.from_numpy(q0)
+    T_ref = np.asarray(cpu.to_numpy(op.flux(q)))
+    rhs_ref = d.to_numpy(op.rhs(q))
+    host = lambda a: np.asarray(cpu.to_numpy(a))
+    fargs = [q0] + [host(a) for a in op._flux_args()]
+    T = stub.run_call_step_b200("dg_ns_flux", {f"_p{k}": a for k, a in enumerate(fargs)})["out"]
+    assert rel_err(T, T_ref) <= TOL_RHS
+    dargs = [q0, T] + [host(a) for a in op._div_args()]
+    # the handle is keyed on the face-map arrays: hand the stub the same ndarrays for both calls
+    dargs[9], dargs[10] = fargs[7], fargs[8]
+    out = stub.run_call_step_b200("dg_ns_div", {f"_p{k}": a for k, a in enumerate(dargs)})["out"]
+    assert rel_err(out, rhs_ref) <= TOL_RHS
+    stub.close()
