@@ -16,8 +16,7 @@ def needs_build() -> bool:
     if not os.path.exists(OUT):
         return True
     t = os.path.getmtime(OUT)
-    deps = SOURCES + ["dgb_kernels.cuh", "dgb_kernels_async.cuh", "dgb_kernels_warp.cuh", "dgb_kernels_flux.cuh",
-                      "dgb_internal.h", os.path.join("..", "..", "include", "dgb200.h")]
+    deps = SOURCES + [f for f in os.listdir(HERE) if f.endswith((".cuh", ".h"))] + [os.path.join("..", "..", "include", "dgb200.h")]
     return any(os.path.getmtime(os.path.join(HERE, d)) > t for d in deps)
 
 

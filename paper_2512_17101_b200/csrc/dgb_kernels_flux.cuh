@@ -38,6 +38,12 @@
 #ifndef DGB_L2_PREFETCH_BLOCKS
 #define DGB_L2_PREFETCH_BLOCKS 0
 #endif
+// pass 2: one buffer for a block's small inputs (q, lam, face Jacobians, connectivity) instead of two: the next
+// block's are staged as soon as the face phase has read these and land during the contraction + store.
+// 15.6 instead of 18.7 KB of shared memory per warp (3D p3), i.e. room for 12 warps instead of 11.
+#ifndef DGB_DIV_SINGLE_SMALL
+#define DGB_DIV_SINGLE_SMALL 0
+#endif
 
 #ifdef DGB_PHASE_TIMING
 // warp 0 of every CTA accumulates the cycles it spends in each phase (scripts/phase_timing_flux.py)
@@ -50,6 +56,18 @@
 
 #ifndef DGB_T_RECORD
 #define DGB_T_RECORD 0
+#endif
+// how the neighbour gathers of pass 2 go through the cache hierarchy: 0 = default (allocate in L1),
+// 1 = ld.global.cg (L2 only: no L1 line per in-flight sector), 2 = ld.global.nc
+#ifndef DGB_GATHER_LD
+#define DGB_GATHER_LD 0
+#endif
+#if DGB_GATHER_LD == 1
+#define DGB_GLD(p) __ldcg(p)
+#elif DGB_GATHER_LD == 2
+#define DGB_GLD(p) __ldg(p)
+#else
+#define DGB_GLD(p) (*(p))
 #endif
 
 namespace dgb {
@@ -516,6 +534,8 @@ struct alignas(16) Div3Small {
   double sj[KW][EL::NF];
   long long conn[KW][EL::NF];
   double rj[KW];
+  __device__ __forceinline__ double qv(int c, int e, int j) const { return Qs[(c * KW + e) * EL::NP + j]; }
+  __device__ __forceinline__ double lamv(int e, int j) const { return Lam[e * EL::NP + j]; }
 };
 
 template <int DIM, int P, int KW>
@@ -528,7 +548,7 @@ struct alignas(16) Div3Warp {
   // stored and DMMA rows do not mix
   double Ts[NCOL * EL::LDV];
   double Fs[NCOL * EL::LDF];
-  Div3Small<DIM, P, KW> sm[2];
+  Div3Small<DIM, P, KW> sm[DGB_DIV_SINGLE_SMALL ? 1 : 2];
 };
 
 template <int DIM, int P, int KW, int NWARPS>
@@ -656,9 +676,9 @@ __device__ __noinline__ VecC<DIM> boundary_operand(int bc, int f, VecC<DIM> qm_,
 // box meshes a third of all face sides are in-block.  `Ts_own` = the block's operand rows; the caller's
 // T rows are the cp.async group with TW younger groups behind it (waited for here, after the first
 // batch of global gathers has been issued).
-template <int DIM, int P, int KW, int NB, bool LAZY, int K0 = 0, bool GH = true, bool INB = false, int TW = 1>
+template <int DIM, int P, int KW, int NB, bool LAZY, int K0 = 0, bool GH = true, bool INB = false, int TW = 1, class SMV>
 __device__ __forceinline__ void div_face_phase(const int* flc, const int* fn, const int* perm,
-                                               const Div3Small<DIM, P, KW>& M, double* Fs, const DiscDev& d,
+                                               const SMV& M, double* Fs, const DiscDev& d,
                                                const double* __restrict__ q, const double* __restrict__ T,
                                                const double* __restrict__ ghost, const double* __restrict__ Tghost,
                                                const Phys& ph, long long e0, int nel, int lane,
@@ -683,7 +703,11 @@ __device__ __forceinline__ void div_face_phase(const int* flc, const int* fn, co
         if (flk >= 0 && e < nel) {
           const long long cn = M.conn[e][f];
           cnk[b] = cn;
+#ifdef DGB_EXP_LOCALGATHER      // timing experiment only (results invalid): every neighbour is the element itself
+          const long long nb = e0 + e;
+#else
           const long long nb = DGB_CONN_NB(cn);
+#endif
           const int nf = DGB_CONN_NF(cn);
           const int jp = fn[nf * NFP + perm[DGB_CONN_PERM(cn) * NFP + m]];
           // boundary faces take nothing from the neighbour slot (it names the element itself)
@@ -698,13 +722,13 @@ __device__ __forceinline__ void div_face_phase(const int* flc, const int* fn, co
             const int r0 = nf == 0 ? 0 : nf - 1;
 #pragma unroll
             for (int c = 0; c < C; ++c) {
-              qp[b][c] = qbase[c * pstride];
-              nbr[b][c] = tbase[(r0 * C + c) * tps];
+              qp[b][c] = DGB_GLD(qbase + c * pstride);
+              nbr[b][c] = DGB_GLD(tbase + (r0 * C + c) * tps);
             }
-            lam_p[b] = tbase[(DIM * C) * tps];
+            lam_p[b] = DGB_GLD(tbase + (DIM * C) * tps);
             if (!LAZY && nf == 0) {
 #pragma unroll
-              for (int rc = 0; rc < (DIM - 1) * C; ++rc) ex[b][rc] = tbase[(C + rc) * tps];
+              for (int rc = 0; rc < (DIM - 1) * C; ++rc) ex[b][rc] = DGB_GLD(tbase + (C + rc) * tps);
             }
           }
         }
@@ -727,10 +751,10 @@ __device__ __forceinline__ void div_face_phase(const int* flc, const int* fn, co
             const double* trow = Ts_own + eb * EL::LDV + jp;
 #pragma unroll
             for (int c = 0; c < C; ++c) {
-              qp[b][c] = M.Qs[(c * KW + eb) * NP + jp];
+              qp[b][c] = M.qv(c, eb, jp);
               nbr[b][c] = trow[c * (KW * EL::LDV) + r0 * EL::NPK];
             }
-            lam_p[b] = M.Lam[eb * NP + jp];
+            lam_p[b] = M.lamv(eb, jp);
             if (nf == 0) {
               if (LAZY) {
 #pragma unroll
@@ -766,9 +790,9 @@ __device__ __forceinline__ void div_face_phase(const int* flc, const int* fn, co
           const double* tbase = (in_ghost ? Tghost : T) + (in_ghost ? nb - E : nb) * t_elem_stride<NPLT, NP>() + jp;
 #pragma unroll
           for (int c = 0; c < C; ++c) {
-            double t = tbase[(C + c) * tps];
+            double t = DGB_GLD(tbase + (C + c) * tps);
 #pragma unroll
-            for (int r = 2; r < DIM; ++r) t += tbase[(r * C + c) * tps];
+            for (int r = 2; r < DIM; ++r) t += DGB_GLD(tbase + (r * C + c) * tps);
             ex[b][c] = t;
           }
         }
@@ -782,10 +806,10 @@ __device__ __forceinline__ void div_face_phase(const int* flc, const int* fn, co
         const int e = flk & 3, f = (flk >> 2) & 3, jm = (flk >> 8) & 255, fm = (flk >> 16) & 255;
         const int nf = DGB_CONN_NF(cnk[b]), bc = DGB_CONN_BC(cnk[b]);
         const double sj = M.sj[e][f];
-        const double lam_m = M.Lam[e * NP + jm];
+        const double lam_m = M.lamv(e, jm);
         double qm[C];
 #pragma unroll
-        for (int c = 0; c < C; ++c) qm[c] = M.Qs[(c * KW + e) * NP + jm];
+        for (int c = 0; c < C; ++c) qm[c] = M.qv(c, e, jm);
         double* fs = Fs + e * EL::LDF + fm;
         if (bc == 0) {
           if (nf == 0) {
@@ -868,6 +892,8 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
   tickets_init(tks, wb, counter, lane);
 
   // cp.async groups retire in order: S(b), T(b), S(b+1), T(b+1), ...
+  constexpr bool SS = DGB_DIV_SINGLE_SMALL != 0;
+  static_assert(!(SS && DGB_DIV_INBLOCK), "in-block neighbours need the double-buffered small inputs");
   DGB_WTICK_INIT
   while (wb < nwblocks) {
     const long long e0 = ebeg + wb * KW;
@@ -875,8 +901,10 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
     const long long wb_next = tickets_next(tks, wstride, counter, lane);
     const long long e1 = ebeg + wb_next * KW;
     const int nel1 = wb_next < nwblocks ? (int)((eend - e1) < (long long)KW ? (eend - e1) : (long long)KW) : 0;
-    if (nel1 > 0) div_stage_small<DIM, P, KW>(W.sm[buf ^ 1], d, q, T, e1, nel1, lane);
-    cp_async_commit();                   // S(b+1)
+    if (!SS) {
+      if (nel1 > 0) div_stage_small<DIM, P, KW>(W.sm[buf ^ 1], d, q, T, e1, nel1, lane);
+      cp_async_commit();                 // S(b+1)
+    }
     if (DGB_L2_PREFETCH_BLOCKS > 0 && !DGB_T_RECORD) {
       const long long wbp = wb_next + DGB_L2_PREFETCH_BLOCKS;
       if (wbp < nwblocks) {
@@ -886,9 +914,10 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
       }
     }
     DGB_WTICK(5);
-    cp_async_wait<2>();                  // S(b) has landed; T(b) and S(b+1) may still be in flight
+    if (SS) cp_async_wait<1>();          // S(b) has landed; T(b) may still be in flight
+    else cp_async_wait<2>();             // S(b) has landed; T(b) and S(b+1) may still be in flight
     __syncwarp();
-    const Div3Small<DIM, P, KW>& M = W.sm[buf];
+    const Div3Small<DIM, P, KW>& M = W.sm[SS ? 0 : buf];
     DGB_WTICK(0);
 
     // ---- face gather + Rusanov.  The own-side flux is linear in the block's own T rows with
@@ -897,6 +926,14 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
     //      Fs = (nbr - sJ max(lam-, lam+) (q- - q+)) / 2,  nbr = sJ F+.n+ gathered from the neighbour.
     div_face_phase<DIM, P, KW, NB, (DGB_DIV_LAZY_EX != 0), 0, GH, (DGB_DIV_INBLOCK != 0), 1>(S.flc, S.fn, S.perm, M, W.Fs, d, q, T, ghost, Tghost, ph, e0, nel, lane, W.Ts);
     DGB_WTICK(1);
+    double rj[WS::NTILE];
+#pragma unroll
+    for (int mt = 0; mt < WS::NTILE; ++mt) rj[mt] = M.rj[(mt * 8 + (lane >> 2)) % KW];
+    if (SS) {
+      __syncwarp();                      // every lane has read the block's small inputs
+      if (nel1 > 0) div_stage_small<DIM, P, KW>(W.sm[0], d, q, T, e1, nel1, lane);
+      cp_async_commit();                 // S(b+1): lands during the contraction and the store
+    }
     cp_async_wait<1>();                  // T(b) has landed
     __syncwarp();
     DGB_WTICK(2);
@@ -909,9 +946,6 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
       for (int ni = 0; ni < EL::NI; ++ni) { acc[mt][ni][0] = 0.0; acc[mt][ni][1] = 0.0; }
     mma_block<EL::NI, WS::NTILE>(acc, W.Ts, EL::LDV, S.Wv, EL::LDV, EL::KV / 4, lane);
     mma_block<EL::NI, WS::NTILE>(acc, W.Fs, EL::LDF, S.Wl, EL::LDF, EL::KF / 4, lane);
-    double rj[WS::NTILE];
-#pragma unroll
-    for (int mt = 0; mt < WS::NTILE; ++mt) rj[mt] = M.rj[(mt * 8 + (lane >> 2)) % KW];
     __syncwarp();                        // all operand rows consumed: the next block may land on them
     DGB_WTICK(3);
     if (nel1 > 0) div_stage_rows<DIM, P, KW>(W.Ts, d, T, e1, nel1, lane);

@@ -1,0 +1,283 @@
+// TMA-staged kernels of the flux arrangement (round 2).
+//
+// ncu on k_nsdiv3 (profiles/r02_ncu_pass2_occupancy.md): the L1/LSU pipe is what saturates first
+// (62 % of its wavefront peak with 8 warps; at 12 warps the warps stall on `mio_throttle` and the
+// kernel gets SLOWER).  A quarter of those wavefronts and ~10 % of the warp instructions are the
+// LDGSTS copies that stage a block's own rows (28 per lane and block for 3D p3, 70 for p4 where the
+// odd row length forces 8-byte copies).  Here a block's rows arrive by the Tensor Memory
+// Accelerator instead: the state and the flux planes are described ONCE per launch as 2-D tensors
+// (plane, element*Np + node) and a block's rows of ALL planes are one box
+// [planes] x [KW*Np doubles] -- one `cp.async.bulk.tensor.2d` (SASS UTMALDG) issued by one lane,
+// completion on an mbarrier, no registers, no LSU wavefronts, no address arithmetic.  The box lands
+// as [plane][element][node], which IS a DMMA operand layout: column (field c, element e) of
+// reference direction r starts at ((r*C + c)*BOXW + e*Np), K runs over the nodes.
+//
+// k_nsdiv8 = pass 2 (operators.py: dg_ns_div), same arithmetic in the same order as k_nsdiv3
+// (bitwise identical results).
+#pragma once
+#include "dgb_kernels_flux.cuh"
+
+#include <cuda.h>
+
+namespace dgb {
+
+__device__ __forceinline__ unsigned smem_addr_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init_(unsigned long long* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_test_(unsigned long long* bar, int parity) {
+  unsigned ok;
+  asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+               : "=r"(ok) : "r"(smem_addr_u32(bar)), "r"(parity) : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_(unsigned long long* bar, int parity) {
+  while (!mbar_test_(bar, parity)) { }
+}
+// one box of a 2-D tensor (x = element*Np + node, y = plane) -> shared memory
+__device__ __forceinline__ void tma_load_2d(void* smem, const CUtensorMap* map, int x, int y, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.tensor.2d.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+               ::"r"(smem_addr_u32(smem)), "l"(reinterpret_cast<unsigned long long>(map)), "r"(smem_addr_u32(bar)),
+                 "r"(x), "r"(y) : "memory");
+}
+// contiguous bytes (multiple of 16, both sides 16-byte aligned) -> shared memory
+__device__ __forceinline__ void bulk_load_1d(void* smem, const void* gmem, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_addr_u32(smem)), "l"(gmem), "r"(bytes), "r"(smem_addr_u32(bar)) : "memory");
+}
+
+// operand fragments from per-lane column offsets (the box layout is not a single row stride when
+// the box width is padded)
+template <int NI, int MT>
+__device__ __forceinline__ void mma_block_off(double (&acc)[MT][NI][2], const double* __restrict__ Xs,
+                                              const int (&aoff)[MT], const double* __restrict__ Ws, int ldw,
+                                              int ksteps, int lane) {
+  const int r = lane >> 2, kq = lane & 3;
+  const double* wp = Ws + r * ldw + kq;
+#pragma unroll 5
+  for (int ks = 0; ks < ksteps; ++ks) {
+    double a[MT], b[NI];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) a[mt] = Xs[aoff[mt] + kq + ks * 4];
+#pragma unroll
+    for (int ni = 0; ni < NI; ++ni) b[ni] = wp[ni * 8 * ldw + ks * 4];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int ni = 0; ni < NI; ++ni) dmma884(acc[mt][ni][0], acc[mt][ni][1], a[mt], b[ni]);
+  }
+}
+
+template <int DIM, int P, int KW>
+struct TmaBox {
+  using EL = ElemT<DIM, P>;
+  // Box width in doubles, a multiple of 16 bytes.  The global address of a box must be 16-byte aligned as well:
+  // with an odd Np a block that starts at an odd element is fetched from one double earlier and read at offset 1
+  // (box_shift), so the box holds one double more than the block.
+  static constexpr int BOXW = (KW * EL::NP + (EL::NP % 2) + 1) / 2 * 2;
+  __device__ static __forceinline__ int box_shift(long long e0) { return (EL::NP % 2) ? (int)((e0 * EL::NP) & 1) : 0; }
+  static constexpr int NPL_T = DIM * EL::C;                  // flux planes in the T box (the wave speed travels apart)
+};
+
+// small per-block geometry, double-buffered, by 8-byte cp.async as before (a few instructions)
+template <int DIM, int P, int KW>
+struct Div8Geo {
+  using EL = ElemT<DIM, P>;
+  double sj[KW][EL::NF];
+  long long conn[KW][EL::NF];
+  double rj[KW];
+};
+
+template <int DIM, int P, int KW>
+struct alignas(128) Div8Warp {
+  using EL = ElemT<DIM, P>;
+  using BX = TmaBox<DIM, P, KW>;
+  static constexpr int NCOL = EL::C * KW;
+  static constexpr int NTILE = (NCOL + 7) / 8;
+  alignas(128) double Tb[BX::NPL_T * BX::BOXW + 8];     // [plane r*C + c][element][node]  (+8: K padding of the last column)
+  alignas(128) double Qb[EL::C * BX::BOXW];             // [field][element][node]
+  alignas(128) double Lam[BX::BOXW];                    // wave speed rows of the block
+  double Fs[NCOL * EL::LDF];
+  Div8Geo<DIM, P, KW> geo[2];
+  unsigned long long bar_q, bar_t;
+};
+
+template <int DIM, int P, int KW, int NWARPS>
+struct Div8Smem {
+  using EL = ElemT<DIM, P>;
+  double Wv[EL::NPR * EL::LDV];
+  double Wl[EL::NPR * EL::LDF];
+  Div8Warp<DIM, P, KW> w[NWARPS];
+  int fn[EL::NF * EL::NFP];
+  int perm[EL::NPERM * EL::NFP];
+  int flc[face_rounds<DIM, P, KW>() * 32];
+};
+
+// what div_face_phase reads of a block (k_nsdiv3 passes its Div3Small)
+template <int DIM, int P, int KW>
+struct Div8View {
+  using EL = ElemT<DIM, P>;
+  const double* Qs; const double* Lam;      // already advanced by the block's box shift
+  const double (*sj)[EL::NF];
+  const long long (*conn)[EL::NF];
+  __device__ __forceinline__ double qv(int c, int e, int j) const { return Qs[c * TmaBox<DIM, P, KW>::BOXW + e * EL::NP + j]; }
+  __device__ __forceinline__ double lamv(int e, int j) const { return Lam[e * EL::NP + j]; }
+};
+
+template <int DIM, int P, int KW, int NWARPS, bool GH>
+__global__ void __launch_bounds__(NWARPS * 32, 1)
+k_nsdiv8(DiscDev d, const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_t,
+         const __grid_constant__ CUtensorMap map_l, const double* __restrict__ q, const double* __restrict__ T,
+         const double* __restrict__ ghost, const double* __restrict__ Tghost,
+         Epilogue ep, Phys ph, long long ebeg, long long eend, long long nwblocks,
+         unsigned long long* __restrict__ counter) {
+  using EL = ElemT<DIM, P>;
+  using WS = Div8Warp<DIM, P, KW>;
+  using BX = TmaBox<DIM, P, KW>;
+  constexpr int C = EL::C, NP = EL::NP, NF = EL::NF, NFP = EL::NFP;
+  constexpr int NT = NWARPS * 32;
+  constexpr int NR = face_rounds<DIM, P, KW>();
+  // face nodes per lane with their gathers in flight together: 2 needs ~230 registers (8 warps), 1 fits 168 (9-12 warps)
+  constexpr int NB = NWARPS > 8 ? 1 : DGB_DIV_NB;
+  constexpr int BOXW = BX::BOXW;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  auto& S = *reinterpret_cast<Div8Smem<DIM, P, KW, NWARPS>*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long E = d.E;
+
+  for (int n = tid; n < EL::NPR * EL::LDV; n += NT) S.Wv[n] = d.Wv2[n];
+  for (int n = tid; n < EL::NPR * EL::LDF; n += NT) S.Wl[n] = d.Wl[n];
+  for (int n = tid; n < NF * NFP; n += NT) S.fn[n] = d.tables[n];
+  for (int n = tid; n < EL::NPERM * NFP; n += NT) S.perm[n] = d.tables[NF * NFP + n];
+  WS& W = S.w[warp];
+  {
+    double* z = reinterpret_cast<double*>(&W);
+    for (int n = lane; n < (int)(sizeof(WS) / 8); n += 32) z[n] = 0.0;
+  }
+  __syncwarp();
+  if (lane == 0) { mbar_init_(&W.bar_q, 1); mbar_init_(&W.bar_t, 1); }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");     // the zero fill above precedes the TMA writes
+  __syncthreads();
+  for (int n = tid; n < NR * 32; n += NT) S.flc[n] = face_lane_code<DIM, P, KW>(S.fn, n);
+  __syncthreads();
+
+  // per-lane operand column offsets inside a box group of C planes (constant for the whole kernel)
+  int aoff[WS::NTILE];
+#pragma unroll
+  for (int mt = 0; mt < WS::NTILE; ++mt) {
+    int col = mt * 8 + (lane >> 2);
+    if (col >= WS::NCOL) col = WS::NCOL - 1;        // padding column: any finite rows, its accumulators are dropped
+    const int c = col / KW, e = col - c * KW;
+    aoff[mt] = c * BOXW + e * NP;
+  }
+  int foff[WS::NTILE];
+#pragma unroll
+  for (int mt = 0; mt < WS::NTILE; ++mt) {
+    int col = mt * 8 + (lane >> 2);
+    if (col >= WS::NCOL) col = WS::NCOL - 1;
+    foff[mt] = col * EL::LDF;
+  }
+
+  auto nel_of = [&](long long wbx) -> int {
+    if (wbx >= nwblocks) return 0;
+    const long long e = ebeg + wbx * KW;
+    return (int)((eend - e) < (long long)KW ? (eend - e) : (long long)KW);
+  };
+  auto issue_q = [&](long long e0) {                  // state box + wave-speed rows -> bar_q   (lane 0)
+    mbar_expect_tx(&W.bar_q, (unsigned)((C + 1) * BOXW * 8));
+    const int x = (int)(e0 * NP) - BX::box_shift(e0);
+    tma_load_2d(W.Qb, &map_q, x, 0, &W.bar_q);
+    tma_load_2d(W.Lam, &map_l, x, 0, &W.bar_q);
+  };
+  auto issue_t = [&](long long e0) {                  // flux-plane box -> bar_t   (lane 0)
+    mbar_expect_tx(&W.bar_t, (unsigned)(BX::NPL_T * BOXW * 8));
+    tma_load_2d(W.Tb, &map_t, (int)(e0 * NP) - BX::box_shift(e0), 0, &W.bar_t);
+  };
+  auto stage_geo = [&](Div8Geo<DIM, P, KW>& g, long long e0, int nelx) {
+    if (lane < nelx * NF) {
+      cp_async8(&g.sj[0][lane], d.sj + e0 * NF + lane);
+      cp_async8(&g.conn[0][lane], d.conn + e0 * NF + lane);
+    }
+    if (lane < nelx) cp_async8(&g.rj[lane], d.rj + e0 + lane);
+  };
+
+  const long long wstride = (long long)gridDim.x * NWARPS;
+  long long wb = (long long)blockIdx.x * NWARPS + warp;
+  if (wb >= nwblocks) return;
+  {
+    const long long e0 = ebeg + wb * KW;
+    if (lane == 0) { issue_q(e0); issue_t(e0); }
+    stage_geo(W.geo[0], e0, nel_of(wb));
+    cp_async_commit();
+  }
+  TicketStream tks;
+  tickets_init(tks, wb, counter, lane);
+
+  for (int it = 0;; ++it) {
+    const int buf = it & 1, par = it & 1;
+    const long long e0 = ebeg + wb * KW;
+    const int nel = nel_of(wb);
+    const long long wb_next = tickets_next(tks, wstride, counter, lane);
+    const int nel1 = nel_of(wb_next);
+    const long long e1 = ebeg + wb_next * KW;
+    if (nel1 > 0) stage_geo(W.geo[buf ^ 1], e1, nel1);
+    cp_async_commit();
+    cp_async_wait<1>();                  // geometry of this block
+    mbar_wait_(&W.bar_q, par);           // state + wave speed of this block
+    __syncwarp();
+    const int sh = BX::box_shift(e0);
+    Div8View<DIM, P, KW> M{W.Qb + sh, W.Lam + sh, W.geo[buf].sj, W.geo[buf].conn};
+
+#ifndef DGB_EXP_NOFACE            // timing experiments only (results invalid)
+    div_face_phase<DIM, P, KW, NB, (DGB_DIV_LAZY_EX != 0), 0, GH, false, 1>(S.flc, S.fn, S.perm, M, W.Fs, d, q, T, ghost,
+                                                                            Tghost, ph, e0, nel, lane, nullptr);
+#endif
+    double rj[WS::NTILE];
+#pragma unroll
+    for (int mt = 0; mt < WS::NTILE; ++mt) rj[mt] = W.geo[buf].rj[(mt * 8 + (lane >> 2)) % KW];
+    __syncwarp();                        // every lane has read the state box: the next one may land on it
+    if (nel1 > 0 && lane == 0) issue_q(e1);
+    mbar_wait_(&W.bar_t, par);           // flux planes of this block
+
+    // ---- tensor-core contraction: volume rows straight from the box, then the face operand rows ----
+    double acc[WS::NTILE][EL::NI][2];
+#pragma unroll
+    for (int mt = 0; mt < WS::NTILE; ++mt)
+#pragma unroll
+      for (int ni = 0; ni < EL::NI; ++ni) { acc[mt][ni][0] = 0.0; acc[mt][ni][1] = 0.0; }
+#ifndef DGB_EXP_NOMMA
+#pragma unroll
+    for (int r = 0; r < DIM; ++r)
+      mma_block_off<EL::NI, WS::NTILE>(acc, W.Tb + r * (C * BOXW) + sh, aoff, S.Wv + r * EL::NPK, EL::LDV, EL::NPK / 4, lane);
+    mma_block_off<EL::NI, WS::NTILE>(acc, W.Fs, foff, S.Wl, EL::LDF, EL::KF / 4, lane);
+#else
+    acc[0][0][0] = W.Tb[aoff[0] + sh + lane] + W.Fs[foff[0] + lane];
+#endif
+    __syncwarp();                        // operand rows consumed
+    if (nel1 > 0 && lane == 0) issue_t(e1);
+
+#pragma unroll
+    for (int mt = 0; mt < WS::NTILE; ++mt) {
+      const int col = mt * 8 + (lane >> 2);
+      const int c = col / KW, e = col - c * KW;
+      if (col < WS::NCOL && e < nel) {
+        const long long rowbase = ((long long)c * E + e0 + e) * NP;
+#pragma unroll
+        for (int ni = 0; ni < EL::NI; ++ni) {
+          const int i = ni * 8 + 2 * (lane & 3);
+          store_pair<NP>(ep, rowbase + i, i, rj[mt] * acc[mt][ni][0], rj[mt] * acc[mt][ni][1]);
+        }
+      }
+    }
+    if (nel1 == 0) break;
+    wb = wb_next;
+  }
+  cp_async_wait<0>();
+}
+
+}  // namespace dgb

@@ -3,6 +3,7 @@
 #include "dgb_internal.h"
 #include "dgb_kernels_flux.cuh"
 #include "dgb_kernels_div7.cuh"
+#include "dgb_kernels_tma.cuh"
 
 #include <cstdlib>
 #include <string>
@@ -12,7 +13,7 @@ namespace {
 // Measured on B200 (profiles/r01_flux_variants.md): pass 1 is fastest with 12 warps (164 registers, four
 // face nodes per lane in flight), pass 2 with 8 warps (235 registers, no spills, NB = 2).
 #ifndef DGB_DIV_KERNEL_DEFAULT
-#define DGB_DIV_KERNEL_DEFAULT 3
+#define DGB_DIV_KERNEL_DEFAULT 8          // TMA-staged pass 2 (profiles/r02_pass2_tma.md)
 #endif
 #ifndef DGB_FLUX_WARPS
 #define DGB_FLUX_WARPS 12
@@ -115,7 +116,88 @@ int launch_div7(const dgb_disc* d, const double* q, const double* T, const doubl
   return DGB_OK;
 }
 
-// DGB_DIV_KERNEL selects the pass-2 kernel at run time: 7 = role-split k_nsdiv7, 3 = warp-autonomous k_nsdiv3
+// ---- TMA-staged pass 2 (k_nsdiv8, dgb_kernels_tma.cuh) ----------------------------------------------------
+#ifndef DGB_DIV8_WARPS
+#define DGB_DIV8_WARPS 10         // measured (3D p3, n=94): 8 warps NB 2 7.71 ms, 10 warps NB 1 7.56 ms, 12 warps NB 1 8.15 ms
+#endif
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) != cudaSuccess ||
+        qr != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return (EncodeTiledFn)p;
+  }();
+  return fn;
+}
+
+// 2-D tensor (x = element*Np + node, y = plane) over `nplanes` planes of `width` doubles, `stride` doubles apart;
+// box = boxw x boxh doubles, no swizzle (the box lands as [plane][x]), out-of-range reads give zeros
+bool make_plane_map(CUtensorMap* m, const double* base, long long width, int nplanes, long long stride, int boxw, int boxh) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc || (((uintptr_t)base) & 15) || (stride * 8) % 16 != 0 || boxw > 256 || boxh > 256 || width <= 0) return false;
+  cuuint64_t gdim[2] = {(cuuint64_t)width, (cuuint64_t)nplanes};
+  cuuint64_t gstr[1] = {(cuuint64_t)stride * 8};
+  cuuint32_t box[2] = {(cuuint32_t)boxw, (cuuint32_t)boxh};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)base, gdim, gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int DIM, int P> struct Cfg8 {
+  static constexpr int KW = DIM == 3 ? 3 : 4;
+  static constexpr size_t per = sizeof(dgb::Div8Warp<DIM, P, KW>);
+  static constexpr size_t fixed = sizeof(dgb::Div8Smem<DIM, P, KW, 1>) - per;
+  static constexpr int NW = fit_warps(fixed, per, DGB_DIV8_WARPS);
+};
+
+// returns 1 when the arrays cannot be described to the TMA unit (alignment): the caller falls back to k_nsdiv3
+template <int DIM, int P>
+int launch_div8(const dgb_disc* d, const double* q, const double* T, const double* ghost, const double* Tghost,
+                const dgb::Epilogue& ep, const dgb::Phys& ph, long long ebeg, long long eend, cudaStream_t st, bool* ok) {
+  using C = Cfg8<DIM, P>;
+  using EL = dgb::ElemT<DIM, P>;
+  using BX = dgb::TmaBox<DIM, P, C::KW>;
+  *ok = false;
+  const long long E = d->dev.E, width = E * EL::NP;
+  if (width >= (1LL << 31)) return DGB_OK;
+  CUtensorMap mq, mt, ml;
+  if (!make_plane_map(&mq, q, width, EL::C, width, BX::BOXW, EL::C)) return DGB_OK;
+  if (!make_plane_map(&mt, T, width, BX::NPL_T, width, BX::BOXW, BX::NPL_T)) return DGB_OK;
+  if (!make_plane_map(&ml, T + (long long)BX::NPL_T * width, width, 1, width, BX::BOXW, 1)) return DGB_OK;
+  *ok = true;
+  auto kern = d->dev.G > 0 ? dgb::k_nsdiv8<DIM, P, C::KW, C::NW, true> : dgb::k_nsdiv8<DIM, P, C::KW, C::NW, false>;
+  const size_t smem = sizeof(dgb::Div8Smem<DIM, P, C::KW, C::NW>);
+  const long long nwb = (eend - ebeg + C::KW - 1) / C::KW;
+  if (nwb == 0) return DGB_OK;
+  static DgbPerDevice configured[2];
+  if (!configured[d->dev.G > 0]()) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured[d->dev.G > 0]() = true; }
+  const long long need = (nwb + C::NW - 1) / C::NW;
+  const int grid = (int)(need < dgb_grid_sms() ? need : dgb_grid_sms());
+  DGB_CUDA(cudaMemsetAsync(d->counters + 1, 0, sizeof(unsigned long long), st));
+  kern<<<grid, C::NW * 32, smem, st>>>(d->dev, mq, mt, ml, q, T, ghost, Tghost, ep, ph, ebeg, eend, nwb, d->counters + 1);
+  DGB_CUDA(cudaGetLastError());
+  return DGB_OK;
+}
+
+template <int DIM, int P>
+int launch_div_any(const dgb_disc* d, const double* q, const double* T, const double* ghost, const double* Tghost,
+                   const dgb::Epilogue& ep, const dgb::Phys& ph, long long ebeg, long long eend, cudaStream_t st, int which) {
+  if (which == 7) return launch_div7<DIM, P>(d, q, T, ghost, Tghost, ep, ph, ebeg, eend, st);
+  if (which == 8) {
+    bool ok = false;
+    const int rc = launch_div8<DIM, P>(d, q, T, ghost, Tghost, ep, ph, ebeg, eend, st, &ok);
+    if (rc != DGB_OK || ok) return rc;
+  }
+  return launch_div<DIM, P>(d, q, T, ghost, Tghost, ep, ph, ebeg, eend, st);
+}
+
+// DGB_DIV_KERNEL selects the pass-2 kernel at run time: 8 = TMA-staged k_nsdiv8 (falls back to 3 when the arrays
+// cannot be described to the TMA unit), 3 = k_nsdiv3 (cp.async staging), 7 = role-split k_nsdiv7
 int div_kernel() { return env_int("DGB_DIV_KERNEL", DGB_DIV_KERNEL_DEFAULT); }   // read per launch: tests toggle it
 
 #ifdef DGB_ONLY_3D_P3   // fast kernel-tuning builds (scripts/ab_variants.py)
@@ -242,8 +324,7 @@ static int ns_div_impl(const dgb_disc* d, const double* q, const double* T, cons
   if (d->dev.G > 0 && !Tghost) return dgb_fail(DGB_ERR_INVALID, "ghost elements need the ghost flux planes");
   dgb::Phys ph; make_phys(ph, d->dim + 2, qfar, phys);
 #define X(DIM, P) if (d->dim == DIM && d->order == P)                                                         \
-    return div_kernel() == 7 ? launch_div7<DIM, P>(d, q, T, ghost, Tghost, ep, ph, ebegin, eend, (cudaStream_t)stream) \
-                             : launch_div<DIM, P>(d, q, T, ghost, Tghost, ep, ph, ebegin, eend, (cudaStream_t)stream);
+    return launch_div_any<DIM, P>(d, q, T, ghost, Tghost, ep, ph, ebegin, eend, (cudaStream_t)stream, div_kernel());
   DGB_FOR_EACH_ELEMENT(X)
 #undef X
   return dgb_fail(DGB_ERR_INVALID, "unsupported (dim, order)");

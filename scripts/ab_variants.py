@@ -30,6 +30,28 @@ VARIANTS = {
     "tk2": ["DGB_TICKET_BLOCKS=2"],
     "euler_w8": ["DGB_EULER_WARPS=8"],
     "div_w12_nb1": ["DGB_DIV_WARPS=12", "DGB_DIV_NB=1"],
+    "tma_w8": ["DGB_DIV_KERNEL_DEFAULT=8"],
+    "tma_w10_nb1": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_DIV8_WARPS=10", "DGB_DIV_NB=1"],
+    "tma_w12_nb1": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_DIV8_WARPS=12", "DGB_DIV_NB=1"],
+    "tma_w8_cg": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_GATHER_LD=1"],
+    "tma_w10_nb1_cg": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_DIV8_WARPS=10", "DGB_DIV_NB=1", "DGB_GATHER_LD=1"],
+    "tma_w12_nb1_cg": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_DIV8_WARPS=12", "DGB_DIV_NB=1", "DGB_GATHER_LD=1"],
+    "tma_w8_nc": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_GATHER_LD=2"],
+    "x_local": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_EXP_LOCALGATHER=1"],
+    "x_nomma": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_EXP_NOMMA=1"],
+    "x_noface": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_EXP_NOFACE=1"],
+    "x_noface_nomma": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_EXP_NOFACE=1", "DGB_EXP_NOMMA=1"],
+    "x_local_w12": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_EXP_LOCALGATHER=1", "DGB_DIV8_WARPS=12", "DGB_DIV_NB=1"],
+    "x_noface_w12": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_EXP_NOFACE=1", "DGB_DIV8_WARPS=12", "DGB_DIV_NB=1"],
+    "tma_w12": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_DIV8_WARPS=12"],
+    "tma_w12_lazy": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_DIV8_WARPS=12", "DGB_DIV_LAZY_EX=1"],
+    "tma_w8_nb4_lazy": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_DIV_NB=4", "DGB_DIV_LAZY_EX=1"],
+    "ss_w8": ["DGB_DIV_SINGLE_SMALL=1"],
+    "ss_w9": ["DGB_DIV_SINGLE_SMALL=1", "DGB_DIV_WARPS=9"],
+    "ss_w10": ["DGB_DIV_SINGLE_SMALL=1", "DGB_DIV_WARPS=10"],
+    "ss_w10_nb1": ["DGB_DIV_SINGLE_SMALL=1", "DGB_DIV_WARPS=10", "DGB_DIV_NB=1"],
+    "ss_w12": ["DGB_DIV_SINGLE_SMALL=1", "DGB_DIV_WARPS=12"],
+    "ss_w12_nb1": ["DGB_DIV_SINGLE_SMALL=1", "DGB_DIV_WARPS=12", "DGB_DIV_NB=1"],
 }
 
 
