@@ -427,7 +427,7 @@ def run_b200(args):
             dom = ("k_euler4 (fused Euler RHS)", ms_div, 80.0)
         else:
             names = ("k_rhs3<viscous> (flux + divergence pass)", "k_grad3 (BR1 gradient pass)") if grad_form else \
-                    ("k_nsdiv3 (divergence + face pass)", "k_nsflux3 (BR1 gradient + flux pass)")
+                    ("k_nsdiv8 (divergence + face pass, TMA-staged)", "k_nsflux3 (BR1 gradient + flux pass)")
             dom = (names[0], ms_div, B_ALG_DIV) if ms_div >= ms_grad else (names[1], ms_grad, B_ALG_GRAD)
         achieved = ndof * dom[2] / (dom[1] * 1e-3) / 1e9
         traffic = None
@@ -444,7 +444,7 @@ def run_b200(args):
                 if grad_form:
                     key = "k_rhs3_viscous" if ms_div >= ms_grad else "k_grad3"
                 else:
-                    key = "k_nsdiv3" if ms_div >= ms_grad else "k_nsflux3"
+                    key = "k_nsdiv8" if ms_div >= ms_grad else "k_nsflux3"
                 if key in tj:
                     traffic = tj[key]["dram_read_bytes"] + tj[key]["dram_write_bytes"]
         if traffic is not None:

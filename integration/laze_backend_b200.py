@@ -117,7 +117,7 @@ def run_call_step_b200(function_name, arrays):
         q, Sw, drdx, jac, lift, nrm, fsc, vm, vp, bc, qfar, phys = p
         disc = _handle(q, Sw, drdx, jac, lift, nrm, fsc, vm, vp, bc)
         dq = _Dev(q)
-        T = _Dev(shape=((q.shape[0] - 2) * q.shape[0] + 1,) + q.shape[1:])
+        T = _Dev(shape=((q.shape[0] - 1) * q.shape[0] + 1,) + q.shape[1:])      # (dim+1)*C + 1 planes, C = dim + 2
         qf, ph = np.ascontiguousarray(qfar.reshape(-1)), np.ascontiguousarray(phys.reshape(-1))
         _check(_lib.dgb_ns_flux(disc, dq.ptr, None, T.ptr, qf.ctypes.data, ph.ctypes.data, None))
         return {"out": T.to_host()}

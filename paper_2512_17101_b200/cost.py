@@ -61,11 +61,14 @@ def cost_report(dim: int, order: int, nelements: int, equations: str = "ns", arr
         out.append(KernelCost("k_euler4", f(C) + geo_grad, f(C), f(C), f(C),
                               dmma(dim * npk + kf), N * 230))
     elif arrangement == "flux":
-        npl = dim * C + 1
-        out.append(KernelCost("k_nsflux3", f(C) + geo_grad, f(npl), f(C), f(npl),
-                              dmma(dim * npk + Nf * nfpk), N * (C * (dim * dim + dim) * rows // Np + 235)))
-        out.append(KernelCost("k_nsdiv3", f(C) + f(npl) + geo_div, f(C), f(C) + f(npl), f(C),
-                              dmma(dim * npk + kf), N * 40))
+        npl = (dim + 1) * C + 1                 # dim + 1 plane groups (the last is the sum of the others) + wave speed
+        gmap = E * 4 * Nf * Nfp                 # 32-bit gather map
+        out.append(KernelCost("k_nsflux3", f(C) + geo_grad + gmap, f(npl), f(C), f(npl),
+                              dmma(dim * npk + Nf * nfpk), N * (C * (dim * dim + dim) * rows // Np + 245)))
+        # pass 2 streams q, the dim*C volume planes and the wave speed (TMA boxes) and reaches the sum planes only
+        # through the neighbour gathers: every plane is read from HBM once
+        out.append(KernelCost("k_nsdiv8", f(C) + f(npl) + geo_div + gmap, f(C), f(C) + f(npl), f(C),
+                              dmma(dim * npk + kf), N * 30))
     else:
         out.append(KernelCost("k_grad3", f(C) + geo_grad, f(dim * C), f(C), f(dim * C),
                               dmma(dim * npk + Nf * nfpk), N * 150))

@@ -84,6 +84,12 @@ __global__ void k_build_conn(const long long* __restrict__ vm, const long long* 
   conn[idx] = packed;
 }
 
+// the validated int64 neighbour map of the API narrowed to 32 bits: what the lean face phases gather through
+__global__ void k_build_gidx(const long long* __restrict__ vp, long long n, unsigned* __restrict__ gidx) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) gidx[i] = (unsigned)vp[i];
+}
+
 __global__ void k_expand_conn(const long long* __restrict__ conn, const int* __restrict__ tables,
                               long long E, int Np, int Nf, int Nfp,
                               long long* __restrict__ vm, long long* __restrict__ vp) {
@@ -389,6 +395,12 @@ int dgb_disc_create(dgb_disc** out, int dim, int order, int64_t E, int64_t G, co
   if (ce != cudaSuccess) { dgb_disc_destroy(d); return fail(DGB_ERR_CUDA, cudaGetErrorString(ce)); }
   if (err_host >= 100) { dgb_disc_destroy(d); return fail(DGB_ERR_OUT_OF_BOUNDS, "face index map leaves [0, (E+G)*Np)"); }
   if (err_host) { dgb_disc_destroy(d); return fail(DGB_ERR_BAD_MAP, "face index maps are not a conforming simplex face map"); }
+  if (E > 0 && (E + G) * Np < (1LL << 32)) {
+    const long long n = E * Nf * Nfp;
+    if (cudaMalloc((void**)&d->gidx, sizeof(unsigned) * (size_t)n) != cudaSuccess) { dgb_disc_destroy(d); return fail(DGB_ERR_CUDA, "gather map"); }
+    k_build_gidx<<<(unsigned)((n + 255) / 256), 256, 0, st>>>((const long long*)vmap_p_dev, n, d->gidx);
+    if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) { dgb_disc_destroy(d); return fail(DGB_ERR_CUDA, "gather map kernel"); }
+  }
   if (cudaMalloc((void**)&d->timing, sizeof(long long) * 8 * 4096) != cudaSuccess ||
       cudaMemsetAsync(d->timing, 0, sizeof(long long) * 8 * 4096, st) != cudaSuccess) {
     dgb_disc_destroy(d); return fail(DGB_ERR_CUDA, "timing buffer");
@@ -400,7 +412,7 @@ int dgb_disc_create(dgb_disc** out, int dim, int order, int64_t E, int64_t G, co
   d->dev.E = E; d->dev.G = G;
   d->dev.Wv = d->Wv; d->dev.Wl = d->Wl; d->dev.Wq = d->Wq; d->dev.Wf = d->Wf; d->dev.Wv2 = d->Wv2;
   d->dev.drdx = drdx_dev; d->dev.normals = normals_dev; d->dev.fscale = fscale_dev;
-  d->dev.conn = d->conn; d->dev.tables = d->tables;
+  d->dev.conn = d->conn; d->dev.tables = d->tables; d->dev.gidx = d->gidx;
   d->bc_kind = bc_kind_dev;
   *out = d;
   return DGB_OK;
@@ -409,7 +421,7 @@ int dgb_disc_create(dgb_disc** out, int dim, int order, int64_t E, int64_t G, co
 int dgb_disc_destroy(dgb_disc* d) {
   if (!d) return DGB_OK;
   dgb_disc_free_jacobian(d);
-  cudaFree(d->Wv2); cudaFree(d->Wv); cudaFree(d->Wl); cudaFree(d->Wq); cudaFree(d->Wf); cudaFree(d->conn); cudaFree(d->tables); cudaFree(d->timing); cudaFree(d->counters);
+  cudaFree(d->Wv2); cudaFree(d->Wv); cudaFree(d->Wl); cudaFree(d->Wq); cudaFree(d->Wf); cudaFree(d->conn); cudaFree(d->gidx); cudaFree(d->tables); cudaFree(d->timing); cudaFree(d->counters);
   delete d;
   return DGB_OK;
 }

@@ -27,6 +27,7 @@ struct dgb_disc {
   dgb::DiscDev dev{};
   double *Wv = nullptr, *Wl = nullptr, *Wq = nullptr, *Wf = nullptr, *Wv2 = nullptr;
   long long* conn = nullptr;
+  unsigned* gidx = nullptr;                 // 32-bit gather map (DiscDev::gidx)
   long long* timing = nullptr;
   unsigned long long* counters = nullptr;   // work counters: [0] gradient / flux pass, [1] divergence pass
   int* tables = nullptr;

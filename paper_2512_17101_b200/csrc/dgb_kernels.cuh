@@ -63,6 +63,9 @@ struct DiscDev {
   const double* fscale;  // [E][NF]
   const long long* conn; // [E][NF] packed
   const int* tables;     // face_nodes [NF][NFP] then face_perms [NPERM][NFP]
+  const unsigned* gidx;  // [E][NF*NFP] gather map: node index (nb*NP + jp) of the matching neighbour node in the
+                         // (owned | ghost) node space = the int64 map vmap_p of the API narrowed to 32 bits;
+                         // null when (E+G)*NP does not fit
   // flux arrangement (dgb_kernels_flux.cuh), bound by dgb_disc_set_jacobian
   const double* jac;     // [E] volume Jacobian
   const double* sj;      // [E][NF] face Jacobian = fscale * jac

@@ -7,14 +7,14 @@
 // ONCE, by its owner, at the end of pass 1 while the BR1 gradient is still on chip:
 //
 //   k_nsflux3  (pass 1)  rows -> face averages -> DMMA (Sw_r q, lift_f q*) -> grad q into shared
-//                        memory -> pointwise F = F_inv - F_visc -> T[r][c] = sum_x (J dr/dx)[r][x] F[x][c]
-//                        and lam = |u| + c  ->  HBM  (dim*C + 1 planes instead of dim*C)
-//   k_nsdiv3   (pass 2)  T rows arrive by cp.async straight into the DMMA operand layout (no
+//                        memory -> pointwise F = F_inv - F_visc -> T[r][c] = sum_x (J dr/dx)[r][x] F[x][c],
+//                        their sum over r (plane group dim) and lam = |u| + c  ->  HBM  ((dim+1)*C + 1 planes)
+//   k_nsdiv3/8 (pass 2)  T rows arrive by cp.async / TMA straight into the DMMA operand layout (no
 //                        pointwise volume work at all); per face node the kernel gathers the
-//                        neighbour's q, lam and T rows: sJ F+.n = -(face 0 ? sum_r T+[r] : -T+[nf-1]),
-//                        own side the same signed sum of its own rows -> Rusanov -> DMMA -> 1/J -> store.
+//                        neighbour's q, lam and ONE plane group: sJ F+.n+ = (face 0 ? T+[dim] : -T+[nf-1]),
+//                        own side folded into the volume matrix -> Rusanov -> DMMA -> 1/J -> store.
 //
-// Algorithmic HBM bytes per DOF (3D): pass 1 reads 40, writes 128; pass 2 reads 168, writes 40.
+// HBM bytes per DOF (3D): pass 1 reads 40, writes 168; pass 2 streams 168, gathers q/lam/one group, writes 40.
 #pragma once
 #include "dgb_kernels.cuh"
 #include "dgb_kernels_async.cuh"
@@ -22,12 +22,6 @@
 
 #ifndef DGB_DIV_NB
 #define DGB_DIV_NB 2
-#endif
-#ifndef DGB_DIV_INBLOCK
-#define DGB_DIV_INBLOCK 0
-#endif
-#ifndef DGB_DIV_LAZY_EX
-#define DGB_DIV_LAZY_EX 0
 #endif
 #ifndef DGB_TICKET_BLOCKS
 #define DGB_TICKET_BLOCKS 1
@@ -41,6 +35,10 @@
 // pass 2: one buffer for a block's small inputs (q, lam, face Jacobians, connectivity) instead of two: the next
 // block's are staged as soon as the face phase has read these and land during the contraction + store.
 // 15.6 instead of 18.7 KB of shared memory per warp (3D p3), i.e. room for 12 warps instead of 11.
+// pass 1: neighbour nodes from the 32-bit gather map (1) or decoded from the connectivity word (0)
+#ifndef DGB_FLUX_LEAN
+#define DGB_FLUX_LEAN 0
+#endif
 #ifndef DGB_DIV_SINGLE_SMALL
 #define DGB_DIV_SINGLE_SMALL 0
 #endif
@@ -54,9 +52,6 @@
 #define DGB_WTICK_INIT
 #endif
 
-#ifndef DGB_T_RECORD
-#define DGB_T_RECORD 0
-#endif
 // how the neighbour gathers of pass 2 go through the cache hierarchy: 0 = default (allocate in L1),
 // 1 = ld.global.cg (L2 only: no L1 line per in-flight sector), 2 = ld.global.nc
 #ifndef DGB_GATHER_LD
@@ -72,14 +67,12 @@
 
 namespace dgb {
 
-// Addressing of the flux planes T (pass 1 writes, pass 2 streams and gathers):
-//   plane-major   T[pl][e][j]  (DGB_T_RECORD 0): the (dim*C+1, E, Np) array of the operator program as is;
-//   record-major  T[e][pl][j]  (DGB_T_RECORD 1): all planes of an element in one (dim*C+1)*Np*8-byte
-//                 record, so a face gather (q excepted) and a block's rows touch one DRAM page.
+// The flux planes T are the ((dim+1)*C + 1, E, Np) array of the operator program as it is (plane-major).  A
+// record-major layout (all planes of an element contiguous) was measured in round 1: +3 %, not adopted.
 template <int NPL, int NP>
-__host__ __device__ __forceinline__ long long t_elem_stride() { return DGB_T_RECORD ? (long long)NPL * NP : (long long)NP; }
+__host__ __device__ __forceinline__ long long t_elem_stride() { return (long long)NP; }
 template <int NPL, int NP>
-__host__ __device__ __forceinline__ long long t_plane_stride(long long nelem) { return DGB_T_RECORD ? (long long)NP : nelem * NP; }
+__host__ __device__ __forceinline__ long long t_plane_stride(long long nelem) { return nelem * NP; }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -188,7 +181,9 @@ __device__ __forceinline__ void prefetch_block_rows(const double* __restrict__ a
 template <int DIM, int P>
 struct FluxT {
   using EL = ElemT<DIM, P>;
-  static constexpr int NPL = DIM * EL::C + 1;                    // planes of T: contravariant flux + wave speed
+  static constexpr int NG = DIM + 1;                             // plane groups: T[0..dim-1] and their sum
+  static constexpr int LAMPL = NG * EL::C;                       // plane of the wave speed
+  static constexpr int NPL = NG * EL::C + 1;                     // planes of T
   // q* rows of the gradient pass; a tile's 8 rows are reused for its 8 columns x DIM directions of grad q
   static constexpr int LDSX = ldpad((EL::NF * EL::NFPK > DIM * EL::NP) ? EL::NF * EL::NFPK : DIM * EL::NP);
 };
@@ -204,7 +199,29 @@ struct FluxGeo {
   double fsc[KW][EL::NF];
   long long conn[KW][EL::NF];
   double jac[KW];
+  alignas(16) unsigned gi[DGB_FLUX_LEAN ? KW * EL::NFT : 4];      // the block's slice of the gather map (DiscDev::gidx)
 };
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
+}
+
+// a block's slice of the 32-bit gather map -> shared memory
+template <int DIM, int NFT, int NFP>
+__device__ __forceinline__ void stage_gather_map(unsigned* dst, const unsigned* __restrict__ gidx, long long e0, int nel, int lane) {
+  if (gidx == nullptr) return;
+  if (DIM == 3) {                    // NFT = 4 NFP words per element: 16-byte chunks, always aligned
+    for (int t = lane; t < nel * NFP; t += 32) cp_async16(dst + 4 * t, gidx + e0 * NFT + 4 * t);
+  } else {
+    for (int t = lane; t < nel * NFT; t += 32) cp_async4(dst + t, gidx + e0 * NFT + t);
+  }
+}
+
+template <int NP>
+__host__ __device__ constexpr int grad_row_swizzle(int k) {
+  return (NP % 8 == 4) ? ((k & 4) | ((k & 1) << 1) | ((k >> 1) & 1)) : k;      // NP*8 bytes = 32 (mod 64): p3 tets (Np = 20)
+}
 
 template <int DIM, int P, int KW>
 struct alignas(16) Flux3Warp {
@@ -269,6 +286,7 @@ __device__ __forceinline__ void flux_stage_async(double* Qs, FluxGeo<DIM, P, KW>
     cp_async8(&g.conn[0][lane], d.conn + e0 * NF + lane);
   }
   if (lane < nel) cp_async8(&g.jac[lane], d.jac + e0 + lane);
+  if (DGB_FLUX_LEAN) stage_gather_map<DIM, EL::NFT, EL::NFP>(g.gi, d.gidx, e0, nel, lane);
 }
 
 template <int DIM, int P, int KW, int NWARPS, bool GH>
@@ -315,6 +333,12 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
   // consumed at the top of the block's own iteration.
   double qpE[NR][C];
   long long cnkE[NR];
+#if DGB_FLUX_LEAN
+  const bool lean = d.gidx != nullptr;
+#else
+  constexpr bool lean = false;
+#endif
+  const unsigned enp = (unsigned)(E * NP);
   auto issue_gathers = [&](const FluxGeo<DIM, P, KW>& g, int nelx) {
 #pragma unroll
     for (int k = 0; k < NR; ++k) {
@@ -324,11 +348,20 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
       if (flk >= 0 && e < nelx) {
         const long long cn = g.conn[e][f];
         cnkE[k] = cn;
-        const long long nb = DGB_CONN_NB(cn);
-        const int jp = S.fn[DGB_CONN_NF(cn) * NFP + S.perm[DGB_CONN_PERM(cn) * NFP + m]];
-        const bool in_ghost = GH && nb >= E;
-        const long long pstride = (in_ghost ? G : E) * NP;
-        const double* pbase = (in_ghost ? ghost : q) + (in_ghost ? nb - E : nb) * NP + jp;
+        const double* pbase;
+        long long pstride;
+        if (lean) {                  // neighbour node straight from the gather map
+          const unsigned gi = g.gi[e * NFT + ((flk >> 16) & 255)];
+          const bool in_ghost = GH && gi >= enp;
+          pstride = (in_ghost ? G : E) * NP;
+          pbase = in_ghost ? ghost + (gi - enp) : q + gi;
+        } else {                     // (E+G)*Np beyond 32 bits: decode the connectivity word
+          const long long nb = DGB_CONN_NB(cn);
+          const int jp = S.fn[DGB_CONN_NF(cn) * NFP + S.perm[DGB_CONN_PERM(cn) * NFP + m]];
+          const bool in_ghost = GH && nb >= E;
+          pstride = (in_ghost ? G : E) * NP;
+          pbase = (in_ghost ? ghost : q) + (in_ghost ? nb - E : nb) * NP + jp;
+        }
 #pragma unroll
         for (int c = 0; c < C; ++c) qpE[k][c] = pbase[c * pstride];
       }
@@ -425,6 +458,10 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
       const int k8 = lane >> 2;
       const int col = tile * 8 + k8;
       const int c = col / KW, e = col - c * KW;
+      // rows of grad q are NP doubles apart: for even NP consecutive columns of a quarter warp would overlap in
+      // half their banks (2-way conflicts on every 16-byte store, ncu: 7.5 wavefronts instead of 4); swapping
+      // bits 0 and 1 of the column puts them 2 rows = 64 bytes (mod 128) apart
+      const int k8s = grad_row_swizzle<NP>(k8);
       if (col < WS::NCOL && e < nel) {
         double* sg = W.Ss + tile * 8 * LDSX;
         double m[DIM][DIM];               // m[r][x] = -dr/dx[r][x]
@@ -444,10 +481,10 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
 #pragma unroll
             for (int r = 1; r < DIM; ++r) { v0 += m[r][x] * z0[r]; v1 += m[r][x] * z1[r]; }
             if (NP % 2 == 0) {
-              if (i < NP) *reinterpret_cast<double2*>(sg + (x * 8 + k8) * NP + i) = make_double2(v0, v1);
+              if (i < NP) *reinterpret_cast<double2*>(sg + (x * 8 + k8s) * NP + i) = make_double2(v0, v1);
             } else {
-              if (i < NP) sg[(x * 8 + k8) * NP + i] = v0;
-              if (i + 1 < NP) sg[(x * 8 + k8) * NP + i + 1] = v1;
+              if (i < NP) sg[(x * 8 + k8s) * NP + i] = v0;
+              if (i + 1 < NP) sg[(x * 8 + k8s) * NP + i + 1] = v1;
             }
           }
         }
@@ -473,7 +510,7 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
         for (int c = 0; c < C; ++c) {
           const int col = c * KW + e;
           qq[c] = Qs[col * EL::LDQ + j];
-          const double* sg = W.Ss + (col >> 3) * 8 * LDSX + (col & 7) * NP + j;
+          const double* sg = W.Ss + (col >> 3) * 8 * LDSX + grad_row_swizzle<NP>(col & 7) * NP + j;
 #pragma unroll
           for (int x = 0; x < DIM; ++x) g[x][c] = sg[x * 8 * NP];
         }
@@ -487,9 +524,10 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
 #pragma unroll
           for (int c = 1; c < C; ++c) F[x][c] -= Fv[x][c];
         const double J = geo.jac[e];
-        constexpr int NPLT = DIM * C + 1;
+        constexpr int NPLT = FluxT<DIM, P>::NPL;
         const long long t_ps = t_plane_stride<NPLT, NP>(E);
         double* out = T + (e0 + e) * t_elem_stride<NPLT, NP>() + j;
+        double tsum[C];
 #pragma unroll
         for (int r = 0; r < DIM; ++r) {
           double m[DIM];
@@ -500,18 +538,13 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
             double acc = m[0] * F[0][c];
 #pragma unroll
             for (int x = 1; x < DIM; ++x) acc += m[x] * F[x][c];
-#if DGB_STREAMING_STORES
-            __stcs(out + (r * C + c) * t_ps, acc);
-#else
             out[(r * C + c) * t_ps] = acc;
-#endif
+            tsum[c] = r == 0 ? acc : tsum[c] + acc;      // (T0 + T1) + T2, the order of the operator program
           }
         }
-#if DGB_STREAMING_STORES
-        __stcs(out + (DIM * C) * t_ps, wavespeed<DIM>(s, ph.gamma));
-#else
-        out[(DIM * C) * t_ps] = wavespeed<DIM>(s, ph.gamma);
-#endif
+#pragma unroll
+        for (int c = 0; c < C; ++c) out[(DIM * C + c) * t_ps] = tsum[c];
+        out[FluxT<DIM, P>::LAMPL * t_ps] = wavespeed<DIM>(s, ph.gamma);
       }
     }
     __syncwarp();
@@ -583,7 +616,7 @@ __device__ __forceinline__ void div_stage_small(Div3Small<DIM, P, KW>& M, const 
         if (CH == 2) cp_async16(qs + c * (KW * NP), qg + c * pstride);
         else cp_async8(qs + c * (KW * NP), qg + c * pstride);
       }
-      const double* lg = T + (e0 + e) * t_elem_stride<DIM * C + 1, NP>() + j + (DIM * C) * t_plane_stride<DIM * C + 1, NP>(d.E);
+      const double* lg = T + (e0 + e) * NP + j + FluxT<DIM, P>::LAMPL * pstride;
       if (CH == 2) cp_async16(M.Lam + e * NP + j, lg);
       else cp_async8(M.Lam + e * NP + j, lg);
     }
@@ -600,7 +633,7 @@ __device__ __forceinline__ void div_stage_rows(double* Ts, const DiscDev& d, con
                                                int lane) {
   using EL = ElemT<DIM, P>;
   constexpr int C = EL::C, NP = EL::NP;
-  const long long pstride = t_plane_stride<DIM * C + 1, NP>(d.E);
+  const long long pstride = d.E * NP;
   constexpr int CH = (NP % 2 == 0) ? 2 : 1, NPC = NP / CH;
 #pragma unroll
   for (int t0 = 0; t0 < KW * NPC; t0 += 32) {
@@ -608,7 +641,7 @@ __device__ __forceinline__ void div_stage_rows(double* Ts, const DiscDev& d, con
     const int e = t / NPC, j = CH * (t - e * NPC);
     if (t < KW * NPC && e < nel) {
       double* ts = Ts + e * EL::LDV + j;
-      const double* tg = T + (e0 + e) * t_elem_stride<DIM * C + 1, NP>() + j;
+      const double* tg = T + (e0 + e) * NP + j;
 #pragma unroll 1
       for (int r = 0; r < DIM; ++r) {
 #pragma unroll
@@ -640,13 +673,7 @@ __device__ __noinline__ VecC<DIM> boundary_operand(int bc, int f, VecC<DIM> qm_,
 #pragma unroll
   for (int c = 0; c < C; ++c) {
     qm[c] = qm_.v[c]; qb[c] = qm_.v[c];
-    if (f == 0) {
-      own[c] = Tnode[c * pstride];
-#pragma unroll
-      for (int r = 1; r < DIM; ++r) own[c] += Tnode[(r * C + c) * pstride];
-    } else {
-      own[c] = -Tnode[((f - 1) * C + c) * pstride];
-    }
+    own[c] = f == 0 ? Tnode[(DIM * C + c) * pstride] : -Tnode[((f - 1) * C + c) * pstride];
   }
   bc_state<DIM, true>(bc, qm, nrm, ph, qb);
   Prim<DIM> sb, sm;
@@ -663,35 +690,25 @@ __device__ __noinline__ VecC<DIM> boundary_operand(int bc, int f, VecC<DIM> qm_,
   return out;
 }
 
-// Face phase of pass 2 for one block: gather the neighbour's q, lam and signed T rows of every face
-// node, Rusanov penalty, operand rows  Fs = (nbr - sJ max(lam-, lam+) (q- - q+)) / 2  with
-// nbr = sJ F+.n+ (the own-side half lives in the folded volume matrix Wv2).  NB face nodes per
-// lane have their gathers in flight together; with LAZY the DIM-1 extra rows a neighbour's face 0
-// needs are fetched in a second wave (fewer live registers).
-//
-// INB: a neighbour inside the warp's own block is read from SHARED memory (its q, lam and T rows are
-// staged there anyway) instead of being gathered from L2.  ncu (profiles/r02_pass2_lsu.md): pass 2 is
-// bound by the L1/LSU wavefront queue, and two thirds of its wavefronts are these gathers -- every
-// (face, plane) row costs two 128-byte lines whatever the lane mapping.  With the Kuhn ordering of the
-// box meshes a third of all face sides are in-block.  `Ts_own` = the block's operand rows; the caller's
-// T rows are the cp.async group with TW younger groups behind it (waited for here, after the first
-// batch of global gathers has been issued).
-template <int DIM, int P, int KW, int NB, bool LAZY, int K0 = 0, bool GH = true, bool INB = false, int TW = 1, class SMV>
+// Face phase of pass 2 for one block: gather the neighbour's q, lam and the plane group of T its face selects
+// (group dim = sum of the others for its face 0, minus group nf-1 otherwise), Rusanov penalty, operand rows
+//   Fs = (nbr - sJ max(lam-, lam+) (q- - q+)) / 2,   nbr = sJ F+.n+
+// (the own-side half lives in the folded volume matrix Wv2).  NB face nodes per lane have their gathers in
+// flight together.  `M` gives the block's own q / lam rows, face Jacobians and connectivity.
+template <int DIM, int P, int KW, int NB, bool GH = true, class SMV>
 __device__ __forceinline__ void div_face_phase(const int* flc, const int* fn, const int* perm,
                                                const SMV& M, double* Fs, const DiscDev& d,
                                                const double* __restrict__ q, const double* __restrict__ T,
                                                const double* __restrict__ ghost, const double* __restrict__ Tghost,
-                                               const Phys& ph, long long e0, int nel, int lane,
-                                               const double* Ts_own = nullptr) {
+                                               const Phys& ph, long long e0, int nel, int lane) {
   using EL = ElemT<DIM, P>;
-  constexpr int C = EL::C, NP = EL::NP, NF = EL::NF, NFP = EL::NFP, NFT = EL::NFT;
+  constexpr int C = EL::C, NP = EL::NP, NF = EL::NF, NFP = EL::NFP;
   constexpr int NR = face_rounds<DIM, P, KW>();
-  constexpr int NEX = LAZY ? C : (DIM - 1) * C;
-  constexpr int NPLT = DIM * C + 1;
+  constexpr int LAMPL = FluxT<DIM, P>::LAMPL;
   const long long E = d.E, G = d.G;
 #pragma unroll 1
-  for (int k0 = K0; k0 < NR; k0 += NB) {
-    double qp[NB][C], nbr[NB][C], ex[NB][NEX], lam_p[NB];
+  for (int k0 = 0; k0 < NR; k0 += NB) {
+    double qp[NB][C], nbr[NB][C], lam_p[NB];
     long long cnk[NB];
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
@@ -710,91 +727,18 @@ __device__ __forceinline__ void div_face_phase(const int* flc, const int* fn, co
 #endif
           const int nf = DGB_CONN_NF(cn);
           const int jp = fn[nf * NFP + perm[DGB_CONN_PERM(cn) * NFP + m]];
-          // boundary faces take nothing from the neighbour slot (it names the element itself)
-          const bool skip = INB && (DGB_CONN_BC(cn) != 0 || (nb >= e0 && nb < e0 + nel));
-          if (!skip) {
-            const bool in_ghost = GH && nb >= E;
-            const long long nbl = in_ghost ? nb - E : nb;
-            const long long pstride = (in_ghost ? G : E) * NP;
-            const long long tps = t_plane_stride<NPLT, NP>(in_ghost ? G : E);
-            const double* qbase = (in_ghost ? ghost : q) + nbl * NP + jp;
-            const double* tbase = (in_ghost ? Tghost : T) + nbl * t_elem_stride<NPLT, NP>() + jp;
-            const int r0 = nf == 0 ? 0 : nf - 1;
-#pragma unroll
-            for (int c = 0; c < C; ++c) {
-              qp[b][c] = DGB_GLD(qbase + c * pstride);
-              nbr[b][c] = DGB_GLD(tbase + (r0 * C + c) * tps);
-            }
-            lam_p[b] = DGB_GLD(tbase + (DIM * C) * tps);
-            if (!LAZY && nf == 0) {
-#pragma unroll
-              for (int rc = 0; rc < (DIM - 1) * C; ++rc) ex[b][rc] = DGB_GLD(tbase + (C + rc) * tps);
-            }
-          }
-        }
-      }
-    }
-    if (INB) {
-      if (k0 == K0) { cp_async_wait<TW>(); __syncwarp(); }      // the block's own T rows have landed
-#pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        const int k = k0 + b;
-        if (k < NR && cnk[b] >= 0 && DGB_CONN_BC(cnk[b]) == 0) {
-          const long long nb = DGB_CONN_NB(cnk[b]);
-          if (nb >= e0 && nb < e0 + nel) {
-            const int eb = (int)(nb - e0);
-            const int flk = flc[k * 32 + lane];
-            const int m = (flk >> 4) & 15;
-            const int nf = DGB_CONN_NF(cnk[b]);
-            const int jp = fn[nf * NFP + perm[DGB_CONN_PERM(cnk[b]) * NFP + m]];
-            const int r0 = nf == 0 ? 0 : nf - 1;
-            const double* trow = Ts_own + eb * EL::LDV + jp;
-#pragma unroll
-            for (int c = 0; c < C; ++c) {
-              qp[b][c] = M.qv(c, eb, jp);
-              nbr[b][c] = trow[c * (KW * EL::LDV) + r0 * EL::NPK];
-            }
-            lam_p[b] = M.lamv(eb, jp);
-            if (nf == 0) {
-              if (LAZY) {
-#pragma unroll
-                for (int c = 0; c < C; ++c) {
-                  double t = trow[c * (KW * EL::LDV) + EL::NPK];
-#pragma unroll
-                  for (int r = 2; r < DIM; ++r) t += trow[c * (KW * EL::LDV) + r * EL::NPK];
-                  ex[b][c] = t;
-                }
-              } else {
-#pragma unroll
-                for (int r = 1; r < DIM; ++r)
-#pragma unroll
-                  for (int c = 0; c < C; ++c) ex[b][(r - 1) * C + c] = trow[c * (KW * EL::LDV) + r * EL::NPK];
-              }
-            }
-          }
-        }
-      }
-    }
-    if (LAZY) {
-#pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        const int k = k0 + b;
-        const bool inblk = INB && cnk[b] >= 0 && DGB_CONN_NB(cnk[b]) >= e0 && DGB_CONN_NB(cnk[b]) < e0 + nel;
-        if (k < NR && cnk[b] >= 0 && !inblk && DGB_CONN_NF(cnk[b]) == 0 && DGB_CONN_BC(cnk[b]) == 0) {
-          const int flk = flc[k * 32 + lane];
-          const long long nb = DGB_CONN_NB(cnk[b]);
-          const int m = (flk >> 4) & 15;
-          const int jp = fn[perm[DGB_CONN_PERM(cnk[b]) * NFP + m]];
           const bool in_ghost = GH && nb >= E;
-          const long long tps = t_plane_stride<NPLT, NP>(in_ghost ? G : E);
-          const double* tbase = (in_ghost ? Tghost : T) + (in_ghost ? nb - E : nb) * t_elem_stride<NPLT, NP>() + jp;
+          const long long nbl = in_ghost ? nb - E : nb;
+          const long long pstride = (in_ghost ? G : E) * NP;
+          const double* qbase = (in_ghost ? ghost : q) + nbl * NP + jp;
+          const double* tbase = (in_ghost ? Tghost : T) + nbl * NP + jp;
+          const int grp = nf == 0 ? DIM : nf - 1;
 #pragma unroll
           for (int c = 0; c < C; ++c) {
-            double t = DGB_GLD(tbase + (C + c) * tps);
-#pragma unroll
-            for (int r = 2; r < DIM; ++r) t += DGB_GLD(tbase + (r * C + c) * tps);
-            ex[b][c] = t;
+            qp[b][c] = DGB_GLD(qbase + c * pstride);
+            nbr[b][c] = DGB_GLD(tbase + (grp * C + c) * pstride);
           }
+          lam_p[b] = DGB_GLD(tbase + LAMPL * pstride);
         }
       }
     }
@@ -812,29 +756,15 @@ __device__ __forceinline__ void div_face_phase(const int* flc, const int* fn, co
         for (int c = 0; c < C; ++c) qm[c] = M.qv(c, e, jm);
         double* fs = Fs + e * EL::LDF + fm;
         if (bc == 0) {
-          if (nf == 0) {
+          const double hs = nf == 0 ? 0.5 : -0.5;
+          const double pen = 0.5 * (sj * fmax(lam_m, lam_p[b]));
 #pragma unroll
-            for (int c = 0; c < C; ++c) {
-              if (LAZY) {
-                nbr[b][c] += ex[b][c];
-              } else {
-#pragma unroll
-                for (int r = 1; r < DIM; ++r) nbr[b][c] += ex[b][(r - 1) * C + c];
-              }
-            }
-          } else {
-#pragma unroll
-            for (int c = 0; c < C; ++c) nbr[b][c] = -nbr[b][c];
-          }
-          const double pen = sj * fmax(lam_m, lam_p[b]);
-#pragma unroll
-          for (int c = 0; c < C; ++c) fs[c * (KW * EL::LDF)] = 0.5 * (nbr[b][c] - pen * (qm[c] - qp[b][c]));
+          for (int c = 0; c < C; ++c) fs[c * (KW * EL::LDF)] = hs * nbr[b][c] - pen * (qm[c] - qp[b][c]);
         } else {
           VecC<DIM> a_;
 #pragma unroll
           for (int c = 0; c < C; ++c) a_.v[c] = qm[c];
-          const VecC<DIM> fb = boundary_operand<DIM>(bc, f, a_, T + (e0 + e) * t_elem_stride<NPLT, NP>() + jm,
-                                                     t_plane_stride<NPLT, NP>(E), lam_m, sj,
+          const VecC<DIM> fb = boundary_operand<DIM>(bc, f, a_, T + (e0 + e) * NP + jm, E * NP, lam_m, sj,
                                                      d.normals + (e0 + e) * NF + f, E * NF, ph);
 #pragma unroll
           for (int c = 0; c < C; ++c) fs[c * (KW * EL::LDF)] = fb.v[c];
@@ -893,7 +823,6 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
 
   // cp.async groups retire in order: S(b), T(b), S(b+1), T(b+1), ...
   constexpr bool SS = DGB_DIV_SINGLE_SMALL != 0;
-  static_assert(!(SS && DGB_DIV_INBLOCK), "in-block neighbours need the double-buffered small inputs");
   DGB_WTICK_INIT
   while (wb < nwblocks) {
     const long long e0 = ebeg + wb * KW;
@@ -905,11 +834,11 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
       if (nel1 > 0) div_stage_small<DIM, P, KW>(W.sm[buf ^ 1], d, q, T, e1, nel1, lane);
       cp_async_commit();                 // S(b+1)
     }
-    if (DGB_L2_PREFETCH_BLOCKS > 0 && !DGB_T_RECORD) {
+    if (DGB_L2_PREFETCH_BLOCKS > 0) {
       const long long wbp = wb_next + DGB_L2_PREFETCH_BLOCKS;
       if (wbp < nwblocks) {
         const long long ep = ebeg + wbp * KW;
-        prefetch_block_rows<NP, KW>(q, C, E * NP, T, DIM * C + 1, E * NP, ep,
+        prefetch_block_rows<NP, KW>(q, C, E * NP, T, DIM * C, E * NP, ep,
                                     (int)((eend - ep) < (long long)KW ? (eend - ep) : (long long)KW), lane);
       }
     }
@@ -924,7 +853,7 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
     //      constant coefficients and lives in the folded volume matrix, so this phase needs only
     //      q, lam and the connectivity of the block -- not its T rows, which are still landing.
     //      Fs = (nbr - sJ max(lam-, lam+) (q- - q+)) / 2,  nbr = sJ F+.n+ gathered from the neighbour.
-    div_face_phase<DIM, P, KW, NB, (DGB_DIV_LAZY_EX != 0), 0, GH, (DGB_DIV_INBLOCK != 0), 1>(S.flc, S.fn, S.perm, M, W.Fs, d, q, T, ghost, Tghost, ph, e0, nel, lane, W.Ts);
+    div_face_phase<DIM, P, KW, NB, GH>(S.flc, S.fn, S.perm, M, W.Fs, d, q, T, ghost, Tghost, ph, e0, nel, lane);
     DGB_WTICK(1);
     double rj[WS::NTILE];
 #pragma unroll

@@ -17,6 +17,10 @@
 #pragma once
 #include "dgb_kernels_flux.cuh"
 
+#ifndef DGB_DIV8_NB
+#define DGB_DIV8_NB 0              // 0: every round of a block in flight together (8 warps) / one round (more warps)
+#endif
+
 #include <cuda.h>
 
 namespace dgb {
@@ -83,14 +87,111 @@ struct TmaBox {
   static constexpr int NPL_T = DIM * EL::C;                  // flux planes in the T box (the wave speed travels apart)
 };
 
-// small per-block geometry, double-buffered, by 8-byte cp.async as before (a few instructions)
+// small per-block inputs, double-buffered, by cp.async as before (a few instructions): face Jacobians,
+// connectivity words, 1/J and the block's slice of the gather map (DiscDev::gidx)
 template <int DIM, int P, int KW>
-struct Div8Geo {
+struct alignas(16) Div8Geo {
   using EL = ElemT<DIM, P>;
+  alignas(16) unsigned gi[KW * EL::NFT];
   double sj[KW][EL::NF];
   long long conn[KW][EL::NF];
   double rj[KW];
 };
+
+// Everything a lane needs to know about its face node of round k, packed once per kernel from the
+// face-lane code (face_lane_code): bits 0-7 e*NFT + fm (gather-map slot), 8-11 e*NF + f (face slot),
+// 12-19 e*NP + jm (own volume node in the box rows), 20-27 e*LDF + fm (operand entry), 28-29 e; < 0: idle lane.
+template <int DIM, int P, int KW>
+__device__ __forceinline__ int lean_round_word(int flk) {
+  using EL = ElemT<DIM, P>;
+  if (flk < 0) return -1;
+  const int e = flk & 3, f = (flk >> 2) & 3, jm = (flk >> 8) & 255, fm = (flk >> 16) & 255;
+  static_assert(KW * EL::NFT <= 256 && KW * EL::NP <= 256 && KW * EL::LDF <= 256 && KW * EL::NF <= 16, "packing");
+  return (e * EL::NFT + fm) | ((e * EL::NF + f) << 8) | ((e * EL::NP + jm) << 12) | ((e * EL::LDF + fm) << 20) | (e << 28);
+}
+
+// Lean face phase (pass 2): the neighbour's node comes from the precomputed gather map instead of being decoded
+// from the connectivity word through the face-node / permutation tables, every lane carries its per-round
+// constants in one register, and a face selects ONE plane group of T.  Same arithmetic as div_face_phase.
+template <int DIM, int P, int KW, int NB, bool GH>
+__device__ __forceinline__ void div_face_lean(const int (&rw)[face_rounds<DIM, P, KW>()], const Div8Geo<DIM, P, KW>& g,
+                                              const double* __restrict__ Qb, const double* __restrict__ Lam,
+                                              double* __restrict__ Fs, const DiscDev& d,
+                                              const double* __restrict__ q, const double* __restrict__ T,
+                                              const double* __restrict__ ghost, const double* __restrict__ Tghost,
+                                              const Phys& ph, long long e0, int nel) {
+  using EL = ElemT<DIM, P>;
+  constexpr int C = EL::C, NP = EL::NP, NF = EL::NF;
+  constexpr int NR = face_rounds<DIM, P, KW>();
+  constexpr int BOXW = TmaBox<DIM, P, KW>::BOXW;
+  constexpr int LAMPL = FluxT<DIM, P>::LAMPL;
+  const long long ps_own = d.E * NP;
+  const unsigned enp = (unsigned)ps_own;
+  const long long* connf = &g.conn[0][0];
+  const double* sjf = &g.sj[0][0];
+#pragma unroll
+  for (int k0 = 0; k0 < NR; k0 += NB) {          // unrolled: rw[] stays in registers
+    double qp[NB][C], nbr[NB][C], lam_p[NB];
+    int hi[NB];                      // upper half of the connectivity word (neighbour face, bc kind); < 0: nothing to do
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      hi[b] = -1;
+      if (k0 + b < NR) {
+        const int w = rw[k0 + b];
+        if (w >= 0 && ((w >> 28) & 3) < nel) {
+#ifdef DGB_EXP_LOCALGATHER
+          const unsigned gi = (unsigned)(e0 * NP) + ((w >> 12) & 255);      // timing experiment: own node
+#else
+          const unsigned gi = g.gi[w & 255];
+#endif
+          hi[b] = (int)(connf[(w >> 8) & 15] >> 32);
+          const int nf = hi[b] & 7;
+          const int grp = nf == 0 ? DIM : nf - 1;
+          const bool in_ghost = GH && gi >= enp;
+          const long long ps = in_ghost ? d.G * NP : ps_own;
+          const double* qb = in_ghost ? ghost + (gi - enp) : q + gi;
+          const double* tb = in_ghost ? Tghost + (gi - enp) : T + gi;
+          const double* tg = tb + (long long)(grp * C) * ps;
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            qp[b][c] = DGB_GLD(qb + c * ps);
+            nbr[b][c] = DGB_GLD(tg + c * ps);
+          }
+          lam_p[b] = DGB_GLD(tb + LAMPL * ps);
+        }
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      if (k0 + b < NR && hi[b] >= 0) {
+        const int w = rw[k0 + b];
+        const int cofs = (w >> 8) & 15, qofs = (w >> 12) & 255, fofs = (w >> 20) & 255;
+        const int nf = hi[b] & 7, bc = (hi[b] >> 6) & 3;
+        const double sj = sjf[cofs];
+        const double lam_m = Lam[qofs];
+        double qm[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) qm[c] = Qb[c * BOXW + qofs];
+        double* fs = Fs + fofs;
+        if (bc == 0) {
+          const double hs = nf == 0 ? 0.5 : -0.5;
+          const double pen = 0.5 * (sj * fmax(lam_m, lam_p[b]));
+#pragma unroll
+          for (int c = 0; c < C; ++c) fs[c * (KW * EL::LDF)] = hs * nbr[b][c] - pen * (qm[c] - qp[b][c]);
+        } else {
+          const int e = (w >> 28) & 3, f = cofs - e * NF, jm = qofs - e * NP;
+          VecC<DIM> a_;
+#pragma unroll
+          for (int c = 0; c < C; ++c) a_.v[c] = qm[c];
+          const VecC<DIM> fb = boundary_operand<DIM>(bc, f, a_, T + (e0 + e) * NP + jm, ps_own, lam_m, sj,
+                                                     d.normals + (e0 + e) * NF + f, d.E * NF, ph);
+#pragma unroll
+          for (int c = 0; c < C; ++c) fs[c * (KW * EL::LDF)] = fb.v[c];
+        }
+      }
+    }
+  }
+}
 
 template <int DIM, int P, int KW>
 struct alignas(128) Div8Warp {
@@ -117,17 +218,6 @@ struct Div8Smem {
   int flc[face_rounds<DIM, P, KW>() * 32];
 };
 
-// what div_face_phase reads of a block (k_nsdiv3 passes its Div3Small)
-template <int DIM, int P, int KW>
-struct Div8View {
-  using EL = ElemT<DIM, P>;
-  const double* Qs; const double* Lam;      // already advanced by the block's box shift
-  const double (*sj)[EL::NF];
-  const long long (*conn)[EL::NF];
-  __device__ __forceinline__ double qv(int c, int e, int j) const { return Qs[c * TmaBox<DIM, P, KW>::BOXW + e * EL::NP + j]; }
-  __device__ __forceinline__ double lamv(int e, int j) const { return Lam[e * EL::NP + j]; }
-};
-
 template <int DIM, int P, int KW, int NWARPS, bool GH>
 __global__ void __launch_bounds__(NWARPS * 32, 1)
 k_nsdiv8(DiscDev d, const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_t,
@@ -141,8 +231,9 @@ k_nsdiv8(DiscDev d, const __grid_constant__ CUtensorMap map_q, const __grid_cons
   constexpr int C = EL::C, NP = EL::NP, NF = EL::NF, NFP = EL::NFP;
   constexpr int NT = NWARPS * 32;
   constexpr int NR = face_rounds<DIM, P, KW>();
-  // face nodes per lane with their gathers in flight together: 2 needs ~230 registers (8 warps), 1 fits 168 (9-12 warps)
-  constexpr int NB = NWARPS > 8 ? 1 : DGB_DIV_NB;
+  // face nodes per lane with their gathers in flight together: all NR rounds of a block at 8 warps (11 values per
+  // node: 88 registers for 3D p3), one round at 9-12 warps (168 registers)
+  constexpr int NB = DGB_DIV8_NB > 0 ? DGB_DIV8_NB : (NWARPS > 8 ? 1 : NR);
   constexpr int BOXW = BX::BOXW;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   auto& S = *reinterpret_cast<Div8Smem<DIM, P, KW, NWARPS>*>(smem_raw);
@@ -183,6 +274,10 @@ k_nsdiv8(DiscDev d, const __grid_constant__ CUtensorMap map_q, const __grid_cons
     foff[mt] = col * EL::LDF;
   }
 
+  int rw[NR];                        // per-round constants of this lane (div_face_lean)
+#pragma unroll
+  for (int k = 0; k < NR; ++k) rw[k] = lean_round_word<DIM, P, KW>(S.flc[k * 32 + lane]);
+
   auto nel_of = [&](long long wbx) -> int {
     if (wbx >= nwblocks) return 0;
     const long long e = ebeg + wbx * KW;
@@ -204,6 +299,7 @@ k_nsdiv8(DiscDev d, const __grid_constant__ CUtensorMap map_q, const __grid_cons
       cp_async8(&g.conn[0][lane], d.conn + e0 * NF + lane);
     }
     if (lane < nelx) cp_async8(&g.rj[lane], d.rj + e0 + lane);
+    stage_gather_map<DIM, EL::NFT, EL::NFP>(g.gi, d.gidx, e0, nelx, lane);
   };
 
   const long long wstride = (long long)gridDim.x * NWARPS;
@@ -231,11 +327,8 @@ k_nsdiv8(DiscDev d, const __grid_constant__ CUtensorMap map_q, const __grid_cons
     mbar_wait_(&W.bar_q, par);           // state + wave speed of this block
     __syncwarp();
     const int sh = BX::box_shift(e0);
-    Div8View<DIM, P, KW> M{W.Qb + sh, W.Lam + sh, W.geo[buf].sj, W.geo[buf].conn};
-
 #ifndef DGB_EXP_NOFACE            // timing experiments only (results invalid)
-    div_face_phase<DIM, P, KW, NB, (DGB_DIV_LAZY_EX != 0), 0, GH, false, 1>(S.flc, S.fn, S.perm, M, W.Fs, d, q, T, ghost,
-                                                                            Tghost, ph, e0, nel, lane, nullptr);
+    div_face_lean<DIM, P, KW, NB, GH>(rw, W.geo[buf], W.Qb + sh, W.Lam + sh, W.Fs, d, q, T, ghost, Tghost, ph, e0, nel);
 #endif
     double rj[WS::NTILE];
 #pragma unroll

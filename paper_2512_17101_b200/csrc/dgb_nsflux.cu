@@ -2,7 +2,6 @@
 // launch configuration.  Kernels: dgb_kernels_flux.cuh.
 #include "dgb_internal.h"
 #include "dgb_kernels_flux.cuh"
-#include "dgb_kernels_div7.cuh"
 #include "dgb_kernels_tma.cuh"
 
 #include <cstdlib>
@@ -77,48 +76,10 @@ int launch_div(const dgb_disc* d, const double* q, const double* T, const double
 }
 
 
-// ---- role-split pass 2 (k_nsdiv7, dgb_kernels_div7.cuh): 4 consumer warps + NPROD producer warps ----
-#ifndef DGB_DIV7_PRODUCERS
-#define DGB_DIV7_PRODUCERS 8
-#endif
-#ifndef DGB_DIV7_NB
-#define DGB_DIV7_NB 1
-#endif
-#ifndef DGB_DIV7_WREGS
-#define DGB_DIV7_WREGS 76          // doubles of W fragments a consumer lane may keep in registers
-#endif
-template <int DIM, int P> struct Cfg7 {
-  using EL = dgb::ElemT<DIM, P>;
-  static constexpr int KW = DIM == 3 ? 3 : 4;
-  static constexpr int per_tile = EL::KV / 4 + EL::KF / 4;
-  static constexpr int NIR = DGB_DIV7_WREGS / per_tile < EL::NI ? DGB_DIV7_WREGS / per_tile : EL::NI;
-  static constexpr size_t per = sizeof(dgb::Div7Prod<DIM, P, KW>);
-  static constexpr size_t fixed = sizeof(dgb::Div7Smem<DIM, P, KW, 1, NIR>) - per;
-  static constexpr int NPROD = fit_warps(fixed, per, DGB_DIV7_PRODUCERS);
-};
-
-template <int DIM, int P>
-int launch_div7(const dgb_disc* d, const double* q, const double* T, const double* ghost, const double* Tghost,
-                const dgb::Epilogue& ep, const dgb::Phys& ph, long long ebeg, long long eend, cudaStream_t st) {
-  using C = Cfg7<DIM, P>;
-  auto kern = d->dev.G > 0 ? dgb::k_nsdiv7<DIM, P, C::KW, C::NPROD, C::NIR, DGB_DIV7_NB, true>
-                           : dgb::k_nsdiv7<DIM, P, C::KW, C::NPROD, C::NIR, DGB_DIV7_NB, false>;
-  const size_t smem = sizeof(dgb::Div7Smem<DIM, P, C::KW, C::NPROD, C::NIR>);
-  const long long nwb = (eend - ebeg + C::KW - 1) / C::KW;
-  if (nwb == 0) return DGB_OK;
-  static DgbPerDevice configured[2];
-  if (!configured[d->dev.G > 0]()) { DGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); configured[d->dev.G > 0]() = true; }
-  const long long need = (nwb + C::NPROD - 1) / C::NPROD;
-  const int grid = (int)(need < dgb_grid_sms() ? need : dgb_grid_sms());
-  DGB_CUDA(cudaMemsetAsync(d->counters + 1, 0, sizeof(unsigned long long), st));
-  kern<<<grid, 128 + 128 * ((C::NPROD + 3) / 4), smem, st>>>(d->dev, q, T, ghost, Tghost, ep, ph, ebeg, eend, nwb, d->counters + 1);
-  DGB_CUDA(cudaGetLastError());
-  return DGB_OK;
-}
-
 // ---- TMA-staged pass 2 (k_nsdiv8, dgb_kernels_tma.cuh) ----------------------------------------------------
 #ifndef DGB_DIV8_WARPS
-#define DGB_DIV8_WARPS 10         // measured (3D p3, n=94): 8 warps NB 2 7.71 ms, 10 warps NB 1 7.56 ms, 12 warps NB 1 8.15 ms
+#define DGB_DIV8_WARPS 8          // measured (3D p3, n=94, profiles/r02_pass2_tma.md): 8 warps with all 4 rounds in flight 6.69 ms,
+                                  // 8 warps NB 2 7.86 ms, 10 warps NB 1 8.34 ms, 12 warps NB 1 8.56 ms
 #endif
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -164,11 +125,11 @@ int launch_div8(const dgb_disc* d, const double* q, const double* T, const doubl
   using BX = dgb::TmaBox<DIM, P, C::KW>;
   *ok = false;
   const long long E = d->dev.E, width = E * EL::NP;
-  if (width >= (1LL << 31)) return DGB_OK;
+  if (width >= (1LL << 31) || !d->dev.gidx) return DGB_OK;
   CUtensorMap mq, mt, ml;
   if (!make_plane_map(&mq, q, width, EL::C, width, BX::BOXW, EL::C)) return DGB_OK;
   if (!make_plane_map(&mt, T, width, BX::NPL_T, width, BX::BOXW, BX::NPL_T)) return DGB_OK;
-  if (!make_plane_map(&ml, T + (long long)BX::NPL_T * width, width, 1, width, BX::BOXW, 1)) return DGB_OK;
+  if (!make_plane_map(&ml, T + (long long)dgb::FluxT<DIM, P>::LAMPL * width, width, 1, width, BX::BOXW, 1)) return DGB_OK;
   *ok = true;
   auto kern = d->dev.G > 0 ? dgb::k_nsdiv8<DIM, P, C::KW, C::NW, true> : dgb::k_nsdiv8<DIM, P, C::KW, C::NW, false>;
   const size_t smem = sizeof(dgb::Div8Smem<DIM, P, C::KW, C::NW>);
@@ -187,7 +148,6 @@ int launch_div8(const dgb_disc* d, const double* q, const double* T, const doubl
 template <int DIM, int P>
 int launch_div_any(const dgb_disc* d, const double* q, const double* T, const double* ghost, const double* Tghost,
                    const dgb::Epilogue& ep, const dgb::Phys& ph, long long ebeg, long long eend, cudaStream_t st, int which) {
-  if (which == 7) return launch_div7<DIM, P>(d, q, T, ghost, Tghost, ep, ph, ebeg, eend, st);
   if (which == 8) {
     bool ok = false;
     const int rc = launch_div8<DIM, P>(d, q, T, ghost, Tghost, ep, ph, ebeg, eend, st, &ok);
@@ -197,7 +157,8 @@ int launch_div_any(const dgb_disc* d, const double* q, const double* T, const do
 }
 
 // DGB_DIV_KERNEL selects the pass-2 kernel at run time: 8 = TMA-staged k_nsdiv8 (falls back to 3 when the arrays
-// cannot be described to the TMA unit), 3 = k_nsdiv3 (cp.async staging), 7 = role-split k_nsdiv7
+// cannot be described to the TMA unit), 3 = k_nsdiv3 (cp.async staging).  The role-split k_nsdiv7 of round 2
+// (measured slower, profiles/r02_pass2_experiments.md) was retired with the sum planes.
 int div_kernel() { return env_int("DGB_DIV_KERNEL", DGB_DIV_KERNEL_DEFAULT); }   // read per launch: tests toggle it
 
 #ifdef DGB_ONLY_3D_P3   // fast kernel-tuning builds (scripts/ab_variants.py)

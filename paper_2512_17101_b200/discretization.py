@@ -59,9 +59,15 @@ class DGDiscretization:
             fm[r, r + 1] = -1.0
         lhs = geo.fscale[None] * geo.normals                        # (x, E, Nf)
         assert np.allclose(lhs, np.einsum("rf,rxe->xef", fm, geo.drdx), rtol=1e-12, atol=1e-12)
+        # The flux arrangement stores that sum as a plane group of its own (operators.py: dg_ns_flux), so a face
+        # selects exactly ONE of dim + 1 groups: face 0 -> +group dim, face f >= 1 -> -group f-1.
+        fm = np.zeros((self.dim + 1, Nf))
+        fm[self.dim, 0] = 1.0
+        for r in range(self.dim):
+            fm[r, r + 1] = -1.0
         self.facemat_host = fm
-        self.facemat = f(fm.reshape(self.dim, Nf, 1))               # (d, Nf, 1), broadcasts over elements
-        self.facemat_p = f(np.ascontiguousarray(fm[:, mesh.nbr_face]).reshape(self.dim, E, Nf, 1))
+        self.facemat = f(fm.reshape(self.dim + 1, Nf, 1))           # (d+1, Nf, 1), broadcasts over elements
+        self.facemat_p = f(np.ascontiguousarray(fm[:, mesh.nbr_face]).reshape(self.dim + 1, E, Nf, 1))
         self.vmap_m = f(vmap_m.reshape(-1))                         # (E*Nf*Nfp,) int64
         self.vmap_p = f(vmap_p.reshape(-1))
         self.bc_kind = f(bc_kind.reshape(E, Nf, 1))                 # (E, Nf, 1) int64

@@ -214,6 +214,11 @@ def dg_ns_rhs_rk(actx, f, q, gq, x1, x2, coef, Sw, drdx, lift, normals, fscale, 
     return {"out1": o1, "out2": o2}
 
 
+def flux_planes(dim: int) -> int:
+    """Planes of the array ``dg_ns_flux`` returns: dim + 1 groups of C = dim + 2 flux planes and the wave speed."""
+    return (dim + 1) * (dim + 2) + 1
+
+
 def _bind_jacobian(actx, disc, jac, facemat=None):
     """Bind the volume Jacobian argument to the handle (once) -- dgb_disc_set_jacobian."""
     if getattr(disc, "jac_id", None) == id(jac):
@@ -233,14 +238,14 @@ def _check_facemat(disc, facemat, facemat_p):
     if getattr(disc, "facemat_ok", None) == (id(facemat), id(facemat_p)):
         return
     dim, Nf = disc.dim, disc.Nf
-    want = np.zeros((dim, Nf))
-    want[:, 0] = 1.0
+    want = np.zeros((dim + 1, Nf))
+    want[dim, 0] = 1.0
     for r in range(dim):
         want[r, r + 1] = -1.0
-    got = np.asarray(facemat.host_value(), dtype=np.float64).reshape(dim, Nf)
+    got = np.asarray(facemat.host_value(), dtype=np.float64).reshape(dim + 1, Nf)
     if not np.array_equal(got, want):
-        raise errors.BindingMismatch("facemat is not the simplex face/gradient incidence matrix")
-    if tuple(facemat_p.shape) != (dim, disc.E, Nf, 1):
+        raise errors.BindingMismatch("facemat is not the simplex face/plane-group selection matrix")
+    if tuple(facemat_p.shape) != (dim + 1, disc.E, Nf, 1):
         raise errors.BindingMismatch(f"facemat_p has shape {tuple(facemat_p.shape)}")
     disc.facemat_ok = (id(facemat), id(facemat_p))
 
@@ -259,7 +264,7 @@ def dg_ns_flux(actx, f, *args):
     disc = get_disc(actx, dim, q, G, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind)
     _bind_jacobian(actx, disc, jac)
     qf, ph = _host_vec(qfar, dim + 2), _host_vec(phys, 4)
-    out = actx.empty((dim * (dim + 2) + 1,) + tuple(q.shape[1:]))
+    out = actx.empty((flux_planes(dim),) + tuple(q.shape[1:]))
     _cabi.check(actx.lib.dgb_ns_flux(disc.handle, q.ptr, gptr, out.ptr, qf.ctypes.data, ph.ctypes.data, actx._st),
                 "dg_ns_flux")
     actx.launch_count += 1
@@ -271,7 +276,7 @@ def _div_common(actx, f, q, T, ghost, Tghost, Sw, jac, lift, normals, fscale, fa
     dim = f.dg_dim
     q = _f64(actx, q, "q")
     T = _f64(actx, T, "T")
-    npl = dim * (dim + 2) + 1
+    npl = flux_planes(dim)
     if tuple(T.shape) != (npl,) + tuple(q.shape[1:]):
         raise errors.BindingMismatch(f"flux planes have shape {tuple(T.shape)}, expected {(npl,) + tuple(q.shape[1:])}")
     G, g, gptr = _ghost_ptr(actx, ghost, (dim + 2,), q.shape[-1])
@@ -350,7 +355,7 @@ def ns_flux_range(actx, op, q, ghost, T, lo, hi):
 def ns_div_range(actx, op, q, T, ghost, Tghost, out, lo, hi):
     """``out[:, lo:hi] = dg_ns_div(q, T)[:, lo:hi]`` (dgb_ns_div_range)."""
     q = _f64(actx, q, "q")
-    npl = op.dim * (op.dim + 2) + 1
+    npl = flux_planes(op.dim)
     G, g, gptr = _ghost_ptr(actx, ghost, (op.dim + 2,), q.shape[-1])
     TG, tg, tgptr = _ghost_ptr(actx, Tghost, (npl,), q.shape[-1])
     disc = _op_disc(actx, op, q, G)

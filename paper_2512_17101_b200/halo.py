@@ -383,7 +383,7 @@ class HaloExchange:
         actx, nI, E = self.actx, self.plan.n_interior, self.plan.nlocal
         dim = op.dim
         t1 = self._begin(q.data)                                            # batch 1 in flight ...
-        T = actx.empty((dim * (dim + 2) + 1,) + tuple(q.data.shape[1:]))
+        T = actx.empty((fused.flux_planes(dim),) + tuple(q.data.shape[1:]))
         self._reserve(True)
         fused.ns_flux_range(actx, op, q.data, self._ghost_of(t1), T, 0, nI)  # ... under pass 1 of the interior
         self._reserve(False)

@@ -33,8 +33,8 @@ The Navier-Stokes right-hand side exists in two algebraically identical arrangem
 scheme.  ``rhs_grad_form`` = ``dg_ns_grad`` (pass 1 writes ``grad q``) + ``dg_ns_rhs`` (pass 2
 evaluates every flux).  ``rhs`` (default) = ``dg_ns_flux`` + ``dg_ns_div``: pass 1 finishes the BR1
 gradient in registers, evaluates the total flux ``F = F_inv - F_visc`` once per node and stores its
-contravariant, Jacobian-scaled components ``T[r] = sum_x (J dr/dx)[r,x] F[x]`` plus the local wave
-speed; pass 2 is then a pure contraction: the volume term contracts ``T`` directly, and the
+contravariant, Jacobian-scaled components ``T[r] = sum_x (J dr/dx)[r,x] F[x]``, their sum over ``r`` and the
+local wave speed; pass 2 is then a pure contraction: the volume term contracts ``T`` directly, and the
 scaled normal flux of either side of a face is a signed sum of ``T`` rows (``facemat``), so the
 neighbour's flux is *gathered*, not recomputed.  Each face flux is evaluated once per node
 instead of three times (own volume, own face, neighbour's face), which is what makes the B200
@@ -300,8 +300,10 @@ def _make_ns_rhs(dim, with_ghost):
 
 def _make_ns_flux(dim, with_ghost):
     """Pass 1 of the flux arrangement: BR1 gradient -> total flux -> contravariant components.
-    Returns ``(dim*C + 1, E, Np)``: planes ``r*C + c`` hold ``T[r][c] = sum_x jac*drdx[r,x] *
-    (F_inv - F_visc)[x][c]`` and the last plane the wave speed ``|u| + c``."""
+    Returns ``((dim+1)*C + 1, E, Np)``: planes ``r*C + c`` (``r < dim``) hold ``T[r][c] = sum_x jac*drdx[r,x] *
+    (F_inv - F_visc)[x][c]``, planes ``dim*C + c`` their sum over ``r`` (the scaled normal flux of face 0, stored so
+    that a neighbour gathers ONE plane per field whatever face it sees) and the last plane the wave speed
+    ``|u| + c``."""
     grad = _make_ns_grad(dim, with_ghost)
 
     def body(actx, q, ghost, Sw, drdx, jac, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, phys):
@@ -321,8 +323,11 @@ def _make_ns_flux(dim, with_ghost):
                 for x in range(dim)]
         fstack = actx.np.stack([actx.np.stack(fx) for fx in ftot])            # (d, C, E, Np)
         T = actx.np.einsum("rxe,e,xcej->rcej", drdx, jac, fstack)
+        tsum = T[0] + T[1]
+        for r in range(2, dim):
+            tsum = tsum + T[r]
         lam = _wavespeed(actx, gamma, qc, vel, p, dim)
-        return actx.np.concatenate([actx.np.reshape(T, (dim * C, E, Np)), actx.np.reshape(lam, (1, E, Np))])
+        return actx.np.concatenate([actx.np.reshape(T, (dim * C, E, Np)), tsum, actx.np.reshape(lam, (1, E, Np))])
 
     if with_ghost:
         def dg_ns_flux(q, ghost, Sw, drdx, jac, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, phys):
@@ -337,14 +342,15 @@ def _make_ns_flux(dim, with_ghost):
 
 def _make_ns_div(dim, with_ghost):
     """Pass 2 of the flux arrangement: ``rhs = (1/J) (sum_r Sw_r T_r - lift(sJ F*.n))`` with
-    ``sJ F-.n = sum_r facemat[f,r] T-[r]`` and ``sJ F+.n = -sum_r facemat[f+,r] T+[r]``
-    (``facemat_p`` is ``facemat`` of the neighbour's face, per face)."""
+    ``sJ F-.n = sum_g facemat[g,f] T-[g]`` and ``sJ F+.n = -sum_g facemat[g,f+] T+[g]`` over the ``dim + 1`` plane
+    groups of ``dg_ns_flux`` (``T[dim]`` = sum of the others: face 0 selects it, face ``f >= 1`` selects ``-T[f-1]``;
+    ``facemat_p`` is ``facemat`` of the neighbour's face, per face)."""
     def body(actx, q, T, ghost, Tghost, Sw, jac, lift, normals, fscale, facemat, facemat_p, vmap_m, vmap_p,
              bc_kind, qfar, phys):
         C, E, Np = q.shape
         Nf = dim + 1
         Nfp = lift.shape[1] // Nf
-        L = C + dim * C + 1
+        L = C + (dim + 1) * C + 1
         gamma = phys[0]
         vol = actx.np.einsum("rij,rcej->cei", Sw, actx.np.reshape(T[0:dim * C], (dim, C, E, Np)))
         planes = actx.np.concatenate([q, T])                                   # (L, E, Np)
@@ -358,7 +364,7 @@ def _make_ns_div(dim, with_ghost):
         for c in range(C):
             o = facemat[0] * tm[C + c]
             n = facemat_p[0] * tp[C + c]
-            for r in range(1, dim):
+            for r in range(1, dim + 1):
                 o = o + facemat[r] * tm[C + r * C + c]
                 n = n + facemat_p[r] * tp[C + r * C + c]
             own.append(o)

@@ -42,7 +42,7 @@ class DeviceRK4:
         self.q = actx.empty(shape)
         self._d2d(self.q, actx._contiguous(q0.data))
         self.s1, self.s2, self.acc = actx.empty(shape), actx.empty(shape), actx.empty(shape)
-        self.T = actx.empty((dim * (dim + 2) + 1,) + shape[1:]) if self.viscous else None
+        self.T = actx.empty((fused.flux_planes(dim),) + shape[1:]) if self.viscous else None
         d = op.dcoll
         self.disc = fused.get_disc(actx, dim, self.q, 0, d.Sw, d.drdx, d.lift, d.normals, d.fscale, d.vmap_m, d.vmap_p,
                                    d.bc_kind)

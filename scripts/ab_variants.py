@@ -15,37 +15,30 @@ PKG = os.path.join(ROOT, "paper_2512_17101_b200")
 
 VARIANTS = {
     "timing": ["DGB_PHASE_TIMING=1"],                 # scripts/phase_timing_flux.py
-    "timing7": ["DGB_PHASE_TIMING=1", "DGB_DIV_KERNEL_DEFAULT=7"],   # scripts/phase_timing_div7.py
     "base": [],
-    "noinb": ["DGB_DIV_INBLOCK=0"],
-    "div7": ["DGB_DIV_KERNEL_DEFAULT=7"],
-    "div7_nb2": ["DGB_DIV_KERNEL_DEFAULT=7", "DGB_DIV7_NB=2"],
-    "div7_nb2_lazy": ["DGB_DIV_KERNEL_DEFAULT=7", "DGB_DIV7_NB=2", "DGB_DIV7_LAZY_EX=1"],
-    "div7_lazy": ["DGB_DIV_KERNEL_DEFAULT=7", "DGB_DIV7_LAZY_EX=1"],
-    "div7_p7": ["DGB_DIV_KERNEL_DEFAULT=7", "DGB_DIV7_PRODUCERS=7"],
-    "div7_p6": ["DGB_DIV_KERNEL_DEFAULT=7", "DGB_DIV7_PRODUCERS=6"],
-    "trecord": ["DGB_T_RECORD=1"],                    # record-major flux planes (experiment: rhs only)
     "flux_w14": ["DGB_FLUX_WARPS=16"],
     "stcs": ["DGB_STREAMING_STORES=1"],
     "tk2": ["DGB_TICKET_BLOCKS=2"],
     "euler_w8": ["DGB_EULER_WARPS=8"],
     "div_w12_nb1": ["DGB_DIV_WARPS=12", "DGB_DIV_NB=1"],
-    "tma_w8": ["DGB_DIV_KERNEL_DEFAULT=8"],
-    "tma_w10_nb1": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_DIV8_WARPS=10", "DGB_DIV_NB=1"],
-    "tma_w12_nb1": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_DIV8_WARPS=12", "DGB_DIV_NB=1"],
-    "tma_w8_cg": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_GATHER_LD=1"],
-    "tma_w10_nb1_cg": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_DIV8_WARPS=10", "DGB_DIV_NB=1", "DGB_GATHER_LD=1"],
-    "tma_w12_nb1_cg": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_DIV8_WARPS=12", "DGB_DIV_NB=1", "DGB_GATHER_LD=1"],
-    "tma_w8_nc": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_GATHER_LD=2"],
-    "x_local": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_EXP_LOCALGATHER=1"],
-    "x_nomma": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_EXP_NOMMA=1"],
-    "x_noface": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_EXP_NOFACE=1"],
-    "x_noface_nomma": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_EXP_NOFACE=1", "DGB_EXP_NOMMA=1"],
-    "x_local_w12": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_EXP_LOCALGATHER=1", "DGB_DIV8_WARPS=12", "DGB_DIV_NB=1"],
-    "x_noface_w12": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_EXP_NOFACE=1", "DGB_DIV8_WARPS=12", "DGB_DIV_NB=1"],
-    "tma_w12": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_DIV8_WARPS=12"],
-    "tma_w12_lazy": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_DIV8_WARPS=12", "DGB_DIV_LAZY_EX=1"],
-    "tma_w8_nb4_lazy": ["DGB_DIV_KERNEL_DEFAULT=8", "DGB_DIV_NB=4", "DGB_DIV_LAZY_EX=1"],
+    "f_nolean": ["DGB_FLUX_LEAN=0"],
+    "f_nolean_w11": ["DGB_FLUX_LEAN=0", "DGB_FLUX_WARPS=11"],
+    "f_w11": ["DGB_FLUX_WARPS=11"],
+    "f_w10": ["DGB_FLUX_WARPS=10"],
+    "f_w8": ["DGB_FLUX_WARPS=8"],
+    "d12_nb2": ["DGB_DIV8_WARPS=12", "DGB_DIV8_NB=2"],
+    "d12_nb2_cg": ["DGB_DIV8_WARPS=12", "DGB_DIV8_NB=2", "DGB_GATHER_LD=1"],
+    "d12_nb4_cg": ["DGB_DIV8_WARPS=12", "DGB_DIV8_NB=4", "DGB_GATHER_LD=1"],
+    "d10_nb2": ["DGB_DIV8_WARPS=10", "DGB_DIV8_NB=2"],
+    "k3": ["DGB_DIV_KERNEL_DEFAULT=3"],
+    "w8": ["DGB_DIV8_WARPS=8"],
+    "w8_nb1": ["DGB_DIV8_WARPS=8", "DGB_DIV_NB=1"],
+    "w8_nb4": ["DGB_DIV8_WARPS=8", "DGB_DIV_NB=4"],
+    "w12": ["DGB_DIV8_WARPS=12"],
+    "w12_cg": ["DGB_DIV8_WARPS=12", "DGB_GATHER_LD=1"],
+    "x_local": ["DGB_EXP_LOCALGATHER=1"],
+    "x_nomma": ["DGB_EXP_NOMMA=1"],
+    "x_noface": ["DGB_EXP_NOFACE=1"],
     "ss_w8": ["DGB_DIV_SINGLE_SMALL=1"],
     "ss_w9": ["DGB_DIV_SINGLE_SMALL=1", "DGB_DIV_WARPS=9"],
     "ss_w10": ["DGB_DIV_SINGLE_SMALL=1", "DGB_DIV_WARPS=10"],

@@ -168,6 +168,24 @@ def test_midsize_parity(gpu, order, n, bc):
             assert rel_err(dg.to_numpy(o2), 0.5 * qq - 2.0 * ref) <= TOL_RHS
 
 
+@pytest.mark.parametrize("dim,order,n,bc", [(3, 3, 2, "mixed"), (3, 3, 12, "mixed"), (3, 4, 6, "mixed"), (3, 2, 5, "periodic"),
+                                            (3, 1, 5, "mixed"), (2, 3, 9, "mixed"), (2, 4, 7, "periodic"), (2, 1, 7, "farfield")])
+def test_tma_staged_pass2_is_bitwise_equal_to_cp_async_pass2(gpu, dim, order, n, bc, monkeypatch):
+    """k_nsdiv8 (default: rows by TMA boxes, neighbours through the 32-bit gather map, all rounds of a block in
+    flight) against k_nsdiv3 (cp.async staging, connectivity decoded per node): same arithmetic in the same order,
+    so the right-hand sides and the fused RK outputs must be bitwise equal -- odd Np (shifted boxes) included."""
+    d = make_dcoll(gpu, dim, order, n, bc)
+    op = NavierStokesOperator(d, farfield=FARFIELD[dim], mu=2e-2)
+    q = d.from_numpy(random_state(dim, d.nelements, d.Np, seed=3))
+    outs = {}
+    for k in ("3", "8"):
+        monkeypatch.setenv("DGB_DIV_KERNEL", k)
+        o1, o2 = op.rhs_rk(q, q, q, (1.0, 0.25, 0.5, -2.0))
+        outs[k] = (d.to_numpy(op.rhs(q)), d.to_numpy(o1), d.to_numpy(o2))
+    for a, b in zip(outs["3"], outs["8"]):
+        assert np.isfinite(a).all() and np.array_equal(a, b)
+
+
 def test_run_to_run_bitwise(gpu):
     """No atomics anywhere on the path: two evaluations are bitwise identical."""
     d = make_dcoll(gpu, 3, 3, 3, "periodic")
