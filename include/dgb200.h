@@ -155,6 +155,20 @@ int dgb_ns_div_range(const dgb_disc* disc, const double* q_dev, const double* T_
                      const double* qfar_host, const double* phys_host,
                      int64_t ebegin, int64_t eend, void* stream);
 
+/* ---- multi-species reactive Navier-Stokes (BASELINE configs[4]): the outlined functions dg_ms_flux / dg_ms_div of
+ *      multispecies.py (Call nodes of the reference: adfg.py:722-803; op families: IndexLambda with exp / truediv,
+ *      /root/reference/pkg/src/laze/expr.py:265-289, Einsum adfg.py:563-608, Indexing :502-560) on the same fused
+ *      kernels instantiated for C = dim + 2 + 3 fields.  q: (C, E, Np); T: ((dim+1)*C + 1, E, Np) plane groups as
+ *      in dgb_ns_flux; transport_host = [mu, kappa, D]; mixture_host = [ns = 3, R[ns], cv[ns], h0[ns], A, Ta,
+ *      reactant, product]; boundary faces take qfar_host (C values) as exterior state; eend < 0 = all elements. ---- */
+int dgb_ms_flux_range(const dgb_disc* disc, const double* q_dev, const double* ghost_dev, double* T_dev,
+                      const double* qfar_host, const double* transport_host, const double* mixture_host,
+                      int64_t ebegin, int64_t eend, void* stream);
+int dgb_ms_div_range(const dgb_disc* disc, const double* q_dev, const double* T_dev,
+                     const double* ghost_dev, const double* Tghost_dev, double* rhs_dev,
+                     const double* qfar_host, const double* transport_host, const double* mixture_host,
+                     int64_t ebegin, int64_t eend, void* stream);
+
 /* ---- halo packing: element rows <-> contiguous message (Send / Receive payloads,
  *      adfg.py:380-399,834-869).  dst[c, i, :] = src[c, elems[i], :]                        ---- */
 int dgb_pack_elements(double* dst_dev, const double* src_dev, const int64_t* elems_dev,

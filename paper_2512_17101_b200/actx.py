@@ -947,6 +947,8 @@ class B200ArrayContext:
         if impl is None:
             return f
         from . import fused
+        if not fused.supported(f):        # e.g. a species count the fused kernels are not instantiated for
+            return f
         if not fused.body_matches(f):
             # same name, different body (another EOS, another flux ...): the hand-written kernel would
             # silently compute the built-in physics.  Run the body itself, op by op, on the device.

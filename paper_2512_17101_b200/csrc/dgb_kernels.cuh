@@ -15,6 +15,13 @@
 #ifndef DGB_STREAMING_STORES
 #define DGB_STREAMING_STORES 0
 #endif
+// Number of species fields carried next to [rho, rho E, rho u]: 0 = single-species Euler / Navier-Stokes
+// (libdgb200's default translation units); dgb_msflux.cu compiles the SAME kernel templates once more with
+// DGB_NSPEC = 3 (and the namespace renamed) for the multi-species reactive operator (multispecies.py).
+#ifndef DGB_NSPEC
+#define DGB_NSPEC 0
+#endif
+#define DGB_MAX_SPECIES 4
 
 namespace dgb {
 
@@ -25,7 +32,8 @@ constexpr int ldpad(int k) { return (ceil_to(k, 4) % 8 == 4) ? ceil_to(k, 4) : c
 
 template <int DIM, int P>
 struct ElemT {
-  static constexpr int C = DIM + 2;
+  static constexpr int C = DIM + 2 + DGB_NSPEC;  // conserved fields
+  static constexpr int CG = C + (DGB_NSPEC > 0 ? 1 : 0);   // fields whose BR1 gradient pass 1 needs (mixtures: + temperature)
   static constexpr int NF = DIM + 1;
   static constexpr int NP = DIM == 2 ? (P + 1) * (P + 2) / 2 : (P + 1) * (P + 2) * (P + 3) / 6;
   static constexpr int NFP = DIM == 2 ? (P + 1) : (P + 1) * (P + 2) / 2;
@@ -51,6 +59,8 @@ struct ElemT {
 #define DGB_TICK(k) do { } while (0)
 #endif
 
+constexpr int DIM_MAX_FIELDS = 3 + 2 + DGB_MAX_SPECIES;
+
 struct DiscDev {
   long long* timing;     // [grid][8] per-phase cycle counters (debug builds only)
   long long E, G;
@@ -73,7 +83,14 @@ struct DiscDev {
   const double* Wv2;     // [NPR][LDV] volume matrix minus half the lifted own-side face term
 };
 
-struct Phys { double gamma, mu, kappa, rgas; double qfar[5]; };
+struct Phys {
+  double gamma, mu, kappa, rgas;
+  double qfar[DIM_MAX_FIELDS];
+  // mixture (multispecies.py: Mixture): species gas constants, heat capacities, formation enthalpies, Fick
+  // diffusivity, one Arrhenius step species ra -> species rb
+  double dspec, mR[DGB_MAX_SPECIES], mcv[DGB_MAX_SPECIES], mh0[DGB_MAX_SPECIES], arr_A, arr_Ta;
+  int ra, rb;
+};
 
 struct Epilogue {   // out1 = a1*x1 + b1*rhs ; out2 = a2*x2 + b2*rhs
   const double* x1; double* out1; const double* x2; double* out2;
@@ -227,6 +244,152 @@ __device__ __forceinline__ void bc_state(int bc, const double (&qm)[DIM + 2], co
       for (int i = 0; i < DIM; ++i) qp[2 + i] = qm[2 + i] - 2.0 * mn * n[i];
     }
   }
+}
+
+// }}}
+
+// {{{ mixture physics (DGB_NSPEC > 0) -- mirrors multispecies.py line by line
+
+#if DGB_NSPEC > 0
+template <int DIM>
+struct MsPrim { double rho, inv_rho, E, u[DIM], Y[DGB_NSPEC], T, p, R, cv; };
+
+// multispecies.py: _thermo
+template <int DIM>
+__device__ __forceinline__ void ms_thermo(const double (&q)[DIM + 2 + DGB_NSPEC], const Phys& ph, MsPrim<DIM>& s) {
+  s.rho = q[0]; s.E = q[1];
+  s.inv_rho = 1.0 / s.rho;
+  double ke = 0.0;
+#pragma unroll
+  for (int i = 0; i < DIM; ++i) { s.u[i] = q[2 + i] * s.inv_rho; ke = i == 0 ? s.u[i] * s.u[i] : ke + s.u[i] * s.u[i]; }
+  double R = 0.0, cv = 0.0, hf = 0.0;
+#pragma unroll
+  for (int k = 0; k < DGB_NSPEC; ++k) {
+    s.Y[k] = q[2 + DIM + k] * s.inv_rho;
+    R = k == 0 ? ph.mR[0] * s.Y[0] : R + ph.mR[k] * s.Y[k];
+    cv = k == 0 ? ph.mcv[0] * s.Y[0] : cv + ph.mcv[k] * s.Y[k];
+    hf = k == 0 ? ph.mh0[0] * s.Y[0] : hf + ph.mh0[k] * s.Y[k];
+  }
+  s.R = R; s.cv = cv;
+  s.T = (s.E * s.inv_rho - 0.5 * ke - hf) / cv;
+  s.p = s.rho * R * s.T;
+}
+
+// multispecies.py: _inviscid
+template <int DIM>
+__device__ __forceinline__ void ms_inviscid_flux(const double (&q)[DIM + 2 + DGB_NSPEC], const MsPrim<DIM>& s,
+                                                 double (&F)[DIM][DIM + 2 + DGB_NSPEC]) {
+#pragma unroll
+  for (int x = 0; x < DIM; ++x) {
+    F[x][0] = q[2 + x];
+    F[x][1] = s.u[x] * (q[1] + s.p);
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) F[x][2 + i] = q[2 + i] * s.u[x] + (i == x ? s.p : 0.0);
+#pragma unroll
+    for (int k = 0; k < DGB_NSPEC; ++k) F[x][2 + DIM + k] = q[2 + DIM + k] * s.u[x];
+  }
+}
+
+template <int DIM>
+__device__ __forceinline__ double ms_wavespeed(const MsPrim<DIM>& s) {
+  double v2 = 0.0;
+#pragma unroll
+  for (int i = 0; i < DIM; ++i) v2 += s.u[i] * s.u[i];
+  return sqrt(v2) + sqrt((1.0 + s.R / s.cv) * s.p / s.rho);
+}
+
+// multispecies.py: _viscous; g[x][c] = d q_c / d x_x for c < C, g[x][C] = dT / d x_x
+template <int DIM>
+__device__ __forceinline__ void ms_viscous_flux(const MsPrim<DIM>& s, const double (&g)[DIM][DIM + 3 + DGB_NSPEC],
+                                                const Phys& ph, double (&Fv)[DIM][DIM + 2 + DGB_NSPEC]) {
+  constexpr int C = DIM + 2 + DGB_NSPEC;
+  double du[DIM][DIM];
+#pragma unroll
+  for (int i = 0; i < DIM; ++i)
+#pragma unroll
+    for (int x = 0; x < DIM; ++x) du[i][x] = (g[x][2 + i] - s.u[i] * g[x][0]) * s.inv_rho;
+  double div = 0.0;
+#pragma unroll
+  for (int i = 0; i < DIM; ++i) div += du[i][i];
+#pragma unroll
+  for (int x = 0; x < DIM; ++x) {
+    double work = 0.0;
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) {
+      double t = ph.mu * (du[i][x] + du[x][i]);
+      if (i == x) t -= (2.0 / 3.0) * ph.mu * div;
+      Fv[x][2 + i] = t;
+      work += s.u[i] * t;
+    }
+    double heat = ph.kappa * g[x][C];
+#pragma unroll
+    for (int k = 0; k < DGB_NSPEC; ++k) {
+      const double dY = (g[x][2 + DIM + k] - s.Y[k] * g[x][0]) * s.inv_rho;
+      const double jk = (s.rho * ph.dspec) * dY;                 // = -J_k
+      const double hk = ph.mh0[k] + (ph.mcv[k] + ph.mR[k]) * s.T;
+      heat += hk * jk;
+      Fv[x][2 + DIM + k] = jk;
+    }
+    Fv[x][0] = 0.0;
+    Fv[x][1] = work + heat;
+  }
+}
+#endif
+
+// }}}
+
+// {{{ what the flux-arrangement kernels call: single-species or mixture physics behind one interface
+
+// total flux F = F_inv - F_visc at a node and the local wave speed
+template <int DIM>
+__device__ __forceinline__ void pw_total_flux(const double (&qq)[DIM + 2 + DGB_NSPEC],
+                                              const double (&g)[DIM][DIM + 2 + DGB_NSPEC + (DGB_NSPEC > 0 ? 1 : 0)],
+                                              const Phys& ph, double (&F)[DIM][DIM + 2 + DGB_NSPEC], double& lam) {
+  constexpr int C = DIM + 2 + DGB_NSPEC;
+  double Fv[DIM][C];
+#if DGB_NSPEC > 0
+  MsPrim<DIM> s;
+  ms_thermo<DIM>(qq, ph, s);
+  ms_inviscid_flux<DIM>(qq, s, F);
+  ms_viscous_flux<DIM>(s, g, ph, Fv);
+  lam = ms_wavespeed<DIM>(s);
+#else
+  Prim<DIM> s;
+  make_prim<DIM>(qq, ph.gamma, s);
+  inviscid_flux<DIM>(s, F);
+  viscous_flux<DIM>(s, g, ph, Fv);
+  lam = wavespeed<DIM>(s, ph.gamma);
+#endif
+#pragma unroll
+  for (int x = 0; x < DIM; ++x)
+#pragma unroll
+    for (int c = 1; c < C; ++c) F[x][c] -= Fv[x][c];
+}
+
+#if DGB_NSPEC > 0
+template <int DIM>
+__device__ __forceinline__ double pw_temperature(const double (&q)[DIM + 2 + DGB_NSPEC], const Phys& ph) {
+  MsPrim<DIM> s;
+  ms_thermo<DIM>(q, ph, s);
+  return s.T;
+}
+// Arrhenius rate of the one reaction step (multispecies.py: _ms_pass2)
+template <int DIM>
+__device__ __forceinline__ double pw_arrhenius(const double (&q)[DIM + 2 + DGB_NSPEC], const Phys& ph) {
+  return ph.arr_A * q[2 + DIM + ph.ra] * exp((-ph.arr_Ta) / pw_temperature<DIM>(q, ph));
+}
+#endif
+
+// exterior state of a boundary face for the BR1 gradient (pass 1): qp is overwritten
+template <int DIM>
+__device__ __forceinline__ void pw_exterior_state(int bc, const double (&qm)[DIM + 2 + DGB_NSPEC], const double (&n)[DIM],
+                                                  const Phys& ph, double (&qp)[DIM + 2 + DGB_NSPEC]) {
+#if DGB_NSPEC > 0
+#pragma unroll
+  for (int c = 0; c < DIM + 2 + DGB_NSPEC; ++c) qp[c] = ph.qfar[c];       // far-field is the only boundary kind
+#else
+  bc_state<DIM, true>(bc, qm, n, ph, qp);
+#endif
 }
 
 // }}}

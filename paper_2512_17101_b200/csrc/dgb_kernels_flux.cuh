@@ -226,7 +226,7 @@ __host__ __device__ constexpr int grad_row_swizzle(int k) {
 template <int DIM, int P, int KW>
 struct alignas(16) Flux3Warp {
   using EL = ElemT<DIM, P>;
-  static constexpr int NCOL = EL::C * KW;
+  static constexpr int NCOL = EL::CG * KW;     // columns of the BR1 gradient: (field, element), mixtures: + temperature
   static constexpr int NTILE = (NCOL + 7) / 8;
   static constexpr int NCOLP = NTILE * 8;
   double Qs[2][NCOLP * EL::LDQ];
@@ -383,6 +383,19 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
     __syncwarp();
     const double* Qs = W.Qs[buf];
     const FluxGeo<DIM, P, KW>& geo = W.geo[buf];
+#if DGB_NSPEC > 0
+    // mixtures: the temperature is one more field of the BR1 gradient; its rows follow those of q
+    for (int n = lane; n < KW * NP; n += 32) {
+      const int e = n / NP, j = n - e * NP;
+      if (e < nel) {
+        double qq[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) qq[c] = Qs[(c * KW + e) * EL::LDQ + j];
+        W.Qs[buf][(C * KW + e) * EL::LDQ + j] = pw_temperature<DIM>(qq, ph);
+      }
+    }
+    __syncwarp();
+#endif
     if (wb_next < nwblocks) {
       const long long e1 = ebeg + wb_next * KW;
       flux_stage_async<DIM, P, KW>(W.Qs[buf ^ 1], W.geo[buf ^ 1], d, q, e1,
@@ -421,10 +434,13 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
           double nrm[DIM];
 #pragma unroll
           for (int x = 0; x < DIM; ++x) nrm[x] = geo.nrm[x][e][f];
-          bc_state<DIM, true>(bc, qm, nrm, ph, qpE[k]);
+          pw_exterior_state<DIM>(bc, qm, nrm, ph, qpE[k]);
         }
 #pragma unroll
         for (int c = 0; c < C; ++c) W.Ss[(c * KW + e) * LDSX + f * EL::NFPK + m] = 0.5 * (qm[c] + qpE[k][c]);
+#if DGB_NSPEC > 0
+        W.Ss[(C * KW + e) * LDSX + f * EL::NFPK + m] = 0.5 * (Qs[(C * KW + e) * EL::LDQ + jm] + pw_temperature<DIM>(qpE[k], ph));
+#endif
       }
     }
     __syncwarp();
@@ -505,24 +521,17 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
       const int n = n0 + lane;
       const int e = n / NP, j = n - e * NP;
       if (n < KW * NP && e < nel) {
-        double qq[C], g[DIM][C];
+        double qq[C], g[DIM][EL::CG];
 #pragma unroll
-        for (int c = 0; c < C; ++c) {
+        for (int c = 0; c < EL::CG; ++c) {
           const int col = c * KW + e;
-          qq[c] = Qs[col * EL::LDQ + j];
+          if (c < C) qq[c] = Qs[col * EL::LDQ + j];
           const double* sg = W.Ss + (col >> 3) * 8 * LDSX + grad_row_swizzle<NP>(col & 7) * NP + j;
 #pragma unroll
           for (int x = 0; x < DIM; ++x) g[x][c] = sg[x * 8 * NP];
         }
-        Prim<DIM> s;
-        make_prim<DIM>(qq, ph.gamma, s);
-        double F[DIM][C], Fv[DIM][C];
-        inviscid_flux<DIM>(s, F);
-        viscous_flux<DIM>(s, g, ph, Fv);
-#pragma unroll
-        for (int x = 0; x < DIM; ++x)
-#pragma unroll
-          for (int c = 1; c < C; ++c) F[x][c] -= Fv[x][c];
+        double F[DIM][C], lam;
+        pw_total_flux<DIM>(qq, g, ph, F, lam);
         const double J = geo.jac[e];
         constexpr int NPLT = FluxT<DIM, P>::NPL;
         const long long t_ps = t_plane_stride<NPLT, NP>(E);
@@ -544,7 +553,7 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
         }
 #pragma unroll
         for (int c = 0; c < C; ++c) out[(DIM * C + c) * t_ps] = tsum[c];
-        out[FluxT<DIM, P>::LAMPL * t_ps] = wavespeed<DIM>(s, ph.gamma);
+        out[FluxT<DIM, P>::LAMPL * t_ps] = lam;
       }
     }
     __syncwarp();
@@ -656,7 +665,7 @@ __device__ __forceinline__ void div_stage_rows(double* Ts, const DiscDev& d, con
   }
 }
 
-template <int DIM> struct VecC { double v[DIM + 2]; };
+template <int DIM> struct VecC { double v[DIM + 2 + DGB_NSPEC]; };
 
 // Boundary face node (rare): inviscid flux of the exterior state, viscous flux of the interior
 // state (operators.py: f_bnd = own + B).  The own-side term is read from HBM here (the block's
@@ -666,7 +675,7 @@ template <int DIM>
 __device__ __noinline__ VecC<DIM> boundary_operand(int bc, int f, VecC<DIM> qm_, const double* __restrict__ Tnode,
                                                    long long pstride, double lam_m, double sj,
                                                    const double* __restrict__ normals, long long nstride, Phys ph) {
-  constexpr int C = DIM + 2;
+  constexpr int C = DIM + 2 + DGB_NSPEC;
   double nrm[DIM], qm[C], qb[C], own[C];
 #pragma unroll
   for (int x = 0; x < DIM; ++x) nrm[x] = normals[x * nstride];
@@ -675,14 +684,33 @@ __device__ __noinline__ VecC<DIM> boundary_operand(int bc, int f, VecC<DIM> qm_,
     qm[c] = qm_.v[c]; qb[c] = qm_.v[c];
     own[c] = f == 0 ? Tnode[(DIM * C + c) * pstride] : -Tnode[((f - 1) * C + c) * pstride];
   }
+  double fnb[C], fni[C];
+#if DGB_NSPEC > 0
+  // multispecies.py: _ms_pass2 -- far-field exterior state, fnb - fni = n . (F_inv(far) - F_inv(q-))
+  pw_exterior_state<DIM>(bc, qm, nrm, ph, qb);
+  MsPrim<DIM> sb, sm;
+  ms_thermo<DIM>(qb, ph, sb);
+  ms_thermo<DIM>(qm, ph, sm);
+  double Fb[DIM][C], Fm[DIM][C];
+  ms_inviscid_flux<DIM>(qb, sb, Fb);
+  ms_inviscid_flux<DIM>(qm, sm, Fm);
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    double d = nrm[0] * (Fb[0][c] - Fm[0][c]);
+#pragma unroll
+    for (int x = 1; x < DIM; ++x) d += nrm[x] * (Fb[x][c] - Fm[x][c]);
+    fnb[c] = d; fni[c] = 0.0;
+  }
+  const double lam = fmax(lam_m, ms_wavespeed<DIM>(sb));
+#else
   bc_state<DIM, true>(bc, qm, nrm, ph, qb);
   Prim<DIM> sb, sm;
   make_prim<DIM>(qb, ph.gamma, sb);
   make_prim<DIM>(qm, ph.gamma, sm);
-  double fnb[C], fni[C];
   inviscid_normal_flux<DIM>(sb, nrm, fnb);
   inviscid_normal_flux<DIM>(sm, nrm, fni);
   const double lam = fmax(lam_m, wavespeed<DIM>(sb, ph.gamma));
+#endif
   VecC<DIM> out;
 #pragma unroll
   for (int c = 0; c < C; ++c)

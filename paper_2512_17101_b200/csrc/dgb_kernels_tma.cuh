@@ -203,6 +203,7 @@ struct alignas(128) Div8Warp {
   alignas(128) double Qb[EL::C * BX::BOXW];             // [field][element][node]
   alignas(128) double Lam[BX::BOXW];                    // wave speed rows of the block
   double Fs[NCOL * EL::LDF];
+  double Om[DGB_NSPEC > 0 ? KW * EL::NP : 1];           // mixtures: Arrhenius rate at the block's nodes
   Div8Geo<DIM, P, KW> geo[2];
   unsigned long long bar_q, bar_t;
 };
@@ -233,7 +234,7 @@ k_nsdiv8(DiscDev d, const __grid_constant__ CUtensorMap map_q, const __grid_cons
   constexpr int NR = face_rounds<DIM, P, KW>();
   // face nodes per lane with their gathers in flight together: all NR rounds of a block at 8 warps (11 values per
   // node: 88 registers for 3D p3), one round at 9-12 warps (168 registers)
-  constexpr int NB = DGB_DIV8_NB > 0 ? DGB_DIV8_NB : (NWARPS > 8 ? 1 : NR);
+  constexpr int NB = DGB_DIV8_NB > 0 ? DGB_DIV8_NB : (NWARPS > 8 ? 1 : (C <= 5 ? NR : 2));     // 2 C + 1 values per node
   constexpr int BOXW = BX::BOXW;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   auto& S = *reinterpret_cast<Div8Smem<DIM, P, KW, NWARPS>*>(smem_raw);
@@ -333,6 +334,18 @@ k_nsdiv8(DiscDev d, const __grid_constant__ CUtensorMap map_q, const __grid_cons
     double rj[WS::NTILE];
 #pragma unroll
     for (int mt = 0; mt < WS::NTILE; ++mt) rj[mt] = W.geo[buf].rj[(mt * 8 + (lane >> 2)) % KW];
+#if DGB_NSPEC > 0
+    // chemistry: the Arrhenius rate at every node of the block, from the state box while it is still here
+    for (int n = lane; n < KW * NP; n += 32) {
+      const int e = n / NP;
+      if (e < nel) {
+        double qq[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) qq[c] = W.Qb[c * BOXW + n + sh];
+        W.Om[n] = pw_arrhenius<DIM>(qq, ph);
+      }
+    }
+#endif
     __syncwarp();                        // every lane has read the state box: the next one may land on it
     if (nel1 > 0 && lane == 0) issue_q(e1);
     mbar_wait_(&W.bar_t, par);           // flux planes of this block
@@ -360,10 +373,20 @@ k_nsdiv8(DiscDev d, const __grid_constant__ CUtensorMap map_q, const __grid_cons
       const int c = col / KW, e = col - c * KW;
       if (col < WS::NCOL && e < nel) {
         const long long rowbase = ((long long)c * E + e0 + e) * NP;
+#if DGB_NSPEC > 0
+        const double sgn = c == 2 + DIM + ph.ra ? -1.0 : (c == 2 + DIM + ph.rb ? 1.0 : 0.0);     // species a -> species b
+#endif
 #pragma unroll
         for (int ni = 0; ni < EL::NI; ++ni) {
           const int i = ni * 8 + 2 * (lane & 3);
-          store_pair<NP>(ep, rowbase + i, i, rj[mt] * acc[mt][ni][0], rj[mt] * acc[mt][ni][1]);
+          double v0 = rj[mt] * acc[mt][ni][0], v1 = rj[mt] * acc[mt][ni][1];
+#if DGB_NSPEC > 0
+          if (sgn != 0.0) {
+            if (i < NP) v0 += sgn * W.Om[e * NP + i];
+            if (i + 1 < NP) v1 += sgn * W.Om[e * NP + i + 1];
+          }
+#endif
+          store_pair<NP>(ep, rowbase + i, i, v0, v1);
         }
       }
     }

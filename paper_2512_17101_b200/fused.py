@@ -54,14 +54,14 @@ def _i64(actx, a, what):
     return actx._contiguous(a)
 
 
-def get_disc(actx, dim, q, nghost, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind) -> _Disc:
+def get_disc(actx, dim, q, nghost, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, nspecies=0) -> _Disc:
     key = (dim, nghost, id(Sw), id(drdx), id(lift), id(normals), id(fscale), id(vmap_m), id(vmap_p), id(bc_kind))
     disc = actx._discs.get(key)
     if disc is not None:
         return disc
     C_, E, Np = q.shape
-    if C_ != dim + 2:
-        raise errors.ShapeMismatch(f"state has {C_} fields, expected {dim + 2}")
+    if C_ != dim + 2 + nspecies:
+        raise errors.ShapeMismatch(f"state has {C_} fields, expected {dim + 2 + nspecies}")
     order = _ORDER_OF_NP.get((dim, Np))
     if order is None:
         raise errors.ShapeMismatch(f"no simplex element with dim={dim}, Np={Np} (orders 1..4 are built)")
@@ -368,7 +368,90 @@ def ns_div_range(actx, op, q, T, ghost, Tghost, out, lo, hi):
 # }}}
 
 
-FUSED = {"dg_ns_flux": dg_ns_flux, "dg_ns_div": dg_ns_div, "dg_ns_div_rk": dg_ns_div_rk, "dg_euler_rhs": dg_euler_rhs, "dg_ns_grad": dg_ns_grad, "dg_ns_rhs": dg_ns_rhs,
+# {{{ multi-species reactive Navier-Stokes (multispecies.py): dgb_ms_flux / dgb_ms_div
+
+MS_FUSED_SPECIES = 3          # the species count libdgb200 instantiates the kernels for (csrc/dgb_msflux.cu)
+
+
+def ms_flux_planes(dim: int, ns: int) -> int:
+    return (dim + 1) * (dim + 2 + ns) + 1
+
+
+def _ms_params(f, qfar, transport, C_):
+    mix = getattr(f, "dg_mix", None)
+    if mix is None:
+        raise errors.BindingMismatch(f"{f.__name__}: the outlined function carries no mixture (f.dg_mix)")
+    m = np.concatenate([[mix.ns], mix.R, mix.cv, mix.h0, [mix.A, mix.Ta, mix.reaction[0], mix.reaction[1]]]).astype(np.float64)
+    qf = _host_vec(qfar, C_)
+    tr = np.zeros(3) if transport is None else _host_vec(transport, 3)
+    return np.ascontiguousarray(m), qf, np.ascontiguousarray(tr)
+
+
+def _ms_flux(actx, f, q, ghost, Sw, drdx, jac, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, transport):
+    dim, ns = f.dg_dim, f.dg_mix.ns
+    q = _f64(actx, q, "q")
+    G, g, gptr = _ghost_ptr(actx, ghost, (dim + 2 + ns,), q.shape[-1])
+    disc = get_disc(actx, dim, q, G, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, nspecies=ns)
+    _bind_jacobian(actx, disc, jac)
+    m, qf, tr = _ms_params(f, qfar, transport, dim + 2 + ns)
+    out = actx.empty((ms_flux_planes(dim, ns),) + tuple(q.shape[1:]))
+    _cabi.check(actx.lib.dgb_ms_flux_range(disc.handle, q.ptr, gptr, out.ptr, qf.ctypes.data, tr.ctypes.data,
+                                           m.ctypes.data, 0, -1, actx._st), "dg_ms_flux")
+    actx.launch_count += 1
+    return out, disc
+
+
+def _ms_div(actx, f, disc, q, T, ghost, Tghost, jac, facemat, facemat_p, qfar):
+    dim, ns = f.dg_dim, f.dg_mix.ns
+    q = _f64(actx, q, "q")
+    T = _f64(actx, T, "T")
+    npl = ms_flux_planes(dim, ns)
+    if tuple(T.shape) != (npl,) + tuple(q.shape[1:]):
+        raise errors.BindingMismatch(f"flux planes have shape {tuple(T.shape)}, expected {(npl,) + tuple(q.shape[1:])}")
+    G, g, gptr = _ghost_ptr(actx, ghost, (dim + 2 + ns,), q.shape[-1])
+    TG, tg, tgptr = _ghost_ptr(actx, Tghost, (npl,), q.shape[-1])
+    if TG != G:
+        raise errors.BindingMismatch("ghost arrays of q and of the flux planes disagree in size")
+    _bind_jacobian(actx, disc, jac)
+    _check_facemat(disc, facemat, facemat_p)
+    m, qf, tr = _ms_params(f, qfar, None, dim + 2 + ns)
+    out = actx.empty(q.shape)
+    _cabi.check(actx.lib.dgb_ms_div_range(disc.handle, q.ptr, T.ptr, gptr, tgptr, out.ptr, qf.ctypes.data,
+                                          tr.ctypes.data, m.ctypes.data, 0, -1, actx._st), "dg_ms_div")
+    actx.launch_count += 1
+    return out
+
+
+def dg_ms_flux(actx, f, q, ghost, Sw, drdx, jac, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, transport):
+    return _ms_flux(actx, f, q, ghost, Sw, drdx, jac, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, transport)[0]
+
+
+def dg_ms_div(actx, f, q, T, ghost, Tghost, Sw, jac, lift, normals, fscale, facemat, facemat_p, vmap_m, vmap_p, bc_kind, qfar):
+    dim = f.dg_dim
+    G = 0 if ghost is None else ghost.shape[-2]
+    disc = actx._discs.get(("nodrdx", dim, G, id(Sw), id(lift), id(normals), id(fscale), id(vmap_m), id(vmap_p), id(bc_kind)))
+    if disc is None:
+        raise errors.BindingMismatch("dg_ms_div: no discretisation handle for these arrays (call dg_ms_flux first)")
+    return _ms_div(actx, f, disc, q, T, ghost, Tghost, jac, facemat, facemat_p, qfar)
+
+
+def dg_ms_rhs(actx, f, q, Sw, drdx, jac, lift, normals, fscale, facemat, facemat_p, vmap_m, vmap_p, bc_kind, qfar, transport):
+    T, disc = _ms_flux(actx, f, q, None, Sw, drdx, jac, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, transport)
+    return _ms_div(actx, f, disc, q, T, None, None, jac, facemat, facemat_p, qfar)
+
+
+def supported(f) -> bool:
+    """Whether the fused kernels exist for this outlined function's configuration (else: op by op on the device)."""
+    if f.__name__ in ("dg_ms_flux", "dg_ms_div", "dg_ms_rhs"):
+        mix = getattr(f, "dg_mix", None)
+        return mix is not None and mix.ns == MS_FUSED_SPECIES
+    return True
+
+# }}}
+
+
+FUSED = {"dg_ms_flux": dg_ms_flux, "dg_ms_div": dg_ms_div, "dg_ms_rhs": dg_ms_rhs,
+         "dg_ns_flux": dg_ns_flux, "dg_ns_div": dg_ns_div, "dg_ns_div_rk": dg_ns_div_rk, "dg_euler_rhs": dg_euler_rhs, "dg_ns_grad": dg_ns_grad, "dg_ns_rhs": dg_ns_rhs,
          "dg_euler_rhs_rk": dg_euler_rhs_rk, "dg_ns_rhs_rk": dg_ns_rhs_rk}
 
 

@@ -4,10 +4,11 @@ Nothing in the reference defines a mixture EOS, transport model or reaction mech
 "parity unpinned"; §8d c4: "a small builder-chosen mechanism"), so the model is fixed HERE and
 documented; like ``operators.py`` it is written once against the reference's array-context API
 (/root/reference/pkg/src/laze/frontend.py:257-302) and runs unchanged on ``laze.ArrayContext``
-(eager and lazy), on the NumPy oracle and on ``B200ArrayContext``.  On B200 it is NOT hand-fused in
-round 1: every op runs on the generic device kernels of the context (``dgb_einsum``, ``dgb_take``,
-``dgb_ew_*``) -- on the device, without a CPU fallback, but at a fraction of the fused path's speed
-(profiles/r01_multispecies.md).  It exists so that configs[4] has a parity-checked drop-in path.
+(eager and lazy), on the NumPy oracle and on ``B200ArrayContext``.  On B200 the outlined functions
+``dg_ms_flux`` / ``dg_ms_div`` / ``dg_ms_rhs`` are dispatched by name to the fused kernels of the flux
+arrangement instantiated for ``C = d + 2 + ns`` fields (round 2: ``dgb_ms_flux`` / ``dgb_ms_div``, the same
+``k_nsflux3`` / ``k_nsdiv8`` templates with the mixture physics; round 1 ran every op on the generic device
+kernels, profiles/r01_multispecies.md).
 
 Model
 -----
@@ -122,10 +123,12 @@ def _viscous(actx, mix, q, gq, gT, prim, transport, dim):
     return flux
 
 
-def _ms_pass1(actx, mix, dim, q, ghost, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, transport):
-    """BR1 gradient of [q, T] (central flux), then the total flux at every node.  Returns the planes
-    ``[F_x[c] (x-major, dim*C planes), lam]``, shape ``(dim*C + 1, E, Np)`` -- what pass 2 gathers and, on a
-    partitioned mesh, what the second halo exchange carries."""
+def _ms_pass1(actx, mix, dim, q, ghost, Sw, drdx, jac, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, transport):
+    """Pass 1 (``dg_ms_flux``): BR1 gradient of ``[q, T]`` (central flux), then the total flux at every node, stored
+    like ``dg_ns_flux`` of the single-species operator: planes ``r*C + c`` (``r < dim``) hold the contravariant,
+    Jacobian-scaled components ``T[r][c] = sum_x jac*drdx[r,x] (F_inv - F_visc)[x][c]``, planes ``dim*C + c`` their sum
+    over ``r`` and the last plane the mixture wave speed: shape ``((dim+1)*C + 1, E, Np)`` -- what pass 2 contracts and
+    gathers and, on a partitioned mesh, what the second halo exchange carries."""
     C, E, Np = q.shape
     Nf = dim + 1
     Nfp = lift.shape[1] // Nf
@@ -152,70 +155,85 @@ def _ms_pass1(actx, mix, dim, q, ghost, Sw, drdx, lift, normals, fscale, vmap_m,
     gT = [gW[x][C] for x in range(dim)]
     fvis = _viscous(actx, mix, qc, gq, gT, prim, tr, dim)
     ftot = [[finv[x][c] if fvis[x][c] is None else finv[x][c] - fvis[x][c] for c in range(C)] for x in range(dim)]
-    fstack = actx.np.stack([actx.np.stack(fx) for fx in ftot])
-    return actx.np.concatenate([actx.np.reshape(fstack, (dim * C, E, Np)), actx.np.reshape(lam, (1, E, Np))])
+    fstack = actx.np.stack([actx.np.stack(fx) for fx in ftot])                          # (d, C, E, Np)
+    T = actx.np.einsum("rxe,e,xcej->rcej", drdx, jac, fstack)
+    tsum = T[0] + T[1]
+    for r in range(2, dim):
+        tsum = tsum + T[r]
+    return actx.np.concatenate([actx.np.reshape(T, (dim * C, E, Np)), tsum, actx.np.reshape(lam, (1, E, Np))])
 
 
-def _ms_pass2(actx, mix, dim, q, FL, ghost, gFL, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar):
-    """Divergence of the stored flux, Rusanov / central numerical flux from gathered neighbour planes,
-    Arrhenius source."""
+def _ms_pass2(actx, mix, dim, q, T, ghost, Tghost, Sw, jac, lift, normals, fscale, facemat, facemat_p, vmap_m, vmap_p,
+              bc_kind, qfar):
+    """Pass 2 (``dg_ms_div``): ``rhs = (1/J)(sum_r Sw_r T_r - lift(sJ F*.n)) + chemistry``; the scaled normal flux of
+    either side of a face is one plane group of pass 1 (``facemat``, as in ``dg_ns_div``), Rusanov with the mixture
+    wave speed; far-field boundary faces: inviscid flux of the exterior state, viscous flux of the interior one."""
     C, E, Np = q.shape
     Nf = dim + 1
     Nfp = lift.shape[1] // Nf
     ns = mix.ns
+    L = C + (dim + 1) * C + 1
     nrm = [normals[x] for x in range(dim)]
     is_bnd = actx.np.not_equal(bc_kind, BC_NONE)
     far = [qfar[c] for c in range(C)]
-    volf = actx.np.einsum("rij,rxe,xcej->cei", Sw, drdx, actx.np.reshape(FL[0:dim * C], (dim, C, E, Np)))
-    planes = actx.np.concatenate([q, FL])                                               # q, F, lam
-    gplanes = None if ghost is None else actx.np.concatenate([ghost, gFL])
-    L = C + dim * C + 1
+    vol = actx.np.einsum("rij,rcej->cei", Sw, actx.np.reshape(T[0:dim * C], (dim, C, E, Np)))
+    planes = actx.np.concatenate([q, T])                                                # q, plane groups, lam
+    gplanes = None if ghost is None else actx.np.concatenate([ghost, Tghost])
     tm, tp = _traces(actx, planes, gplanes, vmap_m, vmap_p, L, E, Np, Nf, Nfp)
+    sj = fscale * actx.np.reshape(jac, (E, 1, 1))                                       # face Jacobian (E, Nf, 1)
     qm = [tm[c] for c in range(C)]
-    qp = [actx.np.where(is_bnd, far[c], tp[c]) for c in range(C)]
-    # exterior flux on boundary faces: inviscid flux of the far-field state, viscous flux of the interior
+    qp = [tp[c] for c in range(C)]
+    own, nbr = [], []
+    for c in range(C):
+        o = facemat[0] * tm[C + c]
+        n = facemat_p[0] * tp[C + c]
+        for r in range(1, dim + 1):
+            o = o + facemat[r] * tm[C + r * C + c]
+            n = n + facemat_p[r] * tp[C + r * C + c]
+        own.append(o)
+        nbr.append(n)
+    lam_m, lam_p = tm[L - 1], tp[L - 1]
     ffar, lam_far, _ = _inviscid(actx, mix, far, dim)
     fmi, _, _ = _inviscid(actx, mix, qm, dim)
+    lam_b = actx.np.maximum(lam_m, lam_far)
     fstar = []
-    lam_p = actx.np.where(is_bnd, lam_far, tp[L - 1])
-    lmax = actx.np.maximum(tm[L - 1], lam_p)
     for c in range(C):
-        fnm = nrm[0] * tm[C + c]
-        fnp = nrm[0] * tp[C + c]
         fnb = nrm[0] * (ffar[0][c] - fmi[0][c])
         for x in range(1, dim):
-            fnm = fnm + nrm[x] * tm[C + x * C + c]
-            fnp = fnp + nrm[x] * tp[C + x * C + c]
             fnb = fnb + nrm[x] * (ffar[x][c] - fmi[x][c])
-        fplus = actx.np.where(is_bnd, fnm + fnb, fnp)
-        fstar.append(fscale * (0.5 * (fnm + fplus) + 0.5 * lmax * (qm[c] - qp[c])))
+        f_int = 0.5 * (own[c] - nbr[c]) + 0.5 * sj * actx.np.maximum(lam_m, lam_p) * (qm[c] - qp[c])
+        f_bnd = own[c] + 0.5 * sj * fnb + 0.5 * sj * lam_b * (qm[c] - far[c])
+        fstar.append(actx.np.where(is_bnd, f_bnd, f_int))
     fsx = actx.np.reshape(actx.np.stack(fstar), (C, E, Nf * Nfp))
-    rhs = volf - actx.np.einsum("if,cef->cei", lift, fsx)
+    rhs = (vol - actx.np.einsum("if,cef->cei", lift, fsx)) / actx.np.reshape(jac, (E, 1))
     # chemistry: one Arrhenius step a -> b
     qc = [q[c] for c in range(C)]
-    T = _thermo(actx, mix, qc, dim)[2]
+    Tn = _thermo(actx, mix, qc, dim)[2]
     a, b = mix.reaction
-    omega = mix.A * qc[2 + dim + a] * actx.np.exp((-mix.Ta) / T)
+    omega = mix.A * qc[2 + dim + a] * actx.np.exp((-mix.Ta) / Tn)
     zero = 0.0 * omega
     src = [zero] * (2 + dim) + [(-1.0 * omega) if k == a else (omega if k == b else zero) for k in range(ns)]
     return rhs + actx.np.stack(src)
 
 
 def _make_ms_functions(dim, mix):
-    """The outlined functions: ``dg_ms_rhs`` (single domain, both passes), and for partitioned meshes
-    ``dg_ms_flux`` / ``dg_ms_div`` with ghost arrays (the halo of the flux planes is exchanged in between)."""
-    def dg_ms_rhs(q, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, transport):
+    """The outlined functions -- the plugin boundary of the multi-species operator: ``dg_ms_rhs`` (single domain, both
+    passes) and, for partitioned meshes, ``dg_ms_flux`` / ``dg_ms_div`` with ghost arrays (the halo of the flux planes
+    is exchanged in between).  On B200 they are dispatched by name to the fused kernels (``fused.py``,
+    ``dgb_ms_flux`` / ``dgb_ms_div``); the mixture travels with the function (``f.dg_mix``)."""
+    def dg_ms_rhs(q, Sw, drdx, jac, lift, normals, fscale, facemat, facemat_p, vmap_m, vmap_p, bc_kind, qfar, transport):
         actx = dg_ms_rhs.actx
-        FL = _ms_pass1(actx, mix, dim, q, None, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, transport)
-        return _ms_pass2(actx, mix, dim, q, FL, None, None, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar)
+        T = _ms_pass1(actx, mix, dim, q, None, Sw, drdx, jac, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, transport)
+        return _ms_pass2(actx, mix, dim, q, T, None, None, Sw, jac, lift, normals, fscale, facemat, facemat_p, vmap_m,
+                         vmap_p, bc_kind, qfar)
 
-    def dg_ms_flux(q, ghost, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, transport):
-        return _ms_pass1(dg_ms_flux.actx, mix, dim, q, ghost, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind,
-                         qfar, transport)
+    def dg_ms_flux(q, ghost, Sw, drdx, jac, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, transport):
+        return _ms_pass1(dg_ms_flux.actx, mix, dim, q, ghost, Sw, drdx, jac, lift, normals, fscale, vmap_m, vmap_p,
+                         bc_kind, qfar, transport)
 
-    def dg_ms_div(q, FL, ghost, gFL, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar):
-        return _ms_pass2(dg_ms_div.actx, mix, dim, q, FL, ghost, gFL, Sw, drdx, lift, normals, fscale, vmap_m, vmap_p,
-                         bc_kind, qfar)
+    def dg_ms_div(q, T, ghost, Tghost, Sw, jac, lift, normals, fscale, facemat, facemat_p, vmap_m, vmap_p, bc_kind, qfar):
+        return _ms_pass2(dg_ms_div.actx, mix, dim, q, T, ghost, Tghost, Sw, jac, lift, normals, fscale, facemat,
+                         facemat_p, vmap_m, vmap_p, bc_kind, qfar)
     return dg_ms_rhs, dg_ms_flux, dg_ms_div
 
 
@@ -224,10 +242,13 @@ class MultispeciesOperator:
     Boundaries: periodic, or far-field (every tagged boundary face takes ``farfield`` as exterior state)."""
 
     def __init__(self, dcoll: DGDiscretization, mixture: Mixture | None = None, mu=1e-2, kappa=2e-2, diffusivity=1e-2,
-                 farfield=None, graph: bool | None = None):
-        """``graph`` (device contexts only; default on): evaluate the right-hand side through
-        ``actx.compile(f, graph=True)`` -- first call eager, second call captured into one CUDA graph,
-        later calls replayed -- instead of ~800 separately dispatched kernels."""
+                 farfield=None, graph: bool | None = None, fused: bool = True):
+        """``fused`` (default): the outlined functions go through ``actx.outline`` -- on B200 that is the by-name
+        dispatch to the fused kernels; ``fused=False`` runs their bodies op by op on whatever the context provides
+        (the round-1 path, kept as an independent cross-check on the device).  ``graph`` (device contexts only;
+        default on) applies to functions that are NOT fused: evaluate them through ``actx.compile(f, graph=True)`` --
+        first call eager, second call captured into one CUDA graph, later calls replayed -- instead of ~800
+        separately dispatched kernels."""
         self.dcoll, self.actx, self.dim = dcoll, dcoll.actx, dcoll.dim
         self.mix = mixture or Mixture()
         self.ncomp = self.dim + 2 + self.mix.ns
@@ -242,8 +263,11 @@ class MultispeciesOperator:
         for f in _make_ms_functions(self.dim, self.mix):
             f.actx = self.actx
             f.dg_dim = self.dim
-            g = self.actx.outline(f)
-            fns.append(self.actx.compile(g, graph=True) if graph else g)
+            f.dg_mix = self.mix
+            g = self.actx.outline(f) if fused else f
+            # hand-fused on the device (fused.py); a function that is NOT dispatched to the fused kernels (edited
+            # body) runs op by op on the device, where one CUDA graph per right-hand side removes the dispatch cost
+            fns.append(self.actx.compile(g, graph=True) if (graph and not getattr(g, "fused", False)) else g)
         self._f, self._flux, self._div = fns
 
     def state_from_primitive(self, rho, vel, T, Y):
@@ -258,14 +282,21 @@ class MultispeciesOperator:
         parts = [rho, rho * e] + [rho * v for v in vel] + [rho * y for y in Y]
         return np.stack(np.broadcast_arrays(*parts))
 
-    def _geo(self):
+    def flux(self, q, ghost):
+        """Pass 1 on a partitioned mesh: the flux planes of the owned elements (raw array ``((dim+1)*C + 1, E, Np)``)."""
         d = self.dcoll
-        return (d.Sw, d.drdx, d.lift, d.normals, d.fscale, d.vmap_m, d.vmap_p, d.bc_kind, self.qfar)
+        q = q.data if isinstance(q, DOFArray) else q
+        return self._flux(q, ghost, d.Sw, d.drdx, d.jac, d.lift, d.normals, d.fscale, d.vmap_m, d.vmap_p, d.bc_kind,
+                          self.qfar, self.transport)
 
     def rhs(self, q: DOFArray, t=0.0, ghost=None, halo_fn=None) -> DOFArray:
         """Single domain: ``rhs(q)``.  Partitioned: ``ghost`` = halo of ``q`` and ``halo_fn(DOFArray of the flux
         planes) -> their halo`` (second exchange), like ``NavierStokesOperator.rhs``."""
+        d = self.dcoll
+        maps = (d.vmap_m, d.vmap_p, d.bc_kind, self.qfar)
         if ghost is None:
-            return DOFArray(self.actx, self._f(q.data, *self._geo(), self.transport))
-        FL = self._flux(q.data, ghost, *self._geo(), self.transport)
-        return DOFArray(self.actx, self._div(q.data, FL, ghost, halo_fn(DOFArray(self.actx, FL)), *self._geo()))
+            return DOFArray(self.actx, self._f(q.data, d.Sw, d.drdx, d.jac, d.lift, d.normals, d.fscale, d.facemat,
+                                               d.facemat_p, *maps, self.transport))
+        T = self._flux(q.data, ghost, d.Sw, d.drdx, d.jac, d.lift, d.normals, d.fscale, *maps, self.transport)
+        return DOFArray(self.actx, self._div(q.data, T, ghost, halo_fn(DOFArray(self.actx, T)), d.Sw, d.jac, d.lift,
+                                             d.normals, d.fscale, d.facemat, d.facemat_p, *maps))

@@ -15,7 +15,16 @@ MAKERS = {"dg_euler_rhs": operators._make_euler_rhs, "dg_ns_grad": operators._ma
           "dg_ns_div_rk": operators._make_ns_div_rk}
 
 
+def _ms_makers():
+    from paper_2512_17101_b200 import multispecies
+    out = {}
+    for k, name in enumerate(("dg_ms_rhs", "dg_ms_flux", "dg_ms_div")):
+        out[name] = lambda dim, ghost, k=k: multispecies._make_ms_functions(dim, multispecies.Mixture())[k]
+    return out
+
+
 def compute():
+    MAKERS.update(_ms_makers())
     out = {}
     for name, mk in MAKERS.items():
         fps = set()
