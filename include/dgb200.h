@@ -121,9 +121,9 @@ int dgb_ns_rhs_rk(const dgb_disc* disc, const double* q_dev, const double* gradq
  *      FunctionDefinition, adfg.py:722-803).  dgb_disc_set_jacobian binds the volume Jacobian
  *      jac (E) the two functions take as an argument and derives the face Jacobians
  *      fscale*jac and 1/jac on the device; call it once per handle before dgb_ns_flux.
- *   T      (dim*C + 1, E, Np)   planes r*C + c: sum_x jac*drdx[r,x] * (F_inv - F_visc)[x][c] with the BR1
+ *   T      ((dim+1)*C + 1, E, Np)   planes r*C + c (r < dim): sum_x jac*drdx[r,x] * (F_inv - F_visc)[x][c] with the BR1
  *                               gradient of pass 1 folded in; last plane: wave speed |u| + c
- *   Tghost (dim*C + 1, G, Np) or NULL: the same planes of the halo elements (already scaled by
+ *   Tghost ((dim+1)*C + 1, G, Np) or NULL: the same planes of the halo elements (already scaled by
  *                               the sender's Jacobian, so no remote geometry is needed)
  *   all device arrays 16-byte aligned.
  */

@@ -289,6 +289,13 @@ class MultispeciesOperator:
         return self._flux(q, ghost, d.Sw, d.drdx, d.jac, d.lift, d.normals, d.fscale, d.vmap_m, d.vmap_p, d.bc_kind,
                           self.qfar, self.transport)
 
+    def div(self, q, T, ghost=None, Tghost=None) -> DOFArray:
+        """Pass 2 from the flux planes ``T`` of pass 1 (and, on a partitioned mesh, the ghost arrays of both)."""
+        d = self.dcoll
+        q = q.data if isinstance(q, DOFArray) else q
+        return DOFArray(self.actx, self._div(q, T, ghost, Tghost, d.Sw, d.jac, d.lift, d.normals, d.fscale, d.facemat,
+                                             d.facemat_p, d.vmap_m, d.vmap_p, d.bc_kind, self.qfar))
+
     def rhs(self, q: DOFArray, t=0.0, ghost=None, halo_fn=None) -> DOFArray:
         """Single domain: ``rhs(q)``.  Partitioned: ``ghost`` = halo of ``q`` and ``halo_fn(DOFArray of the flux
         planes) -> their halo`` (second exchange), like ``NavierStokesOperator.rhs``."""
