@@ -30,6 +30,9 @@ VARIANTS = {
     "d12_nb2_cg": ["DGB_DIV8_WARPS=12", "DGB_DIV8_NB=2", "DGB_GATHER_LD=1"],
     "d12_nb4_cg": ["DGB_DIV8_WARPS=12", "DGB_DIV8_NB=4", "DGB_GATHER_LD=1"],
     "d10_nb2": ["DGB_DIV8_WARPS=10", "DGB_DIV8_NB=2"],
+    "nb2": ["DGB_DIV8_NB=2"],
+    "nb3": ["DGB_DIV8_NB=3"],
+    "pf2": ["DGB_FLUX_PREFETCH2=1"],
     "k3": ["DGB_DIV_KERNEL_DEFAULT=3"],
     "w8": ["DGB_DIV8_WARPS=8"],
     "w8_nb1": ["DGB_DIV8_WARPS=8", "DGB_DIV_NB=1"],
@@ -60,7 +63,7 @@ def main():
         from paper_2512_17101_b200.csrc.build import FLAGS, HERE
         cflags = [f for f in FLAGS if f != "-shared"] + (["-DDGB_ONLY_3D_P3"] if "--p3only" in sys.argv else [])
         objs = []
-        for src in ("dgb200.cu", "dgb_arrayops.cu"):
+        for src in ("dgb200.cu", "dgb_arrayops.cu", "dgb_msflux.cu"):
             obj = os.path.join("/tmp", src.replace(".cu", ".o"))
             if not os.path.exists(obj) or os.path.getmtime(obj) < max(
                     os.path.getmtime(os.path.join(HERE, f)) for f in os.listdir(HERE) if f.endswith((".cu", ".cuh", ".h"))):
