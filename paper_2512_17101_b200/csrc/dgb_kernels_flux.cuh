@@ -100,6 +100,21 @@ __device__ __forceinline__ long long ticket_block(unsigned long long v, long lon
   return first_dynamic + (long long)__shfl_sync(0xffffffffu, v, 0);
 }
 
+// ptxas turns a predicated atomic on a warp-uniform address into a warp-aggregated one: leader election, ATOMG,
+// and a SHFL of the result RIGHT AFTER it -- which makes the warp wait for the L2 round trip at the draw and defeats
+// the split-phase scheme (ncu: 2.7 % of pass 1's stall samples sit on that SHFL).  An address ptxas cannot prove
+// uniform keeps the atomic a plain single-lane ATOMG: the offset below comes from shared memory and is always 0.
+#ifndef DGB_TICKET_NOAGG
+#define DGB_TICKET_NOAGG 1
+#endif
+__device__ __forceinline__ unsigned long long* ticket_counter(unsigned long long* counter, const int* table, int lane) {
+#if DGB_TICKET_NOAGG
+  return counter + (table[lane & 1] >> 24);           // face-node indices are < 256
+#else
+  return counter;
+#endif
+}
+
 // Tickets in batches of DGB_TICKET_BLOCKS consecutive blocks: one atomic on the (single, hot) work counter
 // per batch instead of per block.  With ~1200 warps drawing a ticket every ~6 us the counter's L2 slice
 // serialises ~200 same-address atomics per microsecond and a ticket drawn a whole block earlier was
@@ -336,7 +351,7 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
   }
   cp_async_commit();
   TicketStream tks;
-  tickets_init(tks, wb, counter, lane);
+  tickets_init(tks, wb, ticket_counter(counter, S.fn, lane), lane);
   DGB_WTICK_INIT
   // Neighbour states of ALL face nodes of a block, issued one phase early (during the pointwise flux
   // phase of the previous block, which is FP64 work and leaves the L1/LSU pipe to the gathers) and
@@ -388,7 +403,7 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
     const long long e0 = ebeg + wb * KW;
     const int nel = (int)((eend - e0) < (long long)KW ? (eend - e0) : (long long)KW);
     // the next block (its ticket was drawn one block ago) starts its trip from HBM now
-    const long long wb_next = tickets_next(tks, wstride, counter, lane);
+    const long long wb_next = tickets_next(tks, wstride, ticket_counter(counter, S.fn, lane), lane);
     cp_async_wait<0>();
     __syncwarp();
     const double* Qs = W.Qs[buf];
@@ -880,7 +895,7 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
     cp_async_commit();
   }
   TicketStream tks;
-  tickets_init(tks, wb, counter, lane);
+  tickets_init(tks, wb, ticket_counter(counter, S.fn, lane), lane);
 
   // cp.async groups retire in order: S(b), T(b), S(b+1), T(b+1), ...
   constexpr bool SS = DGB_DIV_SINGLE_SMALL != 0;
@@ -888,7 +903,7 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
   while (wb < nwblocks) {
     const long long e0 = ebeg + wb * KW;
     const int nel = (int)((eend - e0) < (long long)KW ? (eend - e0) : (long long)KW);
-    const long long wb_next = tickets_next(tks, wstride, counter, lane);
+    const long long wb_next = tickets_next(tks, wstride, ticket_counter(counter, S.fn, lane), lane);
     const long long e1 = ebeg + wb_next * KW;
     const int nel1 = wb_next < nwblocks ? (int)((eend - e1) < (long long)KW ? (eend - e1) : (long long)KW) : 0;
     if (!SS) {
@@ -1077,13 +1092,13 @@ k_euler4(DiscDev d, const double* __restrict__ q, const double* __restrict__ gho
   euler4_stage<DIM, P, KW>(W.Qs, W.geo[0], d, q, ebeg + wb * KW, nel_of(wb), lane);
   cp_async_commit();
   TicketStream tks;
-  tickets_init(tks, wb, counter, lane);
+  tickets_init(tks, wb, ticket_counter(counter, S.fn, lane), lane);
 
   for (int i = 0;; ++i) {
     const int buf = i & 1;
     const long long e0 = ebeg + wb * KW;
     const int nel = nel_of(wb);
-    const long long wb_next = tickets_next(tks, wstride, counter, lane);
+    const long long wb_next = tickets_next(tks, wstride, ticket_counter(counter, S.fn, lane), lane);
     const int nel1 = nel_of(wb_next);
     cp_async_wait<0>();                  // this block's rows + geometry have landed (staged during the previous contraction)
     __syncwarp();

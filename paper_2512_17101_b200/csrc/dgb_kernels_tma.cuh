@@ -313,13 +313,13 @@ k_nsdiv8(DiscDev d, const __grid_constant__ CUtensorMap map_q, const __grid_cons
     cp_async_commit();
   }
   TicketStream tks;
-  tickets_init(tks, wb, counter, lane);
+  tickets_init(tks, wb, ticket_counter(counter, S.fn, lane), lane);
 
   for (int it = 0;; ++it) {
     const int buf = it & 1, par = it & 1;
     const long long e0 = ebeg + wb * KW;
     const int nel = nel_of(wb);
-    const long long wb_next = tickets_next(tks, wstride, counter, lane);
+    const long long wb_next = tickets_next(tks, wstride, ticket_counter(counter, S.fn, lane), lane);
     const int nel1 = nel_of(wb_next);
     const long long e1 = ebeg + wb_next * KW;
     if (nel1 > 0) stage_geo(W.geo[buf ^ 1], e1, nel1);
