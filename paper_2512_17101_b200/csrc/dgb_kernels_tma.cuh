@@ -17,6 +17,12 @@
 #pragma once
 #include "dgb_kernels_flux.cuh"
 
+// 1: gathers of a whole block in flight under the volume half of the contraction (needs every round in flight).
+// Measured slower (n=94: pass 2 6.57 vs 6.37 ms, profiles/r02_pass2_tma.md section 8): the operand loads of the
+// DMMA loop and the returning gathers share the L1/LSU pipe; off.
+#ifndef DGB_DIV8_SPLIT
+#define DGB_DIV8_SPLIT 0
+#endif
 #ifndef DGB_DIV8_NB
 #define DGB_DIV8_NB 0              // 0: every round of a block in flight together (8 warps) / one round (more warps)
 #endif
@@ -113,6 +119,94 @@ __device__ __forceinline__ int lean_round_word(int flk) {
 // Lean face phase (pass 2): the neighbour's node comes from the precomputed gather map instead of being decoded
 // from the connectivity word through the face-node / permutation tables, every lane carries its per-round
 // constants in one register, and a face selects ONE plane group of T.  Same arithmetic as div_face_phase.
+// the two halves of the lean face phase for rounds [k0, k0 + NB): issue the gathers / turn them into operand rows
+template <int DIM, int P, int KW, int NB, bool GH>
+__device__ __forceinline__ void face_lean_issue(int k0, const int (&rw)[face_rounds<DIM, P, KW>()], const Div8Geo<DIM, P, KW>& g,
+                                                const DiscDev& d, const double* __restrict__ q, const double* __restrict__ T,
+                                                const double* __restrict__ ghost, const double* __restrict__ Tghost,
+                                                long long e0, int nel, double (&qp)[NB][ElemT<DIM, P>::C],
+                                                double (&nbr)[NB][ElemT<DIM, P>::C], double (&lam_p)[NB], int (&hi)[NB]) {
+  using EL = ElemT<DIM, P>;
+  constexpr int C = EL::C, NP = EL::NP;
+  constexpr int NR = face_rounds<DIM, P, KW>();
+  constexpr int LAMPL = FluxT<DIM, P>::LAMPL;
+  const long long ps_own = d.E * NP;
+  const unsigned enp = (unsigned)ps_own;
+  const long long* connf = &g.conn[0][0];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    hi[b] = -1;                      // upper half of the connectivity word (neighbour face, bc kind); < 0: nothing to do
+    if (k0 + b < NR) {
+      const int w = rw[k0 + b];
+      if (w >= 0 && ((w >> 28) & 3) < nel) {
+#ifdef DGB_EXP_LOCALGATHER
+        const unsigned gi = (unsigned)(e0 * NP) + ((w >> 12) & 255);      // timing experiment: own node
+#else
+        const unsigned gi = g.gi[w & 255];
+#endif
+        hi[b] = (int)(connf[(w >> 8) & 15] >> 32);
+        const int nf = hi[b] & 7;
+        const int grp = nf == 0 ? DIM : nf - 1;
+        const bool in_ghost = GH && gi >= enp;
+        const long long ps = in_ghost ? d.G * NP : ps_own;
+        const double* qb = in_ghost ? ghost + (gi - enp) : q + gi;
+        const double* tb = in_ghost ? Tghost + (gi - enp) : T + gi;
+        const double* tg = tb + (long long)(grp * C) * ps;
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          qp[b][c] = DGB_GLD(qb + c * ps);
+          nbr[b][c] = DGB_GLD(tg + c * ps);
+        }
+        lam_p[b] = DGB_GLD(tb + LAMPL * ps);
+      }
+    }
+  }
+}
+
+template <int DIM, int P, int KW, int NB>
+__device__ __forceinline__ void face_lean_consume(int k0, const int (&rw)[face_rounds<DIM, P, KW>()], const Div8Geo<DIM, P, KW>& g,
+                                                  const double* __restrict__ Qb, const double* __restrict__ Lam,
+                                                  double* __restrict__ Fs, const DiscDev& d, const double* __restrict__ T,
+                                                  const Phys& ph, long long e0, const double (&qp)[NB][ElemT<DIM, P>::C],
+                                                  const double (&nbr)[NB][ElemT<DIM, P>::C], const double (&lam_p)[NB],
+                                                  const int (&hi)[NB]) {
+  using EL = ElemT<DIM, P>;
+  constexpr int C = EL::C, NP = EL::NP, NF = EL::NF;
+  constexpr int NR = face_rounds<DIM, P, KW>();
+  constexpr int BOXW = TmaBox<DIM, P, KW>::BOXW;
+  const long long ps_own = d.E * NP;
+  const double* sjf = &g.sj[0][0];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    if (k0 + b < NR && hi[b] >= 0) {
+      const int w = rw[k0 + b];
+      const int cofs = (w >> 8) & 15, qofs = (w >> 12) & 255, fofs = (w >> 20) & 255;
+      const int nf = hi[b] & 7, bc = (hi[b] >> 6) & 3;
+      const double sj = sjf[cofs];
+      const double lam_m = Lam[qofs];
+      double qm[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) qm[c] = Qb[c * BOXW + qofs];
+      double* fs = Fs + fofs;
+      if (bc == 0) {
+        const double hs = nf == 0 ? 0.5 : -0.5;
+        const double pen = 0.5 * (sj * fmax(lam_m, lam_p[b]));
+#pragma unroll
+        for (int c = 0; c < C; ++c) fs[c * (KW * EL::LDF)] = hs * nbr[b][c] - pen * (qm[c] - qp[b][c]);
+      } else {
+        const int e = (w >> 28) & 3, f = cofs - e * NF, jm = qofs - e * NP;
+        VecC<DIM> a_;
+#pragma unroll
+        for (int c = 0; c < C; ++c) a_.v[c] = qm[c];
+        const VecC<DIM> fb = boundary_operand<DIM>(bc, f, a_, T + (e0 + e) * NP + jm, ps_own, lam_m, sj,
+                                                   d.normals + (e0 + e) * NF + f, d.E * NF, ph);
+#pragma unroll
+        for (int c = 0; c < C; ++c) fs[c * (KW * EL::LDF)] = fb.v[c];
+      }
+    }
+  }
+}
+
 template <int DIM, int P, int KW, int NB, bool GH>
 __device__ __forceinline__ void div_face_lean(const int (&rw)[face_rounds<DIM, P, KW>()], const Div8Geo<DIM, P, KW>& g,
                                               const double* __restrict__ Qb, const double* __restrict__ Lam,
@@ -120,76 +214,14 @@ __device__ __forceinline__ void div_face_lean(const int (&rw)[face_rounds<DIM, P
                                               const double* __restrict__ q, const double* __restrict__ T,
                                               const double* __restrict__ ghost, const double* __restrict__ Tghost,
                                               const Phys& ph, long long e0, int nel) {
-  using EL = ElemT<DIM, P>;
-  constexpr int C = EL::C, NP = EL::NP, NF = EL::NF;
+  constexpr int C = ElemT<DIM, P>::C;
   constexpr int NR = face_rounds<DIM, P, KW>();
-  constexpr int BOXW = TmaBox<DIM, P, KW>::BOXW;
-  constexpr int LAMPL = FluxT<DIM, P>::LAMPL;
-  const long long ps_own = d.E * NP;
-  const unsigned enp = (unsigned)ps_own;
-  const long long* connf = &g.conn[0][0];
-  const double* sjf = &g.sj[0][0];
 #pragma unroll
   for (int k0 = 0; k0 < NR; k0 += NB) {          // unrolled: rw[] stays in registers
     double qp[NB][C], nbr[NB][C], lam_p[NB];
-    int hi[NB];                      // upper half of the connectivity word (neighbour face, bc kind); < 0: nothing to do
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      hi[b] = -1;
-      if (k0 + b < NR) {
-        const int w = rw[k0 + b];
-        if (w >= 0 && ((w >> 28) & 3) < nel) {
-#ifdef DGB_EXP_LOCALGATHER
-          const unsigned gi = (unsigned)(e0 * NP) + ((w >> 12) & 255);      // timing experiment: own node
-#else
-          const unsigned gi = g.gi[w & 255];
-#endif
-          hi[b] = (int)(connf[(w >> 8) & 15] >> 32);
-          const int nf = hi[b] & 7;
-          const int grp = nf == 0 ? DIM : nf - 1;
-          const bool in_ghost = GH && gi >= enp;
-          const long long ps = in_ghost ? d.G * NP : ps_own;
-          const double* qb = in_ghost ? ghost + (gi - enp) : q + gi;
-          const double* tb = in_ghost ? Tghost + (gi - enp) : T + gi;
-          const double* tg = tb + (long long)(grp * C) * ps;
-#pragma unroll
-          for (int c = 0; c < C; ++c) {
-            qp[b][c] = DGB_GLD(qb + c * ps);
-            nbr[b][c] = DGB_GLD(tg + c * ps);
-          }
-          lam_p[b] = DGB_GLD(tb + LAMPL * ps);
-        }
-      }
-    }
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      if (k0 + b < NR && hi[b] >= 0) {
-        const int w = rw[k0 + b];
-        const int cofs = (w >> 8) & 15, qofs = (w >> 12) & 255, fofs = (w >> 20) & 255;
-        const int nf = hi[b] & 7, bc = (hi[b] >> 6) & 3;
-        const double sj = sjf[cofs];
-        const double lam_m = Lam[qofs];
-        double qm[C];
-#pragma unroll
-        for (int c = 0; c < C; ++c) qm[c] = Qb[c * BOXW + qofs];
-        double* fs = Fs + fofs;
-        if (bc == 0) {
-          const double hs = nf == 0 ? 0.5 : -0.5;
-          const double pen = 0.5 * (sj * fmax(lam_m, lam_p[b]));
-#pragma unroll
-          for (int c = 0; c < C; ++c) fs[c * (KW * EL::LDF)] = hs * nbr[b][c] - pen * (qm[c] - qp[b][c]);
-        } else {
-          const int e = (w >> 28) & 3, f = cofs - e * NF, jm = qofs - e * NP;
-          VecC<DIM> a_;
-#pragma unroll
-          for (int c = 0; c < C; ++c) a_.v[c] = qm[c];
-          const VecC<DIM> fb = boundary_operand<DIM>(bc, f, a_, T + (e0 + e) * NP + jm, ps_own, lam_m, sj,
-                                                     d.normals + (e0 + e) * NF + f, d.E * NF, ph);
-#pragma unroll
-          for (int c = 0; c < C; ++c) fs[c * (KW * EL::LDF)] = fb.v[c];
-        }
-      }
-    }
+    int hi[NB];
+    face_lean_issue<DIM, P, KW, NB, GH>(k0, rw, g, d, q, T, ghost, Tghost, e0, nel, qp, nbr, lam_p, hi);
+    face_lean_consume<DIM, P, KW, NB>(k0, rw, g, Qb, Lam, Fs, d, T, ph, e0, qp, nbr, lam_p, hi);
   }
 }
 
@@ -324,14 +356,43 @@ k_nsdiv8(DiscDev d, const __grid_constant__ CUtensorMap map_q, const __grid_cons
     const long long e1 = ebeg + wb_next * KW;
     if (nel1 > 0) stage_geo(W.geo[buf ^ 1], e1, nel1);
     cp_async_commit();
-    cp_async_wait<1>();                  // geometry of this block
-    mbar_wait_(&W.bar_q, par);           // state + wave speed of this block
+    cp_async_wait<1>();                  // gather map, connectivity, face Jacobians of this block
     __syncwarp();
     const int sh = BX::box_shift(e0);
-#ifndef DGB_EXP_NOFACE            // timing experiments only (results invalid)
-    div_face_lean<DIM, P, KW, NB, GH>(rw, W.geo[buf], W.Qb + sh, W.Lam + sh, W.Fs, d, q, T, ghost, Tghost, ph, e0, nel);
-#endif
+    constexpr bool SPLIT = (DGB_DIV8_SPLIT != 0) && NB >= NR;      // every round in flight: gathers under the volume contraction
+    double acc[WS::NTILE][EL::NI][2];
+#pragma unroll
+    for (int mt = 0; mt < WS::NTILE; ++mt)
+#pragma unroll
+      for (int ni = 0; ni < EL::NI; ++ni) { acc[mt][ni][0] = 0.0; acc[mt][ni][1] = 0.0; }
     double rj[WS::NTILE];
+    if (SPLIT) {
+      // The gathers need only the gather map and the connectivity; the volume half of the contraction needs only the
+      // flux-plane box.  So: all gathers of the block in flight -> volume DMMA (K = dim*Np) while they fly ->
+      // Rusanov from the gathered values and the state box -> lift DMMA (K = Nf*Nfp).
+      double qp[NB][C], nbr[NB][C], lam_p[NB];
+      int hi[NB];
+#ifndef DGB_EXP_NOFACE
+      face_lean_issue<DIM, P, KW, NB, GH>(0, rw, W.geo[buf], d, q, T, ghost, Tghost, e0, nel, qp, nbr, lam_p, hi);
+#endif
+      mbar_wait_(&W.bar_t, par);         // flux planes of this block
+#ifndef DGB_EXP_NOMMA
+#pragma unroll
+      for (int r = 0; r < DIM; ++r)
+        mma_block_off<EL::NI, WS::NTILE>(acc, W.Tb + r * (C * BOXW) + sh, aoff, S.Wv + r * EL::NPK, EL::LDV, EL::NPK / 4, lane);
+#endif
+      __syncwarp();                      // flux-plane rows consumed
+      if (nel1 > 0 && lane == 0) issue_t(e1);
+      mbar_wait_(&W.bar_q, par);         // state + wave speed of this block
+#ifndef DGB_EXP_NOFACE
+      face_lean_consume<DIM, P, KW, NB>(0, rw, W.geo[buf], W.Qb + sh, W.Lam + sh, W.Fs, d, T, ph, e0, qp, nbr, lam_p, hi);
+#endif
+    } else {
+      mbar_wait_(&W.bar_q, par);         // state + wave speed of this block
+#ifndef DGB_EXP_NOFACE            // timing experiments only (results invalid)
+      div_face_lean<DIM, P, KW, NB, GH>(rw, W.geo[buf], W.Qb + sh, W.Lam + sh, W.Fs, d, q, T, ghost, Tghost, ph, e0, nel);
+#endif
+    }
 #pragma unroll
     for (int mt = 0; mt < WS::NTILE; ++mt) rj[mt] = W.geo[buf].rj[(mt * 8 + (lane >> 2)) % KW];
 #if DGB_NSPEC > 0
@@ -348,24 +409,22 @@ k_nsdiv8(DiscDev d, const __grid_constant__ CUtensorMap map_q, const __grid_cons
 #endif
     __syncwarp();                        // every lane has read the state box: the next one may land on it
     if (nel1 > 0 && lane == 0) issue_q(e1);
-    mbar_wait_(&W.bar_t, par);           // flux planes of this block
-
-    // ---- tensor-core contraction: volume rows straight from the box, then the face operand rows ----
-    double acc[WS::NTILE][EL::NI][2];
-#pragma unroll
-    for (int mt = 0; mt < WS::NTILE; ++mt)
-#pragma unroll
-      for (int ni = 0; ni < EL::NI; ++ni) { acc[mt][ni][0] = 0.0; acc[mt][ni][1] = 0.0; }
+    if (!SPLIT) {
+      mbar_wait_(&W.bar_t, par);         // flux planes of this block
 #ifndef DGB_EXP_NOMMA
 #pragma unroll
-    for (int r = 0; r < DIM; ++r)
-      mma_block_off<EL::NI, WS::NTILE>(acc, W.Tb + r * (C * BOXW) + sh, aoff, S.Wv + r * EL::NPK, EL::LDV, EL::NPK / 4, lane);
+      for (int r = 0; r < DIM; ++r)
+        mma_block_off<EL::NI, WS::NTILE>(acc, W.Tb + r * (C * BOXW) + sh, aoff, S.Wv + r * EL::NPK, EL::LDV, EL::NPK / 4, lane);
+#endif
+    }
+    // ---- the face operand rows: lift part of the contraction ----
+#ifndef DGB_EXP_NOMMA
     mma_block_off<EL::NI, WS::NTILE>(acc, W.Fs, foff, S.Wl, EL::LDF, EL::KF / 4, lane);
 #else
     acc[0][0][0] = W.Tb[aoff[0] + sh + lane] + W.Fs[foff[0] + lane];
 #endif
     __syncwarp();                        // operand rows consumed
-    if (nel1 > 0 && lane == 0) issue_t(e1);
+    if (!SPLIT && nel1 > 0 && lane == 0) issue_t(e1);
 
 #pragma unroll
     for (int mt = 0; mt < WS::NTILE; ++mt) {
