@@ -17,11 +17,11 @@
 #pragma once
 #include "dgb_kernels_flux.cuh"
 
-// 1: gathers of a whole block in flight under the volume half of the contraction (needs every round in flight).
-// Measured slower (n=94: pass 2 6.57 vs 6.37 ms, profiles/r02_pass2_tma.md section 8): the operand loads of the
-// DMMA loop and the returning gathers share the L1/LSU pipe; off.
-#ifndef DGB_DIV8_SPLIT
-#define DGB_DIV8_SPLIT 0
+// The schedule "gathers -> volume half of the contraction -> Rusanov -> lift half" was measured in round 2 (slower:
+// pass 2 6.57 vs 6.37 ms at n=94, profiles/r02_pass2_tma.md section 8) and removed.
+// 1: the gathers of the next block are issued before the store epilogue of the current one (every round in flight)
+#ifndef DGB_DIV8_EARLY
+#define DGB_DIV8_EARLY 1
 #endif
 #ifndef DGB_DIV8_NB
 #define DGB_DIV8_NB 0              // 0: every round of a block in flight together (8 warps) / one round (more warps)
@@ -338,11 +338,23 @@ k_nsdiv8(DiscDev d, const __grid_constant__ CUtensorMap map_q, const __grid_cons
   const long long wstride = (long long)gridDim.x * NWARPS;
   long long wb = (long long)blockIdx.x * NWARPS + warp;
   if (wb >= nwblocks) return;
+  // EARLY: the gathers of block b+1 are issued right after the contraction of block b, before its store epilogue,
+  // and consumed at the top of the next iteration -- their L2 round trip (ncu: 17 % of the stall samples sit on the
+  // first use of a gathered value) runs under the epilogue, the ticket, the staging and the mbarrier waits.
+  constexpr bool EARLY = (DGB_DIV8_EARLY != 0) && NB >= NR;
+  constexpr int NG = EARLY ? NB : 1;
+  double gqp[NG][C], gnb[NG][C], glam[NG];
+  int ghi[NG];
   {
     const long long e0 = ebeg + wb * KW;
     if (lane == 0) { issue_q(e0); issue_t(e0); }
     stage_geo(W.geo[0], e0, nel_of(wb));
     cp_async_commit();
+    if (EARLY) {
+      cp_async_wait<0>();
+      __syncwarp();
+      face_lean_issue<DIM, P, KW, NG, GH>(0, rw, W.geo[0], d, q, T, ghost, Tghost, e0, nel_of(wb), gqp, gnb, glam, ghi);
+    }
   }
   TicketStream tks;
   tickets_init(tks, wb, ticket_counter(counter, S.fn, lane), lane);
@@ -356,43 +368,19 @@ k_nsdiv8(DiscDev d, const __grid_constant__ CUtensorMap map_q, const __grid_cons
     const long long e1 = ebeg + wb_next * KW;
     if (nel1 > 0) stage_geo(W.geo[buf ^ 1], e1, nel1);
     cp_async_commit();
-    cp_async_wait<1>();                  // gather map, connectivity, face Jacobians of this block
-    __syncwarp();
+    if (!EARLY) {
+      cp_async_wait<1>();                // gather map, connectivity, face Jacobians of this block
+      __syncwarp();
+    }
     const int sh = BX::box_shift(e0);
-    constexpr bool SPLIT = (DGB_DIV8_SPLIT != 0) && NB >= NR;      // every round in flight: gathers under the volume contraction
-    double acc[WS::NTILE][EL::NI][2];
-#pragma unroll
-    for (int mt = 0; mt < WS::NTILE; ++mt)
-#pragma unroll
-      for (int ni = 0; ni < EL::NI; ++ni) { acc[mt][ni][0] = 0.0; acc[mt][ni][1] = 0.0; }
-    double rj[WS::NTILE];
-    if (SPLIT) {
-      // The gathers need only the gather map and the connectivity; the volume half of the contraction needs only the
-      // flux-plane box.  So: all gathers of the block in flight -> volume DMMA (K = dim*Np) while they fly ->
-      // Rusanov from the gathered values and the state box -> lift DMMA (K = Nf*Nfp).
-      double qp[NB][C], nbr[NB][C], lam_p[NB];
-      int hi[NB];
-#ifndef DGB_EXP_NOFACE
-      face_lean_issue<DIM, P, KW, NB, GH>(0, rw, W.geo[buf], d, q, T, ghost, Tghost, e0, nel, qp, nbr, lam_p, hi);
-#endif
-      mbar_wait_(&W.bar_t, par);         // flux planes of this block
-#ifndef DGB_EXP_NOMMA
-#pragma unroll
-      for (int r = 0; r < DIM; ++r)
-        mma_block_off<EL::NI, WS::NTILE>(acc, W.Tb + r * (C * BOXW) + sh, aoff, S.Wv + r * EL::NPK, EL::LDV, EL::NPK / 4, lane);
-#endif
-      __syncwarp();                      // flux-plane rows consumed
-      if (nel1 > 0 && lane == 0) issue_t(e1);
-      mbar_wait_(&W.bar_q, par);         // state + wave speed of this block
-#ifndef DGB_EXP_NOFACE
-      face_lean_consume<DIM, P, KW, NB>(0, rw, W.geo[buf], W.Qb + sh, W.Lam + sh, W.Fs, d, T, ph, e0, qp, nbr, lam_p, hi);
-#endif
-    } else {
-      mbar_wait_(&W.bar_q, par);         // state + wave speed of this block
-#ifndef DGB_EXP_NOFACE            // timing experiments only (results invalid)
+    mbar_wait_(&W.bar_q, par);           // state + wave speed of this block
+#ifndef DGB_EXP_NOFACE              // timing experiments only (results invalid)
+    if (EARLY)
+      face_lean_consume<DIM, P, KW, NG>(0, rw, W.geo[buf], W.Qb + sh, W.Lam + sh, W.Fs, d, T, ph, e0, gqp, gnb, glam, ghi);
+    else
       div_face_lean<DIM, P, KW, NB, GH>(rw, W.geo[buf], W.Qb + sh, W.Lam + sh, W.Fs, d, q, T, ghost, Tghost, ph, e0, nel);
 #endif
-    }
+    double rj[WS::NTILE];
 #pragma unroll
     for (int mt = 0; mt < WS::NTILE; ++mt) rj[mt] = W.geo[buf].rj[(mt * 8 + (lane >> 2)) % KW];
 #if DGB_NSPEC > 0
@@ -409,22 +397,31 @@ k_nsdiv8(DiscDev d, const __grid_constant__ CUtensorMap map_q, const __grid_cons
 #endif
     __syncwarp();                        // every lane has read the state box: the next one may land on it
     if (nel1 > 0 && lane == 0) issue_q(e1);
-    if (!SPLIT) {
-      mbar_wait_(&W.bar_t, par);         // flux planes of this block
+    mbar_wait_(&W.bar_t, par);           // flux planes of this block
+
+    // ---- tensor-core contraction: volume rows straight from the box, then the face operand rows ----
+    double acc[WS::NTILE][EL::NI][2];
+#pragma unroll
+    for (int mt = 0; mt < WS::NTILE; ++mt)
+#pragma unroll
+      for (int ni = 0; ni < EL::NI; ++ni) { acc[mt][ni][0] = 0.0; acc[mt][ni][1] = 0.0; }
 #ifndef DGB_EXP_NOMMA
 #pragma unroll
-      for (int r = 0; r < DIM; ++r)
-        mma_block_off<EL::NI, WS::NTILE>(acc, W.Tb + r * (C * BOXW) + sh, aoff, S.Wv + r * EL::NPK, EL::LDV, EL::NPK / 4, lane);
-#endif
-    }
-    // ---- the face operand rows: lift part of the contraction ----
-#ifndef DGB_EXP_NOMMA
+    for (int r = 0; r < DIM; ++r)
+      mma_block_off<EL::NI, WS::NTILE>(acc, W.Tb + r * (C * BOXW) + sh, aoff, S.Wv + r * EL::NPK, EL::LDV, EL::NPK / 4, lane);
     mma_block_off<EL::NI, WS::NTILE>(acc, W.Fs, foff, S.Wl, EL::LDF, EL::KF / 4, lane);
 #else
     acc[0][0][0] = W.Tb[aoff[0] + sh + lane] + W.Fs[foff[0] + lane];
 #endif
     __syncwarp();                        // operand rows consumed
-    if (!SPLIT && nel1 > 0 && lane == 0) issue_t(e1);
+    if (nel1 > 0 && lane == 0) issue_t(e1);
+    if (EARLY && nel1 > 0) {
+      cp_async_wait<0>();                // gather map + connectivity of the next block (staged at the top of this one)
+      __syncwarp();
+#ifndef DGB_EXP_NOFACE
+      face_lean_issue<DIM, P, KW, NG, GH>(0, rw, W.geo[buf ^ 1], d, q, T, ghost, Tghost, e1, nel1, gqp, gnb, glam, ghi);
+#endif
+    }
 
 #pragma unroll
     for (int mt = 0; mt < WS::NTILE; ++mt) {

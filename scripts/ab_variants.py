@@ -33,7 +33,7 @@ VARIANTS = {
     "nb2": ["DGB_DIV8_NB=2"],
     "nb3": ["DGB_DIV8_NB=3"],
     "pf2": ["DGB_FLUX_PREFETCH2=1"],
-    "nosplit": ["DGB_DIV8_SPLIT=0"],
+    "noearly": ["DGB_DIV8_EARLY=0"],
     "agg": ["DGB_TICKET_NOAGG=0"],
     "k3": ["DGB_DIV_KERNEL_DEFAULT=3"],
     "w8": ["DGB_DIV8_WARPS=8"],
