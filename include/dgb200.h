@@ -169,6 +169,12 @@ int dgb_ms_div_range(const dgb_disc* disc, const double* q_dev, const double* T_
                      const double* qfar_host, const double* transport_host, const double* mixture_host,
                      int64_t ebegin, int64_t eend, void* stream);
 
+/* the same with the RK stage update fused into the store (north-star item 3), like dgb_ns_div_rk */
+int dgb_ms_div_rk(const dgb_disc* disc, const double* q_dev, const double* T_dev,
+                  const double* ghost_dev, const double* Tghost_dev,
+                  const double* x1_dev, double* out1_dev, const double* x2_dev, double* out2_dev, const double* rk_host,
+                  const double* qfar_host, const double* transport_host, const double* mixture_host, void* stream);
+
 /* ---- halo packing: element rows <-> contiguous message (Send / Receive payloads,
  *      adfg.py:380-399,834-869).  dst[c, i, :] = src[c, elems[i], :]                        ---- */
 int dgb_pack_elements(double* dst_dev, const double* src_dev, const int64_t* elems_dev,

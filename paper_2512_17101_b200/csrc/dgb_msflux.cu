@@ -47,16 +47,14 @@ int dgb_ms_flux_range(const dgb_disc* d, const double* q, const double* ghost, d
   return dgb_fail(DGB_ERR_INVALID, "unsupported (dim, order)");
 }
 
-int dgb_ms_div_range(const dgb_disc* d, const double* q, const double* T, const double* ghost, const double* Tghost,
-                     double* rhs, const double* qfar, const double* transport, const double* mixture,
-                     int64_t ebegin, int64_t eend, void* stream) {
+static int ms_div_impl(const dgb_disc* d, const double* q, const double* T, const double* ghost, const double* Tghost,
+                       const dgb::Epilogue& ep, const double* qfar, const double* transport, const double* mixture,
+                       int64_t ebegin, int64_t eend, void* stream) {
   int rc = check_flux_args(d, ghost, q, T); if (rc) return rc;
-  if (!rhs) return dgb_fail(DGB_ERR_INVALID, "null output");
   if (eend < 0) eend = d->dev.E;
   if ((rc = check_range(d, ebegin, eend))) return rc;
   if (d->dev.G > 0 && !Tghost) return dgb_fail(DGB_ERR_INVALID, "ghost elements need the ghost flux planes");
   dgb::Phys ph; if ((rc = make_ms_phys(ph, d->dim, qfar, transport, mixture))) return rc;
-  dgb::Epilogue ep{nullptr, rhs, nullptr, nullptr, 0.0, 1.0, 0.0, 0.0};
   bool ok = false;
 #define X(DIM, P) if (d->dim == DIM && d->order == P) {                                                             \
     rc = launch_div8<DIM, P>(d, q, T, ghost, Tghost, ep, ph, ebegin, eend, (cudaStream_t)stream, &ok);               \
@@ -65,6 +63,28 @@ int dgb_ms_div_range(const dgb_disc* d, const double* q, const double* T, const 
   DGB_FOR_EACH_ELEMENT(X)
 #undef X
   return dgb_fail(DGB_ERR_INVALID, "unsupported (dim, order)");
+}
+
+int dgb_ms_div_range(const dgb_disc* d, const double* q, const double* T, const double* ghost, const double* Tghost,
+                     double* rhs, const double* qfar, const double* transport, const double* mixture,
+                     int64_t ebegin, int64_t eend, void* stream) {
+  if (!rhs) return dgb_fail(DGB_ERR_INVALID, "null output");
+  dgb::Epilogue ep{nullptr, rhs, nullptr, nullptr, 0.0, 1.0, 0.0, 0.0};
+  return ms_div_impl(d, q, T, ghost, Tghost, ep, qfar, transport, mixture, ebegin, eend, stream);
+}
+
+// pass 2 with the RK stage update fused into the store: out1 = rk[0]*x1 + rk[1]*rhs, out2 = rk[2]*x2 + rk[3]*rhs
+int dgb_ms_div_rk(const dgb_disc* d, const double* q, const double* T, const double* ghost, const double* Tghost,
+                  const double* x1, double* out1, const double* x2, double* out2, const double* rk,
+                  const double* qfar, const double* transport, const double* mixture, void* stream) {
+  if (!out1 || !rk) return dgb_fail(DGB_ERR_INVALID, "out1 and rk are required");
+  if (out1 == q || (out2 && out2 == q) || (x2 && out1 == x2))
+    return dgb_fail(DGB_ERR_INVALID, "RK outputs must not alias the stage input q (neighbours still read it)");
+  if (out2 && !x2) return dgb_fail(DGB_ERR_INVALID, "out2 needs x2");
+  if ((((uintptr_t)x1) | ((uintptr_t)out1) | ((uintptr_t)x2) | ((uintptr_t)out2)) & 15)
+    return dgb_fail(DGB_ERR_INVALID, "RK operands and outputs must be 16-byte aligned");
+  dgb::Epilogue ep{x1, out1, x2, out2, rk[0], rk[1], rk[2], rk[3]};
+  return ms_div_impl(d, q, T, ghost, Tghost, ep, qfar, transport, mixture, 0, -1, stream);
 }
 
 }  // extern "C"

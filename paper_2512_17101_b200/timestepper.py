@@ -25,8 +25,8 @@ from .dofarray import DOFArray
 class DeviceRK4:
     """``stepper = DeviceRK4(op, q0, dt); stepper.step(); ...; q = stepper.state``.
 
-    ``op``: ``NavierStokesOperator`` or ``EulerOperator`` on a ``B200ArrayContext`` (single
-    partition).  ``use_graph=True`` captures one step into a CUDA graph at construction.
+    ``op``: ``NavierStokesOperator``, ``EulerOperator`` or ``MultispeciesOperator`` (3 species: the fused
+    kernels) on a ``B200ArrayContext`` (single partition).  ``use_graph=True`` captures one step into a CUDA graph at construction.
     """
 
     def __init__(self, op, q0: DOFArray, dt: float, use_graph: bool = True):
@@ -36,16 +36,25 @@ class DeviceRK4:
         self.op, self.actx, self.dt = op, actx, float(dt)
         import torch
         self._torch = torch
+        self.multi = hasattr(op, "mix")
         self.viscous = hasattr(op, "flux")
         shape = tuple(q0.data.shape)
         dim = op.dim
+        if self.multi and op.mix.ns != fused.MS_FUSED_SPECIES:
+            raise errors.LazeError("DeviceRK4 needs the fused multi-species kernels (3 species)")
         self.q = actx.empty(shape)
         self._d2d(self.q, actx._contiguous(q0.data))
         self.s1, self.s2, self.acc = actx.empty(shape), actx.empty(shape), actx.empty(shape)
-        self.T = actx.empty((fused.flux_planes(dim),) + shape[1:]) if self.viscous else None
+        npl = fused.ms_flux_planes(dim, op.mix.ns) if self.multi else fused.flux_planes(dim)
+        self.T = actx.empty((npl,) + shape[1:]) if self.viscous else None
         d = op.dcoll
         self.disc = fused.get_disc(actx, dim, self.q, 0, d.Sw, d.drdx, d.lift, d.normals, d.fscale, d.vmap_m, d.vmap_p,
-                                   d.bc_kind)
+                                   d.bc_kind, nspecies=op.mix.ns if self.multi else 0)
+        if self.multi:
+            mix = op.mix
+            self._mix = np.ascontiguousarray(np.concatenate(
+                [[mix.ns], mix.R, mix.cv, mix.h0, [mix.A, mix.Ta, mix.reaction[0], mix.reaction[1]]]).astype(np.float64))
+            self._tr = np.ascontiguousarray(np.asarray(op.transport.host_value(), dtype=np.float64).reshape(3))
         if self.viscous:
             fused._bind_jacobian(actx, self.disc, d.jac)
             fused._check_facemat(self.disc, d.facemat, d.facemat_p)
@@ -76,9 +85,18 @@ class DeviceRK4:
     def _stage(self, qin, x1, out1, x2, out2, coef):
         actx, lib, op = self.actx, self.actx.lib, self.op
         rk = np.asarray(coef, dtype=np.float64)
-        qf, ph = op.qfar_host, op.phys_host
+        qf = op.qfar_host
         o2 = out2.ptr if out2 is not None else None
         x2p = x2.ptr if x2 is not None else None
+        if self.multi:
+            tr, mx = self._tr.ctypes.data, self._mix.ctypes.data
+            _cabi.check(lib.dgb_ms_flux_range(self.disc.handle, qin.ptr, None, self.T.ptr, qf.ctypes.data, tr, mx, 0, -1,
+                                              actx._st), "dg_ms_flux")
+            _cabi.check(lib.dgb_ms_div_rk(self.disc.handle, qin.ptr, self.T.ptr, None, None, x1.ptr, out1.ptr, x2p, o2,
+                                          rk.ctypes.data, qf.ctypes.data, tr, mx, actx._st), "dg_ms_div_rk")
+            actx.launch_count += 2
+            return
+        ph = op.phys_host
         if self.viscous:
             _cabi.check(lib.dgb_ns_flux(self.disc.handle, qin.ptr, None, self.T.ptr, qf.ctypes.data, ph.ctypes.data,
                                         actx._st), "dg_ns_flux")
@@ -125,10 +143,13 @@ class DeviceRK4:
         return np.array([d.dim, d.order, d.nelements, d.Np, int(vp.sum() % (1 << 61)), int(vp[::97].sum() % (1 << 61))],
                         dtype=np.int64)
 
+    def _equations(self) -> str:
+        return "multispecies" if self.multi else ("ns" if self.viscous else "euler")
+
     def save(self, path: str) -> None:
         """Write ``q`` (host copy), the step counter and ``dt``; bit-exact restart with ``restore``."""
         np.savez(path, q=self.actx.to_numpy(self.q), nsteps=np.int64(self.nsteps), dt=np.float64(self.dt),
-                 mesh=self._fingerprint(), equations="ns" if self.viscous else "euler")
+                 mesh=self._fingerprint(), equations=self._equations())
 
     @classmethod
     def restore(cls, op, path: str, use_graph: bool = True) -> "DeviceRK4":
@@ -136,7 +157,7 @@ class DeviceRK4:
         with np.load(path) as ck:
             q, nsteps, dt, mesh, eq = ck["q"], int(ck["nsteps"]), float(ck["dt"]), ck["mesh"], str(ck["equations"])
         stepper = cls(op, DOFArray(op.actx, op.actx.from_numpy(q)), dt, use_graph=use_graph)
-        if not np.array_equal(mesh, stepper._fingerprint()) or eq != ("ns" if stepper.viscous else "euler"):
+        if not np.array_equal(mesh, stepper._fingerprint()) or eq != stepper._equations():
             raise errors.BindingMismatch("checkpoint was written for another mesh / order / equation set")
         stepper.nsteps = nsteps
         return stepper
