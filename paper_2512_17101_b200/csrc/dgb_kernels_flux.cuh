@@ -45,6 +45,13 @@
 #ifndef DGB_FLUX_PREFETCH2
 #define DGB_FLUX_PREFETCH2 0
 #endif
+// pass 1 with ONE buffer for a block's state rows where shared memory limits the number of warps (order 4: 6 -> 8
+// warps; mixtures: 7 -> 8): the next block's rows are staged right after the tensor-core phase and the pointwise phase
+// reads the state from global memory (the rows were staged a moment ago: L2 hits) instead of the buffer.
+// -1: automatic (Np > 20 or mixtures), 0 / 1: off / on
+#ifndef DGB_FLUX_SINGLEQ
+#define DGB_FLUX_SINGLEQ -1
+#endif
 #ifndef DGB_DIV_SINGLE_SMALL
 #define DGB_DIV_SINGLE_SMALL 0
 #endif
@@ -254,7 +261,9 @@ struct alignas(16) Flux3Warp {
   static constexpr int NCOL = EL::CG * KW;     // columns of the BR1 gradient: (field, element), mixtures: + temperature
   static constexpr int NTILE = (NCOL + 7) / 8;
   static constexpr int NCOLP = NTILE * 8;
-  double Qs[2][NCOLP * EL::LDQ];
+  static constexpr bool SINGLEQ = DGB_FLUX_SINGLEQ < 0 ? (EL::NP > 20 || DGB_NSPEC > 0) : (DGB_FLUX_SINGLEQ != 0);
+  static constexpr int NQB = SINGLEQ ? 1 : 2;
+  double Qs[NQB][NCOLP * EL::LDQ];
   double Ss[NCOLP * FluxT<DIM, P>::LDSX];
   double coef[KW][DIM][EL::NS];
   FluxGeo<DIM, P, KW> geo[2];
@@ -272,10 +281,9 @@ struct Flux3Smem {
 };
 
 template <int DIM, int P, int KW>
-__device__ __forceinline__ void flux_stage_async(double* Qs, FluxGeo<DIM, P, KW>& g, const DiscDev& d, const double* q,
-                                                 long long e0, int nel, int lane) {
+__device__ __forceinline__ void flux_stage_rows(double* Qs, const DiscDev& d, const double* q, long long e0, int nel, int lane) {
   using EL = ElemT<DIM, P>;
-  constexpr int C = EL::C, NP = EL::NP, NF = EL::NF;
+  constexpr int C = EL::C, NP = EL::NP;
   const long long E = d.E;
   // a block's rows are KW*NP consecutive doubles of every plane; lane t copies chunk t of each plane
   constexpr int CH = (NP % 2 == 0) ? 2 : 1, NPC = NP / CH;
@@ -293,6 +301,13 @@ __device__ __forceinline__ void flux_stage_async(double* Qs, FluxGeo<DIM, P, KW>
       }
     }
   }
+}
+
+template <int DIM, int P, int KW>
+__device__ __forceinline__ void flux_stage_geo(FluxGeo<DIM, P, KW>& g, const DiscDev& d, long long e0, int nel, int lane) {
+  using EL = ElemT<DIM, P>;
+  constexpr int NF = EL::NF;
+  const long long E = d.E;
   {
     const int e = lane % KW, rx = lane / KW;        // drdx[rx][e]
     if (KW * DIM * DIM <= 32) {
@@ -312,6 +327,13 @@ __device__ __forceinline__ void flux_stage_async(double* Qs, FluxGeo<DIM, P, KW>
   }
   if (lane < nel) cp_async8(&g.jac[lane], d.jac + e0 + lane);
   if (DGB_FLUX_LEAN) stage_gather_map<DIM, EL::NFT, EL::NFP>(g.gi, d.gidx, e0, nel, lane);
+}
+
+template <int DIM, int P, int KW>
+__device__ __forceinline__ void flux_stage_async(double* Qs, FluxGeo<DIM, P, KW>& g, const DiscDev& d, const double* q,
+                                                 long long e0, int nel, int lane) {
+  flux_stage_rows<DIM, P, KW>(Qs, d, q, e0, nel, lane);
+  flux_stage_geo<DIM, P, KW>(g, d, e0, nel, lane);
 }
 
 template <int DIM, int P, int KW, int NWARPS, bool GH>
@@ -335,7 +357,7 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
   for (int n = tid; n < NF * NFP; n += NT) S.fn[n] = d.tables[n];
   for (int n = tid; n < EL::NPERM * NFP; n += NT) S.perm[n] = d.tables[NF * NFP + n];
   WS& W = S.w[warp];
-  for (int n = lane; n < 2 * WS::NCOLP * EL::LDQ; n += 32) W.Qs[0][n] = 0.0;
+  for (int n = lane; n < WS::NQB * WS::NCOLP * EL::LDQ; n += 32) W.Qs[0][n] = 0.0;
   for (int n = lane; n < WS::NCOLP * LDSX; n += 32) W.Ss[n] = 0.0;
   __syncthreads();
 
@@ -406,7 +428,9 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
     const long long wb_next = tickets_next(tks, wstride, ticket_counter(counter, S.fn, lane), lane);
     cp_async_wait<0>();
     __syncwarp();
-    const double* Qs = W.Qs[buf];
+    constexpr bool SQ = WS::SINGLEQ;
+    const int qb = SQ ? 0 : buf;
+    const double* Qs = W.Qs[qb];
     const FluxGeo<DIM, P, KW>& geo = W.geo[buf];
 #if DGB_NSPEC > 0
     // mixtures: the temperature is one more field of the BR1 gradient; its rows follow those of q
@@ -416,15 +440,16 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
         double qq[C];
 #pragma unroll
         for (int c = 0; c < C; ++c) qq[c] = Qs[(c * KW + e) * EL::LDQ + j];
-        W.Qs[buf][(C * KW + e) * EL::LDQ + j] = pw_temperature<DIM>(qq, ph);
+        W.Qs[qb][(C * KW + e) * EL::LDQ + j] = pw_temperature<DIM>(qq, ph);
       }
     }
     __syncwarp();
 #endif
     if (wb_next < nwblocks) {
       const long long e1 = ebeg + wb_next * KW;
-      flux_stage_async<DIM, P, KW>(W.Qs[buf ^ 1], W.geo[buf ^ 1], d, q, e1,
-                                   (int)((eend - e1) < (long long)KW ? (eend - e1) : (long long)KW), lane);
+      const int nel1 = (int)((eend - e1) < (long long)KW ? (eend - e1) : (long long)KW);
+      if (SQ) flux_stage_geo<DIM, P, KW>(W.geo[buf ^ 1], d, e1, nel1, lane);       // the rows follow after the tensor-core phase
+      else flux_stage_async<DIM, P, KW>(W.Qs[buf ^ 1], W.geo[buf ^ 1], d, q, e1, nel1, lane);
     }
     cp_async_commit();
     if (DGB_L2_PREFETCH_BLOCKS > 0) {
@@ -556,8 +581,15 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
     }
     __syncwarp();
     DGB_WTICK(2);
-    if (wb_next < nwblocks) {             // rows + connectivity of the next block have landed by now
-      cp_async_wait<0>();
+    if (SQ) {                             // every reader of the state rows but the pointwise phase is done: restage them
+      if (wb_next < nwblocks) {
+        const long long e1 = ebeg + wb_next * KW;
+        flux_stage_rows<DIM, P, KW>(W.Qs[0], d, q, e1, (int)((eend - e1) < (long long)KW ? (eend - e1) : (long long)KW), lane);
+      }
+      cp_async_commit();
+    }
+    if (wb_next < nwblocks) {             // connectivity (and, double-buffered, the rows) of the next block have landed by now
+      if (SQ) cp_async_wait<1>(); else cp_async_wait<0>();
       __syncwarp();
       const long long e1 = ebeg + wb_next * KW;
       issue_gathers(W.geo[buf ^ 1], (int)((eend - e1) < (long long)KW ? (eend - e1) : (long long)KW));
@@ -573,7 +605,7 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
 #pragma unroll
         for (int c = 0; c < EL::CG; ++c) {
           const int col = c * KW + e;
-          if (c < C) qq[c] = Qs[col * EL::LDQ + j];
+          if (c < C) qq[c] = SQ ? q[((long long)c * E + e0 + e) * NP + j] : Qs[col * EL::LDQ + j];
           const double* sg = W.Ss + (col >> 3) * 8 * LDSX + grad_row_swizzle<NP>(col & 7) * NP + j;
 #pragma unroll
           for (int x = 0; x < DIM; ++x) g[x][c] = sg[x * 8 * NP];

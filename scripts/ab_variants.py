@@ -34,6 +34,7 @@ VARIANTS = {
     "nb3": ["DGB_DIV8_NB=3"],
     "pf2": ["DGB_FLUX_PREFETCH2=1"],
     "noearly": ["DGB_DIV8_EARLY=0"],
+    "nosq": ["DGB_FLUX_SINGLEQ=0"],
     "agg": ["DGB_TICKET_NOAGG=0"],
     "k3": ["DGB_DIV_KERNEL_DEFAULT=3"],
     "w8": ["DGB_DIV8_WARPS=8"],
