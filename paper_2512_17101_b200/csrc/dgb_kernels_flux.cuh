@@ -931,6 +931,7 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
 
   // cp.async groups retire in order: S(b), T(b), S(b+1), T(b+1), ...
   constexpr bool SS = DGB_DIV_SINGLE_SMALL != 0;
+  static_assert(!(SS && DGB_NSPEC > 0), "the mixture source term reads the block's state rows in the epilogue");
   DGB_WTICK_INIT
   while (wb < nwblocks) {
     const long long e0 = ebeg + wb * KW;
@@ -995,9 +996,32 @@ k_nsdiv3(DiscDev d, const double* __restrict__ q, const double* __restrict__ T,
       const int c = col / KW, e = col - c * KW;
       if (col < WS::NCOL && e < nel) {
         const long long rowbase = ((long long)c * E + e0 + e) * NP;
+#if DGB_NSPEC > 0
+        const double sgn = c == 2 + DIM + ph.ra ? -1.0 : (c == 2 + DIM + ph.rb ? 1.0 : 0.0);     // species a -> species b
+#endif
 #pragma unroll
         for (int ni = 0; ni < EL::NI; ++ni) {
           const int i = ni * 8 + 2 * (lane & 3);
+#if DGB_NSPEC > 0
+          // chemistry (fallback kernel: the rate is evaluated per output pair from the block's own state rows, which
+          // stay valid in the double-buffered small inputs until the next block's land)
+          double w0 = 0.0, w1 = 0.0;
+          if (sgn != 0.0 && !SS) {
+            double qq[C];
+            if (i < NP) {
+#pragma unroll
+              for (int cc = 0; cc < C; ++cc) qq[cc] = M.qv(cc, e, i);
+              w0 = sgn * pw_arrhenius<DIM>(qq, ph);
+            }
+            if (i + 1 < NP) {
+#pragma unroll
+              for (int cc = 0; cc < C; ++cc) qq[cc] = M.qv(cc, e, i + 1);
+              w1 = sgn * pw_arrhenius<DIM>(qq, ph);
+            }
+          }
+          store_pair<NP>(ep, rowbase + i, i, rj[mt] * acc[mt][ni][0] + w0, rj[mt] * acc[mt][ni][1] + w1);
+          continue;
+#endif
           store_pair<NP>(ep, rowbase + i, i, rj[mt] * acc[mt][ni][0], rj[mt] * acc[mt][ni][1]);
         }
       }

@@ -55,11 +55,8 @@ static int ms_div_impl(const dgb_disc* d, const double* q, const double* T, cons
   if ((rc = check_range(d, ebegin, eend))) return rc;
   if (d->dev.G > 0 && !Tghost) return dgb_fail(DGB_ERR_INVALID, "ghost elements need the ghost flux planes");
   dgb::Phys ph; if ((rc = make_ms_phys(ph, d->dim, qfar, transport, mixture))) return rc;
-  bool ok = false;
-#define X(DIM, P) if (d->dim == DIM && d->order == P) {                                                             \
-    rc = launch_div8<DIM, P>(d, q, T, ghost, Tghost, ep, ph, ebegin, eend, (cudaStream_t)stream, &ok);               \
-    if (rc == DGB_OK && !ok) return dgb_fail(DGB_ERR_INVALID, "arrays cannot be described to the TMA unit (alignment)"); \
-    return rc; }
+#define X(DIM, P) if (d->dim == DIM && d->order == P)                                                         \
+    return launch_div_any<DIM, P>(d, q, T, ghost, Tghost, ep, ph, ebegin, eend, (cudaStream_t)stream, div_kernel());
   DGB_FOR_EACH_ELEMENT(X)
 #undef X
   return dgb_fail(DGB_ERR_INVALID, "unsupported (dim, order)");

@@ -254,3 +254,20 @@ def test_gpu_device_rk4_multispecies():
         assert np.array_equal(got_g, got_e)
         assert np.all(np.isfinite(got_g)) and rel_err(got_g, ref) <= 1e-10, rel_err(got_g, ref)
         assert rel_err(got_g, q0) > 1e-6                      # the state did move
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dim,order,n,bc", [(3, 3, 3, "periodic"), (3, 4, 3, "farfield"), (2, 3, 5, "farfield")])
+def test_gpu_multispecies_cp_async_fallback(dim, order, n, bc, monkeypatch):
+    """Pass 2 of the mixture on the cp.async kernel (k_nsdiv3<C=8>, what runs when the arrays cannot be described to
+    the TMA unit) against the TMA-staged default: same arithmetic up to the contraction of the source-term add."""
+    from paper_2512_17101_b200 import B200ArrayContext
+    gpu = B200ArrayContext()
+    d = make_dcoll(gpu, dim, order, n, bc)
+    op = MultispeciesOperator(d, Mixture())
+    q = d.from_numpy(ms_state(op, d.nodes()))
+    outs = {}
+    for k in ("8", "3"):
+        monkeypatch.setenv("DGB_DIV_KERNEL", k)
+        outs[k] = d.to_numpy(op.rhs(q))
+    assert np.all(np.isfinite(outs["3"])) and rel_err(outs["3"], outs["8"]) <= 1e-14
