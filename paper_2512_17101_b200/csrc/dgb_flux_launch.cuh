@@ -32,7 +32,10 @@ template <int DIM, int P> struct CfgF {
   static constexpr int KW = DIM == 3 ? 3 : 4;
   static constexpr size_t flux_per = sizeof(dgb::Flux3Warp<DIM, P, KW>);
   static constexpr size_t flux_fixed = sizeof(dgb::Flux3Smem<DIM, P, KW, 1>) - flux_per;
-  static constexpr int NWF = fit_warps(flux_fixed, flux_per, DGB_FLUX_WARPS);
+  // registers are allocated per SM sub-partition: 9-11 warps get the 168 registers of 12 without being 12, so a
+  // configuration that shared memory limits below 12 warps runs 8 (255 registers) rather than 9-11 with spills
+  static constexpr int NWF_fit = fit_warps(flux_fixed, flux_per, DGB_FLUX_WARPS);
+  static constexpr int NWF = (NWF_fit >= 12 || NWF_fit <= 8) ? NWF_fit : 8;
   static constexpr size_t div_per = sizeof(dgb::Div3Warp<DIM, P, KW>);
   static constexpr size_t div_fixed = sizeof(dgb::Div3Smem<DIM, P, KW, 1>) - div_per;
   static constexpr int NWD = fit_warps(div_fixed, div_per, DGB_DIV_WARPS);
