@@ -235,7 +235,10 @@ struct alignas(128) Div8Warp {
   alignas(128) double Qb[EL::C * BX::BOXW];             // [field][element][node]
   alignas(128) double Lam[BX::BOXW];                    // wave speed rows of the block
   double Fs[NCOL * EL::LDF];
-  double Om[DGB_NSPEC > 0 ? KW * EL::NP : 1];           // mixtures: Arrhenius rate at the block's nodes
+  // mixtures: Arrhenius rate at the block's nodes; it lives in the block's gather-map slice (dead once the gathers
+  // are issued) when that is large enough -- the 480 bytes decide between 7 and 8 warps for 3D p3
+  static constexpr bool OM_ALIAS = 2 * EL::NP <= EL::NFT;
+  double Om[(DGB_NSPEC > 0 && !OM_ALIAS) ? KW * EL::NP : 1];
   Div8Geo<DIM, P, KW> geo[2];
   unsigned long long bar_q, bar_t;
 };
@@ -385,13 +388,15 @@ k_nsdiv8(DiscDev d, const __grid_constant__ CUtensorMap map_q, const __grid_cons
     for (int mt = 0; mt < WS::NTILE; ++mt) rj[mt] = W.geo[buf].rj[(mt * 8 + (lane >> 2)) % KW];
 #if DGB_NSPEC > 0
     // chemistry: the Arrhenius rate at every node of the block, from the state box while it is still here
+    double* om = WS::OM_ALIAS ? reinterpret_cast<double*>(W.geo[buf].gi) : W.Om;
+    __syncwarp();                        // (aliased: every lane has read its gather-map words)
     for (int n = lane; n < KW * NP; n += 32) {
       const int e = n / NP;
       if (e < nel) {
         double qq[C];
 #pragma unroll
         for (int c = 0; c < C; ++c) qq[c] = W.Qb[c * BOXW + n + sh];
-        W.Om[n] = pw_arrhenius<DIM>(qq, ph);
+        om[n] = pw_arrhenius<DIM>(qq, ph);
       }
     }
 #endif
@@ -438,8 +443,8 @@ k_nsdiv8(DiscDev d, const __grid_constant__ CUtensorMap map_q, const __grid_cons
           double v0 = rj[mt] * acc[mt][ni][0], v1 = rj[mt] * acc[mt][ni][1];
 #if DGB_NSPEC > 0
           if (sgn != 0.0) {
-            if (i < NP) v0 += sgn * W.Om[e * NP + i];
-            if (i + 1 < NP) v1 += sgn * W.Om[e * NP + i + 1];
+            if (i < NP) v0 += sgn * om[e * NP + i];
+            if (i + 1 < NP) v1 += sgn * om[e * NP + i + 1];
           }
 #endif
           store_pair<NP>(ep, rowbase + i, i, v0, v1);
