@@ -19,6 +19,9 @@ namespace {
 #ifndef DGB_FLUX_WARPS
 #define DGB_FLUX_WARPS 12
 #endif
+#ifndef DGB_FLUX_WARPS_MS          // mixtures: the pointwise phase is heavier; 12 warps (168 registers) spill
+#define DGB_FLUX_WARPS_MS 8
+#endif
 #ifndef DGB_DIV_WARPS
 #define DGB_DIV_WARPS 8
 #endif
@@ -34,7 +37,7 @@ template <int DIM, int P> struct CfgF {
   static constexpr size_t flux_fixed = sizeof(dgb::Flux3Smem<DIM, P, KW, 1>) - flux_per;
   // registers are allocated per SM sub-partition: 9-11 warps get the 168 registers of 12 without being 12, so a
   // configuration that shared memory limits below 12 warps runs 8 (255 registers) rather than 9-11 with spills
-  static constexpr int NWF_fit = fit_warps(flux_fixed, flux_per, DGB_FLUX_WARPS);
+  static constexpr int NWF_fit = fit_warps(flux_fixed, flux_per, DGB_NSPEC > 0 ? DGB_FLUX_WARPS_MS : DGB_FLUX_WARPS);
   static constexpr int NWF = (NWF_fit >= 12 || NWF_fit <= 8) ? NWF_fit : 8;
   static constexpr size_t div_per = sizeof(dgb::Div3Warp<DIM, P, KW>);
   static constexpr size_t div_fixed = sizeof(dgb::Div3Smem<DIM, P, KW, 1>) - div_per;

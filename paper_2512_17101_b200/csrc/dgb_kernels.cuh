@@ -33,7 +33,7 @@ constexpr int ldpad(int k) { return (ceil_to(k, 4) % 8 == 4) ? ceil_to(k, 4) : c
 template <int DIM, int P>
 struct ElemT {
   static constexpr int C = DIM + 2 + DGB_NSPEC;  // conserved fields
-  static constexpr int CG = C + (DGB_NSPEC > 0 ? 1 : 0);   // fields whose BR1 gradient pass 1 needs (mixtures: + temperature)
+  static constexpr int CG = C;                   // fields whose BR1 gradient pass 1 needs (the temperature gradient of mixtures follows by the chain rule)
   static constexpr int NF = DIM + 1;
   static constexpr int NP = DIM == 2 ? (P + 1) * (P + 2) / 2 : (P + 1) * (P + 2) * (P + 3) / 6;
   static constexpr int NFP = DIM == 2 ? (P + 1) : (P + 1) * (P + 2) / 2;
@@ -298,11 +298,10 @@ __device__ __forceinline__ double ms_wavespeed(const MsPrim<DIM>& s) {
   return sqrt(v2) + sqrt((1.0 + s.R / s.cv) * s.p / s.rho);
 }
 
-// multispecies.py: _viscous; g[x][c] = d q_c / d x_x for c < C, g[x][C] = dT / d x_x
+// multispecies.py: _viscous; g[x][c] = d q_c / d x_x; velocity, mass-fraction and temperature gradients by the chain rule
 template <int DIM>
-__device__ __forceinline__ void ms_viscous_flux(const MsPrim<DIM>& s, const double (&g)[DIM][DIM + 3 + DGB_NSPEC],
+__device__ __forceinline__ void ms_viscous_flux(const MsPrim<DIM>& s, const double (&g)[DIM][DIM + 2 + DGB_NSPEC],
                                                 const Phys& ph, double (&Fv)[DIM][DIM + 2 + DGB_NSPEC]) {
-  constexpr int C = DIM + 2 + DGB_NSPEC;
   double du[DIM][DIM];
 #pragma unroll
   for (int i = 0; i < DIM; ++i)
@@ -321,11 +320,19 @@ __device__ __forceinline__ void ms_viscous_flux(const MsPrim<DIM>& s, const doub
       Fv[x][2 + i] = t;
       work += s.u[i] * t;
     }
-    double heat = ph.kappa * g[x][C];
+    double dY[DGB_NSPEC];
+    double de = (g[x][1] - (s.E * s.inv_rho) * g[x][0]) * s.inv_rho;
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) de -= s.u[i] * du[i][x];
 #pragma unroll
     for (int k = 0; k < DGB_NSPEC; ++k) {
-      const double dY = (g[x][2 + DIM + k] - s.Y[k] * g[x][0]) * s.inv_rho;
-      const double jk = (s.rho * ph.dspec) * dY;                 // = -J_k
+      dY[k] = (g[x][2 + DIM + k] - s.Y[k] * g[x][0]) * s.inv_rho;
+      de -= (ph.mh0[k] + ph.mcv[k] * s.T) * dY[k];
+    }
+    double heat = ph.kappa * (de / s.cv);
+#pragma unroll
+    for (int k = 0; k < DGB_NSPEC; ++k) {
+      const double jk = (s.rho * ph.dspec) * dY[k];              // = -J_k
       const double hk = ph.mh0[k] + (ph.mcv[k] + ph.mR[k]) * s.T;
       heat += hk * jk;
       Fv[x][2 + DIM + k] = jk;
@@ -343,7 +350,7 @@ __device__ __forceinline__ void ms_viscous_flux(const MsPrim<DIM>& s, const doub
 // total flux F = F_inv - F_visc at a node and the local wave speed
 template <int DIM>
 __device__ __forceinline__ void pw_total_flux(const double (&qq)[DIM + 2 + DGB_NSPEC],
-                                              const double (&g)[DIM][DIM + 2 + DGB_NSPEC + (DGB_NSPEC > 0 ? 1 : 0)],
+                                              const double (&g)[DIM][DIM + 2 + DGB_NSPEC],
                                               const Phys& ph, double (&F)[DIM][DIM + 2 + DGB_NSPEC], double& lam) {
   constexpr int C = DIM + 2 + DGB_NSPEC;
   double Fv[DIM][C];

@@ -258,7 +258,7 @@ __host__ __device__ constexpr int grad_row_swizzle(int k) {
 template <int DIM, int P, int KW>
 struct alignas(16) Flux3Warp {
   using EL = ElemT<DIM, P>;
-  static constexpr int NCOL = EL::CG * KW;     // columns of the BR1 gradient: (field, element), mixtures: + temperature
+  static constexpr int NCOL = EL::CG * KW;     // columns of the BR1 gradient: (field, element)
   static constexpr int NTILE = (NCOL + 7) / 8;
   static constexpr int NCOLP = NTILE * 8;
   static constexpr bool SINGLEQ = DGB_FLUX_SINGLEQ < 0 ? (EL::NP > 20 || DGB_NSPEC > 0) : (DGB_FLUX_SINGLEQ != 0);
@@ -432,19 +432,6 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
     const int qb = SQ ? 0 : buf;
     const double* Qs = W.Qs[qb];
     const FluxGeo<DIM, P, KW>& geo = W.geo[buf];
-#if DGB_NSPEC > 0
-    // mixtures: the temperature is one more field of the BR1 gradient; its rows follow those of q
-    for (int n = lane; n < KW * NP; n += 32) {
-      const int e = n / NP, j = n - e * NP;
-      if (e < nel) {
-        double qq[C];
-#pragma unroll
-        for (int c = 0; c < C; ++c) qq[c] = Qs[(c * KW + e) * EL::LDQ + j];
-        W.Qs[qb][(C * KW + e) * EL::LDQ + j] = pw_temperature<DIM>(qq, ph);
-      }
-    }
-    __syncwarp();
-#endif
     if (wb_next < nwblocks) {
       const long long e1 = ebeg + wb_next * KW;
       const int nel1 = (int)((eend - e1) < (long long)KW ? (eend - e1) : (long long)KW);
@@ -511,9 +498,6 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
         }
 #pragma unroll
         for (int c = 0; c < C; ++c) W.Ss[(c * KW + e) * LDSX + f * EL::NFPK + m] = 0.5 * (qm[c] + qpE[k][c]);
-#if DGB_NSPEC > 0
-        W.Ss[(C * KW + e) * LDSX + f * EL::NFPK + m] = 0.5 * (Qs[(C * KW + e) * EL::LDQ + jm] + pw_temperature<DIM>(qpE[k], ph));
-#endif
       }
     }
     __syncwarp();

@@ -24,8 +24,8 @@ Model
   ``omega = A rho Y_a exp(-T_a / T)``, source ``-omega`` / ``+omega`` on ``rho Y_a`` / ``rho Y_b`` (the heat
   release is in ``h0``; total energy needs no source);
 * discretisation = the single-species scheme: weak-form nodal DG, Rusanov inviscid flux with the
-  mixture wave speed, BR1 (gradient of the conserved variables AND of ``T``, central flux; viscous
-  flux central), periodic or prescribed far-field exterior state; partitioned meshes through ghost
+  mixture wave speed, BR1 (gradient of the conserved variables with the central flux; velocity, mass-fraction and
+  temperature gradients by the chain rule; viscous flux central), periodic or prescribed far-field exterior state; partitioned meshes through ghost
   arrays (``rhs(q, ghost, halo_fn)``, ``HaloExchange.ms_rhs``).
 """
 from __future__ import annotations
@@ -87,13 +87,16 @@ def _inviscid(actx, mix, q, dim):
         v2 = v2 + vel[i] * vel[i]
     lam = actx.np.sqrt(v2) + actx.np.sqrt((1.0 + R / cv) * p / q[0])
     assert len(flux[0]) == C
-    return flux, lam, (vel, Y, T)
+    return flux, lam, (vel, Y, T, cv)
 
 
-def _viscous(actx, mix, q, gq, gT, prim, transport, dim):
-    """``Fv[x][c]`` from the state, ``gq[x][c] = d q_c/dx_x`` and ``gT[x] = dT/dx_x``."""
+def _viscous(actx, mix, q, gq, prim, transport, dim):
+    """``Fv[x][c]`` from the state and ``gq[x][c] = d q_c/dx_x``.  Velocity, mass-fraction and temperature gradients
+    follow from the gradient of the conserved fields by the chain rule, like the single-species operator
+    (``operators.viscous_flux``): ``T cv(Y) = E/rho - |u|^2/2 - sum Y_k h0_k``, so
+    ``dT = (d(E/rho) - u.du - sum (h0_k + T cv_k) dY_k) / cv``."""
     mu, kappa, D = transport
-    vel, Y, T = prim
+    vel, Y, T, cv = prim
     rho = q[0]
     inv_rho = 1.0 / rho
     du = [[(gq[x][2 + i] - vel[i] * gq[x][0]) * inv_rho for x in range(dim)] for i in range(dim)]
@@ -112,7 +115,12 @@ def _viscous(actx, mix, q, gq, gT, prim, transport, dim):
         work = vel[0] * tau[0]
         for i in range(1, dim):
             work = work + vel[i] * tau[i]
-        heat = kappa * gT[x]
+        de = (gq[x][1] - (q[1] * inv_rho) * gq[x][0]) * inv_rho
+        for i in range(dim):
+            de = de - vel[i] * du[i][x]
+        for k in range(mix.ns):
+            de = de - (float(mix.h0[k]) + float(mix.cv[k]) * T) * dY[k][x]
+        heat = kappa * (de / cv)
         spec = []
         for k in range(mix.ns):
             jk = (rho * D) * dY[k][x]                       # = -J_k
@@ -124,7 +132,7 @@ def _viscous(actx, mix, q, gq, gT, prim, transport, dim):
 
 
 def _ms_pass1(actx, mix, dim, q, ghost, Sw, drdx, jac, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, transport):
-    """Pass 1 (``dg_ms_flux``): BR1 gradient of ``[q, T]`` (central flux), then the total flux at every node, stored
+    """Pass 1 (``dg_ms_flux``): BR1 gradient of ``q`` (central flux), then the total flux at every node, stored
     like ``dg_ns_flux`` of the single-species operator: planes ``r*C + c`` (``r < dim``) hold the contravariant,
     Jacobian-scaled components ``T[r][c] = sum_x jac*drdx[r,x] (F_inv - F_visc)[x][c]``, planes ``dim*C + c`` their sum
     over ``r`` and the last plane the mixture wave speed: shape ``((dim+1)*C + 1, E, Np)`` -- what pass 2 contracts and
@@ -137,23 +145,15 @@ def _ms_pass1(actx, mix, dim, q, ghost, Sw, drdx, jac, lift, normals, fscale, vm
     is_bnd = actx.np.not_equal(bc_kind, BC_NONE)
     qc = [q[c] for c in range(C)]
     finv, lam, prim = _inviscid(actx, mix, qc, dim)
-    W = actx.np.concatenate([q, actx.np.reshape(prim[2], (1, E, Np))])                  # (C+1, E, Np)
-    Wg = None
-    if ghost is not None:
-        gprim = _thermo(actx, mix, [ghost[c] for c in range(C)], dim)
-        Wg = actx.np.concatenate([ghost, actx.np.reshape(gprim[2], (1,) + tuple(ghost.shape[1:]))])
-    vol = actx.np.einsum("rij,rxe,cej->xcei", Sw, drdx, W)
-    wm, wp = _traces(actx, W, Wg, vmap_m, vmap_p, C + 1, E, Np, Nf, Nfp)
+    vol = actx.np.einsum("rij,rxe,cej->xcei", Sw, drdx, q)
+    wm, wp = _traces(actx, q, ghost, vmap_m, vmap_p, C, E, Np, Nf, Nfp)
     far = [qfar[c] for c in range(C)]
-    far_T = _thermo(actx, mix, far, dim)[2]
-    ext = far + [far_T]
-    wpl = [actx.np.where(is_bnd, ext[c], wp[c]) for c in range(C + 1)]
-    wstar = [fscale * (0.5 * (wm[c] + wpl[c])) for c in range(C + 1)]
-    fs = actx.np.stack([actx.np.stack([nrm[x] * wstar[c] for c in range(C + 1)]) for x in range(dim)])
-    gW = actx.np.einsum("if,xcef->xcei", lift, actx.np.reshape(fs, (dim, C + 1, E, Nf * Nfp))) - vol
+    wpl = [actx.np.where(is_bnd, far[c], wp[c]) for c in range(C)]
+    wstar = [fscale * (0.5 * (wm[c] + wpl[c])) for c in range(C)]
+    fs = actx.np.stack([actx.np.stack([nrm[x] * wstar[c] for c in range(C)]) for x in range(dim)])
+    gW = actx.np.einsum("if,xcef->xcei", lift, actx.np.reshape(fs, (dim, C, E, Nf * Nfp))) - vol
     gq = [[gW[x][c] for c in range(C)] for x in range(dim)]
-    gT = [gW[x][C] for x in range(dim)]
-    fvis = _viscous(actx, mix, qc, gq, gT, prim, tr, dim)
+    fvis = _viscous(actx, mix, qc, gq, prim, tr, dim)
     ftot = [[finv[x][c] if fvis[x][c] is None else finv[x][c] - fvis[x][c] for c in range(C)] for x in range(dim)]
     fstack = actx.np.stack([actx.np.stack(fx) for fx in ftot])                          # (d, C, E, Np)
     T = actx.np.einsum("rxe,e,xcej->rcej", drdx, jac, fstack)
