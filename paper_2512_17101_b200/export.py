@@ -342,15 +342,18 @@ class GraphExportContext:
 
 
 def export_rhs_program(mesh, order, q0, equations="ns", name=None, **phys) -> dict:
-    """The right-hand side of ``equations`` ("ns" = flux arrangement, "ns_grad_form", "euler") on ``mesh`` as a
-    program document with the state as the placeholder ``q`` bound to ``q0``."""
+    """The right-hand side of ``equations`` ("ns" = flux arrangement, "ns_grad_form", "euler", "multispecies") on
+    ``mesh`` as a program document with the state as the placeholder ``q`` bound to ``q0``."""
     from .discretization import DGDiscretization
     from .dofarray import DOFArray
     from .operators import EulerOperator, NavierStokesOperator
     ctx = GraphExportContext(name or f"dg_{equations}_rhs")
     d = DGDiscretization(ctx, mesh, order)
     q = DOFArray(ctx, ctx.placeholder("q", np.shape(q0), "f64", value=q0))
-    if equations == "euler":
+    if equations == "multispecies":
+        from .multispecies import MultispeciesOperator
+        out = MultispeciesOperator(d, **phys).rhs(q)
+    elif equations == "euler":
         out = EulerOperator(d, **phys).rhs(q)
     else:
         op = NavierStokesOperator(d, **phys)

@@ -16,13 +16,20 @@ from tests.common import random_state
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 REF = "/root/reference/pkg/src"
-CASES = [("ns", 2, 1, 3, {"mu": 2e-2}), ("ns_grad_form", 2, 2, 3, {"mu": 2e-2}), ("euler", 3, 1, 3, {}), ("ns", 3, 2, 3, {"mu": 1e-2})]
+CASES = [("ns", 2, 1, 3, {"mu": 2e-2}), ("ns_grad_form", 2, 2, 3, {"mu": 2e-2}), ("euler", 3, 1, 3, {}), ("ns", 3, 2, 3, {"mu": 1e-2}),
+         ("multispecies", 2, 2, 3, {})]      # exp / truediv lambdas of the reactive mixture (expr.py:265-289)
 
 
 def _case(equations, dim, order, n, kw):
     mesh = box_mesh((n,) * dim, (-1.0,) * dim, (1.0,) * dim, periodic=(True,) * dim)
     cpu = NumpyArrayContext()
     d = DGDiscretization(cpu, mesh, order)
+    if equations == "multispecies":
+        from paper_2512_17101_b200 import MultispeciesOperator
+        from tests.test_multispecies import ms_state
+        op = MultispeciesOperator(d, **kw)
+        q0 = ms_state(op, d.nodes())
+        return mesh, q0, d.to_numpy(op.rhs(d.from_numpy(q0)))
     q0 = random_state(dim, d.nelements, d.Np, seed=7)
     op = (EulerOperator if equations == "euler" else NavierStokesOperator)(d, **kw)
     f = op.rhs_grad_form if equations == "ns_grad_form" else op.rhs
@@ -40,7 +47,7 @@ def test_exported_program_structure(equations, dim, order, n, kw):
     assert {"placeholder", "data", "call"} <= kinds
     names = sorted(f["name"] for f in doc2["functions"].values())
     assert names == {"ns": ["dg_ns_div", "dg_ns_flux"], "ns_grad_form": ["dg_ns_grad", "dg_ns_rhs"],
-                     "euler": ["dg_euler_rhs"]}[equations]
+                     "euler": ["dg_euler_rhs"], "multispecies": ["dg_ms_rhs"]}[equations]
     # definition before use, inside every table (cli.py:160-176)
     for table, pre in [(doc2["nodes"], set())] + [(f["nodes"], set(f["parameters"])) for f in doc2["functions"].values()]:
         seen = set(pre)
