@@ -7,7 +7,7 @@ from paper_2512_17101_b200 import B200ArrayContext, DeviceRK4, NavierStokesOpera
 from tests.common import make_dcoll, smooth_state
 actx = B200ArrayContext()
 print("| n | DOFs | rk4_step ms | rk4_step_fused ms | DeviceRK4 eager ms | DeviceRK4 graph ms |\n|---|---|---|---|---|---|")
-for n in (4, 8, 16, 32):
+for n in (4, 8, 16, 32, 64):
     d = make_dcoll(actx, 3, 3, n, "periodic")
     op = NavierStokesOperator(d, mu=1e-2)
     q0 = d.from_numpy(smooth_state(d.nodes()))
