@@ -462,4 +462,67 @@ __device__ __forceinline__ void store_pair(const Epilogue& ep, long long idx, in
   }
 }
 
+// Store epilogue of a warp's block: v[mt][ni] = the two values of node pair (ni*8 + 2*(lane&3)) of column mt*8 + lane/4.
+// RK-fused stores with even Np: ALL operands x1 / x2 of the lane are loaded first and the results stored afterwards
+// -- written as load, store, load, store ... the compiler must keep that order (out1 / out2 may alias x1 / x2: the
+// accumulator of the scheme is updated in place) and every pair waits for its own round trip to L2
+// (DeviceRK4 at 31 M DOFs: 24.5 -> 21.7 ms per step).
+template <int NP, int KW, int NCOL, int NTILE, int NI>
+__device__ __forceinline__ void store_block(const Epilogue& ep, const double (&v)[NTILE][NI][2], long long E,
+                                            long long e0, int nel, int lane) {
+  const bool rk_batch = (NP % 2 == 0) && ep.x1 != nullptr;
+  if (rk_batch) {
+    double2 xa[NTILE][NI], xb[NTILE][NI];
+#pragma unroll
+    for (int mt = 0; mt < NTILE; ++mt) {
+      const int col = mt * 8 + (lane >> 2);
+      const int c = col / KW, e = col - c * KW;
+      const bool ok = col < NCOL && e < nel;
+      const long long rowbase = ((long long)c * E + e0 + e) * NP;
+#pragma unroll
+      for (int ni = 0; ni < NI; ++ni) {
+        const int i = ni * 8 + 2 * (lane & 3);
+        xa[mt][ni] = make_double2(0.0, 0.0); xb[mt][ni] = make_double2(0.0, 0.0);
+        if (ok && i < NP) {
+          xa[mt][ni] = *reinterpret_cast<const double2*>(ep.x1 + rowbase + i);
+          if (ep.out2) xb[mt][ni] = *reinterpret_cast<const double2*>(ep.x2 + rowbase + i);
+        }
+      }
+    }
+#pragma unroll
+    for (int mt = 0; mt < NTILE; ++mt) {
+      const int col = mt * 8 + (lane >> 2);
+      const int c = col / KW, e = col - c * KW;
+      if (col < NCOL && e < nel) {
+        const long long rowbase = ((long long)c * E + e0 + e) * NP;
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) {
+          const int i = ni * 8 + 2 * (lane & 3);
+          if (i < NP) {
+            *reinterpret_cast<double2*>(ep.out1 + rowbase + i) =
+                make_double2(ep.a1 * xa[mt][ni].x + ep.b1 * v[mt][ni][0], ep.a1 * xa[mt][ni].y + ep.b1 * v[mt][ni][1]);
+            if (ep.out2)
+              *reinterpret_cast<double2*>(ep.out2 + rowbase + i) =
+                  make_double2(ep.a2 * xb[mt][ni].x + ep.b2 * v[mt][ni][0], ep.a2 * xb[mt][ni].y + ep.b2 * v[mt][ni][1]);
+          }
+        }
+      }
+    }
+    return;
+  }
+#pragma unroll
+  for (int mt = 0; mt < NTILE; ++mt) {
+    const int col = mt * 8 + (lane >> 2);
+    const int c = col / KW, e = col - c * KW;
+    if (col < NCOL && e < nel) {
+      const long long rowbase = ((long long)c * E + e0 + e) * NP;
+#pragma unroll
+      for (int ni = 0; ni < NI; ++ni) {
+        const int i = ni * 8 + 2 * (lane & 3);
+        store_pair<NP>(ep, rowbase + i, i, v[mt][ni][0], v[mt][ni][1]);
+      }
+    }
+  }
+}
+
 }  // namespace dgb

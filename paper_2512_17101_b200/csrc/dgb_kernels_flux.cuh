@@ -1242,19 +1242,7 @@ k_euler4(DiscDev d, const double* __restrict__ q, const double* __restrict__ gho
       for (int ni = 0; ni < EL::NI; ++ni) { acc[mt][ni][0] = 0.0; acc[mt][ni][1] = 0.0; }
     mma_block<EL::NI, WS::NTILE>(acc, W.Ts, EL::LDV, S.Wv, EL::LDV, EL::KV / 4, lane);
     mma_block<EL::NI, WS::NTILE>(acc, W.Fs, EL::LDF, S.Wl, EL::LDF, EL::KF / 4, lane);
-#pragma unroll
-    for (int mt = 0; mt < WS::NTILE; ++mt) {
-      const int col = mt * 8 + (lane >> 2);
-      const int c = col / KW, e = col - c * KW;
-      if (col < WS::NCOL && e < nel) {
-        const long long rowbase = ((long long)c * E + e0 + e) * NP;
-#pragma unroll
-        for (int ni = 0; ni < EL::NI; ++ni) {
-          const int i2 = ni * 8 + 2 * (lane & 3);
-          store_pair<NP>(ep, rowbase + i2, i2, acc[mt][ni][0], acc[mt][ni][1]);
-        }
-      }
-    }
+    store_block<NP, KW, WS::NCOL, WS::NTILE, EL::NI>(ep, acc, E, e0, nel, lane);
     __syncwarp();                        // operand rows free for the next block
     if (nel1 == 0) break;
     wb = wb_next;

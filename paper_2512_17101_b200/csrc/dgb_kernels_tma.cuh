@@ -428,29 +428,27 @@ k_nsdiv8(DiscDev d, const __grid_constant__ CUtensorMap map_q, const __grid_cons
 #endif
     }
 
+    // ---- 1/J (+ chemistry) and the (RK-fused) store ----
 #pragma unroll
     for (int mt = 0; mt < WS::NTILE; ++mt) {
-      const int col = mt * 8 + (lane >> 2);
-      const int c = col / KW, e = col - c * KW;
-      if (col < WS::NCOL && e < nel) {
-        const long long rowbase = ((long long)c * E + e0 + e) * NP;
 #if DGB_NSPEC > 0
-        const double sgn = c == 2 + DIM + ph.ra ? -1.0 : (c == 2 + DIM + ph.rb ? 1.0 : 0.0);     // species a -> species b
+      const int col = mt * 8 + (lane >> 2);
+      const int c = col / KW, e = col < WS::NCOL ? col - c * KW : 0;
+      const double sgn = c == 2 + DIM + ph.ra ? -1.0 : (c == 2 + DIM + ph.rb ? 1.0 : 0.0);     // species a -> species b
 #endif
 #pragma unroll
-        for (int ni = 0; ni < EL::NI; ++ni) {
-          const int i = ni * 8 + 2 * (lane & 3);
-          double v0 = rj[mt] * acc[mt][ni][0], v1 = rj[mt] * acc[mt][ni][1];
+      for (int ni = 0; ni < EL::NI; ++ni) {
+        acc[mt][ni][0] *= rj[mt]; acc[mt][ni][1] *= rj[mt];
 #if DGB_NSPEC > 0
-          if (sgn != 0.0) {
-            if (i < NP) v0 += sgn * om[e * NP + i];
-            if (i + 1 < NP) v1 += sgn * om[e * NP + i + 1];
-          }
-#endif
-          store_pair<NP>(ep, rowbase + i, i, v0, v1);
+        const int i = ni * 8 + 2 * (lane & 3);
+        if (sgn != 0.0 && e < nel) {
+          if (i < NP) acc[mt][ni][0] += sgn * om[e * NP + i];
+          if (i + 1 < NP) acc[mt][ni][1] += sgn * om[e * NP + i + 1];
         }
+#endif
       }
     }
+    store_block<NP, KW, WS::NCOL, WS::NTILE, EL::NI>(ep, acc, E, e0, nel, lane);
     if (nel1 == 0) break;
     wb = wb_next;
   }
