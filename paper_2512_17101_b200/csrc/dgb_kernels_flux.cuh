@@ -32,26 +32,24 @@
 #ifndef DGB_L2_PREFETCH_BLOCKS
 #define DGB_L2_PREFETCH_BLOCKS 0
 #endif
-// pass 2: one buffer for a block's small inputs (q, lam, face Jacobians, connectivity) instead of two: the next
-// block's are staged as soon as the face phase has read these and land during the contraction + store.
-// 15.6 instead of 18.7 KB of shared memory per warp (3D p3), i.e. room for 12 warps instead of 11.
-// pass 1: neighbour nodes from the 32-bit gather map (1) or decoded from the connectivity word (0)
-#ifndef DGB_FLUX_LEAN
-#define DGB_FLUX_LEAN 0
-#endif
-// pass 1: when block b is taken, pull the rows and the geometry of the block AFTER the next one (its ticket is
-// already drawn: the stream is two deep) into L2, so that the cp.async staging issued one block later hits L2:
-// ncu attributes 8.5 % of the kernel's stall samples to waiting for that staging.
-#ifndef DGB_FLUX_PREFETCH2
-#define DGB_FLUX_PREFETCH2 0
-#endif
 // pass 1 with ONE buffer for a block's state rows where shared memory limits the number of warps (order 4: 6 -> 8
 // warps; mixtures: 7 -> 8): the next block's rows are staged right after the tensor-core phase and the pointwise phase
 // reads the state from global memory (the rows were staged a moment ago: L2 hits) instead of the buffer.
 // -1: automatic (Np > 20 or mixtures), 0 / 1: off / on
+// pass 1 tensor-core phase: one column tile at a time (0), all column tiles of a block in one sweep (1), or all tiles
+// with U_0 first and the Z_r chains started from -U_0 (2: 24 accumulator registers fewer per tile).  Sharing the W
+// fragments across tiles takes the operand LDS from 1.33 to 0.83 per DMMA.  Measured (profiles/r02_pass2_tma.md, section 12):
+// neutral on 3D p3 (12 warps, 168 registers: the step is power-bound), -1 % / -3 % of pass 1 where the launch has
+// 8 warps and 255 registers anyway.  -1: automatic (2 for order 4 or mixtures, not both: that one spills; else 0)
+#ifndef DGB_FLUX_MT
+#define DGB_FLUX_MT -1
+#endif
 #ifndef DGB_FLUX_SINGLEQ
 #define DGB_FLUX_SINGLEQ -1
 #endif
+// cp.async pass 2 (k_nsdiv3): one buffer for a block's small inputs (q, lam, face Jacobians, connectivity) instead of
+// two: the next block's are staged as soon as the face phase has read these and land during the contraction + store
+// (15.6 instead of 18.7 KB of shared memory per warp at 3D p3; measured no faster: off)
 #ifndef DGB_DIV_SINGLE_SMALL
 #define DGB_DIV_SINGLE_SMALL 0
 #endif
@@ -231,7 +229,6 @@ struct FluxGeo {
   double fsc[KW][EL::NF];
   long long conn[KW][EL::NF];
   double jac[KW];
-  alignas(16) unsigned gi[DGB_FLUX_LEAN ? KW * EL::NFT : 4];      // the block's slice of the gather map (DiscDev::gidx)
 };
 
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
@@ -326,7 +323,6 @@ __device__ __forceinline__ void flux_stage_geo(FluxGeo<DIM, P, KW>& g, const Dis
     cp_async8(&g.conn[0][lane], d.conn + e0 * NF + lane);
   }
   if (lane < nel) cp_async8(&g.jac[lane], d.jac + e0 + lane);
-  if (DGB_FLUX_LEAN) stage_gather_map<DIM, EL::NFT, EL::NFP>(g.gi, d.gidx, e0, nel, lane);
 }
 
 template <int DIM, int P, int KW>
@@ -380,12 +376,6 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
   // consumed at the top of the block's own iteration.
   double qpE[NR][C];
   long long cnkE[NR];
-#if DGB_FLUX_LEAN
-  const bool lean = d.gidx != nullptr;
-#else
-  constexpr bool lean = false;
-#endif
-  const unsigned enp = (unsigned)(E * NP);
   auto issue_gathers = [&](const FluxGeo<DIM, P, KW>& g, int nelx) {
 #pragma unroll
     for (int k = 0; k < NR; ++k) {
@@ -395,20 +385,11 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
       if (flk >= 0 && e < nelx) {
         const long long cn = g.conn[e][f];
         cnkE[k] = cn;
-        const double* pbase;
-        long long pstride;
-        if (lean) {                  // neighbour node straight from the gather map
-          const unsigned gi = g.gi[e * NFT + ((flk >> 16) & 255)];
-          const bool in_ghost = GH && gi >= enp;
-          pstride = (in_ghost ? G : E) * NP;
-          pbase = in_ghost ? ghost + (gi - enp) : q + gi;
-        } else {                     // (E+G)*Np beyond 32 bits: decode the connectivity word
-          const long long nb = DGB_CONN_NB(cn);
-          const int jp = S.fn[DGB_CONN_NF(cn) * NFP + S.perm[DGB_CONN_PERM(cn) * NFP + m]];
-          const bool in_ghost = GH && nb >= E;
-          pstride = (in_ghost ? G : E) * NP;
-          pbase = (in_ghost ? ghost : q) + (in_ghost ? nb - E : nb) * NP + jp;
-        }
+        const long long nb = DGB_CONN_NB(cn);
+        const int jp = S.fn[DGB_CONN_NF(cn) * NFP + S.perm[DGB_CONN_PERM(cn) * NFP + m]];
+        const bool in_ghost = GH && nb >= E;
+        const long long pstride = (in_ghost ? G : E) * NP;
+        const double* pbase = (in_ghost ? ghost : q) + (in_ghost ? nb - E : nb) * NP + jp;
 #pragma unroll
         for (int c = 0; c < C; ++c) qpE[k][c] = pbase[c * pstride];
       }
@@ -447,29 +428,6 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
                                     (int)((eend - ep) < (long long)KW ? (eend - ep) : (long long)KW), lane);
       }
     }
-#if DGB_FLUX_PREFETCH2 && DGB_TICKET_DEPTH > 1 && DGB_TICKET_BLOCKS == 1
-    {
-      const long long wb2 = ticket_block(tks.pending, wstride);        // drawn one block ago: back by now
-      if (wb2 < nwblocks) {
-        const long long e2 = ebeg + wb2 * KW;
-        const int nel2 = (int)((eend - e2) < (long long)KW ? (eend - e2) : (long long)KW);
-        if (NP % 2 == 0) {
-          prefetch_block_rows<NP, KW>(q, C, E * NP, q, 0, 0, e2, nel2, lane);
-        } else {
-          for (int n = lane; n < C * ((KW * NP * 8 + 127) / 128 + 1); n += 32) {
-            const int c = n / ((KW * NP * 8 + 127) / 128 + 1), l = n - c * ((KW * NP * 8 + 127) / 128 + 1);
-            l2_prefetch_line(reinterpret_cast<const char*>(q + (long long)c * E * NP + e2 * NP) + 128 * l);
-          }
-        }
-        // geometry: one line each covers a block's slice
-        if (lane < DIM * DIM) l2_prefetch_line(d.drdx + (long long)lane * E + e2);
-        else if (lane < DIM * DIM + DIM) l2_prefetch_line(d.normals + ((long long)(lane - DIM * DIM) * E + e2) * NF);
-        else if (lane == DIM * DIM + DIM) l2_prefetch_line(d.fscale + e2 * NF);
-        else if (lane == DIM * DIM + DIM + 1) l2_prefetch_line(d.conn + e2 * NF);
-        else if (lane == DIM * DIM + DIM + 2) l2_prefetch_line(d.jac + e2);
-      }
-    }
-#endif
     DGB_WTICK(0);
 
     // ---- face averages q* (central flux, boundary states) -> Ss; metric coefficients ---------
@@ -503,61 +461,85 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
     __syncwarp();
     DGB_WTICK(1);
 
-    // ---- tensor-core contractions, one 8-column tile at a time; grad q of the tile -> its Ss rows ----
+    // ---- tensor-core contractions; grad q of a column tile -> its Ss rows ----
     // On a simplex  fscale n_x (face f) = sum_r a[f][r] dr/dx[r][x]  with a[0][r] = 1, a[r+1][r] = -1, so
     //   grad_x q = sum_f fscale n_x lift_f q*_f - sum_r dr/dx[r][x] Sw_r q
     //            = -sum_r dr/dx[r][x] (Z_r - U_0),   Z_r = Sw_r q + lift_{r+1} q*_{r+1},  U_0 = lift_0 q*_0:
     // DIM+1 accumulator sets instead of DIM+NF (Z_r simply continues its k-loop over the face-(r+1)
     // operand rows) and DIM*DIM + DIM FP64 operations per value in the combination instead of
     // DIM*(DIM+NF).
+    // MTF column tiles share every W fragment load (DGB_FLUX_MT)
+    constexpr int MTMODE = DGB_FLUX_MT >= 0 ? DGB_FLUX_MT : (((NP > 20) != (DGB_NSPEC > 0)) ? 2 : 0);
+    constexpr int MTF = MTMODE ? WS::NTILE : 1;
 #pragma unroll 1
-    for (int tile = 0; tile < WS::NTILE; ++tile) {
-      double accZ[DIM][1][NI][2], accU[1][NI][2];
+    for (int tile0 = 0; tile0 < WS::NTILE; tile0 += MTF) {
+      double accZ[DIM][MTF][NI][2];
+      constexpr bool UFIRST = MTMODE == 2;     // Z_r - U_0 accumulated in place: the chain of Z_r starts from -U_0
+      {
+        double accU[MTF][NI][2];
 #pragma unroll
-      for (int s = 0; s < DIM; ++s)
+        for (int mt = 0; mt < MTF; ++mt)
 #pragma unroll
-        for (int ni = 0; ni < NI; ++ni) { accZ[s][0][ni][0] = 0.0; accZ[s][0][ni][1] = 0.0; }
+          for (int ni = 0; ni < NI; ++ni) { accU[mt][ni][0] = 0.0; accU[mt][ni][1] = 0.0; }
+        if (UFIRST) mma_block<NI, MTF>(accU, W.Ss + tile0 * 8 * LDSX, LDSX, S.Wf, EL::LDL, EL::NFPK / 4, lane);
 #pragma unroll
-      for (int ni = 0; ni < NI; ++ni) { accU[0][ni][0] = 0.0; accU[0][ni][1] = 0.0; }
+        for (int mt = 0; mt < MTF; ++mt)
+#pragma unroll
+          for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+            for (int s = 0; s < DIM; ++s) {
+              accZ[s][mt][ni][0] = UFIRST ? -accU[mt][ni][0] : 0.0;
+              accZ[s][mt][ni][1] = UFIRST ? -accU[mt][ni][1] : 0.0;
+            }
+      }
 #pragma unroll
       for (int r = 0; r < DIM; ++r) {
-        mma_block<NI, 1>(accZ[r], Qs + tile * 8 * EL::LDQ, EL::LDQ, S.Wq + r * EL::NPR * EL::LDQ, EL::LDQ,
-                         EL::NPK / 4, lane);
-        mma_block<NI, 1>(accZ[r], W.Ss + tile * 8 * LDSX + (r + 1) * EL::NFPK, LDSX,
-                         S.Wf + (r + 1) * EL::NPR * EL::LDL, EL::LDL, EL::NFPK / 4, lane);
+        mma_block<NI, MTF>(accZ[r], Qs + tile0 * 8 * EL::LDQ, EL::LDQ, S.Wq + r * EL::NPR * EL::LDQ, EL::LDQ,
+                           EL::NPK / 4, lane);
+        mma_block<NI, MTF>(accZ[r], W.Ss + tile0 * 8 * LDSX + (r + 1) * EL::NFPK, LDSX,
+                           S.Wf + (r + 1) * EL::NPR * EL::LDL, EL::LDL, EL::NFPK / 4, lane);
       }
-      mma_block<NI, 1>(accU, W.Ss + tile * 8 * LDSX, LDSX, S.Wf, EL::LDL, EL::NFPK / 4, lane);
-      __syncwarp();                       // every lane has read this tile's q* rows: they may be overwritten
+      double accU[MTF][NI][2];
+#pragma unroll
+      for (int mt = 0; mt < MTF; ++mt)
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) { accU[mt][ni][0] = 0.0; accU[mt][ni][1] = 0.0; }
+      if (!UFIRST) mma_block<NI, MTF>(accU, W.Ss + tile0 * 8 * LDSX, LDSX, S.Wf, EL::LDL, EL::NFPK / 4, lane);
+      __syncwarp();                       // every lane has read these tiles' q* rows: they may be overwritten
       const int k8 = lane >> 2;
-      const int col = tile * 8 + k8;
-      const int c = col / KW, e = col - c * KW;
       // rows of grad q are NP doubles apart: for even NP consecutive columns of a quarter warp would overlap in
       // half their banks (2-way conflicts on every 16-byte store, ncu: 7.5 wavefronts instead of 4); swapping
       // bits 0 and 1 of the column puts them 2 rows = 64 bytes (mod 128) apart
       const int k8s = grad_row_swizzle<NP>(k8);
-      if (col < WS::NCOL && e < nel) {
-        double* sg = W.Ss + tile * 8 * LDSX;
-        double m[DIM][DIM];               // m[r][x] = -dr/dx[r][x]
 #pragma unroll
-        for (int r = 0; r < DIM; ++r)
+      for (int mt = 0; mt < MTF; ++mt) {
+        const int tile = tile0 + mt;
+        const int col = tile * 8 + k8;
+        const int c = col / KW, e = col - c * KW;
+        if (col < WS::NCOL && e < nel) {
+          double* sg = W.Ss + tile * 8 * LDSX;
+          double m[DIM][DIM];               // m[r][x] = -dr/dx[r][x]
 #pragma unroll
-          for (int x = 0; x < DIM; ++x) m[r][x] = -geo.drdx[r * DIM + x][e];
+          for (int r = 0; r < DIM; ++r)
 #pragma unroll
-        for (int ni = 0; ni < NI; ++ni) {
-          double z0[DIM], z1[DIM];
+            for (int x = 0; x < DIM; ++x) m[r][x] = -geo.drdx[r * DIM + x][e];
 #pragma unroll
-          for (int r = 0; r < DIM; ++r) { z0[r] = accZ[r][0][ni][0] - accU[0][ni][0]; z1[r] = accZ[r][0][ni][1] - accU[0][ni][1]; }
-          const int i = ni * 8 + 2 * (lane & 3);
+          for (int ni = 0; ni < NI; ++ni) {
+            double z0[DIM], z1[DIM];
 #pragma unroll
-          for (int x = 0; x < DIM; ++x) {
-            double v0 = m[0][x] * z0[0], v1 = m[0][x] * z1[0];
+            for (int r = 0; r < DIM; ++r) { z0[r] = accZ[r][mt][ni][0] - accU[mt][ni][0]; z1[r] = accZ[r][mt][ni][1] - accU[mt][ni][1]; }
+            const int i = ni * 8 + 2 * (lane & 3);
 #pragma unroll
-            for (int r = 1; r < DIM; ++r) { v0 += m[r][x] * z0[r]; v1 += m[r][x] * z1[r]; }
-            if (NP % 2 == 0) {
-              if (i < NP) *reinterpret_cast<double2*>(sg + (x * 8 + k8s) * NP + i) = make_double2(v0, v1);
-            } else {
-              if (i < NP) sg[(x * 8 + k8s) * NP + i] = v0;
-              if (i + 1 < NP) sg[(x * 8 + k8s) * NP + i + 1] = v1;
+            for (int x = 0; x < DIM; ++x) {
+              double v0 = m[0][x] * z0[0], v1 = m[0][x] * z1[0];
+#pragma unroll
+              for (int r = 1; r < DIM; ++r) { v0 += m[r][x] * z0[r]; v1 += m[r][x] * z1[r]; }
+              if (NP % 2 == 0) {
+                if (i < NP) *reinterpret_cast<double2*>(sg + (x * 8 + k8s) * NP + i) = make_double2(v0, v1);
+              } else {
+                if (i < NP) sg[(x * 8 + k8s) * NP + i] = v0;
+                if (i + 1 < NP) sg[(x * 8 + k8s) * NP + i + 1] = v1;
+              }
             }
           }
         }

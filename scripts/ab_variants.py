@@ -16,13 +16,15 @@ PKG = os.path.join(ROOT, "paper_2512_17101_b200")
 VARIANTS = {
     "timing": ["DGB_PHASE_TIMING=1"],                 # scripts/phase_timing_flux.py
     "base": [],
+    "mt": ["DGB_FLUX_MT=1"],
+    "mtu": ["DGB_FLUX_MT=2"],
+    "mtu_w8": ["DGB_FLUX_MT=2", "DGB_FLUX_WARPS=8"],
+    "mt_w8": ["DGB_FLUX_MT=1", "DGB_FLUX_WARPS=8"],
     "flux_w14": ["DGB_FLUX_WARPS=16"],
     "stcs": ["DGB_STREAMING_STORES=1"],
     "tk2": ["DGB_TICKET_BLOCKS=2"],
     "euler_w8": ["DGB_EULER_WARPS=8"],
     "div_w12_nb1": ["DGB_DIV_WARPS=12", "DGB_DIV_NB=1"],
-    "f_nolean": ["DGB_FLUX_LEAN=0"],
-    "f_nolean_w11": ["DGB_FLUX_LEAN=0", "DGB_FLUX_WARPS=11"],
     "f_w11": ["DGB_FLUX_WARPS=11"],
     "f_w10": ["DGB_FLUX_WARPS=10"],
     "f_w8": ["DGB_FLUX_WARPS=8"],
@@ -32,7 +34,6 @@ VARIANTS = {
     "d10_nb2": ["DGB_DIV8_WARPS=10", "DGB_DIV8_NB=2"],
     "nb2": ["DGB_DIV8_NB=2"],
     "nb3": ["DGB_DIV8_NB=3"],
-    "pf2": ["DGB_FLUX_PREFETCH2=1"],
     "noearly": ["DGB_DIV8_EARLY=0"],
     "nosq": ["DGB_FLUX_SINGLEQ=0"],
     "agg": ["DGB_TICKET_NOAGG=0"],
