@@ -381,6 +381,10 @@ def _ms_params(f, qfar, transport, C_):
     mix = getattr(f, "dg_mix", None)
     if mix is None:
         raise errors.BindingMismatch(f"{f.__name__}: the outlined function carries no mixture (f.dg_mix)")
+    return _mix_params(mix, qfar, transport, C_)
+
+
+def _mix_params(mix, qfar, transport, C_):
     m = np.concatenate([[mix.ns], mix.R, mix.cv, mix.h0, [mix.A, mix.Ta, mix.reaction[0], mix.reaction[1]]]).astype(np.float64)
     qf = _host_vec(qfar, C_)
     tr = np.zeros(3) if transport is None else _host_vec(transport, 3)
@@ -420,6 +424,48 @@ def _ms_div(actx, f, disc, q, T, ghost, Tghost, jac, facemat, facemat_p, qfar):
                                           tr.ctypes.data, m.ctypes.data, 0, -1, actx._st), "dg_ms_div")
     actx.launch_count += 1
     return out
+
+
+def _ms_op_disc(actx, op, q, nghost):
+    d = op.dcoll
+    disc = get_disc(actx, op.dim, q, nghost, d.Sw, d.drdx, d.lift, d.normals, d.fscale, d.vmap_m, d.vmap_p, d.bc_kind,
+                    nspecies=op.mix.ns)
+    _bind_jacobian(actx, disc, d.jac)
+    return disc
+
+
+def _ms_op_fused(op):
+    """The sub-range launches bypass the outlined bodies: refuse when their source no longer matches the kernels."""
+    if not (getattr(op._flux, "fused", False) and getattr(op._div, "fused", False)):
+        raise errors.BindingMismatch("multi-species sub-range launches need the fused dg_ms_flux / dg_ms_div "
+                                     "(operator built with fused=False, or an edited body)")
+
+
+def ms_flux_range(actx, op, q, ghost, T, lo, hi):
+    """``T[:, lo:hi] = dg_ms_flux(q)[:, lo:hi]`` (dgb_ms_flux_range) for a ``MultispeciesOperator``."""
+    _ms_op_fused(op)
+    q = _f64(actx, q, "q")
+    G, g, gptr = _ghost_ptr(actx, ghost, (op.ncomp,), q.shape[-1])
+    disc = _ms_op_disc(actx, op, q, G)
+    m, qf, tr = _mix_params(op.mix, op.qfar, op.transport, op.ncomp)
+    _cabi.check(actx.lib.dgb_ms_flux_range(disc.handle, q.ptr, gptr, T.ptr, qf.ctypes.data, tr.ctypes.data,
+                                           m.ctypes.data, int(lo), int(hi), actx._st), "dg_ms_flux (range)")
+    actx.launch_count += 1
+
+
+def ms_div_range(actx, op, q, T, ghost, Tghost, out, lo, hi):
+    """``out[:, lo:hi] = dg_ms_div(q, T)[:, lo:hi]`` (dgb_ms_div_range) for a ``MultispeciesOperator``."""
+    _ms_op_fused(op)
+    q = _f64(actx, q, "q")
+    npl = ms_flux_planes(op.dim, op.mix.ns)
+    G, g, gptr = _ghost_ptr(actx, ghost, (op.ncomp,), q.shape[-1])
+    TG, tg, tgptr = _ghost_ptr(actx, Tghost, (npl,), q.shape[-1])
+    disc = _ms_op_disc(actx, op, q, G)
+    _check_facemat(disc, op.dcoll.facemat, op.dcoll.facemat_p)
+    m, qf, tr = _mix_params(op.mix, op.qfar, None, op.ncomp)
+    _cabi.check(actx.lib.dgb_ms_div_range(disc.handle, q.ptr, T.ptr, gptr, tgptr, out.ptr, qf.ctypes.data,
+                                          tr.ctypes.data, m.ctypes.data, int(lo), int(hi), actx._st), "dg_ms_div (range)")
+    actx.launch_count += 1
 
 
 def dg_ms_flux(actx, f, q, ghost, Sw, drdx, jac, lift, normals, fscale, vmap_m, vmap_p, bc_kind, qfar, transport):

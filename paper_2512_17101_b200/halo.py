@@ -401,9 +401,30 @@ class HaloExchange:
         return DOFArray(actx, out)
 
     def ms_rhs(self, op, q: DOFArray) -> DOFArray:
-        """Multispecies operator (array program on the generic ops): state halos, then flux-plane halos."""
-        ghost = self.exchange(q.data)
-        return op.rhs(q, ghost=ghost, halo_fn=lambda FL: self.exchange(FL.data))
+        """Multi-species operator: state halos, then flux-plane halos; with the fused kernels each exchange runs
+        under the interior range of its pass, like ``ns_rhs``."""
+        if not (self._can_overlap() and getattr(op._flux, "fused", False) and getattr(op._div, "fused", False)):
+            ghost = self.exchange(q.data)
+            return op.rhs(q, ghost=ghost, halo_fn=lambda FL: self.exchange(FL.data))
+        from . import fused
+        actx, nI, E = self.actx, self.plan.n_interior, self.plan.nlocal
+        t1 = self._begin(q.data)
+        T = actx.empty((fused.ms_flux_planes(op.dim, op.mix.ns),) + tuple(q.data.shape[1:]))
+        self._reserve(True)
+        fused.ms_flux_range(actx, op, q.data, self._ghost_of(t1), T, 0, nI)
+        self._reserve(False)
+        ghost = self._end(t1)
+        fused.ms_flux_range(actx, op, q.data, ghost, T, nI, E)
+        t2 = self._begin(T)
+        out = actx.empty(q.data.shape)
+        self._reserve(True)
+        fused.ms_div_range(actx, op, q.data, T, ghost, self._ghost_of(t2), out, 0, nI)
+        self._reserve(False)
+        tghost = self._end(t2)
+        fused.ms_div_range(actx, op, q.data, T, ghost, tghost, out, nI, E)
+        self._release(t1)
+        self._release(t2)
+        return DOFArray(actx, out)
 
     def ns_rhs_grad_form(self, op, q: DOFArray) -> DOFArray:
         ghost = self.exchange(q.data)
