@@ -115,6 +115,9 @@ def box_mesh(counts, lo, hi, periodic=None, morton: bool = True) -> Mesh:
     return mesh
 
 
+_KEY_LIMIT = 2.0 ** 62        # packed face keys stay below this (tests lower it to force the two-level path)
+
+
 def _connect(dim: int, vertices: np.ndarray, vid: np.ndarray) -> Mesh:
     """Face matching by sorted global vertex ids; integer-exact."""
     E = vid.shape[0]
@@ -123,11 +126,16 @@ def _connect(dim: int, vertices: np.ndarray, vid: np.ndarray) -> Mesh:
     fvid = vid[:, fv]                                   # (E, Nf, dim) in local ascending order
     srt = np.sort(fvid, axis=2)
     nvert = int(vid.max()) + 1
-    if float(nvert) ** dim >= 2.0 ** 62:
-        raise ValueError("mesh too large for packed face keys")
     key = np.zeros((E, Nf), dtype=np.int64)
+    span = 1.0                                           # upper bound of the keys packed so far
     for a in range(dim):
+        if span * nvert >= _KEY_LIMIT:                   # would overflow: rank the partial keys first (equality-preserving)
+            if float(E * Nf) * nvert >= 2.0 ** 62:
+                raise ValueError("mesh too large for packed face keys")
+            key = np.unique(key.ravel(), return_inverse=True)[1].reshape(E, Nf).astype(np.int64)
+            span = float(E * Nf)
         key = key * nvert + srt[..., a]
+        span *= nvert
     flat = key.ravel()
     order = np.argsort(flat, kind="stable")
     sk = flat[order]

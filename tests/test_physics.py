@@ -96,3 +96,16 @@ def test_isentropic_vortex_convergence():
         errs.append(d.norm_l2(d.to_numpy(q) - _vortex(d.nodes(), T)))
     rate = np.log2(errs[0] / errs[1])
     assert rate > 2.5, (errs, rate)
+
+
+@pytest.mark.parametrize("dims,per", [((4, 4, 4), True), ((5, 4, 3), False), ((6, 5), True)])
+def test_mesh_connectivity_with_two_level_face_keys(dims, per, monkeypatch):
+    """Meshes whose packed face keys (nvert**dim) would overflow 62 bits (periodic 3D boxes beyond n = 118) rank the
+    partial keys first; forced here on small meshes, the connectivity must not change."""
+    from paper_2512_17101_b200.dg import mesh as M
+    dim = len(dims)
+    a = M.box_mesh(dims, (-1,) * dim, (1,) * dim, periodic=(per,) * dim)
+    monkeypatch.setattr(M, "_KEY_LIMIT", 2.0 ** 9)
+    b = M.box_mesh(dims, (-1,) * dim, (1,) * dim, periodic=(per,) * dim)
+    for f in ("nbr_elem", "nbr_face", "nbr_perm", "btag"):
+        assert np.array_equal(getattr(a, f), getattr(b, f)), f
