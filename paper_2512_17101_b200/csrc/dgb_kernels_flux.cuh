@@ -44,6 +44,15 @@
 #ifndef DGB_FLUX_MT
 #define DGB_FLUX_MT -1
 #endif
+// pass 1: unroll factor of the pointwise node loop (2 lane rounds at order 3, 4 at order 4; ~10 KB of SASS per copy).
+// Not unrolled, the kernel is 33 instead of 40 KB at order 3 (57 / 76 at order 4; the L1.5 instruction cache holds 32 KB):
+// pass 1 -0.5 % at order 3, -1.9 % at order 4 (profiles/r02_pass2_tma.md section 13)
+#ifndef DGB_FLUX_PW_UNROLL
+#define DGB_FLUX_PW_UNROLL 1
+#endif
+#ifndef DGB_EULER_PW_UNROLL
+#define DGB_EULER_PW_UNROLL 1
+#endif
 #ifndef DGB_FLUX_SINGLEQ
 #define DGB_FLUX_SINGLEQ -1
 #endif
@@ -562,7 +571,8 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
     }
 
     // ---- pointwise: total flux at every node, contravariant + Jacobian-scaled, and the wave speed ----
-#pragma unroll
+    constexpr int PWU = DGB_FLUX_PW_UNROLL;
+#pragma unroll PWU
     for (int n0 = 0; n0 < KW * NP; n0 += 32) {
       const int n = n0 + lane;
       const int e = n / NP, j = n - e * NP;
@@ -1148,7 +1158,8 @@ k_euler4(DiscDev d, const double* __restrict__ q, const double* __restrict__ gho
     }
 
     // ---- volume flux -> contravariant operand rows, wave speed ---------------------------------
-#pragma unroll
+    constexpr int PWU = DGB_EULER_PW_UNROLL;
+#pragma unroll PWU
     for (int n0 = 0; n0 < KW * NP; n0 += 32) {
       const int n = n0 + lane;
       const int e = n / NP, j = n - e * NP;

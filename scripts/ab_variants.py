@@ -16,6 +16,8 @@ PKG = os.path.join(ROOT, "paper_2512_17101_b200")
 VARIANTS = {
     "timing": ["DGB_PHASE_TIMING=1"],                 # scripts/phase_timing_flux.py
     "base": [],
+    "pwu4": ["DGB_FLUX_PW_UNROLL=4"],
+    "epwu1": ["DGB_EULER_PW_UNROLL=1"],
     "mt": ["DGB_FLUX_MT=1"],
     "mtu": ["DGB_FLUX_MT=2"],
     "mtu_w8": ["DGB_FLUX_MT=2", "DGB_FLUX_WARPS=8"],
