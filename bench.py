@@ -35,10 +35,10 @@ PHYS = dict(gamma=1.4, mu=1e-3, prandtl=0.72, rgas=1.0)
 CPU_REPS = 16          # RHS evaluations per process in one CPU sample (~10-15 s of CPU work)
 
 
-def workload_name(n, workload="ns"):
+def workload_name(n, workload="ns", species=3):
     E = 6 * n ** 3
     if workload == "multispecies":
-        return (f"3D multi-species reactive Navier-Stokes DG RHS (3 species, 1 Arrhenius step, C = 8 fields; fused kernels "
+        return (f"3D multi-species reactive Navier-Stokes DG RHS ({species} species, 1 Arrhenius step, C = {5 + species} fields; fused kernels "
                 f"dgb_ms_flux + dgb_ms_div), Kuhn tets order {ORDER}, periodic {n}^3 box per GPU: {E} elements, "
                 f"{E * NP} DOFs per GPU (BASELINE configs[4])")
     if workload == "euler":
@@ -317,7 +317,9 @@ def run_b200(args):
     multi = args.workload == "multispecies"
     if multi:
         from paper_2512_17101_b200 import Mixture, MultispeciesOperator
-        op = MultispeciesOperator(d, Mixture())
+        mixtures = {2: dict(R=(1.0, 0.8), cv=(2.5, 2.0), h0=(0.5, -0.5), reaction=(0, 1)), 3: {},
+                    4: dict(R=(1.0, 0.8, 1.2, 0.9), cv=(2.5, 2.0, 3.0, 2.2), h0=(0.5, -0.5, 0.0, 0.1), reaction=(0, 3))}
+        op = MultispeciesOperator(d, Mixture(**mixtures[args.species]))
     elif euler:
         from paper_2512_17101_b200 import EulerOperator
         op = EulerOperator(d, gamma=PHYS["gamma"])
@@ -327,9 +329,9 @@ def run_b200(args):
     ndof = E * Np
     ncomp = op.ncomp if multi else DIM + 2
     q_host = actx.pinned_empty((ncomp, E, Np))
-    if multi:       # smooth seeded state: rho, u, T perturbed, three mass fractions
+    if multi:       # smooth seeded state: rho, u, T perturbed, the mass fractions
         rng = np.random.default_rng(20251217 + rank)
-        Y = rng.uniform(0.2, 0.4, (3, E, Np)); Y /= Y.sum(axis=0)
+        Y = rng.uniform(0.2, 0.4, (args.species, E, Np)); Y /= Y.sum(axis=0)
         q_host[...] = op.state_from_primitive(rng.uniform(0.9, 1.1, (E, Np)), rng.uniform(-0.1, 0.1, (DIM, E, Np)),
                                               rng.uniform(0.9, 1.1, (E, Np)), Y)
     else:
@@ -423,8 +425,8 @@ def run_b200(args):
         ms_grad = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
         ms_div = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
         if multi:       # the NS split of the 72 C bytes: pass 1 reads q, writes d C planes; pass 2 reads both, writes rhs
-            dom = (("k_nsdiv8<C=8> (dgb_ms_div)", ms_div, 40.0 * ncomp) if ms_div >= ms_grad else
-                   ("k_nsflux3<C=8> (dgb_ms_flux)", ms_grad, 32.0 * ncomp))
+            dom = ((f"k_nsdiv8<C={ncomp}> (dgb_ms_div)", ms_div, 40.0 * ncomp) if ms_div >= ms_grad else
+                   (f"k_nsflux3<C={ncomp}> (dgb_ms_flux)", ms_grad, 32.0 * ncomp))
         elif euler:
             dom = ("k_euler4 (fused Euler RHS)", ms_div, 80.0)
         else:
@@ -541,8 +543,8 @@ def run_b200(args):
             "higher_is_better": True, "scaling": "strong" if (strong and world > 1) else "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"numa_node_bound": numa_node,
-                       "workload": workload_name(n, args.workload) if not (strong and world > 1) else
-                       workload_name(n, args.workload).replace("per GPU", "in total"),
+                       "workload": workload_name(n, args.workload, args.species) if not (strong and world > 1) else
+                       workload_name(n, args.workload, args.species).replace("per GPU", "in total"),
                        "elements_per_gpu": E, "dofs_per_gpu": ndof, "order": ORDER, "dim": DIM,
                        "l2_policy": "inputs larger than L2 (q 4.0 GB, grad q 12 GB per GPU vs 126 MB L2)"
                        if ndof * 40 > 126e6 * 4 else "inputs comparable to L2: reduced size, not the headline config",
@@ -588,6 +590,7 @@ def main():
                          "pack kernel stores into the neighbour's ghost array through CUDA-IPC peer memory (NVLink)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N>1: weak = one n^3 box per GPU in a ring (default); strong = one n^3 box partitioned over the GPUs")
+    ap.add_argument("--species", type=int, default=3, choices=[2, 3, 4], help="--workload multispecies: species count")
     ap.add_argument("--workload", default="ns", choices=["ns", "euler", "multispecies"],
                     help="ns = BASELINE configs[2] (headline); euler = configs[1] (3D Euler, read q + write rhs = 80 B/DOF)")
     args = ap.parse_args()

@@ -158,8 +158,8 @@ int dgb_ns_div_range(const dgb_disc* disc, const double* q_dev, const double* T_
 /* ---- multi-species reactive Navier-Stokes (BASELINE configs[4]): the outlined functions dg_ms_flux / dg_ms_div of
  *      multispecies.py (Call nodes of the reference: adfg.py:722-803; op families: IndexLambda with exp / truediv,
  *      /root/reference/pkg/src/laze/expr.py:265-289, Einsum adfg.py:563-608, Indexing :502-560) on the same fused
- *      kernels instantiated for C = dim + 2 + 3 fields.  q: (C, E, Np); T: ((dim+1)*C + 1, E, Np) plane groups as
- *      in dgb_ns_flux; transport_host = [mu, kappa, D]; mixture_host = [ns = 3, R[ns], cv[ns], h0[ns], A, Ta,
+ *      kernels instantiated for C = dim + 2 + ns fields, ns = 2, 3 or 4 (DGB_ERR_INVALID otherwise).  q: (C, E, Np); T: ((dim+1)*C + 1, E, Np) plane groups as
+ *      in dgb_ns_flux; transport_host = [mu, kappa, D]; mixture_host = [ns, R[ns], cv[ns], h0[ns], A, Ta,
  *      reactant, product]; boundary faces take qfar_host (C values) as exterior state; eend < 0 = all elements. ---- */
 int dgb_ms_flux_range(const dgb_disc* disc, const double* q_dev, const double* ghost_dev, double* T_dev,
                       const double* qfar_host, const double* transport_host, const double* mixture_host,

@@ -7,7 +7,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 OUT = os.path.join(os.path.dirname(HERE), "libdgb200.so")
-SOURCES = ["dgb200.cu", "dgb_nsflux.cu", "dgb_msflux.cu", "dgb_arrayops.cu"]
+SOURCES = ["dgb200.cu", "dgb_nsflux.cu", "dgb_msflux.cu", "dgb_msflux2.cu", "dgb_msflux3.cu", "dgb_msflux4.cu", "dgb_arrayops.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-shared", "-Xcompiler", "-fPIC"]
 

@@ -1,6 +1,6 @@
-// Launch configuration of the flux-arrangement kernels (k_nsflux3 + k_nsdiv8 / k_nsdiv3), shared by the two
-// translation units that instantiate them: dgb_nsflux.cu (single-species, DGB_NSPEC = 0) and dgb_msflux.cu (the
-// multi-species operator: the same templates compiled once more with DGB_NSPEC = 3).
+// Launch configuration of the flux-arrangement kernels (k_nsflux3 + k_nsdiv8 / k_nsdiv3), shared by the
+// translation units that instantiate them: dgb_nsflux.cu (single-species, DGB_NSPEC = 0) and dgb_msflux{2,3,4}.cu (the
+// multi-species operator: the same templates compiled once more per species count, DGB_NSPEC = 2, 3, 4).
 #pragma once
 #include "dgb_internal.h"
 #include "dgb_kernels_flux.cuh"

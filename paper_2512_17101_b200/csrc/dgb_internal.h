@@ -5,6 +5,8 @@
 
 #include <string>
 
+#define DGB_HIDDEN __attribute__((visibility("hidden")))   // shared between translation units, not exported
+
 int dgb_fail(int code, const std::string& msg);   // records the message for dgb_last_error()
 int dgb_num_sms();                                // SMs of the CURRENT device
 int dgb_grid_sms();                               // SMs a persistent kernel may occupy: dgb_num_sms() minus the reserve (dgb_set_sm_reserve)

@@ -16,8 +16,8 @@
 #define DGB_STREAMING_STORES 0
 #endif
 // Number of species fields carried next to [rho, rho E, rho u]: 0 = single-species Euler / Navier-Stokes
-// (libdgb200's default translation units); dgb_msflux.cu compiles the SAME kernel templates once more with
-// DGB_NSPEC = 3 (and the namespace renamed) for the multi-species reactive operator (multispecies.py).
+// (libdgb200's default translation units); dgb_msflux{2,3,4}.cu compile the SAME kernel templates once more with
+// DGB_NSPEC = 2, 3, 4 (and the namespace renamed per count) for the multi-species reactive operator (multispecies.py).
 #ifndef DGB_NSPEC
 #define DGB_NSPEC 0
 #endif

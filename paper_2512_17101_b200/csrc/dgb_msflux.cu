@@ -1,87 +1,51 @@
-// Multi-species reactive Navier-Stokes (BASELINE configs[4], multispecies.py: dg_ms_flux / dg_ms_div) on the fused
-// kernels of the flux arrangement: this translation unit compiles the SAME templates (k_nsflux3, k_nsdiv8) once
-// more with DGB_NSPEC = 3 extra species fields -- C = dim + 5 conserved fields, the temperature as one more field
-// of the BR1 gradient, the mixture physics of dgb_kernels.cuh, the Arrhenius source in the store epilogue of pass
-// 2.  The namespace of the templates is renamed so that the two instantiation sets cannot collide in libdgb200.so;
-// the plain structs the handle carries (DiscDev, Phys, Epilogue) do not depend on the field count.
-#define DGB_NSPEC 3
-#define dgb dgbms3
-#include "dgb_flux_launch.cuh"
+// Public entry points of the fused multi-species operator: dispatch on the species count (mixture[0]) to the
+// translation unit that instantiates the kernel templates for it (dgb_msflux2.cu, dgb_msflux3.cu, dgb_msflux4.cu).
+#include "dgb_internal.h"
 
-namespace {
-
-constexpr int kNS = DGB_NSPEC;
-
-// mixture = [ns, R[ns], cv[ns], h0[ns], A, Ta, reactant, product]; transport = [mu, kappa, D]
-int make_ms_phys(dgb::Phys& ph, int dim, const double* qfar, const double* transport, const double* mixture) {
-  if (!qfar || !transport || !mixture) return dgb_fail(DGB_ERR_INVALID, "qfar, transport and mixture are required");
-  if ((int)mixture[0] != kNS) return dgb_fail(DGB_ERR_INVALID, "the fused multi-species kernels are built for 3 species");
-  ph = dgb::Phys{};
-  ph.mu = transport[0]; ph.kappa = transport[1]; ph.dspec = transport[2];
-  for (int c = 0; c < dim + 2 + kNS; ++c) ph.qfar[c] = qfar[c];
-  for (int k = 0; k < kNS; ++k) { ph.mR[k] = mixture[1 + k]; ph.mcv[k] = mixture[1 + kNS + k]; ph.mh0[k] = mixture[1 + 2 * kNS + k]; }
-  ph.arr_A = mixture[1 + 3 * kNS]; ph.arr_Ta = mixture[2 + 3 * kNS];
-  ph.ra = (int)mixture[3 + 3 * kNS]; ph.rb = (int)mixture[4 + 3 * kNS];
-  if (ph.ra < 0 || ph.ra >= kNS || ph.rb < 0 || ph.rb >= kNS) return dgb_fail(DGB_ERR_INVALID, "reaction species out of range");
-  return DGB_OK;
-}
-
-int check_range(const dgb_disc* d, int64_t ebegin, int64_t eend) {
-  if (ebegin < 0 || eend > d->dev.E || ebegin > eend) return dgb_fail(DGB_ERR_INVALID, "element range outside [0, E]");
-  return DGB_OK;
-}
-
-}  // namespace
+#define DGB_MS_COUNTS(X) X(2) X(3) X(4)
 
 extern "C" {
 
-int dgb_ms_flux_range(const dgb_disc* d, const double* q, const double* ghost, double* T, const double* qfar,
-                      const double* transport, const double* mixture, int64_t ebegin, int64_t eend, void* stream) {
-  int rc = check_flux_args(d, ghost, q, T); if (rc) return rc;
-  if (eend < 0) eend = d->dev.E;
-  if ((rc = check_range(d, ebegin, eend))) return rc;
-  dgb::Phys ph; if ((rc = make_ms_phys(ph, d->dim, qfar, transport, mixture))) return rc;
-#define X(DIM, P) if (d->dim == DIM && d->order == P) return launch_flux<DIM, P>(d, q, ghost, T, ph, ebegin, eend, (cudaStream_t)stream);
-  DGB_FOR_EACH_ELEMENT(X)
+#define X(K)                                                                                                              \
+  DGB_HIDDEN int dgb_ms_flux_range_ns##K(const dgb_disc*, const double*, const double*, double*, const double*, const double*, \
+                                         const double*, int64_t, int64_t, void*);                                         \
+  DGB_HIDDEN int dgb_ms_div_range_ns##K(const dgb_disc*, const double*, const double*, const double*, const double*, double*, \
+                                        const double*, const double*, const double*, int64_t, int64_t, void*);            \
+  DGB_HIDDEN int dgb_ms_div_rk_ns##K(const dgb_disc*, const double*, const double*, const double*, const double*,        \
+                                     const double*, double*, const double*, double*, const double*, const double*,        \
+                                     const double*, const double*, void*);
+DGB_MS_COUNTS(X)
 #undef X
-  return dgb_fail(DGB_ERR_INVALID, "unsupported (dim, order)");
+
+static int no_count(const double* mixture) {
+  if (!mixture) return dgb_fail(DGB_ERR_INVALID, "qfar, transport and mixture are required");
+  return dgb_fail(DGB_ERR_INVALID, "the fused multi-species kernels are built for 2, 3 and 4 species");
 }
 
-static int ms_div_impl(const dgb_disc* d, const double* q, const double* T, const double* ghost, const double* Tghost,
-                       const dgb::Epilogue& ep, const double* qfar, const double* transport, const double* mixture,
-                       int64_t ebegin, int64_t eend, void* stream) {
-  int rc = check_flux_args(d, ghost, q, T); if (rc) return rc;
-  if (eend < 0) eend = d->dev.E;
-  if ((rc = check_range(d, ebegin, eend))) return rc;
-  if (d->dev.G > 0 && !Tghost) return dgb_fail(DGB_ERR_INVALID, "ghost elements need the ghost flux planes");
-  dgb::Phys ph; if ((rc = make_ms_phys(ph, d->dim, qfar, transport, mixture))) return rc;
-#define X(DIM, P) if (d->dim == DIM && d->order == P)                                                         \
-    return launch_div_any<DIM, P>(d, q, T, ghost, Tghost, ep, ph, ebegin, eend, (cudaStream_t)stream, div_kernel());
-  DGB_FOR_EACH_ELEMENT(X)
+int dgb_ms_flux_range(const dgb_disc* d, const double* q, const double* ghost, double* T, const double* qfar,
+                      const double* transport, const double* mixture, int64_t ebegin, int64_t eend, void* stream) {
+#define X(K) if (mixture && (int)mixture[0] == K) return dgb_ms_flux_range_ns##K(d, q, ghost, T, qfar, transport, mixture, ebegin, eend, stream);
+  DGB_MS_COUNTS(X)
 #undef X
-  return dgb_fail(DGB_ERR_INVALID, "unsupported (dim, order)");
+  return no_count(mixture);
 }
 
 int dgb_ms_div_range(const dgb_disc* d, const double* q, const double* T, const double* ghost, const double* Tghost,
                      double* rhs, const double* qfar, const double* transport, const double* mixture,
                      int64_t ebegin, int64_t eend, void* stream) {
-  if (!rhs) return dgb_fail(DGB_ERR_INVALID, "null output");
-  dgb::Epilogue ep{nullptr, rhs, nullptr, nullptr, 0.0, 1.0, 0.0, 0.0};
-  return ms_div_impl(d, q, T, ghost, Tghost, ep, qfar, transport, mixture, ebegin, eend, stream);
+#define X(K) if (mixture && (int)mixture[0] == K) return dgb_ms_div_range_ns##K(d, q, T, ghost, Tghost, rhs, qfar, transport, mixture, ebegin, eend, stream);
+  DGB_MS_COUNTS(X)
+#undef X
+  return no_count(mixture);
 }
 
-// pass 2 with the RK stage update fused into the store: out1 = rk[0]*x1 + rk[1]*rhs, out2 = rk[2]*x2 + rk[3]*rhs
 int dgb_ms_div_rk(const dgb_disc* d, const double* q, const double* T, const double* ghost, const double* Tghost,
                   const double* x1, double* out1, const double* x2, double* out2, const double* rk,
                   const double* qfar, const double* transport, const double* mixture, void* stream) {
-  if (!out1 || !rk) return dgb_fail(DGB_ERR_INVALID, "out1 and rk are required");
-  if (out1 == q || (out2 && out2 == q) || (x2 && out1 == x2))
-    return dgb_fail(DGB_ERR_INVALID, "RK outputs must not alias the stage input q (neighbours still read it)");
-  if (out2 && !x2) return dgb_fail(DGB_ERR_INVALID, "out2 needs x2");
-  if ((((uintptr_t)x1) | ((uintptr_t)out1) | ((uintptr_t)x2) | ((uintptr_t)out2)) & 15)
-    return dgb_fail(DGB_ERR_INVALID, "RK operands and outputs must be 16-byte aligned");
-  dgb::Epilogue ep{x1, out1, x2, out2, rk[0], rk[1], rk[2], rk[3]};
-  return ms_div_impl(d, q, T, ghost, Tghost, ep, qfar, transport, mixture, 0, -1, stream);
+#define X(K) if (mixture && (int)mixture[0] == K) return dgb_ms_div_rk_ns##K(d, q, T, ghost, Tghost, x1, out1, x2, out2, rk, qfar, transport, mixture, stream);
+  DGB_MS_COUNTS(X)
+#undef X
+  return no_count(mixture);
 }
 
 }  // extern "C"

@@ -370,7 +370,7 @@ def ns_div_range(actx, op, q, T, ghost, Tghost, out, lo, hi):
 
 # {{{ multi-species reactive Navier-Stokes (multispecies.py): dgb_ms_flux / dgb_ms_div
 
-MS_FUSED_SPECIES = 3          # the species count libdgb200 instantiates the kernels for (csrc/dgb_msflux.cu)
+MS_FUSED_SPECIES = (2, 3, 4)  # the species counts libdgb200 instantiates the kernels for (csrc/dgb_msflux{2,3,4}.cu)
 
 
 def ms_flux_planes(dim: int, ns: int) -> int:
@@ -490,7 +490,7 @@ def supported(f) -> bool:
     """Whether the fused kernels exist for this outlined function's configuration (else: op by op on the device)."""
     if f.__name__ in ("dg_ms_flux", "dg_ms_div", "dg_ms_rhs"):
         mix = getattr(f, "dg_mix", None)
-        return mix is not None and mix.ns == MS_FUSED_SPECIES
+        return mix is not None and mix.ns in MS_FUSED_SPECIES
     return True
 
 # }}}

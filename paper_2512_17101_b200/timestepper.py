@@ -40,8 +40,8 @@ class DeviceRK4:
         self.viscous = hasattr(op, "flux")
         shape = tuple(q0.data.shape)
         dim = op.dim
-        if self.multi and op.mix.ns != fused.MS_FUSED_SPECIES:
-            raise errors.LazeError("DeviceRK4 needs the fused multi-species kernels (3 species)")
+        if self.multi and op.mix.ns not in fused.MS_FUSED_SPECIES:
+            raise errors.LazeError("DeviceRK4 needs the fused multi-species kernels (2, 3 or 4 species)")
         self.q = actx.empty(shape)
         self._d2d(self.q, actx._contiguous(q0.data))
         self.s1, self.s2, self.acc = actx.empty(shape), actx.empty(shape), actx.empty(shape)

@@ -69,7 +69,7 @@ def main():
         from paper_2512_17101_b200.csrc.build import FLAGS, HERE
         cflags = [f for f in FLAGS if f != "-shared"] + (["-DDGB_ONLY_3D_P3"] if "--p3only" in sys.argv else [])
         objs = []
-        for src in ("dgb200.cu", "dgb_arrayops.cu", "dgb_msflux.cu"):
+        for src in ("dgb200.cu", "dgb_arrayops.cu", "dgb_msflux.cu", "dgb_msflux2.cu", "dgb_msflux3.cu", "dgb_msflux4.cu"):
             obj = os.path.join("/tmp", src.replace(".cu", ".o"))
             if not os.path.exists(obj) or os.path.getmtime(obj) < max(
                     os.path.getmtime(os.path.join(HERE, f)) for f in os.listdir(HERE) if f.endswith((".cu", ".cuh", ".h"))):

@@ -102,6 +102,32 @@ def test_gpu_parity_multispecies(dim, order, n, bc):
     assert rel_err(got2, ref) <= 1e-12 and rel_err(got, got2) <= 1e-12
 
 
+MIXTURES = {
+    2: dict(R=(1.0, 0.8), cv=(2.5, 2.0), h0=(0.5, -0.5), reaction=(0, 1)),
+    4: dict(R=(1.0, 0.8, 1.2, 0.9), cv=(2.5, 2.0, 3.0, 2.2), h0=(0.5, -0.5, 0.0, 0.1), reaction=(0, 3)),
+    5: dict(R=(1.0, 0.8, 1.2, 0.9, 1.1), cv=(2.5, 2.0, 3.0, 2.2, 2.6), h0=(0.5, -0.5, 0.0, 0.1, -0.2), reaction=(1, 4)),
+}
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("ns,dim,order,n,bc", [(2, 3, 3, 3, "periodic"), (2, 2, 4, 4, "farfield"), (4, 3, 3, 3, "farfield"),
+                                               (4, 3, 4, 3, "periodic"), (4, 2, 2, 5, "farfield"), (2, 3, 3, 10, "farfield"),
+                                               (4, 3, 3, 8, "farfield"), (5, 3, 2, 3, "periodic")])
+def test_gpu_parity_species_counts(ns, dim, order, n, bc):
+    """The fused kernels are instantiated for 2, 3 and 4 species (csrc/dgb_msflux{2,3,4}.cu); any other count runs the
+    same program op by op on the device.  Both against the oracle, incl. mid-size meshes (tens of blocks per warp)."""
+    from paper_2512_17101_b200 import B200ArrayContext, fused
+    gpu, cpu = B200ArrayContext(), NumpyArrayContext()
+    dc, dg = make_dcoll(cpu, dim, order, n, bc), make_dcoll(gpu, dim, order, n, bc)
+    oc, og = MultispeciesOperator(dc, Mixture(**MIXTURES[ns])), MultispeciesOperator(dg, Mixture(**MIXTURES[ns]))
+    assert bool(getattr(og._flux, "fused", False)) == (ns in fused.MS_FUSED_SPECIES)
+    q0 = ms_state(oc, dc.nodes())
+    ref = dc.to_numpy(oc.rhs(dc.from_numpy(q0)))
+    got = dg.to_numpy(og.rhs(dg.from_numpy(q0)))
+    assert np.all(np.isfinite(got)) and rel_err(got, ref) <= 1e-12, rel_err(got, ref)
+
+
 @pytest.mark.gpu
 @pytest.mark.timeout(900)
 @pytest.mark.parametrize("order,n,bc", [(3, 12, "farfield"), (3, 8, "periodic"), (4, 6, "farfield")])
