@@ -23,6 +23,11 @@
 #ifndef DGB_DIV8_EARLY
 #define DGB_DIV8_EARLY 1
 #endif
+// face phase as a rolled loop over batches of 3 rounds (no early gathers): -1 automatic (order 4: 64 -> 44 KB of SASS,
+// pass 2 -3.6 %; order 3 keeps the unrolled loop with every round in flight: rolled it is 15 % slower), 0 / 1 off / on
+#ifndef DGB_DIV8_ROLLED
+#define DGB_DIV8_ROLLED -1
+#endif
 #ifndef DGB_DIV8_NB
 #define DGB_DIV8_NB 0              // 0: every round of a block in flight together (8 warps) / one round (more warps)
 #endif
@@ -225,6 +230,29 @@ __device__ __forceinline__ void div_face_lean(const int (&rw)[face_rounds<DIM, P
   }
 }
 
+// The same with a ROLLED loop over the batches (the per-round words come from shared memory instead of registers):
+// a third of the code for order 4, where the kernel is twice the size of the L1.5 instruction cache
+template <int DIM, int P, int KW, int NB, bool GH>
+__device__ __forceinline__ void div_face_lean_rolled(const int* __restrict__ flc, int lane, const Div8Geo<DIM, P, KW>& g,
+                                                     const double* __restrict__ Qb, const double* __restrict__ Lam,
+                                                     double* __restrict__ Fs, const DiscDev& d,
+                                                     const double* __restrict__ q, const double* __restrict__ T,
+                                                     const double* __restrict__ ghost, const double* __restrict__ Tghost,
+                                                     const Phys& ph, long long e0, int nel) {
+  constexpr int C = ElemT<DIM, P>::C;
+  constexpr int NR = face_rounds<DIM, P, KW>();
+#pragma unroll 1
+  for (int k0 = 0; k0 < NR; k0 += NB) {
+    int rwb[NR];
+#pragma unroll
+    for (int b = 0; b < NR; ++b) rwb[b] = (b < NB && k0 + b < NR) ? lean_round_word<DIM, P, KW>(flc[(k0 + b) * 32 + lane]) : -1;
+    double qp[NB][C], nbr[NB][C], lam_p[NB];
+    int hi[NB];
+    face_lean_issue<DIM, P, KW, NB, GH>(0, rwb, g, d, q, T, ghost, Tghost, e0, nel, qp, nbr, lam_p, hi);
+    face_lean_consume<DIM, P, KW, NB>(0, rwb, g, Qb, Lam, Fs, d, T, ph, e0, qp, nbr, lam_p, hi);
+  }
+}
+
 template <int DIM, int P, int KW>
 struct alignas(128) Div8Warp {
   using EL = ElemT<DIM, P>;
@@ -269,7 +297,8 @@ k_nsdiv8(DiscDev d, const __grid_constant__ CUtensorMap map_q, const __grid_cons
   constexpr int NR = face_rounds<DIM, P, KW>();
   // face nodes per lane with their gathers in flight together: all NR rounds of a block at 8 warps (11 values per
   // node: 88 registers for 3D p3), one round at 9-12 warps (168 registers)
-  constexpr int NB = DGB_DIV8_NB > 0 ? DGB_DIV8_NB : (NWARPS > 8 ? 1 : (C <= 5 ? NR : 2));     // 2 C + 1 values per node
+  constexpr bool ROLLED = DGB_DIV8_ROLLED >= 0 ? DGB_DIV8_ROLLED != 0 : (NP > 20 && DGB_NSPEC == 0);
+  constexpr int NB = DGB_DIV8_NB > 0 ? DGB_DIV8_NB : (ROLLED ? (C <= 5 ? 3 : 2) : (NWARPS > 8 ? 1 : (C <= 5 ? NR : 2)));     // 2 C + 1 values per node
   constexpr int BOXW = BX::BOXW;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   auto& S = *reinterpret_cast<Div8Smem<DIM, P, KW, NWARPS>*>(smem_raw);
@@ -344,7 +373,7 @@ k_nsdiv8(DiscDev d, const __grid_constant__ CUtensorMap map_q, const __grid_cons
   // EARLY: the gathers of block b+1 are issued right after the contraction of block b, before its store epilogue,
   // and consumed at the top of the next iteration -- their L2 round trip (ncu: 17 % of the stall samples sit on the
   // first use of a gathered value) runs under the epilogue, the ticket, the staging and the mbarrier waits.
-  constexpr bool EARLY = (DGB_DIV8_EARLY != 0) && NB >= NR;
+  constexpr bool EARLY = (DGB_DIV8_EARLY != 0) && NB >= NR && !ROLLED;
   constexpr int NG = EARLY ? NB : 1;
   double gqp[NG][C], gnb[NG][C], glam[NG];
   int ghi[NG];
@@ -380,6 +409,8 @@ k_nsdiv8(DiscDev d, const __grid_constant__ CUtensorMap map_q, const __grid_cons
 #ifndef DGB_EXP_NOFACE              // timing experiments only (results invalid)
     if (EARLY)
       face_lean_consume<DIM, P, KW, NG>(0, rw, W.geo[buf], W.Qb + sh, W.Lam + sh, W.Fs, d, T, ph, e0, gqp, gnb, glam, ghi);
+    else if (ROLLED)
+      div_face_lean_rolled<DIM, P, KW, NB, GH>(S.flc, lane, W.geo[buf], W.Qb + sh, W.Lam + sh, W.Fs, d, q, T, ghost, Tghost, ph, e0, nel);
     else
       div_face_lean<DIM, P, KW, NB, GH>(rw, W.geo[buf], W.Qb + sh, W.Lam + sh, W.Fs, d, q, T, ghost, Tghost, ph, e0, nel);
 #endif

@@ -16,6 +16,9 @@ PKG = os.path.join(ROOT, "paper_2512_17101_b200")
 VARIANTS = {
     "timing": ["DGB_PHASE_TIMING=1"],                 # scripts/phase_timing_flux.py
     "base": [],
+    "roll2": ["DGB_DIV8_ROLLED=1"],
+    "roll3": ["DGB_DIV8_ROLLED=1", "DGB_DIV8_NB=3"],
+    "roll1": ["DGB_DIV8_ROLLED=1", "DGB_DIV8_NB=1"],
     "pwu4": ["DGB_FLUX_PW_UNROLL=4"],
     "epwu1": ["DGB_EULER_PW_UNROLL=1"],
     "mt": ["DGB_FLUX_MT=1"],
