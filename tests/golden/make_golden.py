@@ -3,7 +3,7 @@ REAL reference package (/root/reference/pkg/src/laze): its eager context, its la
 (graph passes -> scalar IR -> loop passes -> NumPy interpreter) and its eager_eval oracle.
 
 Run in the build container only (the reference does not travel to the GPU box):
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py [--ms-only]
 Small cases only: the lazy interpreter runs at ~0.1 MDOF/s.
 """
 import os
@@ -34,7 +34,8 @@ def main():
     sys.path.insert(0, "/root/reference/pkg/src")
     global laze
     import laze  # the real reference; only available in the build container
-    for name, dim, order, n, bc, opname, kw, state in CASES:
+    only_ms = "--ms-only" in sys.argv           # regenerate only the multi-species vectors
+    for name, dim, order, n, bc, opname, kw, state in ([] if only_ms else CASES):
         eager = laze.ArrayContext(mode="eager")
         probe = make_dcoll(eager, dim, order, n, bc)
         q0 = random_state(dim, probe.nelements, probe.Np, seed=11) if state == "random" else smooth_state(probe.nodes())
@@ -48,6 +49,22 @@ def main():
             print(f"{name:26s} {k:5s} lazy-vs-eager rel diff {np.abs(res_l[k] - v).max() / scale:.2e}")
         np.savez_compressed(os.path.join(HERE, name + ".npz"), **payload)
 
+    # the multi-species reactive operator (BASELINE configs[4]) through both reference contexts
+    from paper_2512_17101_b200 import Mixture, MultispeciesOperator
+    from tests.common import MS_GOLDEN_CASES, MS_MIXTURES, ms_state
+    for name, dim, order, n, bc, ns in MS_GOLDEN_CASES:
+        res = {}
+        for mode in ("eager", "lazy"):
+            actx = laze.ArrayContext(mode=mode)
+            d = make_dcoll(actx, dim, order, n, bc)
+            op = MultispeciesOperator(d, Mixture(**MS_MIXTURES[ns]))
+            q0 = ms_state(op, d.nodes())
+            res[mode] = np.asarray(actx.to_numpy(op.rhs(d.from_numpy(q0)).data))
+        print(f"{name:26s} rhs   lazy-vs-eager rel diff {np.abs(res['lazy'] - res['eager']).max() / max(np.abs(res['eager']).max(), 1.0):.2e}")
+        np.savez_compressed(os.path.join(HERE, name + ".npz"), q0=q0, eager_rhs=res["eager"], lazy_rhs=res["lazy"])
+
+    if only_ms:
+        return
     # 20 RK4 steps of the 2D isentropic-vortex-sized Euler case through the reference's eager context
     eager = laze.ArrayContext(mode="eager")
     d = make_dcoll(eager, 2, 3, 4, "periodic")

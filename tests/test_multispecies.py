@@ -9,25 +9,9 @@ import pytest
 
 from oracle.laze_port import NumpyArrayContext, rel_err
 from paper_2512_17101_b200 import EulerOperator, Mixture, MultispeciesOperator
-from tests.common import make_dcoll, smooth_state
+from tests.common import MS_GOLDEN_CASES, MS_MIXTURES, make_dcoll, ms_state, smooth_state
 
 REF = "/root/reference/pkg/src"
-
-
-def ms_state(op, nodes, seed=0):
-    """Smooth multispecies state on nodes (dim, E, Np)."""
-    dim = nodes.shape[0]
-    r2 = (nodes ** 2).sum(axis=0)
-    bump = np.exp(-r2 / (2 * 0.4 ** 2))
-    rho = 1.0 + 0.1 * bump
-    vel = [0.1 * np.sin(np.pi * nodes[(i + 1) % dim]) for i in range(dim)]
-    T = 1.0 + 0.2 * bump
-    ns = op.mix.ns
-    Y = [np.full_like(rho, 1.0 / ns) for _ in range(ns)]
-    if ns > 1:
-        Y[0] = Y[0] + 0.1 * bump
-        Y[-1] = Y[-1] - 0.1 * bump
-    return op.state_from_primitive(rho, vel, T, Y)
 
 
 def test_reduces_to_euler_for_one_inert_species():
@@ -102,11 +86,7 @@ def test_gpu_parity_multispecies(dim, order, n, bc):
     assert rel_err(got2, ref) <= 1e-12 and rel_err(got, got2) <= 1e-12
 
 
-MIXTURES = {
-    2: dict(R=(1.0, 0.8), cv=(2.5, 2.0), h0=(0.5, -0.5), reaction=(0, 1)),
-    4: dict(R=(1.0, 0.8, 1.2, 0.9), cv=(2.5, 2.0, 3.0, 2.2), h0=(0.5, -0.5, 0.0, 0.1), reaction=(0, 3)),
-    5: dict(R=(1.0, 0.8, 1.2, 0.9, 1.1), cv=(2.5, 2.0, 3.0, 2.2, 2.6), h0=(0.5, -0.5, 0.0, 0.1, -0.2), reaction=(1, 4)),
-}
+MIXTURES = MS_MIXTURES
 
 
 @pytest.mark.gpu
@@ -297,3 +277,36 @@ def test_gpu_multispecies_cp_async_fallback(dim, order, n, bc, monkeypatch):
         monkeypatch.setenv("DGB_DIV_KERNEL", k)
         outs[k] = d.to_numpy(op.rhs(q))
     assert np.all(np.isfinite(outs["3"])) and rel_err(outs["3"], outs["8"]) <= 1e-14
+
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.mark.parametrize("case", MS_GOLDEN_CASES, ids=[c[0] for c in MS_GOLDEN_CASES])
+def test_multispecies_program_matches_reference_golden(case):
+    """The oracle context against vectors the REAL reference produced for the multi-species program
+    (tests/golden/make_golden.py: laze eager context and lazy compile pipeline)."""
+    name, dim, order, n, bc, ns = case
+    g = np.load(os.path.join(GOLD, name + ".npz"))
+    actx = NumpyArrayContext()
+    d = make_dcoll(actx, dim, order, n, bc)
+    op = MultispeciesOperator(d, Mixture(**MS_MIXTURES[ns]))
+    assert np.array_equal(ms_state(op, d.nodes()), g["q0"])
+    rhs = d.to_numpy(op.rhs(d.from_numpy(g["q0"])))
+    assert np.array_equal(rhs, g["eager_rhs"])
+    assert rel_err(rhs, g["lazy_rhs"]) <= 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", MS_GOLDEN_CASES, ids=[c[0] for c in MS_GOLDEN_CASES])
+def test_gpu_multispecies_matches_reference_golden(case):
+    """The fused multi-species kernels against the REAL reference's vectors."""
+    from paper_2512_17101_b200 import B200ArrayContext
+    name, dim, order, n, bc, ns = case
+    g = np.load(os.path.join(GOLD, name + ".npz"))
+    gpu = B200ArrayContext()
+    d = make_dcoll(gpu, dim, order, n, bc)
+    op = MultispeciesOperator(d, Mixture(**MS_MIXTURES[ns]))
+    assert getattr(op._f, "fused", False)
+    got = d.to_numpy(op.rhs(d.from_numpy(g["q0"])))
+    assert rel_err(got, g["eager_rhs"]) <= 1e-12 and rel_err(got, g["lazy_rhs"]) <= 1e-12
