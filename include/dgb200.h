@@ -154,6 +154,13 @@ int dgb_ns_div_range(const dgb_disc* disc, const double* q_dev, const double* T_
                      const double* ghost_dev, const double* Tghost_dev, double* rhs_dev,
                      const double* qfar_host, const double* phys_host,
                      int64_t ebegin, int64_t eend, void* stream);
+/* dgb_ns_div_rk on a sub-range: the partitioned right-hand side with the RK stage update fused into the store of
+ * pass 2 (north-star items 3 and 4 together; halo.py: HaloExchange.ns_rhs_rk); eend < 0 = all elements */
+int dgb_ns_div_rk_range(const dgb_disc* disc, const double* q_dev, const double* T_dev,
+                        const double* ghost_dev, const double* Tghost_dev,
+                        const double* x1_dev, double* out1_dev, const double* x2_dev, double* out2_dev,
+                        const double* rk_host, const double* qfar_host, const double* phys_host,
+                        int64_t ebegin, int64_t eend, void* stream);
 
 /* ---- multi-species reactive Navier-Stokes (BASELINE configs[4]): the outlined functions dg_ms_flux / dg_ms_div of
  *      multispecies.py (Call nodes of the reference: adfg.py:722-803; op families: IndexLambda with exp / truediv,

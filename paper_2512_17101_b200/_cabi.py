@@ -20,7 +20,7 @@ SYMBOLS = [
     "dgb_disc_create", "dgb_disc_destroy", "dgb_disc_expand_maps", "dgb_debug_phase_cycles",
     "dgb_euler_rhs", "dgb_ns_grad", "dgb_ns_rhs", "dgb_euler_rhs_rk", "dgb_ns_rhs_rk",
     "dgb_disc_set_jacobian", "dgb_ns_flux", "dgb_ns_div", "dgb_ns_div_rk",
-    "dgb_euler_rhs_range", "dgb_ns_flux_range", "dgb_ns_div_range", "dgb_ms_flux_range", "dgb_ms_div_range", "dgb_ms_div_rk",
+    "dgb_euler_rhs_range", "dgb_ns_flux_range", "dgb_ns_div_range", "dgb_ns_div_rk_range", "dgb_ms_flux_range", "dgb_ms_div_range", "dgb_ms_div_rk",
     "dgb_pack_elements", "dgb_pack_elements_to", "dgb_ipc_alloc", "dgb_ipc_open", "dgb_ipc_close",
     "dgb_flag_signal", "dgb_flag_wait",
     "dgb_ew_binary", "dgb_ew_unary", "dgb_ew_where", "dgb_copy_strided", "dgb_copy_scatter", "dgb_take", "dgb_take_deferred",
@@ -108,6 +108,7 @@ def load():
     lib.dgb_euler_rhs_range.argtypes = [vp, dp, dp, dp, vp, vp, i64, i64, vp]
     lib.dgb_ns_flux_range.argtypes = [vp, dp, dp, dp, vp, vp, i64, i64, vp]
     lib.dgb_ns_div_range.argtypes = [vp, dp, dp, dp, dp, dp, vp, vp, i64, i64, vp]
+    lib.dgb_ns_div_rk_range.argtypes = [vp, dp, dp, dp, dp, dp, dp, dp, dp, vp, vp, vp, i64, i64, vp]
     lib.dgb_ms_flux_range.argtypes = [vp, dp, dp, dp, vp, vp, vp, i64, i64, vp]
     lib.dgb_ms_div_range.argtypes = [vp, dp, dp, dp, dp, dp, vp, vp, vp, i64, i64, vp]
     lib.dgb_ms_div_rk.argtypes = [vp, dp, dp, dp, dp, dp, dp, dp, dp, vp, vp, vp, vp, vp]

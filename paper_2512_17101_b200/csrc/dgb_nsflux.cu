@@ -128,9 +128,9 @@ int dgb_ns_div_range(const dgb_disc* d, const double* q, const double* T, const 
   return ns_div_impl(d, q, T, ghost, Tghost, ep, qfar, phys, stream, ebegin, eend);
 }
 
-int dgb_ns_div_rk(const dgb_disc* d, const double* q, const double* T, const double* ghost, const double* Tghost,
-                  const double* x1, double* out1, const double* x2, double* out2, const double* rk,
-                  const double* qfar, const double* phys, void* stream) {
+int dgb_ns_div_rk_range(const dgb_disc* d, const double* q, const double* T, const double* ghost, const double* Tghost,
+                        const double* x1, double* out1, const double* x2, double* out2, const double* rk,
+                        const double* qfar, const double* phys, int64_t ebegin, int64_t eend, void* stream) {
   if (!out1 || !rk) return dgb_fail(DGB_ERR_INVALID, "out1 and rk are required");
   if (out1 == q || (out2 && out2 == q) || (x2 && out1 == x2))
     return dgb_fail(DGB_ERR_INVALID, "RK outputs must not alias the stage input q (neighbours still read it)");
@@ -138,7 +138,13 @@ int dgb_ns_div_rk(const dgb_disc* d, const double* q, const double* T, const dou
   if ((((uintptr_t)x1) | ((uintptr_t)out1) | ((uintptr_t)x2) | ((uintptr_t)out2)) & 15)
     return dgb_fail(DGB_ERR_INVALID, "RK operands and outputs must be 16-byte aligned");
   dgb::Epilogue ep{x1, out1, x2, out2, rk[0], rk[1], rk[2], rk[3]};
-  return ns_div_impl(d, q, T, ghost, Tghost, ep, qfar, phys, stream);
+  return ns_div_impl(d, q, T, ghost, Tghost, ep, qfar, phys, stream, ebegin, eend);
+}
+
+int dgb_ns_div_rk(const dgb_disc* d, const double* q, const double* T, const double* ghost, const double* Tghost,
+                  const double* x1, double* out1, const double* x2, double* out2, const double* rk,
+                  const double* qfar, const double* phys, void* stream) {
+  return dgb_ns_div_rk_range(d, q, T, ghost, Tghost, x1, out1, x2, out2, rk, qfar, phys, 0, -1, stream);
 }
 
 }  // extern "C"

@@ -365,6 +365,25 @@ def ns_div_range(actx, op, q, T, ghost, Tghost, out, lo, hi):
                                           op.phys_host.ctypes.data, int(lo), int(hi), actx._st), "dg_ns_div (range)")
     actx.launch_count += 1
 
+def ns_div_rk_range(actx, op, q, T, ghost, Tghost, x1, out1, x2, out2, coef, lo, hi):
+    """``out1[:, lo:hi] = a1 x1 + b1 rhs``, ``out2[:, lo:hi] = a2 x2 + b2 rhs`` with ``rhs = dg_ns_div(q, T)``
+    (dgb_ns_div_rk_range): the RK stage update fused into pass 2 of a partitioned right-hand side."""
+    q = _f64(actx, q, "q")
+    npl = flux_planes(op.dim)
+    G, g, gptr = _ghost_ptr(actx, ghost, (op.dim + 2,), q.shape[-1])
+    TG, tg, tgptr = _ghost_ptr(actx, Tghost, (npl,), q.shape[-1])
+    disc = _op_disc(actx, op, q, G)
+    _bind_jacobian(actx, disc, op.dcoll.jac)
+    _check_facemat(disc, op.dcoll.facemat, op.dcoll.facemat_p)
+    x1, x2 = _f64(actx, x1, "x1"), _f64(actx, x2, "x2")
+    if x1.shape != q.shape or x2.shape != q.shape or out1.shape != q.shape or out2.shape != q.shape:
+        raise errors.BindingMismatch("RK operands and outputs must have the shape of the state")
+    rk = np.ascontiguousarray(np.asarray(coef, dtype=np.float64).reshape(4))
+    _cabi.check(actx.lib.dgb_ns_div_rk_range(disc.handle, q.ptr, T.ptr, gptr, tgptr, x1.ptr, out1.ptr, x2.ptr, out2.ptr,
+                                             rk.ctypes.data, op.qfar_host.ctypes.data, op.phys_host.ctypes.data,
+                                             int(lo), int(hi), actx._st), "dg_ns_div_rk (range)")
+    actx.launch_count += 1
+
 # }}}
 
 

@@ -400,6 +400,35 @@ class HaloExchange:
         self._release(t2)
         return DOFArray(actx, out)
 
+    def ns_rhs_rk(self, op, q: DOFArray, x1: DOFArray, x2: DOFArray, coef, t=0.0):
+        """``(a1*x1 + b1*rhs(q), a2*x2 + b2*rhs(q))`` on a partitioned mesh, ``coef = (a1, b1, a2, b2)``: the stage update
+        is fused into the store of pass 2 (``dgb_ns_div_rk_range``) on the device; elsewhere (oracle context, no
+        overlap) it is the exchange-then-compute right-hand side followed by array arithmetic.  Same contract as
+        ``NavierStokesOperator.rhs_rk``, so ``rk4_step_fused(PartitionedOperator(halo, op), q, t, dt)`` steps in time."""
+        a1, b1, a2, b2 = (float(c) for c in coef)
+        if not self._can_overlap():
+            r = self.ns_rhs(op, q)
+            return a1 * x1 + b1 * r, a2 * x2 + b2 * r
+        from . import fused
+        actx, nI, E = self.actx, self.plan.n_interior, self.plan.nlocal
+        t1 = self._begin(q.data)
+        T = actx.empty((fused.flux_planes(op.dim),) + tuple(q.data.shape[1:]))
+        self._reserve(True)
+        fused.ns_flux_range(actx, op, q.data, self._ghost_of(t1), T, 0, nI)
+        self._reserve(False)
+        ghost = self._end(t1)
+        fused.ns_flux_range(actx, op, q.data, ghost, T, nI, E)
+        t2 = self._begin(T)
+        o1, o2 = actx.empty(q.data.shape), actx.empty(q.data.shape)
+        self._reserve(True)
+        fused.ns_div_rk_range(actx, op, q.data, T, ghost, self._ghost_of(t2), x1.data, o1, x2.data, o2, (a1, b1, a2, b2), 0, nI)
+        self._reserve(False)
+        tghost = self._end(t2)
+        fused.ns_div_rk_range(actx, op, q.data, T, ghost, tghost, x1.data, o1, x2.data, o2, (a1, b1, a2, b2), nI, E)
+        self._release(t1)
+        self._release(t2)
+        return DOFArray(actx, o1), DOFArray(actx, o2)
+
     def ms_rhs(self, op, q: DOFArray) -> DOFArray:
         """Multi-species operator: state halos, then flux-plane halos; with the fused kernels each exchange runs
         under the interior range of its pass, like ``ns_rhs``."""
@@ -430,6 +459,20 @@ class HaloExchange:
         ghost = self.exchange(q.data)
         return op.rhs_grad_form(q, ghost=ghost, halo_fn=lambda gq: self.exchange(gq.data))
     # }}}
+
+
+class PartitionedOperator:
+    """``rhs`` / ``rhs_rk`` of a Navier-Stokes operator on one rank of a partitioned mesh (halo exchanges inside), with
+    the interface ``rk4_step`` / ``rk4_step_fused`` expect of an operator."""
+
+    def __init__(self, halo: HaloExchange, op):
+        self.halo, self.op, self.actx, self.dim, self.dcoll = halo, op, op.actx, op.dim, op.dcoll
+
+    def rhs(self, q: DOFArray, t=0.0) -> DOFArray:
+        return self.halo.ns_rhs(self.op, q)
+
+    def rhs_rk(self, q: DOFArray, x1: DOFArray, x2: DOFArray, coef, t=0.0):
+        return self.halo.ns_rhs_rk(self.op, q, x1, x2, coef, t)
 
 
 def ring_slab_halo(actx, mesh, ncells_x, rank, nranks, order, lo_x=-1.0, hi_x=1.0, transport="nccl"):

@@ -324,3 +324,80 @@ def test_two_ranks_one_gpu_multispecies(transport):
     pass, two ranks sharing the one GPU (gloo staging / CUDA-IPC peer stores)."""
     sys.path.insert(0, ROOT)
     assert _check_ms(_run("partition", device=True, transport=transport, target=_ms_worker)) <= 1e-12
+
+
+def _rk_worker(rank, world, port, mode, outq, device=False, transport="nccl"):
+    """A few RK4 steps on a partitioned mesh with the stage update fused into pass 2 (``HaloExchange.ns_rhs_rk``)."""
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2512_17101_b200 import DGDiscretization, NavierStokesOperator, box_mesh, rk4_step, rk4_step_fused
+        from paper_2512_17101_b200.dg.partition import interior_first, partition_elements, rank_mesh
+        from paper_2512_17101_b200.halo import HaloExchange, PartitionedOperator, TorchCommunicator
+        from oracle.laze_port import NumpyArrayContext
+        from tests.common import smooth_state
+        if device:
+            from paper_2512_17101_b200 import B200ArrayContext
+            actx = B200ArrayContext()
+        else:
+            actx = NumpyArrayContext()
+        comm = TorchCommunicator()
+        base = box_mesh((3,) * 3, (-1,) * 3, (1,) * 3, periodic=(True,) * 3)
+        dref = DGDiscretization(NumpyArrayContext(), base, 2)
+        q0 = smooth_state(dref.nodes())
+        local, plan = rank_mesh(base, partition_elements(base, world), rank)
+        q0 = q0[:, plan.global_ids, :]
+        if device:
+            local, plan = interior_first(local, plan)
+            q0 = q0[:, plan.local_perm, :]
+        d = DGDiscretization(actx, local, 2, ghost_elements=plan.nghost)
+        halo = HaloExchange(actx, plan, comm, d.Np, transport=transport)
+        pop = PartitionedOperator(halo, NavierStokesOperator(d, mu=2e-2))
+        qf, qu, t, dt = d.from_numpy(q0), d.from_numpy(q0), 0.0, 2e-3
+        for _ in range(4):
+            qf = rk4_step_fused(pop, qf, t, dt)
+            qu = rk4_step(pop.rhs, qu, t, dt)
+            t += dt
+        halo.close()
+        outq.put((rank, plan.global_ids, d.to_numpy(qf), d.to_numpy(qu)))
+    finally:
+        dist.destroy_process_group()
+
+
+def _check_rk(res):
+    from oracle.laze_port import NumpyArrayContext, rel_err
+    from paper_2512_17101_b200 import DGDiscretization, NavierStokesOperator, box_mesh, rk4_step
+    from tests.common import smooth_state
+    actx = NumpyArrayContext()
+    mesh = box_mesh((3,) * 3, (-1,) * 3, (1,) * 3, periodic=(True,) * 3)
+    d = DGDiscretization(actx, mesh, 2)
+    op = NavierStokesOperator(d, mu=2e-2)
+    q, t, dt = d.from_numpy(smooth_state(d.nodes())), 0.0, 2e-3
+    for _ in range(4):
+        q = rk4_step(op.rhs, q, t, dt)
+        t += dt
+    ref = d.to_numpy(q)
+    fused_, plain = np.empty_like(ref), np.empty_like(ref)
+    for rank, ids, qf, qu in res:
+        fused_[:, ids, :], plain[:, ids, :] = qf, qu
+    return rel_err(fused_, ref), rel_err(plain, ref)
+
+
+@pytest.mark.timeout(600)
+def test_partitioned_fused_rk_matches_single_domain():
+    """rk4_step_fused over a PartitionedOperator (2 gloo ranks, oracle context) == single-domain rk4_step."""
+    sys.path.insert(0, ROOT)
+    ef, eu = _check_rk(_run("partition", world=2, target=_rk_worker))
+    assert ef <= 1e-13 and eu <= 1e-13
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("transport", ["nccl", "peer"])
+def test_two_ranks_one_gpu_fused_rk(transport):
+    """The same on the device: dgb_ns_div_rk_range on the interior and boundary ranges, both exchanges overlapped."""
+    sys.path.insert(0, ROOT)
+    ef, eu = _check_rk(_run("partition", device=True, transport=transport, target=_rk_worker))
+    assert ef <= 1e-12 and eu <= 1e-12
