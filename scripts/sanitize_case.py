@@ -6,7 +6,7 @@ import numpy as np
 from paper_2512_17101_b200 import B200ArrayContext, EulerOperator, Mixture, MultispeciesOperator, NavierStokesOperator
 from tests.common import FARFIELD, make_dcoll, random_state
 actx = B200ArrayContext()
-for dim, order, n, bc in [(3, 3, 2, "mixed"), (3, 3, 3, "periodic"), (2, 4, 3, "mixed"), (3, 4, 2, "farfield")]:
+for dim, order, n, bc in [(3, 3, 2, "mixed"), (3, 3, 3, "periodic"), (2, 4, 3, "mixed"), (3, 4, 2, "farfield"), (3, 4, 3, "periodic")]:
     d = make_dcoll(actx, dim, order, n, bc)
     q = d.from_numpy(random_state(dim, d.nelements, d.Np, seed=2))
     ns = NavierStokesOperator(d, farfield=FARFIELD[dim], mu=2e-2)
@@ -18,12 +18,14 @@ for dim, order, n, bc in [(3, 3, 2, "mixed"), (3, 3, 3, "periodic"), (2, 4, 3, "
     vals = [float(np.abs(d.to_numpy(x)).max()) for x in (r, a, b, e, e1, e2)]
     assert all(np.isfinite(v) for v in vals)
     if bc in ("periodic", "farfield"):                     # the multi-species instantiation of the same kernels (C = dim + 5)
-        ms = MultispeciesOperator(d, Mixture())
-        rng = np.random.default_rng(4)
-        E, Np = d.nelements, d.Np
-        Y = rng.uniform(0.2, 0.5, (3, E, Np)); Y /= Y.sum(0)
-        qm = d.from_numpy(ms.state_from_primitive(rng.uniform(0.9, 1.1, (E, Np)), [rng.uniform(-0.1, 0.1, (E, Np)) for _ in range(dim)],
-                                                  rng.uniform(0.9, 1.1, (E, Np)), list(Y)))
-        v = float(np.abs(d.to_numpy(ms.rhs(qm))).max())
-        assert np.isfinite(v)
+        from tests.common import MS_MIXTURES
+        for nspec in (2, 3, 4):                            # one translation unit per species count
+            ms = MultispeciesOperator(d, Mixture(**MS_MIXTURES[nspec]))
+            rng = np.random.default_rng(4)
+            E, Np = d.nelements, d.Np
+            Y = rng.uniform(0.2, 0.5, (nspec, E, Np)); Y /= Y.sum(0)
+            qm = d.from_numpy(ms.state_from_primitive(rng.uniform(0.9, 1.1, (E, Np)), [rng.uniform(-0.1, 0.1, (E, Np)) for _ in range(dim)],
+                                                      rng.uniform(0.9, 1.1, (E, Np)), list(Y)))
+            v = float(np.abs(d.to_numpy(ms.rhs(qm))).max())
+            assert np.isfinite(v) and ms._f.fused
     print(dim, order, n, bc, "ok", flush=True)
