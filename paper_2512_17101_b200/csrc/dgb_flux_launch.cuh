@@ -148,7 +148,10 @@ int launch_div8(const dgb_disc* d, const double* q, const double* T, const doubl
   const long long need = (nwb + C::NW - 1) / C::NW;
   const int grid = (int)(need < dgb_grid_sms() ? need : dgb_grid_sms());
   DGB_CUDA(cudaMemsetAsync(d->counters + 1, 0, sizeof(unsigned long long), st));
-  kern<<<grid, C::NW * 32, smem, st>>>(d->dev, mq, mt, ml, q, T, ghost, Tghost, ep, ph, ebeg, eend, nwb, d->counters + 1);
+  dgb::GatherPlanes<EL::C> gp;
+  for (int c = 0; c < EL::C; ++c) { gp.q[c] = q + c * width; gp.t[c] = T + c * width; }
+  gp.lam = T + (long long)dgb::FluxT<DIM, P>::LAMPL * width;
+  kern<<<grid, C::NW * 32, smem, st>>>(d->dev, mq, mt, ml, q, T, ghost, Tghost, ep, ph, ebeg, eend, nwb, d->counters + 1, gp);
   DGB_CUDA(cudaGetLastError());
   return DGB_OK;
 }

@@ -25,6 +25,10 @@
 #endif
 // face phase as a rolled loop over batches of 3 rounds (no early gathers): -1 automatic (order 4: 64 -> 44 KB of SASS,
 // pass 2 -3.6 %; order 3 keeps the unrolled loop with every round in flight: rolled it is 15 % slower), 0 / 1 off / on
+// single-domain gathers addressed from opaque plane base pointers (GatherPlanes): pass 2 -0.1 ... -0.9 %
+#ifndef DGB_DIV8_PLANEBASE
+#define DGB_DIV8_PLANEBASE 1
+#endif
 #ifndef DGB_DIV8_ROLLED
 #define DGB_DIV8_ROLLED -1
 #endif
@@ -121,6 +125,16 @@ __device__ __forceinline__ int lean_round_word(int flk) {
   return (e * EL::NFT + fm) | ((e * EL::NF + f) << 8) | ((e * EL::NP + jm) << 12) | ((e * EL::LDF + fm) << 20) | (e << 28);
 }
 
+// Plane base pointers of the gathered arrays as kernel parameters (constant bank): written q + c*stride, the compiler
+// chains the 64-bit addresses from plane to plane (2 dependent instructions per value); opaque bases make every
+// address one independent multiply-add on the lane's offset.
+template <int C>
+struct GatherPlanes {
+  const double* q[C];
+  const double* t[C];
+  const double* lam;
+};
+
 // Lean face phase (pass 2): the neighbour's node comes from the precomputed gather map instead of being decoded
 // from the connectivity word through the face-node / permutation tables, every lane carries its per-round
 // constants in one register, and a face selects ONE plane group of T.  Same arithmetic as div_face_phase.
@@ -130,7 +144,8 @@ __device__ __forceinline__ void face_lean_issue(int k0, const int (&rw)[face_rou
                                                 const DiscDev& d, const double* __restrict__ q, const double* __restrict__ T,
                                                 const double* __restrict__ ghost, const double* __restrict__ Tghost,
                                                 long long e0, int nel, double (&qp)[NB][ElemT<DIM, P>::C],
-                                                double (&nbr)[NB][ElemT<DIM, P>::C], double (&lam_p)[NB], int (&hi)[NB]) {
+                                                double (&nbr)[NB][ElemT<DIM, P>::C], double (&lam_p)[NB], int (&hi)[NB],
+                                                const GatherPlanes<ElemT<DIM, P>::C>& gp) {
   using EL = ElemT<DIM, P>;
   constexpr int C = EL::C, NP = EL::NP;
   constexpr int NR = face_rounds<DIM, P, KW>();
@@ -152,6 +167,20 @@ __device__ __forceinline__ void face_lean_issue(int k0, const int (&rw)[face_rou
         hi[b] = (int)(connf[(w >> 8) & 15] >> 32);
         const int nf = hi[b] & 7;
         const int grp = nf == 0 ? DIM : nf - 1;
+#if DGB_DIV8_PLANEBASE
+        if (!GH) {
+          // single domain: every address is (plane base, uniform across the warp) + one per-lane offset -- no
+          // serial chain of 64-bit address updates from plane to plane
+          const long long goff = (long long)(grp * C) * ps_own + gi;
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            qp[b][c] = __ldg(gp.q[c] + gi);          // q and T are read-only in this kernel (the C ABI rejects
+            nbr[b][c] = __ldg(gp.t[c] + goff);        // RK outputs that alias q)
+          }
+          lam_p[b] = __ldg(gp.lam + gi);
+          continue;
+        }
+#endif
         const bool in_ghost = GH && gi >= enp;
         const long long ps = in_ghost ? d.G * NP : ps_own;
         const double* qb = in_ghost ? ghost + (gi - enp) : q + gi;
@@ -218,14 +247,15 @@ __device__ __forceinline__ void div_face_lean(const int (&rw)[face_rounds<DIM, P
                                               double* __restrict__ Fs, const DiscDev& d,
                                               const double* __restrict__ q, const double* __restrict__ T,
                                               const double* __restrict__ ghost, const double* __restrict__ Tghost,
-                                              const Phys& ph, long long e0, int nel) {
+                                              const Phys& ph, long long e0, int nel,
+                                              const GatherPlanes<ElemT<DIM, P>::C>& gp) {
   constexpr int C = ElemT<DIM, P>::C;
   constexpr int NR = face_rounds<DIM, P, KW>();
 #pragma unroll
   for (int k0 = 0; k0 < NR; k0 += NB) {          // unrolled: rw[] stays in registers
     double qp[NB][C], nbr[NB][C], lam_p[NB];
     int hi[NB];
-    face_lean_issue<DIM, P, KW, NB, GH>(k0, rw, g, d, q, T, ghost, Tghost, e0, nel, qp, nbr, lam_p, hi);
+    face_lean_issue<DIM, P, KW, NB, GH>(k0, rw, g, d, q, T, ghost, Tghost, e0, nel, qp, nbr, lam_p, hi, gp);
     face_lean_consume<DIM, P, KW, NB>(k0, rw, g, Qb, Lam, Fs, d, T, ph, e0, qp, nbr, lam_p, hi);
   }
 }
@@ -238,7 +268,8 @@ __device__ __forceinline__ void div_face_lean_rolled(const int* __restrict__ flc
                                                      double* __restrict__ Fs, const DiscDev& d,
                                                      const double* __restrict__ q, const double* __restrict__ T,
                                                      const double* __restrict__ ghost, const double* __restrict__ Tghost,
-                                                     const Phys& ph, long long e0, int nel) {
+                                                     const Phys& ph, long long e0, int nel,
+                                                     const GatherPlanes<ElemT<DIM, P>::C>& gp) {
   constexpr int C = ElemT<DIM, P>::C;
   constexpr int NR = face_rounds<DIM, P, KW>();
 #pragma unroll 1
@@ -248,7 +279,7 @@ __device__ __forceinline__ void div_face_lean_rolled(const int* __restrict__ flc
     for (int b = 0; b < NR; ++b) rwb[b] = (b < NB && k0 + b < NR) ? lean_round_word<DIM, P, KW>(flc[(k0 + b) * 32 + lane]) : -1;
     double qp[NB][C], nbr[NB][C], lam_p[NB];
     int hi[NB];
-    face_lean_issue<DIM, P, KW, NB, GH>(0, rwb, g, d, q, T, ghost, Tghost, e0, nel, qp, nbr, lam_p, hi);
+    face_lean_issue<DIM, P, KW, NB, GH>(0, rwb, g, d, q, T, ghost, Tghost, e0, nel, qp, nbr, lam_p, hi, gp);
     face_lean_consume<DIM, P, KW, NB>(0, rwb, g, Qb, Lam, Fs, d, T, ph, e0, qp, nbr, lam_p, hi);
   }
 }
@@ -288,7 +319,7 @@ k_nsdiv8(DiscDev d, const __grid_constant__ CUtensorMap map_q, const __grid_cons
          const __grid_constant__ CUtensorMap map_l, const double* __restrict__ q, const double* __restrict__ T,
          const double* __restrict__ ghost, const double* __restrict__ Tghost,
          Epilogue ep, Phys ph, long long ebeg, long long eend, long long nwblocks,
-         unsigned long long* __restrict__ counter) {
+         unsigned long long* __restrict__ counter, const GatherPlanes<ElemT<DIM, P>::C> gp) {
   using EL = ElemT<DIM, P>;
   using WS = Div8Warp<DIM, P, KW>;
   using BX = TmaBox<DIM, P, KW>;
@@ -385,7 +416,7 @@ k_nsdiv8(DiscDev d, const __grid_constant__ CUtensorMap map_q, const __grid_cons
     if (EARLY) {
       cp_async_wait<0>();
       __syncwarp();
-      face_lean_issue<DIM, P, KW, NG, GH>(0, rw, W.geo[0], d, q, T, ghost, Tghost, e0, nel_of(wb), gqp, gnb, glam, ghi);
+      face_lean_issue<DIM, P, KW, NG, GH>(0, rw, W.geo[0], d, q, T, ghost, Tghost, e0, nel_of(wb), gqp, gnb, glam, ghi, gp);
     }
   }
   TicketStream tks;
@@ -410,9 +441,9 @@ k_nsdiv8(DiscDev d, const __grid_constant__ CUtensorMap map_q, const __grid_cons
     if (EARLY)
       face_lean_consume<DIM, P, KW, NG>(0, rw, W.geo[buf], W.Qb + sh, W.Lam + sh, W.Fs, d, T, ph, e0, gqp, gnb, glam, ghi);
     else if (ROLLED)
-      div_face_lean_rolled<DIM, P, KW, NB, GH>(S.flc, lane, W.geo[buf], W.Qb + sh, W.Lam + sh, W.Fs, d, q, T, ghost, Tghost, ph, e0, nel);
+      div_face_lean_rolled<DIM, P, KW, NB, GH>(S.flc, lane, W.geo[buf], W.Qb + sh, W.Lam + sh, W.Fs, d, q, T, ghost, Tghost, ph, e0, nel, gp);
     else
-      div_face_lean<DIM, P, KW, NB, GH>(rw, W.geo[buf], W.Qb + sh, W.Lam + sh, W.Fs, d, q, T, ghost, Tghost, ph, e0, nel);
+      div_face_lean<DIM, P, KW, NB, GH>(rw, W.geo[buf], W.Qb + sh, W.Lam + sh, W.Fs, d, q, T, ghost, Tghost, ph, e0, nel, gp);
 #endif
     double rj[WS::NTILE];
 #pragma unroll
@@ -455,7 +486,7 @@ k_nsdiv8(DiscDev d, const __grid_constant__ CUtensorMap map_q, const __grid_cons
       cp_async_wait<0>();                // gather map + connectivity of the next block (staged at the top of this one)
       __syncwarp();
 #ifndef DGB_EXP_NOFACE
-      face_lean_issue<DIM, P, KW, NG, GH>(0, rw, W.geo[buf ^ 1], d, q, T, ghost, Tghost, e1, nel1, gqp, gnb, glam, ghi);
+      face_lean_issue<DIM, P, KW, NG, GH>(0, rw, W.geo[buf ^ 1], d, q, T, ghost, Tghost, e1, nel1, gqp, gnb, glam, ghi, gp);
 #endif
     }
 
