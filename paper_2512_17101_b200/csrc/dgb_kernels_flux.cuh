@@ -39,9 +39,10 @@
 // pass 1 tensor-core phase: one column tile at a time (0), all column tiles of a block in one sweep (1), or all tiles
 // with U_0 first and the Z_r chains started from -U_0 (2: 24 accumulator registers fewer per tile).  Sharing the W
 // fragments across tiles takes the operand LDS from 1.33 to 0.83 per DMMA.  Measured (profiles/r02_pass2_tma.md, section 12):
-// neutral on 3D p3 (12 warps, 168 registers: the step is power-bound), -1 % / -3 % of pass 1 where the launch has
-// 8 warps and 255 registers anyway.  -1: automatic (2 for order 4 or mixtures -- not both, and at most 10 accumulator
-// tiles per set: beyond that it spills --, else 0)
+// -1 % / -3 % of pass 1 where the launch has 8 warps and 255 registers (order 4, mixtures); at 3D p3 (12 warps, 168
+// registers, 20 B of spills) equal over 10 timed steps and +0.8 % GDOF/s over 20 / 50 / 100 steps (fewer shared-memory
+// reads: the step runs at the board power cap).  -1: automatic (2 up to 10 accumulator tiles per set -- beyond that it
+// spills --, else 0)
 #ifndef DGB_FLUX_MT
 #define DGB_FLUX_MT -1
 #endif
@@ -479,7 +480,7 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
     // operand rows) and DIM*DIM + DIM FP64 operations per value in the combination instead of
     // DIM*(DIM+NF).
     // MTF column tiles share every W fragment load (DGB_FLUX_MT)
-    constexpr int MTMODE = DGB_FLUX_MT >= 0 ? DGB_FLUX_MT : (((NP > 20) != (DGB_NSPEC > 0)) && WS::NTILE * NI <= 10 ? 2 : 0);
+    constexpr int MTMODE = DGB_FLUX_MT >= 0 ? DGB_FLUX_MT : (WS::NTILE * NI <= 10 ? 2 : 0);
     constexpr int MTF = MTMODE ? WS::NTILE : 1;
 #pragma unroll 1
     for (int tile0 = 0; tile0 < WS::NTILE; tile0 += MTF) {
