@@ -55,6 +55,11 @@
 #ifndef DGB_EULER_PW_UNROLL
 #define DGB_EULER_PW_UNROLL 1
 #endif
+// pass 1: the flux planes are written once and not read again by this kernel: streaming stores (st.global.cs) keep
+// L2 for the neighbour gathers
+#ifndef DGB_FLUX_T_STCS
+#define DGB_FLUX_T_STCS 0
+#endif
 #ifndef DGB_FLUX_SINGLEQ
 #define DGB_FLUX_SINGLEQ -1
 #endif
@@ -232,6 +237,14 @@ struct FluxT {
 // ------------------------------------------------------------------------------------------
 // pass 1: BR1 gradient -> total flux -> contravariant planes
 // ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void DGB_T_STORE(double* p, double v) {
+#if DGB_FLUX_T_STCS
+  __stcs(p, v);
+#else
+  *p = v;
+#endif
+}
+
 template <int DIM, int P, int KW>
 struct FluxGeo {
   using EL = ElemT<DIM, P>;
@@ -594,6 +607,7 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
         constexpr int NPLT = FluxT<DIM, P>::NPL;
         const long long t_ps = t_plane_stride<NPLT, NP>(E);
         double* out = T + (e0 + e) * t_elem_stride<NPLT, NP>() + j;
+        constexpr int LAMPL_ = FluxT<DIM, P>::LAMPL;
         double tsum[C];
 #pragma unroll
         for (int r = 0; r < DIM; ++r) {
@@ -605,13 +619,13 @@ k_nsflux3(DiscDev d, const double* __restrict__ q, const double* __restrict__ gh
             double acc = m[0] * F[0][c];
 #pragma unroll
             for (int x = 1; x < DIM; ++x) acc += m[x] * F[x][c];
-            out[(r * C + c) * t_ps] = acc;
+            DGB_T_STORE(out + (r * C + c) * t_ps, acc);
             tsum[c] = r == 0 ? acc : tsum[c] + acc;      // (T0 + T1) + T2, the order of the operator program
           }
         }
 #pragma unroll
-        for (int c = 0; c < C; ++c) out[(DIM * C + c) * t_ps] = tsum[c];
-        out[FluxT<DIM, P>::LAMPL * t_ps] = lam;
+        for (int c = 0; c < C; ++c) DGB_T_STORE(out + (DIM * C + c) * t_ps, tsum[c]);
+        DGB_T_STORE(out + LAMPL_ * t_ps, lam);
       }
     }
     __syncwarp();

@@ -16,6 +16,8 @@ PKG = os.path.join(ROOT, "paper_2512_17101_b200")
 VARIANTS = {
     "timing": ["DGB_PHASE_TIMING=1"],                 # scripts/phase_timing_flux.py
     "base": [],
+    "tcs": ["DGB_FLUX_T_STCS=1"],
+    "tcs_ocs": ["DGB_FLUX_T_STCS=1", "DGB_STREAMING_STORES=1"],
     "nopb": ["DGB_DIV8_PLANEBASE=0"],
     "roll2": ["DGB_DIV8_ROLLED=1"],
     "roll3": ["DGB_DIV8_ROLLED=1", "DGB_DIV8_NB=3"],
