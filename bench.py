@@ -580,7 +580,8 @@ def main():
     ap.add_argument("--n", "--cells", dest="n", type=int, default=94, help="cells per axis per GPU (94 -> 4,983,504 elements, 99.67M DOFs); under torchrun spell it --cells "
                          "(argparse in torch.distributed.run rejects `--n` as an ambiguous abbreviation of its own options)")
     ap.add_argument("--cpu-n", type=int, default=10, help="cells per axis of each CPU-baseline sample mesh")
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=20,
+                    help="streamed end-to-end evaluations timed (pipeline fill and drain included); at most --steps")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--order", type=int, default=3, help="polynomial order (headline: 3)")
